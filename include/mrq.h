@@ -1,0 +1,161 @@
+/*
+ * mrq.h -- C ABI of libmrq, the B200-native batched IVF-MRQ query path.
+ *
+ * MRQ = Minimized Residual Quantization, arXiv 2411.06158 (citations "P:N" are
+ * lines of its LaTeX source PAPER.md).  The library implements the paper's
+ * query process (Algorithm 2) for a batch of queries against an
+ * IVF index whose build-time artefacts (Algorithm 1 L1-L6: PCA
+ * matrix, eigenvalues, IVF centroids and assignment, plus the quantizer's
+ * random rotation P_r) come from a build file.  Encoding (Alg.1 L3-L8)
+ * runs on the GPU at load time.
+ *
+ * All functions return 0 (MRQ_OK) on success or a negative mrq_err; the
+ * message of the last failure on the calling thread is mrq_last_error().
+ * There is no CPU fallback: a missing GPU or a CUDA failure is an error.
+ *
+ * Numeric contract: every quantity that
+ * decides a bit, a level, a flag or an ordering is computed in fp64 with
+ * left-to-right sums and no fused multiply-add, so codes, bit-planes, flags
+ * and returned ids are bit-identical to the fp64 oracle (oracle/).
+ */
+#ifndef MRQ_H
+#define MRQ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mrq_index mrq_index;  /* opaque; owns all device memory of one rank */
+
+typedef enum {
+    MRQ_OK = 0,
+    MRQ_EINVAL = -1,      /* InvalidConfig: bad K, nprobe, eps0, m, mode, sizes, NULL    */
+    MRQ_EDIM = -2,        /* DimensionMismatch: D, d or n differ from the build file     */
+    MRQ_EFORMAT = -3,     /* FormatError: truncated/corrupt build file (message: offset) */
+    MRQ_EVERSION = -4,    /* VersionMismatch: bad magic or version                       */
+    MRQ_EDEGENERATE = -5, /* DegenerateData                                              */
+    MRQ_ECUDA = -6,       /* CUDA runtime failure (no device, launch error, ...)         */
+    MRQ_ENOMEM = -7,      /* device or host allocation failed                            */
+    MRQ_ENCCL = -8,       /* NCCL failure (multi-GPU)                                    */
+    MRQ_EIO = -9          /* cannot open/read the build file                             */
+} mrq_err;
+
+/* Multi-GPU placement.  NULL, or world == 1, means one GPU (the current device
+ * when device < 0).  With world > 1 every rank calls every function with
+ * identical arguments; IVF lists are sharded across ranks (greedy by size) and
+ * results are merged with an NCCL all-gather (nccl_unique_id: 128 bytes, the
+ * same on all ranks). */
+typedef struct {
+    int32_t rank, world, device;
+    const void *nccl_unique_id;
+} mrq_dist_cfg;
+
+/* Search parameters (Alg.2 inputs N^probe, eps0, m). */
+typedef struct {
+    int32_t K;            /* results per query, 1 <= K <= 1024                               */
+    int32_t nprobe;       /* probed lists, 1 <= nprobe <= min(k, 1024)                       */
+    double eps0;          /* Eq.5 confidence parameter, > 0; default 1.9              */
+    double m;             /* Chebyshev multiplier (Eq.7), > 0; default 4.0             */
+    int32_t mode;         /* 0 FULL (IVF-MRQ+: stage 1 + stage 2), 1 STAGE1_ONLY (IVF-MRQ),
+                             2 EXACT (exact distance of every probed candidate)              */
+    int32_t tau_schedule; /* 0 TIGHT, 1 LOOSE (DESIGN.md decision T)                          */
+    int32_t seed_mult;    /* K' = seed_mult * K seeds (>= 1; default 2)                        */
+    double resid_scale;   /* eps_r = (resid_scale * m) * sigma; 2 = distance domain (default) */
+} mrq_search_params;
+
+/* Per-call counters (summed over queries) and per-stage device milliseconds
+ * (CUDA events on the library's stream; filled only when stats != NULL, which
+ * makes the call synchronous). */
+typedef struct {
+    uint64_t scanned;      /* candidates whose code was scanned                 */
+    uint64_t stage1_pass;  /* |F1|: LB1 < tau0                                  */
+    uint64_t stage2_pass;  /* |F2|: dis_o' - eps_r < tau1                       */
+    uint64_t exact;        /* distinct exact distances computed (F2 u S0 u S1)  */
+    uint64_t seeds;        /* |S0| + |S1|                                        */
+    double ms_total, ms_qprep, ms_probe, ms_quant, ms_seed, ms_scan, ms_stage2, ms_rerank, ms_topk, ms_comm;
+} mrq_stats;
+
+/*
+ * Load an index.  build_file: path of an MRQBLD01 file (format below).
+ * base: HOST pointer, row-major n x D float32, borrowed for the call (copied
+ * to the device).  D and d must equal the file's; n must equal its N.
+ * Encodes every vector on the GPU (Alg.1 L3-L8): PCA rotation, head/tail
+ * split, centring on the own centroid, sign code under P_r, stored factors.
+ * On success *out owns the device memory until mrq_free.
+ * Errors: MRQ_EIO, MRQ_EVERSION, MRQ_EFORMAT, MRQ_EDIM, MRQ_EINVAL (d < 2,
+ * d > D, NULL), MRQ_ECUDA, MRQ_ENOMEM, MRQ_ENCCL.
+ */
+int mrq_index_load(const char *build_file, const float *base, int64_t n, int32_t D, int32_t d,
+                   const mrq_dist_cfg *dist, mrq_index **out);
+
+/*
+ * Batched search with HOST buffers: queries row-major nq x D float32
+ * (borrowed); out_ids (nq x K int64) and out_dist (nq x K float32) are
+ * caller-owned.  Row i of the outputs belongs to query i; within a row the
+ * results are ascending (distance, id); distance = exact squared L2 in the
+ * PCA-rotated space rounded to float32.  Fewer than K
+ * candidates: the tail is padded with id -1, distance +inf.  Synchronous.
+ * nq = 0 is valid and returns immediately.
+ */
+int mrq_search_batch(mrq_index *idx, const float *queries, int64_t nq, const mrq_search_params *p,
+                     int64_t *out_ids, float *out_dist, mrq_stats *stats);
+
+/*
+ * Same with DEVICE buffers (queries, out_ids, out_dist in device memory of
+ * the index's GPU) on `stream` (a cudaStream_t; 0 = the library's stream).
+ * Asynchronous unless stats != NULL.  Scratch is owned by the index and grows
+ * on demand (growing synchronizes once).
+ */
+int mrq_search_batch_device(mrq_index *idx, const float *d_queries, int64_t nq, const mrq_search_params *p,
+                            int64_t *d_out_ids, float *d_out_dist, mrq_stats *stats, void *stream);
+
+/* Free the index (NULL-safe): device memory, streams, NCCL communicator. */
+void mrq_free(mrq_index *idx);
+
+/* Thread-local message of the last error (never NULL). */
+const char *mrq_last_error(void);
+
+/* Index facts: n, D, d, k, W (code words), npad (list slots), local lists. */
+int mrq_index_info(const mrq_index *idx, int64_t *n, int32_t *D, int32_t *d, int32_t *k, int64_t *npad);
+
+/*
+ * Test hook: copy the named internal device buffer of the index or of the
+ * LAST search into host memory.  *bytes_needed receives its size; with
+ * dst == NULL only the size is reported.  Names and layouts (DESIGN.md
+ * "HBM layout"): "list_off" u32[k+1] slot offsets, "list_size" u32[k],
+ * "ids" u32[npad], "codes" u32[W][npad], "f1" "f2" "f3" "xr2" f32[npad],
+ * "heads" f32[npad][d], "tails" f32[npad][D-d], "Rc" f64[k][d], and per
+ * search: "qp" f64[nq][D], "qr2" "eps_r" "tau0" "tau1" f64[nq],
+ * "probe" u32[nq][np], "probe_qn2" f64[nq][np], "planes" u32[nq][np][4][W],
+ * "qconst" f64[nq][np][8], "f1_off" u64[nq], "f1_cnt" u32[nq], "f1_pos" u32[..],
+ * "f1_diso" f64[..], "f2_cnt" u32[nq], "f2_pos" u32[..], "f2_exact" f64[..],
+ * "s0_cnt" u32[nq], "s0_pos" u32[nq][Kp], "s0_exact" f64[nq][Kp], "s1_cnt",
+ * "s1_pos", "s1_exact".
+ * Errors: MRQ_EINVAL (unknown name, dst too small), MRQ_ECUDA.
+ */
+int mrq_debug_fetch(mrq_index *idx, const char *name, void *dst, size_t dst_bytes, size_t *bytes_needed);
+
+/*
+ * Test hook: set a debug switch of the index.  "dump_dis" = 1 makes every
+ * later search also write dis' and LB1 of every scanned candidate (debug
+ * buffers "dbg_dis", "dbg_lb1" f64, per query at f1_off[q] in probe order,
+ * then slot order).  Errors: MRQ_EINVAL (unknown name).
+ */
+int mrq_debug_set(mrq_index *idx, const char *name, int64_t value);
+
+/*
+ * Build file MRQBLD01 (little-endian), written by oracle/build.py:
+ *   char magic[8] "MRQBLD01"; u32 version (=1); u32 D; u32 d; u32 k; u64 N;
+ *   u64 flags (=0); char base_sha256_hex[64];
+ *   f64 mu[D]; f64 P[D*D] (row i = i-th principal axis, eigenvalue
+ *   descending); f64 lambda[D]; f64 R[d*d] (y = R t); f64 centroids[k*d];
+ *   u32 assign[N]; char end[8] "MRQEND01".
+ */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MRQ_H */

@@ -1,0 +1,744 @@
+// mrq_api.cu -- the C ABI of libmrq (include/mrq.h): build-file parsing, HBM
+// layout and GPU encoding at load, and the batched search pipeline.
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "mrq_internal.cuh"
+#include "mrq_kernels.cuh"
+#include "mrq_probe_tc.cuh"
+#include "mrq_comm.cuh"
+
+// ------------------------------------------------------------------ errors
+static thread_local char g_err[1024] = "";
+
+void mrq_set_error(const char *fmt, ...)
+{
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof g_err, fmt, ap);
+    va_end(ap);
+}
+
+extern "C" const char *mrq_last_error(void) { return g_err; }
+
+#define TRY(expr)                        \
+    do {                                 \
+        int _rc = (expr);                \
+        if (_rc != MRQ_OK) return _rc;   \
+    } while (0)
+
+static int dalloc(mrq_index *ix, void **p, size_t bytes)
+{
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e != cudaSuccess) {
+        mrq_set_error("cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+        return MRQ_ENOMEM;
+    }
+    ix->owned.push_back(*p);
+    return MRQ_OK;
+}
+
+template <class T>
+static int upload(mrq_index *ix, T **dst, const T *src, size_t count)
+{
+    TRY(dalloc(ix, (void **)dst, count * sizeof(T)));
+    MRQ_CUDA_TRY(cudaMemcpy(*dst, src, count * sizeof(T), cudaMemcpyHostToDevice));
+    return MRQ_OK;
+}
+
+int mrq_scratch(mrq_index *ix, const char *name, size_t bytes, void **out)
+{
+    if (bytes == 0) bytes = 16;
+    DevArr &a = ix->scratch[name];
+    if (a.bytes < bytes) {
+        if (a.p) cudaFree(a.p);
+        a.p = nullptr;
+        size_t want = bytes + bytes / 8;
+        cudaError_t e = cudaMalloc(&a.p, want);
+        if (e != cudaSuccess) {
+            a.bytes = 0;
+            mrq_set_error("scratch %s: cudaMalloc(%zu) failed: %s", name, want, cudaGetErrorString(e));
+            return MRQ_ENOMEM;
+        }
+        a.bytes = want;
+    }
+    *out = a.p;
+    return MRQ_OK;
+}
+
+#define SCR(name, T, count, var) TRY(mrq_scratch(ix, name, (size_t)(count) * sizeof(T), (void **)&(var)))
+
+// -------------------------------------------------------------- build file
+struct BuildFile {
+    uint32_t D = 0, d = 0, k = 0;
+    uint64_t N = 0;
+    std::vector<double> mu, P, lam, R, C;
+    std::vector<uint32_t> assign;
+};
+
+static int read_build_file(const char *path, BuildFile &b)
+{
+    FILE *f = fopen(path, "rb");
+    if (!f) {
+        mrq_set_error("cannot open build file '%s'", path);
+        return MRQ_EIO;
+    }
+    std::vector<unsigned char> buf;
+    unsigned char tmp[1 << 16];
+    size_t r;
+    while ((r = fread(tmp, 1, sizeof tmp, f)) > 0) buf.insert(buf.end(), tmp, tmp + r);
+    fclose(f);
+    if (buf.size() < 104 || memcmp(buf.data(), "MRQBLD01", 8) != 0) {
+        mrq_set_error("build file '%s': bad magic (VersionMismatch)", path);
+        return MRQ_EVERSION;
+    }
+    uint32_t ver;
+    memcpy(&ver, buf.data() + 8, 4);
+    if (ver != 1) {
+        mrq_set_error("build file '%s': version %u != 1", path, ver);
+        return MRQ_EVERSION;
+    }
+    memcpy(&b.D, buf.data() + 12, 4);
+    memcpy(&b.d, buf.data() + 16, 4);
+    memcpy(&b.k, buf.data() + 20, 4);
+    memcpy(&b.N, buf.data() + 24, 8);
+    size_t off = 104;
+    auto take = [&](std::vector<double> &v, size_t n) -> bool {
+        if (off + n * 8 > buf.size()) return false;
+        v.resize(n);
+        memcpy(v.data(), buf.data() + off, n * 8);
+        off += n * 8;
+        return true;
+    };
+    const size_t D = b.D, d = b.d, k = b.k;
+    if (!take(b.mu, D) || !take(b.P, D * D) || !take(b.lam, D) || !take(b.R, d * d) || !take(b.C, k * d)) {
+        mrq_set_error("build file '%s': truncated at offset %zu (FormatError)", path, off);
+        return MRQ_EFORMAT;
+    }
+    if (off + b.N * 4 + 8 > buf.size()) {
+        mrq_set_error("build file '%s': truncated at offset %zu (FormatError)", path, off);
+        return MRQ_EFORMAT;
+    }
+    b.assign.resize(b.N);
+    memcpy(b.assign.data(), buf.data() + off, b.N * 4);
+    off += b.N * 4;
+    if (memcmp(buf.data() + off, "MRQEND01", 8) != 0) {
+        mrq_set_error("build file '%s': bad end marker at offset %zu (FormatError)", path, off);
+        return MRQ_EFORMAT;
+    }
+    for (uint64_t n = 0; n < b.N; n++)
+        if (b.assign[n] >= b.k) {
+            mrq_set_error("build file '%s': assignment %u >= k at vector %llu (FormatError)", path, b.assign[n],
+                          (unsigned long long)n);
+            return MRQ_EFORMAT;
+        }
+    return MRQ_OK;
+}
+
+// -------------------------------------------------------------------- load
+static int load_impl(mrq_index *ix, const char *build_file, const float *base, int64_t n, int32_t D, int32_t d,
+                     const mrq_dist_cfg *dist)
+{
+    if (!build_file || !base) {
+        mrq_set_error("NULL build_file or base");
+        return MRQ_EINVAL;
+    }
+    if (d < 2 || d > D) {
+        mrq_set_error("InvalidConfig: need 2 <= d <= D (d=%d, D=%d)", d, D);
+        return MRQ_EINVAL;
+    }
+    BuildFile b;
+    TRY(read_build_file(build_file, b));
+    if ((int32_t)b.D != D || (int32_t)b.d != d) {
+        mrq_set_error("DimensionMismatch: file D=%u d=%u, call D=%d d=%d", b.D, b.d, D, d);
+        return MRQ_EDIM;
+    }
+    if ((int64_t)b.N != n) {
+        mrq_set_error("DimensionMismatch: file N=%llu, call n=%lld", (unsigned long long)b.N, (long long)n);
+        return MRQ_EDIM;
+    }
+    ix->N = n;
+    ix->D = D;
+    ix->d = d;
+    ix->k = (int)b.k;
+    ix->W = (d + 31) / 32;
+    if (!supported_W(ix->W)) {
+        mrq_set_error("InvalidConfig: d=%d (ceil(d/32)=%d code words) not supported", d, ix->W);
+        return MRQ_EINVAL;
+    }
+    const int k = ix->k, W = ix->W;
+
+    // multi-GPU placement: owned lists (greedy by size), device
+    int ndev = 0;
+    MRQ_CUDA_TRY(cudaGetDeviceCount(&ndev));
+    if (ndev < 1) {
+        mrq_set_error("no CUDA device");
+        return MRQ_ECUDA;
+    }
+    ix->rank = dist ? dist->rank : 0;
+    ix->world = dist && dist->world > 1 ? dist->world : 1;
+    ix->device = dist && dist->device >= 0 ? dist->device : -1;
+    if (ix->device < 0) MRQ_CUDA_TRY(cudaGetDevice(&ix->device));
+    MRQ_CUDA_TRY(cudaSetDevice(ix->device));
+    MRQ_CUDA_TRY(cudaDeviceGetAttribute(&ix->sm_count, cudaDevAttrMultiProcessorCount, ix->device));
+    MRQ_CUDA_TRY(cudaStreamCreateWithFlags(&ix->stream, cudaStreamNonBlocking));
+    for (auto &e : ix->ev) MRQ_CUDA_TRY(cudaEventCreate(&e));
+
+    std::vector<uint32_t> cnt(k, 0);
+    for (int64_t i = 0; i < n; i++) cnt[b.assign[i]]++;
+    std::vector<uint8_t> own(k, 1);
+    if (ix->world > 1) {
+        std::vector<uint32_t> owner;
+        mrq_shard_lists(cnt, ix->world, owner);
+        for (int c = 0; c < k; c++) own[c] = owner[c] == (uint32_t)ix->rank;
+        TRY(mrq_comm_init(ix, dist->nccl_unique_id));
+    }
+    // list slots: owned lists only, each start aligned to MRQ_SLOT_ALIGN
+    ix->h_list_off.assign(k + 1, 0);
+    ix->h_list_size.assign(k, 0);
+    uint64_t pos = 0;
+    for (int c = 0; c < k; c++) {
+        ix->h_list_off[c] = (uint32_t)pos;
+        ix->h_list_size[c] = own[c] ? cnt[c] : 0;
+        pos += ix->h_list_size[c];
+        pos = (pos + MRQ_SLOT_ALIGN - 1) / MRQ_SLOT_ALIGN * MRQ_SLOT_ALIGN;
+        ix->max_list = std::max(ix->max_list, ix->h_list_size[c]);
+    }
+    ix->h_list_off[k] = (uint32_t)pos;
+    ix->npad = (int64_t)((pos + 128 + 127) / 128 * 128);   // scan tiles may read 128 slots past a list
+    if (ix->npad >= (int64_t)0xFFFFFFF0ll) {
+        mrq_set_error("index too large for 32-bit slots");
+        return MRQ_EINVAL;
+    }
+    const int64_t npad = ix->npad;
+    std::vector<uint32_t> slot_of(n, 0xFFFFFFFFu), ids(npad, MRQ_PAD_ID), fill(k, 0);
+    for (int64_t i = 0; i < n; i++) {
+        const uint32_t c = b.assign[i];
+        if (!own[c]) continue;
+        const uint32_t s = ix->h_list_off[c] + fill[c]++;
+        slot_of[i] = s;
+        ids[s] = (uint32_t)i;
+    }
+
+    // replicated model: mu, P^T, lambda, R^T, centroids (+ transposed/fp32 copies)
+    std::vector<double> PT((size_t)D * D), RT((size_t)d * d);
+    for (int i = 0; i < D; i++)
+        for (int j = 0; j < D; j++) PT[(size_t)j * D + i] = b.P[(size_t)i * D + j];
+    for (int j = 0; j < d; j++)
+        for (int i = 0; i < d; i++) RT[(size_t)i * d + j] = b.R[(size_t)j * d + i];
+    std::vector<float> C32T((size_t)d * k), C32((size_t)k * d), cn32(k);
+    double cmax = 0.0;
+    for (int c = 0; c < k; c++) {
+        double s = 0.0;
+        for (int i = 0; i < d; i++) {
+            const double v = b.C[(size_t)c * d + i];
+            C32T[(size_t)i * k + c] = (float)v;
+            C32[(size_t)c * d + i] = (float)v;
+            s += v * v;
+        }
+        cn32[c] = (float)s;
+        cmax = std::max(cmax, std::sqrt(s));
+    }
+    ix->cmax = cmax * (1.0 + 1e-9) + 1e-300;
+    TRY(upload(ix, &ix->mu, b.mu.data(), D));
+    TRY(upload(ix, &ix->PT, PT.data(), PT.size()));
+    TRY(upload(ix, &ix->lam, b.lam.data(), D));
+    TRY(upload(ix, &ix->RT, RT.data(), RT.size()));
+    TRY(upload(ix, &ix->C, b.C.data(), b.C.size()));
+    TRY(upload(ix, &ix->C32T, C32T.data(), C32T.size()));
+    TRY(upload(ix, &ix->C32, C32.data(), C32.size()));
+    TRY(upload(ix, &ix->cn32, cn32.data(), cn32.size()));
+    TRY(upload(ix, &ix->list_off, ix->h_list_off.data(), k + 1));
+    TRY(upload(ix, &ix->list_size, ix->h_list_size.data(), k));
+    TRY(upload(ix, &ix->ids, ids.data(), npad));
+    TRY(dalloc(ix, (void **)&ix->Rc, (size_t)k * d * 8));
+    k_rc<<<(k + 7) / 8, 256, 0, ix->stream>>>(ix->C, ix->RT, k, d, W, ix->Rc);
+
+    // encoded index in HBM (slot order)
+    TRY(dalloc(ix, (void **)&ix->codes, (size_t)W * npad * 4));
+    TRY(dalloc(ix, (void **)&ix->f1, (size_t)npad * 4));
+    TRY(dalloc(ix, (void **)&ix->f2, (size_t)npad * 4));
+    TRY(dalloc(ix, (void **)&ix->f3, (size_t)npad * 4));
+    TRY(dalloc(ix, (void **)&ix->xr2, (size_t)npad * 4));
+    TRY(dalloc(ix, (void **)&ix->heads, (size_t)npad * d * 4));
+    TRY(dalloc(ix, (void **)&ix->tails, (size_t)npad * std::max(D - d, 1) * 4));
+    MRQ_CUDA_TRY(cudaMemsetAsync(ix->codes, 0, (size_t)W * npad * 4, ix->stream));
+    MRQ_CUDA_TRY(cudaMemsetAsync(ix->f1, 0, (size_t)npad * 4, ix->stream));
+    MRQ_CUDA_TRY(cudaMemsetAsync(ix->f2, 0, (size_t)npad * 4, ix->stream));
+    MRQ_CUDA_TRY(cudaMemsetAsync(ix->f3, 0, (size_t)npad * 4, ix->stream));
+    MRQ_CUDA_TRY(cudaMemsetAsync(ix->xr2, 0, (size_t)npad * 4, ix->stream));
+
+    // encode owned vectors in chunks (Alg.1 L3-L8 on the GPU)
+    std::vector<uint32_t> own_ids;
+    own_ids.reserve(n);
+    for (int64_t i = 0; i < n; i++)
+        if (slot_of[i] != 0xFFFFFFFFu) own_ids.push_back((uint32_t)i);
+    const int64_t CH = 65536;
+    float *dX = nullptr;
+    double *dXp = nullptr;
+    uint32_t *dAssign = nullptr, *dSlot = nullptr;
+    TRY(mrq_scratch(ix, "enc_x", (size_t)CH * D * 4, (void **)&dX));
+    TRY(mrq_scratch(ix, "enc_xp", (size_t)CH * D * 8, (void **)&dXp));
+    TRY(mrq_scratch(ix, "enc_assign", (size_t)CH * 4, (void **)&dAssign));
+    TRY(mrq_scratch(ix, "enc_slot", (size_t)CH * 4, (void **)&dSlot));
+    std::vector<float> hx((size_t)CH * D);
+    std::vector<uint32_t> ha(CH), hs(CH);
+    const int enc_warps = 8;
+    const size_t enc_smem = (size_t)enc_warps * 2 * d * 8;
+    if (enc_smem > 48 * 1024)
+        MRQ_CUDA_TRY(cudaFuncSetAttribute(k_encode_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)enc_smem));
+    for (int64_t s = 0; s < (int64_t)own_ids.size(); s += CH) {
+        const int64_t m = std::min<int64_t>(CH, (int64_t)own_ids.size() - s);
+        for (int64_t r = 0; r < m; r++) {
+            const uint32_t id = own_ids[s + r];
+            memcpy(&hx[(size_t)r * D], base + (size_t)id * D, (size_t)D * 4);
+            ha[r] = b.assign[id];
+            hs[r] = slot_of[id];
+        }
+        MRQ_CUDA_TRY(cudaMemcpyAsync(dX, hx.data(), (size_t)m * D * 4, cudaMemcpyHostToDevice, ix->stream));
+        MRQ_CUDA_TRY(cudaMemcpyAsync(dAssign, ha.data(), (size_t)m * 4, cudaMemcpyHostToDevice, ix->stream));
+        MRQ_CUDA_TRY(cudaMemcpyAsync(dSlot, hs.data(), (size_t)m * 4, cudaMemcpyHostToDevice, ix->stream));
+        dim3 grid((D + 31) / 32, (unsigned)((m + 31) / 32));
+        k_project<<<grid, dim3(32, 8), 0, ix->stream>>>(dX, m, D, ix->mu, ix->PT, dXp);
+        k_encode_finish<<<(unsigned)((m + enc_warps - 1) / enc_warps), enc_warps * 32, enc_smem, ix->stream>>>(
+            dXp, 0, m, D, d, W, dAssign, dSlot, ix->C, ix->RT, npad, ix->heads, ix->tails, ix->xr2, ix->codes, ix->f1,
+            ix->f2, ix->f3);
+        MRQ_CUDA_TRY(cudaGetLastError());
+        MRQ_CUDA_TRY(cudaStreamSynchronize(ix->stream));   // hx is reused
+    }
+    MRQ_CUDA_TRY(cudaStreamSynchronize(ix->stream));
+    for (const char *nm : {"enc_x", "enc_xp", "enc_assign", "enc_slot"}) {
+        DevArr &a = ix->scratch[nm];
+        if (a.p) cudaFree(a.p);
+        ix->scratch.erase(nm);
+    }
+    TRY(mrq_probe_tc_init(ix));
+    return MRQ_OK;
+}
+
+extern "C" int mrq_index_load(const char *build_file, const float *base, int64_t n, int32_t D, int32_t d,
+                              const mrq_dist_cfg *dist, mrq_index **out)
+{
+    if (!out) {
+        mrq_set_error("NULL out");
+        return MRQ_EINVAL;
+    }
+    *out = nullptr;
+    mrq_index *ix = new mrq_index();
+    int rc = load_impl(ix, build_file, base, n, D, d, dist);
+    if (rc != MRQ_OK) {
+        mrq_free(ix);
+        return rc;
+    }
+    *out = ix;
+    return MRQ_OK;
+}
+
+extern "C" void mrq_free(mrq_index *ix)
+{
+    if (!ix) return;
+    if (ix->device >= 0) cudaSetDevice(ix->device);
+    if (ix->stream) cudaStreamSynchronize(ix->stream);
+    for (void *p : ix->owned) cudaFree(p);
+    for (auto &kv : ix->scratch)
+        if (kv.second.p) cudaFree(kv.second.p);
+    mrq_probe_tc_free(ix);
+    mrq_comm_free(ix);
+    for (auto &e : ix->ev)
+        if (e) cudaEventDestroy(e);
+    if (ix->stream) cudaStreamDestroy(ix->stream);
+    delete ix;
+}
+
+extern "C" int mrq_index_info(const mrq_index *ix, int64_t *n, int32_t *D, int32_t *d, int32_t *k, int64_t *npad)
+{
+    if (!ix) {
+        mrq_set_error("NULL index");
+        return MRQ_EINVAL;
+    }
+    if (n) *n = ix->N;
+    if (D) *D = ix->D;
+    if (d) *d = ix->d;
+    if (k) *k = ix->k;
+    if (npad) *npad = ix->npad;
+    return MRQ_OK;
+}
+
+// ------------------------------------------------------------------ search
+static int pow2_at_least(int x)
+{
+    int s = 1;
+    while (s < x) s <<= 1;
+    return s;
+}
+
+static int set_smem(const void *fn, size_t bytes)
+{
+    if (bytes > 48 * 1024) MRQ_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    return MRQ_OK;
+}
+
+static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_search_params *p, int64_t *d_ids,
+                       float *d_dist, mrq_stats *stats, cudaStream_t st)
+{
+    const int D = ix->D, d = ix->d, k = ix->k, W = ix->W;
+    const int K = p->K, np = std::min(p->nprobe, k);
+    const int Kp = p->seed_mult * K;
+    const int mode = p->mode, tight = p->tau_schedule == 0;
+    const double isd = 1.0 / std::sqrt((double)d);
+    const bool timed = stats != nullptr;
+    if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[0], st));
+
+    double *qp, *qr2, *eps_r, *r0, *qnorm, *tau0, *tau1, *probe_qn2, *qconst, *s0_exact, *s1_exact;
+    float *qd32, *approx;
+    uint32_t *probe, *planes, *s0_cnt, *s0_pos, *s1_cnt, *s1_pos, *f1_cnt, *f2_cnt, *exact_cnt, *fallback;
+    uint64_t *cand_cnt, *f1_off;
+    SCR("qp", double, nq * D, qp);
+    SCR("qr2", double, nq, qr2);
+    SCR("eps_r", double, nq, eps_r);
+    SCR("r0", double, nq * d, r0);
+    SCR("qnorm", double, nq, qnorm);
+    SCR("qd32", float, nq * d, qd32);
+    SCR("tau0", double, nq, tau0);
+    SCR("tau1", double, nq, tau1);
+    SCR("probe", uint32_t, nq * np, probe);
+    SCR("probe_qn2", double, nq * np, probe_qn2);
+    SCR("planes", uint32_t, nq * np * MRQ_BQ * W, planes);
+    SCR("qconst", double, nq * np * 8, qconst);
+    SCR("cand_cnt", uint64_t, nq + 1, cand_cnt);
+    SCR("f1_off", uint64_t, nq + 1, f1_off);
+    SCR("s0_cnt", uint32_t, nq, s0_cnt);
+    SCR("s0_pos", uint32_t, nq * Kp, s0_pos);
+    SCR("s0_exact", double, nq * Kp, s0_exact);
+    SCR("s1_cnt", uint32_t, nq, s1_cnt);
+    SCR("s1_pos", uint32_t, nq * Kp, s1_pos);
+    SCR("s1_exact", double, nq * Kp, s1_exact);
+    SCR("f1_cnt", uint32_t, nq, f1_cnt);
+    SCR("f2_cnt", uint32_t, nq, f2_cnt);
+    SCR("exact_cnt", uint32_t, nq, exact_cnt);
+    SCR("fallback", uint32_t, 1, fallback);
+    MRQ_CUDA_TRY(cudaMemsetAsync(fallback, 0, 4, st));
+
+    // ---- a1: query projection (Alg.2 L1-L4)
+    {
+        dim3 grid((D + 31) / 32, (unsigned)((nq + 31) / 32));
+        k_project<<<grid, dim3(32, 8), 0, st>>>(d_q, nq, D, ix->mu, ix->PT, qp);
+        k_qtail<<<(unsigned)((nq + 7) / 8), 256, 0, st>>>(qp, nq, D, d, W, ix->lam, ix->RT, p->resid_scale, p->m, qr2,
+                                                          eps_r, r0, qd32, qnorm);
+    }
+    if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[1], st));
+
+    // ---- a2: probe (Alg.2 L7): screen + exact selection
+    {
+        SCR("approx", float, nq * k, approx);
+        double kappa;
+        if (mrq_probe_tc_enabled(ix)) {
+            TRY(mrq_probe_tc_run(ix, qd32, nq, approx, st));
+            kappa = mrq_probe_tc_kappa(ix);
+        } else {
+            dim3 grid((k + 255) / 256, (unsigned)((nq + 7) / 8));
+            k_probe_approx<<<grid, 256, 8 * d * sizeof(float), st>>>(qd32, nq, d, k, ix->C32T, approx);
+            kappa = std::ldexp(1.0, -24) * (2.0 * d + 8.0);
+        }
+        const int cap = std::min(k, std::max(4 * np + 256, 1024));
+        const int S = pow2_at_least(np + 256);
+        const size_t smem = (size_t)k * 4 + (size_t)cap * 4 + 16 + (size_t)d * 8 + (size_t)S * sizeof(SelItem);
+        TRY(set_smem((const void *)k_probe_select, smem));
+        k_probe_select<<<(unsigned)nq, 256, smem, st>>>(approx, nq, k, d, np, qp, D, ix->C, qnorm, ix->cmax, kappa,
+                                                        cap, S, probe, probe_qn2, fallback);
+    }
+    if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[2], st));
+
+    // ---- a3: per-(query, list) quantization into bit-planes
+    {
+        const int64_t warps = nq * np;
+        k_quant<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(probe, probe_qn2, nq, np, d, W, r0, ix->Rc, qr2, p->eps0,
+                                                             planes, qconst);
+        k_cand_count<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(probe, nq, np, ix->list_size, cand_cnt);
+        k_exclusive_scan<<<1, 1024, 0, st>>>(cand_cnt, nq, f1_off);
+    }
+    uint64_t total = 0;
+    MRQ_CUDA_TRY(cudaMemcpyAsync(&total, f1_off + nq, 8, cudaMemcpyDeviceToHost, st));
+    MRQ_CUDA_TRY(cudaStreamSynchronize(st));
+    ix->last_total = total;
+    uint32_t *f1_pos, *f2_pos;
+    double *f1_head, *f1_diso, *f2_head, *f2_exact;
+    SCR("f1_pos", uint32_t, total, f1_pos);
+    SCR("f1_head", double, total, f1_head);
+    SCR("f1_diso", double, total, f1_diso);
+    SCR("f2_pos", uint32_t, total, f2_pos);
+    SCR("f2_head", double, total, f2_head);
+    SCR("f2_exact", double, total, f2_exact);
+    if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[3], st));
+
+    // ---- a4: seeds S0 and tau0 (decision T); EXACT mode scans everything
+    if (mode == 2) {
+        std::vector<double> inf(nq, INFINITY);
+        MRQ_CUDA_TRY(cudaMemcpyAsync(tau0, inf.data(), nq * 8, cudaMemcpyHostToDevice, st));
+        MRQ_CUDA_TRY(cudaMemsetAsync(s0_cnt, 0, nq * 4, st));
+        MRQ_CUDA_TRY(cudaStreamSynchronize(st));
+    } else {
+        const int pool_cap = Kp + (int)ix->max_list;
+        SelItem *pool;
+        SCR("pool", SelItem, nq * pool_cap, pool);
+        const int S = pow2_at_least(std::max(Kp + 256, 512));
+        LaunchSeed a;
+        a.nq = nq;
+        a.smem = (size_t)D * 8 + 8 * 32 * 33 * 4 + (size_t)S * sizeof(SelItem);
+        a.probe = probe; a.np = np; a.K = K; a.Kp = Kp; a.D = D; a.d = d; a.npad = ix->npad;
+        a.list_off = ix->list_off; a.list_size = ix->list_size; a.ids = ix->ids; a.codes = ix->codes;
+        a.f1 = ix->f1; a.f2 = ix->f2; a.f3 = ix->f3; a.heads = ix->heads; a.tails = ix->tails;
+        a.planes = planes; a.qconst = qconst; a.qp = qp; a.eps_r = eps_r; a.isd = isd;
+        a.pool_cap = pool_cap; a.S = S; a.pool = pool; a.s0_cnt = s0_cnt; a.s0_pos = s0_pos;
+        a.s0_exact = s0_exact; a.tau0 = tau0;
+        TRY(mrq_seed_smem_attr(W, a.smem));
+        launch_seed(W, a, st);
+        if (ix->world > 1) TRY(mrq_comm_seeds(ix, nq, K, Kp, s0_cnt, s0_pos, s0_exact, tau0, st));
+    }
+    if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[4], st));
+
+    // ---- a5: the code scan -> F1
+    {
+        LaunchScan a;
+        a.nq = nq;
+        a.smem = (size_t)(np + 1) * 4;
+        a.probe = probe; a.np = np; a.npad = ix->npad; a.list_off = ix->list_off; a.list_size = ix->list_size;
+        a.codes = ix->codes; a.f1 = ix->f1; a.f2 = ix->f2; a.f3 = ix->f3; a.planes = planes; a.qconst = qconst;
+        a.eps_r = eps_r; a.tau0 = tau0; a.isd = isd; a.f1_off = f1_off; a.f1_cnt = f1_cnt; a.f1_pos = f1_pos;
+        launch_scan(W, a, st);
+        if (ix->dbg_dump_dis) {
+            double *dd, *dl;
+            SCR("dbg_dis", double, total, dd);
+            SCR("dbg_lb1", double, total, dl);
+            launch_scan_dbg(W, a, dd, dl, st);
+        }
+    }
+    if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[5], st));
+
+    // ---- a6: stage 2 -> F2 (and S1, tau1)
+    {
+        const int S = pow2_at_least(std::max(std::max(Kp, 2 * Kp) + 256, 512));
+        const size_t smem = (size_t)D * 8 + 8 * 32 * 33 * 4 + (size_t)S * sizeof(SelItem);
+        TRY(set_smem((const void *)k_stage2, smem));
+        k_stage2<<<(unsigned)nq, 256, smem, st>>>(mode, tight, K, Kp, D, d, ix->ids, ix->heads, ix->tails, ix->xr2, qp,
+                                                  qr2, eps_r, tau0, f1_off, f1_cnt, f1_pos, f1_head, f1_diso, s0_cnt,
+                                                  s0_pos, s0_exact, s1_cnt, s1_pos, s1_exact, S, tau1, f2_cnt, f2_pos,
+                                                  f2_head);
+        if (ix->world > 1 && mode == 0 && tight)
+            TRY(mrq_comm_tau1(ix, nq, K, Kp, s0_cnt, s0_pos, s0_exact, s1_cnt, s1_pos, s1_exact, tau1, st));
+    }
+    if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[6], st));
+
+    // ---- a7: exact re-rank of F2
+    {
+        const size_t smem = (size_t)std::max(D - d, 1) * 8 + 8 * 32 * 33 * 4;
+        TRY(set_smem((const void *)k_rerank, smem));
+        k_rerank<<<(unsigned)nq, 256, smem, st>>>(D, d, ix->tails, qp, f1_off, f2_cnt, f2_pos, f2_head, f2_exact);
+    }
+    if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[7], st));
+
+    // ---- a8: per-query top-K
+    {
+        const int S = pow2_at_least(std::max(K + 256, 512));
+        const size_t smem = (size_t)2 * Kp * 4 + 16 + (size_t)S * sizeof(SelItem);
+        TRY(set_smem((const void *)k_topk, smem));
+        k_topk<<<(unsigned)nq, 256, smem, st>>>(K, Kp, ix->ids, s0_cnt, s0_pos, s0_exact, s1_cnt, s1_pos, s1_exact,
+                                                f1_off, f2_cnt, f2_pos, f2_exact, S, d_ids, d_dist, exact_cnt);
+    }
+    if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[8], st));
+    // ---- a9: multi-GPU merge (NCCL all-gather of per-rank top-K)
+    if (ix->world > 1) TRY(mrq_comm_merge(ix, nq, K, d_ids, d_dist, st));
+    if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[9], st));
+    MRQ_CUDA_TRY(cudaGetLastError());
+
+    ix->last_nq = nq;
+    ix->last_np = np;
+    ix->last_K = K;
+    ix->last_Kp = Kp;
+    if (timed) {
+        MRQ_CUDA_TRY(cudaEventSynchronize(ix->ev[9]));
+        float ms[10];
+        for (int i = 1; i <= 9; i++) MRQ_CUDA_TRY(cudaEventElapsedTime(&ms[i], ix->ev[i - 1], ix->ev[i]));
+        float tot;
+        MRQ_CUDA_TRY(cudaEventElapsedTime(&tot, ix->ev[0], ix->ev[9]));
+        memset(stats, 0, sizeof *stats);
+        stats->ms_total = tot;
+        stats->ms_qprep = ms[1];
+        stats->ms_probe = ms[2];
+        stats->ms_quant = ms[3];
+        stats->ms_seed = ms[4];
+        stats->ms_scan = ms[5];
+        stats->ms_stage2 = ms[6];
+        stats->ms_rerank = ms[7];
+        stats->ms_topk = ms[8];
+        stats->ms_comm = ms[9];
+        std::vector<uint32_t> h(nq);
+        auto sum32 = [&](const uint32_t *dv) -> uint64_t {
+            if (cudaMemcpy(h.data(), dv, nq * 4, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
+            uint64_t s = 0;
+            for (auto v : h) s += v;
+            return s;
+        };
+        stats->scanned = total;
+        stats->stage1_pass = sum32(f1_cnt);
+        stats->stage2_pass = sum32(f2_cnt);
+        stats->exact = sum32(exact_cnt);
+        stats->seeds = sum32(s0_cnt) + sum32(s1_cnt);
+    }
+    return MRQ_OK;
+}
+
+static int check_params(const mrq_index *ix, int64_t nq, const mrq_search_params *p)
+{
+    if (!ix || !p) {
+        mrq_set_error("NULL index or params");
+        return MRQ_EINVAL;
+    }
+    if (nq < 0 || p->K < 1 || p->K > MRQ_MAX_K || p->nprobe < 1 || p->nprobe > MRQ_MAX_NPROBE ||
+        p->nprobe > ix->k || !(p->eps0 > 0) || !(p->m > 0) || p->mode < 0 || p->mode > 2 ||
+        p->tau_schedule < 0 || p->tau_schedule > 1 || p->seed_mult < 1 || !(p->resid_scale > 0)) {
+        mrq_set_error("InvalidConfig: K=%d nprobe=%d (k=%d) eps0=%g m=%g mode=%d tau=%d seed_mult=%d rscale=%g",
+                      p->K, p->nprobe, ix->k, p->eps0, p->m, p->mode, p->tau_schedule, p->seed_mult,
+                      p->resid_scale);
+        return MRQ_EINVAL;
+    }
+    return MRQ_OK;
+}
+
+extern "C" int mrq_search_batch_device(mrq_index *ix, const float *d_queries, int64_t nq, const mrq_search_params *p,
+                                       int64_t *d_out_ids, float *d_out_dist, mrq_stats *stats, void *stream)
+{
+    TRY(check_params(ix, nq, p));
+    if (nq == 0) {
+        if (stats) memset(stats, 0, sizeof *stats);
+        return MRQ_OK;
+    }
+    if (!d_queries || !d_out_ids || !d_out_dist) {
+        mrq_set_error("NULL buffer");
+        return MRQ_EINVAL;
+    }
+    MRQ_CUDA_TRY(cudaSetDevice(ix->device));
+    cudaStream_t st = stream ? (cudaStream_t)stream : ix->stream;
+    return search_impl(ix, d_queries, nq, p, d_out_ids, d_out_dist, stats, st);
+}
+
+extern "C" int mrq_search_batch(mrq_index *ix, const float *queries, int64_t nq, const mrq_search_params *p,
+                                int64_t *out_ids, float *out_dist, mrq_stats *stats)
+{
+    TRY(check_params(ix, nq, p));
+    if (nq == 0) {
+        if (stats) memset(stats, 0, sizeof *stats);
+        return MRQ_OK;
+    }
+    if (!queries || !out_ids || !out_dist) {
+        mrq_set_error("NULL buffer");
+        return MRQ_EINVAL;
+    }
+    MRQ_CUDA_TRY(cudaSetDevice(ix->device));
+    float *dq;
+    int64_t *dids;
+    float *ddist;
+    SCR("in_q", float, nq * ix->D, dq);
+    SCR("out_ids", int64_t, nq * p->K, dids);
+    SCR("out_dist", float, nq * p->K, ddist);
+    MRQ_CUDA_TRY(cudaMemcpyAsync(dq, queries, (size_t)nq * ix->D * 4, cudaMemcpyHostToDevice, ix->stream));
+    TRY(search_impl(ix, dq, nq, p, dids, ddist, stats, ix->stream));
+    MRQ_CUDA_TRY(cudaMemcpyAsync(out_ids, dids, (size_t)nq * p->K * 8, cudaMemcpyDeviceToHost, ix->stream));
+    MRQ_CUDA_TRY(cudaMemcpyAsync(out_dist, ddist, (size_t)nq * p->K * 4, cudaMemcpyDeviceToHost, ix->stream));
+    MRQ_CUDA_TRY(cudaStreamSynchronize(ix->stream));
+    return MRQ_OK;
+}
+
+// ------------------------------------------------------------- debug fetch
+extern "C" int mrq_debug_fetch(mrq_index *ix, const char *name, void *dst, size_t dst_bytes, size_t *bytes_needed)
+{
+    if (!ix || !name) {
+        mrq_set_error("NULL index or name");
+        return MRQ_EINVAL;
+    }
+    const int64_t npad = ix->npad, nq = ix->last_nq;
+    const int k = ix->k, d = ix->d, D = ix->D, W = ix->W, np = ix->last_np, Kp = ix->last_Kp;
+    const void *src = nullptr;
+    size_t bytes = 0;
+    std::string nm(name);
+    struct E {
+        const char *n;
+        const void *p;
+        size_t b;
+    } fixed[] = {
+        {"list_off", ix->list_off, (size_t)(k + 1) * 4}, {"list_size", ix->list_size, (size_t)k * 4},
+        {"ids", ix->ids, (size_t)npad * 4},              {"codes", ix->codes, (size_t)W * npad * 4},
+        {"f1", ix->f1, (size_t)npad * 4},                {"f2", ix->f2, (size_t)npad * 4},
+        {"f3", ix->f3, (size_t)npad * 4},                {"xr2", ix->xr2, (size_t)npad * 4},
+        {"heads", ix->heads, (size_t)npad * d * 4},      {"tails", ix->tails, (size_t)npad * std::max(D - d, 0) * 4},
+        {"Rc", ix->Rc, (size_t)k * d * 8},
+    };
+    for (auto &e : fixed)
+        if (nm == e.n) {
+            src = e.p;
+            bytes = e.b;
+        }
+    if (!src) {
+        struct S {
+            const char *n;
+            size_t b;
+        } per[] = {
+            {"qp", (size_t)nq * D * 8},        {"qr2", (size_t)nq * 8},
+            {"eps_r", (size_t)nq * 8},         {"tau0", (size_t)nq * 8},
+            {"tau1", (size_t)nq * 8},          {"r0", (size_t)nq * d * 8},
+            {"probe", (size_t)nq * np * 4},    {"probe_qn2", (size_t)nq * np * 8},
+            {"planes", (size_t)nq * np * MRQ_BQ * W * 4}, {"qconst", (size_t)nq * np * 8 * 8},
+            {"f1_off", (size_t)(nq + 1) * 8},  {"f1_cnt", (size_t)nq * 4},
+            {"f2_cnt", (size_t)nq * 4},        {"s0_cnt", (size_t)nq * 4},
+            {"s1_cnt", (size_t)nq * 4},        {"exact_cnt", (size_t)nq * 4},
+            {"s0_pos", (size_t)nq * Kp * 4},   {"s0_exact", (size_t)nq * Kp * 8},
+            {"s1_pos", (size_t)nq * Kp * 4},   {"s1_exact", (size_t)nq * Kp * 8},
+            {"f1_pos", (size_t)ix->last_total * 4}, {"f1_head", (size_t)ix->last_total * 8},
+            {"f1_diso", (size_t)ix->last_total * 8}, {"f2_pos", (size_t)ix->last_total * 4},
+            {"f2_head", (size_t)ix->last_total * 8}, {"f2_exact", (size_t)ix->last_total * 8},
+            {"fallback", 4}, {"approx", (size_t)nq * k * 4},
+            {"dbg_dis", (size_t)ix->last_total * 8}, {"dbg_lb1", (size_t)ix->last_total * 8},
+        };
+        for (auto &e : per)
+            if (nm == e.n) {
+                auto it = ix->scratch.find(nm);
+                if (it == ix->scratch.end()) break;
+                src = it->second.p;
+                bytes = e.b;
+            }
+    }
+    if (!src) {
+        mrq_set_error("unknown or unavailable debug buffer '%s'", name);
+        return MRQ_EINVAL;
+    }
+    if (bytes_needed) *bytes_needed = bytes;
+    if (!dst) return MRQ_OK;
+    if (dst_bytes < bytes) {
+        mrq_set_error("debug buffer '%s' needs %zu bytes", name, bytes);
+        return MRQ_EINVAL;
+    }
+    MRQ_CUDA_TRY(cudaSetDevice(ix->device));
+    MRQ_CUDA_TRY(cudaStreamSynchronize(ix->stream));
+    MRQ_CUDA_TRY(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+    return MRQ_OK;
+}
+
+extern "C" int mrq_debug_set(mrq_index *ix, const char *name, int64_t value)
+{
+    if (!ix || !name) {
+        mrq_set_error("NULL index or name");
+        return MRQ_EINVAL;
+    }
+    if (std::string(name) == "dump_dis") {
+        ix->dbg_dump_dis = (int)value;
+        return MRQ_OK;
+    }
+    mrq_set_error("unknown debug switch '%s'", name);
+    return MRQ_EINVAL;
+}

@@ -1,0 +1,962 @@
+// mrq_kernels.cu -- the B200 kernels of the batched IVF-MRQ query path.
+//
+// Citations "P:N" are lines of the paper's LaTeX source.  Every
+// fp64 expression keeps the evaluation order written here (compiled with
+// --fmad=false), which is the canonical order of DESIGN.md: sums run left to
+// right over increasing index, products and sums round separately.
+#include "mrq_internal.cuh"
+#include "mrq_kernels.cuh"
+#include "mrq_comm.cuh"
+
+// ===================================================================== a0/a1
+// x_p = P (x - mu) (Alg.1 L3 P:283 for base vectors, Alg.2 L1 P:303 for
+// queries).  Output r, dimension i: sum_{j=0}^{D-1} P[i][j] * (x[r][j] - mu[j])
+// accumulated j ascending.  Register-tiled across rows and outputs only (the
+// reduction order per output is untouched): a 32-output x 32-row tile per
+// 256-thread block, each P element read once per tile.
+__global__ void __launch_bounds__(256) k_project(const float *__restrict__ X, int64_t nrows, int D,
+                                                 const double *__restrict__ mu, const double *__restrict__ PT,
+                                                 double *__restrict__ out)
+{
+    __shared__ double us[32][33];
+    __shared__ double ps[32][33];
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int i0 = blockIdx.x * 32;
+    const int64_t r0 = (int64_t)blockIdx.y * 32;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int j0 = 0; j0 < D; j0 += 32) {
+        for (int rr = ty; rr < 32; rr += 8) {
+            int64_t r = r0 + rr;
+            int j = j0 + tx;
+            us[rr][tx] = (r < nrows && j < D) ? ((double)X[r * D + j] - mu[j]) : 0.0;
+            int jj = j0 + rr, i = i0 + tx;
+            ps[rr][tx] = (jj < D && i < D) ? PT[(int64_t)jj * D + i] : 0.0;
+        }
+        __syncthreads();
+        const int jn = min(32, D - j0);
+        for (int jj = 0; jj < jn; jj++) {
+            const double p = ps[jj][tx];
+#pragma unroll
+            for (int q = 0; q < 4; q++) acc[q] = acc[q] + us[ty * 4 + q][jj] * p;
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        int64_t r = r0 + ty * 4 + q;
+        int i = i0 + tx;
+        if (r < nrows && i < D) out[r * D + i] = acc[q];
+    }
+}
+
+// ======================================================================= a0
+// Alg.1 L4-L8, one warp per vector, results scattered to the
+// vector's list slot.  t = x_d - c_{a(x)}; y = R t (y_j = sum_i R[j][i] t_i);
+// bit_j = [y_j >= 0]; u = <x_bar, x_b> = sum|y_j| / (sqrt(d) ||t||), clamped
+// to 1, = 1 when t = 0; stored fp32 factors f1 = ||t||^2 + ||x_r||^2,
+// f2 = ||t||/u, f3 = ||t|| sqrt(1-u^2)/(u sqrt(d-1)) (Eq.4/Eq.5 readings
+// A-1/A-2 of DESIGN.md).
+__global__ void k_encode_finish(const double *__restrict__ xp, int64_t n0, int64_t cnt, int D, int d, int W,
+                                const uint32_t *__restrict__ assign, const uint32_t *__restrict__ slot_of,
+                                const double *__restrict__ C, const double *__restrict__ RT, int64_t npad,
+                                float *__restrict__ heads, float *__restrict__ tails, float *__restrict__ xr2o,
+                                uint32_t *__restrict__ codes, float *__restrict__ f1, float *__restrict__ f2,
+                                float *__restrict__ f3)
+{
+    extern __shared__ double esm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t v = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    if (v >= cnt) return;
+    double *t = esm + (size_t)warp * 2 * d;
+    double *y = t + d;
+    const double *row = xp + v * D;
+    const int64_t n = n0 + v;
+    const uint32_t c = assign[n];
+    const int64_t slot = slot_of[n];
+    for (int i = lane; i < d; i += 32) {
+        t[i] = row[i] - C[(int64_t)c * d + i];
+        heads[slot * d + i] = (float)row[i];
+    }
+    for (int i = d + lane; i < D; i += 32) tails[slot * (D - d) + (i - d)] = (float)row[i];
+    __syncwarp();
+    for (int w = 0; w < W; w++) {
+        const int j = w * 32 + lane;
+        double acc = 0.0;
+        if (j < d) {
+            for (int i = 0; i < d; i++) acc = acc + RT[(int64_t)i * d + j] * t[i];
+            y[j] = acc;
+        }
+        unsigned bits = __ballot_sync(0xffffffffu, j < d && acc >= 0.0);
+        if (lane == 0) codes[(int64_t)w * npad + slot] = bits;
+    }
+    __syncwarp();
+    if (lane == 0) {
+        double xr2 = 0.0;
+        for (int i = d; i < D; i++) xr2 = xr2 + row[i] * row[i];
+        double n2 = 0.0;
+        for (int i = 0; i < d; i++) n2 = n2 + t[i] * t[i];
+        double abssum = 0.0;
+        for (int j = 0; j < d; j++) abssum = abssum + fabs(y[j]);
+        double u = 1.0;
+        if (n2 != 0.0) {
+            u = abssum / (sqrt((double)d) * sqrt(n2));
+            if (u > 1.0) u = 1.0;
+        }
+        const double nrm = sqrt(n2);
+        xr2o[slot] = (float)xr2;
+        f1[slot] = (float)(n2 + xr2);
+        f2[slot] = (float)(nrm / u);
+        f3[slot] = (float)(nrm * (sqrt(1.0 - u * u) / (u * sqrt((double)(d - 1)))));
+    }
+}
+
+// R c_j for every centroid (warp per centroid): Rc[c][j] = sum_i R[j][i] C[c][i].
+__global__ void k_rc(const double *__restrict__ C, const double *__restrict__ RT, int k, int d, int W,
+                     double *__restrict__ Rc)
+{
+    const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (c >= k) return;
+    for (int w = 0; w < W; w++) {
+        const int j = w * 32 + lane;
+        if (j < d) {
+            double acc = 0.0;
+            for (int i = 0; i < d; i++) acc = acc + RT[(int64_t)i * d + j] * C[(int64_t)c * d + i];
+            Rc[(int64_t)c * d + j] = acc;
+        }
+    }
+}
+
+// ======================================================================= a1
+// Alg.2 L2-L4, warp per query: ||q_r||^2, sigma^2 = sum_{i>=d}
+// q_i^2 lambda_i (Eq.6), eps_r = (resid_scale m) sigma (Eq.7 / Alg.2
+// L11, reading A-5), r0 = R q_d; plus the fp32 q_d and ||q_d|| the probe uses.
+__global__ void k_qtail(const double *__restrict__ qp, int64_t nq, int D, int d, int W,
+                        const double *__restrict__ lam, const double *__restrict__ RT, double rscale, double m,
+                        double *__restrict__ qr2o, double *__restrict__ eps_r, double *__restrict__ r0,
+                        float *__restrict__ qd32, double *__restrict__ qnorm)
+{
+    const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (q >= nq) return;
+    const double *row = qp + q * D;
+    for (int w = 0; w < W; w++) {
+        const int j = w * 32 + lane;
+        if (j < d) {
+            double acc = 0.0;
+            for (int i = 0; i < d; i++) acc = acc + RT[(int64_t)i * d + j] * row[i];
+            r0[q * d + j] = acc;
+            qd32[q * d + j] = (float)row[j];
+        }
+    }
+    if (lane == 0) {
+        double a = 0.0, s2 = 0.0;
+        for (int i = d; i < D; i++) {
+            a = a + row[i] * row[i];
+            s2 = s2 + (row[i] * row[i]) * lam[i];
+        }
+        qr2o[q] = a;
+        eps_r[q] = (rscale * m) * sqrt(s2);
+        double n2 = 0.0;
+        for (int i = 0; i < d; i++) n2 = n2 + row[i] * row[i];
+        qnorm[q] = sqrt(n2);
+    }
+}
+
+// ======================================================================= a2
+// Probe screen on CUDA cores (fallback when the tcgen05 GEMM is not used):
+// approx[q][c] = sum_i (q~_i - c~_i)^2 in fp32 with q~, c~ the fp32 roundings.
+// The exact selection happens in k_probe_select.
+__global__ void __launch_bounds__(256) k_probe_approx(const float *__restrict__ qd32, int64_t nq, int d, int k,
+                                                      const float *__restrict__ C32T, float *__restrict__ approx)
+{
+    constexpr int QB = 8;
+    extern __shared__ float qs[];   // QB x d
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t q0 = (int64_t)blockIdx.y * QB;
+    for (int i = threadIdx.x; i < QB * d; i += blockDim.x) {
+        int64_t q = q0 + i / d;
+        qs[i] = q < nq ? qd32[q * d + i % d] : 0.f;
+    }
+    __syncthreads();
+    if (c >= k) return;
+    float acc[QB];
+#pragma unroll
+    for (int b = 0; b < QB; b++) acc[b] = 0.f;
+    for (int i = 0; i < d; i++) {
+        const float cv = C32T[(int64_t)i * k + c];
+#pragma unroll
+        for (int b = 0; b < QB; b++) {
+            float t = qs[b * d + i] - cv;
+            acc[b] = acc[b] + t * t;
+        }
+    }
+#pragma unroll
+    for (int b = 0; b < QB; b++)
+        if (q0 + b < nq) approx[(q0 + b) * k + c] = acc[b];
+}
+
+// Exact top-nprobe from a screened distance row (Alg.2 L7).  The
+// screen value a_c of every centroid is within delta_q of the exact
+// ||q_d - c||^2 (bound derived in DESIGN.md "probe exactness"), so every
+// member of the exact top-np has a_c <= a_(np) + 2 delta_q, where a_(np) is the
+// np-th smallest screen value.  Those candidates are rescored in fp64 (left
+// to right over i) and the np smallest (qn2, c) are kept.  If the candidate
+// set exceeds `cap`, all k centroids are rescored.
+//
+// Screens: kind 0 = fp32 direct difference (k_probe_approx), kind 1 =
+// ||c||^2 - 2<q,c> from the tf32 tensor-core GEMM (q-independent ||q||^2
+// omitted; the bound is the same shift-free form).
+__global__ void __launch_bounds__(256) k_probe_select(const float *__restrict__ approx, int64_t nq, int k, int d,
+                                                      int np, const double *__restrict__ qp, int D,
+                                                      const double *__restrict__ C, const double *__restrict__ qnorm,
+                                                      double cmax, double kappa, int cap, int S,
+                                                      uint32_t *__restrict__ probe, double *__restrict__ probe_qn2,
+                                                      uint32_t *__restrict__ fallback_cnt)
+{
+    extern __shared__ unsigned char psm[];
+    uint32_t *keys = (uint32_t *)psm;                            // k
+    uint32_t *cand = keys + k;                                   // cap
+    double *qs = (double *)(((uintptr_t)(cand + cap) + 15) & ~(uintptr_t)15);   // d
+    SelItem *buf = (SelItem *)(qs + d);                          // S
+    __shared__ uint32_t hist[256];
+    __shared__ uint32_t sh_sel, sh_rem, sh_n;
+    const int64_t q = blockIdx.x;
+    const float *row = approx + q * k;
+    for (int i = threadIdx.x; i < k; i += blockDim.x) keys[i] = f2key(row[i]);
+    for (int i = threadIdx.x; i < d; i += blockDim.x) qs[i] = qp[q * D + i];
+    if (threadIdx.x == 0) sh_n = 0;
+    __syncthreads();
+    // radix select of the np-th smallest key
+    uint32_t prefix = 0, mask = 0;
+    uint32_t rem = (uint32_t)np;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+        __syncthreads();
+        for (int i = threadIdx.x; i < k; i += blockDim.x) {
+            uint32_t key = keys[i];
+            if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t cum = 0, sel = 255;
+            for (int b = 0; b < 256; b++) {
+                if (cum + hist[b] >= rem) { sel = b; break; }
+                cum += hist[b];
+            }
+            sh_sel = sel;
+            sh_rem = rem - cum;
+        }
+        __syncthreads();
+        prefix |= sh_sel << shift;
+        mask |= 0xFFu << shift;
+        rem = sh_rem;
+        __syncthreads();
+    }
+    const double a_np = (double)key2f(prefix);
+    const double g = qnorm[q] + cmax;
+    const double thr = a_np + 2.0 * (kappa * (g * g));
+    for (int i = threadIdx.x; i < k; i += blockDim.x) {
+        if ((double)row[i] <= thr) {
+            uint32_t at = atomicAdd(&sh_n, 1u);
+            if (at < (uint32_t)cap) cand[at] = i;
+        }
+    }
+    __syncthreads();
+    const bool all = sh_n > (uint32_t)cap;
+    const int nc = all ? k : (int)sh_n;
+    if (all && threadIdx.x == 0) atomicAdd(fallback_cnt, 1u);
+    auto get = [&](int i) -> SelItem {
+        const uint32_t c = all ? (uint32_t)i : cand[i];
+        const double *cr = C + (int64_t)c * d;
+        double acc = 0.0;
+        for (int j = 0; j < d; j++) {
+            double t = qs[j] - cr[j];
+            acc = acc + t * t;
+        }
+        SelItem s;
+        s.key = acc;
+        s.id = c;
+        s.pay = c;
+        return s;
+    };
+    const int L = min(np, nc);
+    block_select(buf, S, np, nc, get);
+    for (int p = threadIdx.x; p < np; p += blockDim.x) {
+        probe[q * np + p] = p < L ? buf[p].id : 0xFFFFFFFFu;
+        probe_qn2[q * np + p] = p < L ? buf[p].key : __longlong_as_double(0x7ff0000000000000ll);
+    }
+}
+
+// ======================================================================= a3
+// Per (query, probed list), warp-wide (Alg.2 L4-L5; readings
+// A-12/A-13/A-27): r = R q_d - R c (unnormalized), lo/hi = min/max r,
+// delta = (hi - lo)/15, L_j = clamp(floor((r_j - lo)/delta + 0.5), 0, 15)
+// (all 0 when delta = 0), bit-planes p_b = {j : bit b of L_j}, and the
+// constants of the scan epilogue:
+//   A = 2 lo, Bc = 2 delta, C0 = d lo + delta sum L, g1 = ||q_d-c||^2 + ||q_r||^2,
+//   eb = (2 eps0) ||q_d - c||          (Eq.5 distance-domain scale, A-6)
+__global__ void k_quant(const uint32_t *__restrict__ probe, const double *__restrict__ probe_qn2, int64_t nq,
+                        int np, int d, int W, const double *__restrict__ r0, const double *__restrict__ Rc,
+                        const double *__restrict__ qr2, double eps0, uint32_t *__restrict__ planes,
+                        double *__restrict__ qconst)
+{
+    const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (gw >= nq * np) return;
+    const int64_t q = gw / np;
+    const uint32_t c = probe[gw];
+    uint32_t *pl = planes + gw * (MRQ_BQ * W);
+    double *qc = qconst + gw * 8;
+    if (c == 0xFFFFFFFFu) {          // fewer than np lists exist
+        for (int i = lane; i < MRQ_BQ * W; i += 32) pl[i] = 0;
+        if (lane < 8) qc[lane] = 0.0;
+        return;
+    }
+    const double qn2 = probe_qn2[gw];
+    double lo = __longlong_as_double(0x7ff0000000000000ll), hi = -lo;
+    double rv[16];
+#pragma unroll
+    for (int w = 0; w < 16; w++) {
+        if (w < W) {
+            const int j = w * 32 + lane;
+            if (j < d) {
+                rv[w] = r0[q * d + j] - Rc[(int64_t)c * d + j];
+                lo = fmin(lo, rv[w]);
+                hi = fmax(hi, rv[w]);
+            }
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    const double delta = (hi - lo) / 15.0;
+    int sumL = 0;
+#pragma unroll
+    for (int w = 0; w < 16; w++) {
+        if (w < W) {
+            const int j = w * 32 + lane;
+            int v = 0;
+            if (j < d && delta > 0.0) {
+                double f = floor((rv[w] - lo) / delta + 0.5);
+                v = f < 0.0 ? 0 : (f > 15.0 ? 15 : (int)f);
+            }
+            sumL += v;
+#pragma unroll
+            for (int b = 0; b < MRQ_BQ; b++) {
+                unsigned word = __ballot_sync(0xffffffffu, j < d && ((v >> b) & 1));
+                if (lane == 0) pl[b * W + w] = word;
+            }
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) sumL += __shfl_xor_sync(0xffffffffu, sumL, o);
+    if (lane == 0) {
+        qc[0] = 2.0 * lo;                                  // A
+        qc[1] = 2.0 * delta;                               // Bc
+        qc[2] = (double)d * lo + delta * (double)sumL;     // C0
+        qc[3] = qn2 + qr2[q];                              // g1
+        qc[4] = (2.0 * eps0) * sqrt(qn2);                  // eb
+        qc[5] = lo;
+        qc[6] = delta;
+        qc[7] = (double)sumL;
+    }
+}
+
+// Candidate count per query (sum of its probed list sizes) ...
+__global__ void k_cand_count(const uint32_t *__restrict__ probe, int64_t nq, int np,
+                             const uint32_t *__restrict__ list_size, uint64_t *__restrict__ cnt)
+{
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nq) return;
+    uint64_t s = 0;
+    for (int p = 0; p < np; p++) {
+        uint32_t c = probe[q * np + p];
+        if (c != 0xFFFFFFFFu) s += list_size[c];
+    }
+    cnt[q] = s;
+}
+
+// ... and its exclusive prefix sum (one block; out[nq] = total).
+__global__ void k_exclusive_scan(const uint64_t *__restrict__ in, int64_t n, uint64_t *__restrict__ out)
+{
+    __shared__ uint64_t warp_sums[32];
+    __shared__ uint64_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int64_t base = 0; base < n; base += blockDim.x) {
+        const int64_t i = base + threadIdx.x;
+        uint64_t v = i < n ? in[i] : 0;
+        uint64_t x = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) warp_sums[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            uint64_t s = lane < (int)(blockDim.x >> 5) ? warp_sums[lane] : 0;
+            for (int o = 1; o < 32; o <<= 1) {
+                uint64_t y = __shfl_up_sync(0xffffffffu, s, o);
+                if (lane >= o) s += y;
+            }
+            warp_sums[lane] = s;
+        }
+        __syncthreads();
+        const uint64_t before = carry + (warp > 0 ? warp_sums[warp - 1] : 0) + (x - v);
+        if (i < n) out[i] = before;
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) carry = before + v;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[n] = carry;
+}
+
+// ================================================================ a4 / a5
+// The scan epilogue shared by the seed pass and the scan (Eq.4
+// with A-1; Eq.5 P:255 with A-2/A-6; Alg.2 L12 P:314):
+//   S = sum_b 2^b popc(code & p_b) = sum_{bit_j=1} L_j,  pop = popc(code)
+//   ip = ((A pop + Bc S) - C0) / sqrt(d)        = <x_hat, r_bar>
+//   dis' = (f1 + g1) - 2 (f2 ip)
+//   LB1 = (dis' - eb f3) - eps_r
+template <int W>
+__device__ __forceinline__ double mrq_lb1(const uint32_t *code, const uint32_t *pl, const double *qc, double isd,
+                                          double eps_r, float f1, float f2, float f3, double *dis_out)
+{
+    int pop = 0;
+#pragma unroll
+    for (int w = 0; w < W; w++) pop += __popc(code[w]);
+    int S = 0;
+#pragma unroll
+    for (int b = 0; b < MRQ_BQ; b++) {
+        int s = 0;
+#pragma unroll
+        for (int w = 0; w < W; w++) s += __popc(code[w] & pl[b * W + w]);
+        S += s << b;
+    }
+    const double t1 = qc[0] * (double)pop;
+    const double t2 = qc[1] * (double)S;
+    const double t4 = (t1 + t2) - qc[2];
+    const double ip = t4 * isd;
+    const double t5 = (double)f1 + qc[3];
+    const double t6 = (double)f2 * ip;
+    const double dis = t5 - 2.0 * t6;
+    *dis_out = dis;
+    return (dis - qc[4] * (double)f3) - eps_r;
+}
+
+// Seeds S0 and tau0 (decision T of DESIGN.md, replacing "tau <- threshold of
+// the result queue", Alg.2 L9 P:311): the probed lists in probe order until
+// they hold >= K' candidates form the pool; S0 = the K' smallest (dis', id)
+// of the pool; their exact distances ||x_p - q_p||^2 (Alg.2 L14 P:316);
+// tau0 = K-th smallest exact over S0 (+inf if |S0| < K).  Block per query.
+template <int W>
+__global__ void __launch_bounds__(256) k_seed(
+    const uint32_t *__restrict__ probe, int np, int K, int Kp, int D, int d, int64_t npad,
+    const uint32_t *__restrict__ list_off, const uint32_t *__restrict__ list_size,
+    const uint32_t *__restrict__ ids, const uint32_t *__restrict__ codes, const float *__restrict__ f1,
+    const float *__restrict__ f2, const float *__restrict__ f3, const float *__restrict__ heads,
+    const float *__restrict__ tails, const uint32_t *__restrict__ planes, const double *__restrict__ qconst,
+    const double *__restrict__ qp, const double *__restrict__ eps_r_arr, double isd, int pool_cap, int S,
+    SelItem *__restrict__ pool, uint32_t *__restrict__ s0_cnt, uint32_t *__restrict__ s0_pos,
+    double *__restrict__ s0_exact, double *__restrict__ tau0)
+{
+    extern __shared__ unsigned char ssm[];
+    double *qs = (double *)ssm;                              // D
+    float *tiles = (float *)(qs + D);                        // 8 warps x 32 x 33
+    SelItem *buf = (SelItem *)(tiles + 8 * 32 * 33);         // S
+    __shared__ int sh_npool, sh_lists;
+    const int64_t q = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const double eps_r = eps_r_arr[q];
+    for (int i = threadIdx.x; i < D; i += blockDim.x) qs[i] = qp[q * D + i];
+    if (threadIdx.x == 0) {
+        int cum = 0, p = 0;
+        while (p < np && cum < Kp) {
+            uint32_t c = probe[q * np + p];
+            if (c != 0xFFFFFFFFu) cum += list_size[c];
+            p++;
+        }
+        sh_npool = cum;
+        sh_lists = p;
+    }
+    __syncthreads();
+    SelItem *qpool = pool + q * pool_cap;
+    // dis' of the pool, in probe order
+    int at = 0;
+    for (int p = 0; p < sh_lists; p++) {
+        const uint32_t c = probe[q * np + p];
+        if (c == 0xFFFFFFFFu) continue;
+        const uint32_t off = list_off[c], sz = list_size[c];
+        const uint32_t *pl = planes + (q * np + p) * (MRQ_BQ * W);
+        const double *qc = qconst + (q * np + p) * 8;
+        for (uint32_t e = threadIdx.x; e < sz; e += blockDim.x) {
+            const uint32_t slot = off + e;
+            uint32_t code[W];
+#pragma unroll
+            for (int w = 0; w < W; w++) code[w] = codes[(int64_t)w * npad + slot];
+            double dis;
+            mrq_lb1<W>(code, pl, qc, isd, eps_r, f1[slot], f2[slot], f3[slot], &dis);
+            SelItem s;
+            s.key = dis;
+            s.id = ids[slot];
+            s.pay = slot;
+            qpool[at + e] = s;
+        }
+        at += sz;
+    }
+    __syncthreads();
+    const int ns0 = block_select(buf, S, Kp, sh_npool, [&](int i) { return qpool[i]; });
+    // exact distances of S0: warp w handles entries w*32 .. (chunks of 32)
+    float *tile = tiles + warp * 32 * 33;
+    for (int e0 = warp * 32; e0 < ns0; e0 += 8 * 32) {
+        const int e = e0 + lane;
+        const bool valid = e < ns0;
+        const uint32_t slot = valid ? buf[e].pay : 0u;
+        double acc = warp_rows_sqdist(heads, d, 0, slot, valid, d, qs, 0.0, tile);
+        if (D > d) acc = warp_rows_sqdist(tails, D - d, 0, slot, valid, D - d, qs + d, acc, tile);
+        if (valid) {
+            s0_pos[q * Kp + e] = slot;
+            s0_exact[q * Kp + e] = acc;
+        }
+    }
+    __syncthreads();
+    // tau0 = K-th smallest exact over S0 (ids are distinct)
+    block_select(buf, S, K, ns0, [&](int i) {
+        SelItem s;
+        s.key = s0_exact[q * Kp + i];
+        s.id = ids[s0_pos[q * Kp + i]];
+        s.pay = i;
+        return s;
+    });
+    if (threadIdx.x == 0) {
+        s0_cnt[q] = ns0;
+        tau0[q] = ns0 >= K ? buf[K - 1].key : __longlong_as_double(0x7ff0000000000000ll);
+    }
+}
+
+// The code scan (hot loop of Alg.2 L7-L12): block per query, every
+// warp streams (list, 128-slot chunk) tiles of the query's probed lists.  Each
+// lane reads 4 consecutive slots with 128-bit loads: W code words (word-major
+// planes codes[w][slot]) and f1/f2/f3; evaluates LB1 in registers and appends
+// slots with LB1 < tau0 (stage 1, F1) to the query's segment of f1_pos.
+template <int W>
+__global__ void __launch_bounds__(256) k_scan(
+    const uint32_t *__restrict__ probe, int np, int64_t npad, const uint32_t *__restrict__ list_off,
+    const uint32_t *__restrict__ list_size, const uint32_t *__restrict__ codes, const float *__restrict__ f1,
+    const float *__restrict__ f2, const float *__restrict__ f3, const uint32_t *__restrict__ planes,
+    const double *__restrict__ qconst, const double *__restrict__ eps_r_arr, const double *__restrict__ tau0_arr,
+    double isd, const uint64_t *__restrict__ f1_off, uint32_t *__restrict__ f1_cnt, uint32_t *__restrict__ f1_pos)
+{
+    extern __shared__ unsigned char csm[];
+    uint32_t *tile_pre = (uint32_t *)csm;     // np + 1
+    __shared__ uint32_t sh_cnt;
+    const int64_t q = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nwarps = blockDim.x >> 5;
+    if (threadIdx.x == 0) {
+        uint32_t acc = 0;
+        for (int p = 0; p < np; p++) {
+            tile_pre[p] = acc;
+            uint32_t c = probe[q * np + p];
+            if (c != 0xFFFFFFFFu) acc += (list_size[c] + 127) / 128;
+        }
+        tile_pre[np] = acc;
+        sh_cnt = 0;
+    }
+    __syncthreads();
+    const double eps_r = eps_r_arr[q], tau0 = tau0_arr[q];
+    uint32_t *out = f1_pos + f1_off[q];
+    const uint32_t ntiles = tile_pre[np];
+    int p = 0;
+    uint32_t pl[MRQ_BQ * W];
+    double qc[5];
+    int cur_p = -1;
+    for (uint32_t t = warp; t < ntiles; t += nwarps) {
+        while (tile_pre[p + 1] <= t) p++;
+        if (p != cur_p) {
+            cur_p = p;
+            const uint32_t *g = planes + (q * np + p) * (MRQ_BQ * W);
+#pragma unroll
+            for (int i = 0; i < MRQ_BQ * W; i++) pl[i] = g[i];
+            const double *gc = qconst + (q * np + p) * 8;
+#pragma unroll
+            for (int i = 0; i < 5; i++) qc[i] = gc[i];
+        }
+        const uint32_t c = probe[q * np + p];
+        const uint32_t lstart = list_off[c], lend = lstart + list_size[c];
+        const uint32_t base = lstart + (t - tile_pre[p]) * 128 + lane * 4;
+        uint4 cw[W];
+#pragma unroll
+        for (int w = 0; w < W; w++) cw[w] = __ldg((const uint4 *)(codes + (int64_t)w * npad + base));
+        const float4 a1 = __ldg((const float4 *)(f1 + base));
+        const float4 a2 = __ldg((const float4 *)(f2 + base));
+        const float4 a3 = __ldg((const float4 *)(f3 + base));
+        bool fl[4];
+#pragma unroll
+        for (int r = 0; r < 4; r++) {
+            uint32_t code[W];
+#pragma unroll
+            for (int w = 0; w < W; w++) code[w] = r == 0 ? cw[w].x : r == 1 ? cw[w].y : r == 2 ? cw[w].z : cw[w].w;
+            const float v1 = r == 0 ? a1.x : r == 1 ? a1.y : r == 2 ? a1.z : a1.w;
+            const float v2 = r == 0 ? a2.x : r == 1 ? a2.y : r == 2 ? a2.z : a2.w;
+            const float v3 = r == 0 ? a3.x : r == 1 ? a3.y : r == 2 ? a3.z : a3.w;
+            double dis;
+            const double lb1 = mrq_lb1<W>(code, pl, qc, isd, eps_r, v1, v2, v3, &dis);
+            fl[r] = (base + r < lend) && (lb1 < tau0);
+        }
+        const unsigned b0 = __ballot_sync(0xffffffffu, fl[0]), b1 = __ballot_sync(0xffffffffu, fl[1]);
+        const unsigned b2 = __ballot_sync(0xffffffffu, fl[2]), b3 = __ballot_sync(0xffffffffu, fl[3]);
+        const int n0 = __popc(b0), n1 = __popc(b1), n2 = __popc(b2), n3 = __popc(b3);
+        const int tot = n0 + n1 + n2 + n3;
+        if (tot) {
+            uint32_t wb = 0;
+            if (lane == 0) wb = atomicAdd(&sh_cnt, (uint32_t)tot);
+            wb = __shfl_sync(0xffffffffu, wb, 0);
+            const unsigned lt = (1u << lane) - 1u;
+            if (fl[0]) out[wb + __popc(b0 & lt)] = base;
+            if (fl[1]) out[wb + n0 + __popc(b1 & lt)] = base + 1;
+            if (fl[2]) out[wb + n0 + n1 + __popc(b2 & lt)] = base + 2;
+            if (fl[3]) out[wb + n0 + n1 + n2 + __popc(b3 & lt)] = base + 3;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) f1_cnt[q] = sh_cnt;
+}
+
+// ======================================================================= a6
+// Stage 2 (Alg.2 L13 P:315; "Optimization" P:327 read as A-7): for every F1
+// entry HEAD = ||x_d - q_d||^2 (left to right over i < d) and
+// dis_o' = (HEAD + ||x_r||^2) + ||q_r||^2.  TIGHT: S1 = the K' smallest
+// (dis_o', id) of F1, their exact distances (HEAD continued over the tail),
+// tau1 = K-th smallest distinct exact over S0 u S1; LOOSE: tau1 = tau0.
+// F2 = {e in F1 : dis_o' - eps_r < tau1} (FULL) or F1 (STAGE1_ONLY / EXACT).
+__global__ void __launch_bounds__(256) k_stage2(
+    int mode, int tight, int K, int Kp, int D, int d, const uint32_t *__restrict__ ids,
+    const float *__restrict__ heads, const float *__restrict__ tails, const float *__restrict__ xr2,
+    const double *__restrict__ qp, const double *__restrict__ qr2_arr, const double *__restrict__ eps_r_arr,
+    const double *__restrict__ tau0_arr, const uint64_t *__restrict__ f1_off, const uint32_t *__restrict__ f1_cnt,
+    const uint32_t *__restrict__ f1_pos, double *__restrict__ f1_head, double *__restrict__ f1_diso,
+    const uint32_t *__restrict__ s0_cnt, const uint32_t *__restrict__ s0_pos, const double *__restrict__ s0_exact,
+    uint32_t *__restrict__ s1_cnt, uint32_t *__restrict__ s1_pos, double *__restrict__ s1_exact, int S,
+    double *__restrict__ tau1_arr, uint32_t *__restrict__ f2_cnt, uint32_t *__restrict__ f2_pos,
+    double *__restrict__ f2_head)
+{
+    extern __shared__ unsigned char tsm[];
+    double *qs = (double *)tsm;                              // D
+    float *tiles = (float *)(qs + D);                        // 8 x 32 x 33
+    SelItem *buf = (SelItem *)(tiles + 8 * 32 * 33);         // S
+    __shared__ uint32_t sh_cnt;
+    __shared__ double sh_tau1;
+    __shared__ uint32_t sh_dups;
+    const int64_t q = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nwarps = blockDim.x >> 5;
+    for (int i = threadIdx.x; i < D; i += blockDim.x) qs[i] = qp[q * D + i];
+    if (threadIdx.x == 0) sh_cnt = 0;
+    __syncthreads();
+    const uint64_t base = f1_off[q];
+    const int n1 = (int)f1_cnt[q];
+    const double qr2 = qr2_arr[q], eps_r = eps_r_arr[q];
+    float *tile = tiles + warp * 32 * 33;
+    for (int e0 = warp * 32; e0 < n1; e0 += nwarps * 32) {
+        const int e = e0 + lane;
+        const bool valid = e < n1;
+        const uint32_t slot = valid ? f1_pos[base + e] : 0u;
+        const double head = warp_rows_sqdist(heads, d, 0, slot, valid, d, qs, 0.0, tile);
+        if (valid) {
+            f1_head[base + e] = head;
+            f1_diso[base + e] = (head + (double)xr2[slot]) + qr2;
+        }
+    }
+    __syncthreads();
+    double tau1 = tau0_arr[q];
+    if (mode == 0 && tight) {
+        const int ns1 = block_select(buf, S, Kp, n1, [&](int i) {
+            SelItem s;
+            s.key = f1_diso[base + i];
+            s.id = ids[f1_pos[base + i]];
+            s.pay = (uint32_t)i;
+            return s;
+        });
+        for (int e0 = warp * 32; e0 < ns1; e0 += nwarps * 32) {
+            const int e = e0 + lane;
+            const bool valid = e < ns1;
+            const uint32_t ent = valid ? buf[e].pay : 0u;
+            const uint32_t slot = valid ? f1_pos[base + ent] : 0u;
+            double acc = valid ? f1_head[base + ent] : 0.0;
+            if (D > d) acc = warp_rows_sqdist(tails, D - d, 0, slot, valid, D - d, qs + d, acc, tile);
+            if (valid) {
+                s1_pos[q * Kp + e] = slot;
+                s1_exact[q * Kp + e] = acc;
+            }
+        }
+        __syncthreads();
+        const int ns0 = (int)s0_cnt[q];
+        if (threadIdx.x == 0) sh_dups = 0;
+        __syncthreads();
+        for (int j = threadIdx.x; j < ns1; j += blockDim.x) {
+            const uint32_t sl = s1_pos[q * Kp + j];
+            bool dup = false;
+            for (int t = 0; t < ns0; t++) dup |= (s0_pos[q * Kp + t] == sl);
+            if (dup) atomicAdd(&sh_dups, 1u);
+        }
+        __syncthreads();
+        const int distinct = ns0 + ns1 - (int)sh_dups;
+        // K-th smallest distinct exact over S0 u S1 (S1 members already in S0 are skipped)
+        block_select(buf, S, K, ns0 + ns1, [&](int i) {
+            SelItem s;
+            if (i < ns0) {
+                s.key = s0_exact[q * Kp + i];
+                s.id = ids[s0_pos[q * Kp + i]];
+            } else {
+                const int j = i - ns0;
+                const uint32_t sl = s1_pos[q * Kp + j];
+                bool dup = false;
+                for (int t = 0; t < ns0; t++) dup |= (s0_pos[q * Kp + t] == sl);
+                s.key = dup ? __longlong_as_double(0x7ff0000000000000ll) : s1_exact[q * Kp + j];
+                s.id = dup ? 0xFFFFFFFFu : ids[sl];
+            }
+            s.pay = i;
+            return s;
+        });
+        if (threadIdx.x == 0) {
+            sh_tau1 = distinct >= K ? buf[K - 1].key : __longlong_as_double(0x7ff0000000000000ll);
+            s1_cnt[q] = ns1;
+        }
+        __syncthreads();
+        tau1 = sh_tau1;
+    } else if (threadIdx.x == 0) {
+        s1_cnt[q] = 0;
+    }
+    if (threadIdx.x == 0) tau1_arr[q] = tau1;
+    // F2
+    for (int e0 = 0; e0 < n1; e0 += blockDim.x) {
+        const int e = e0 + threadIdx.x;
+        bool pass = false;
+        if (e < n1) pass = (mode != 0) || (f1_diso[base + e] - eps_r < tau1);
+        const unsigned bal = __ballot_sync(0xffffffffu, pass);
+        uint32_t wb = 0;
+        if (lane == 0 && bal) wb = atomicAdd(&sh_cnt, (uint32_t)__popc(bal));
+        wb = __shfl_sync(0xffffffffu, wb, 0);
+        if (pass) {
+            const uint32_t at = wb + __popc(bal & ((1u << lane) - 1u));
+            f2_pos[base + at] = f1_pos[base + e];
+            f2_head[base + at] = f1_head[base + e];
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) f2_cnt[q] = sh_cnt;
+}
+
+// ======================================================================= a7
+// Exact re-rank of F2 (Alg.2 L14 P:316): exact = HEAD continued over the
+// tail, i.e. ||x_p - q_p||^2 left to right over i = 0..D-1 (A-8).
+__global__ void __launch_bounds__(256) k_rerank(int D, int d, const float *__restrict__ tails,
+                                                const double *__restrict__ qp, const uint64_t *__restrict__ f1_off,
+                                                const uint32_t *__restrict__ f2_cnt, const uint32_t *__restrict__ f2_pos,
+                                                const double *__restrict__ f2_head, double *__restrict__ f2_exact)
+{
+    extern __shared__ unsigned char rsm[];
+    double *qs = (double *)rsm;                              // D - d
+    float *tiles = (float *)(qs + (D - d > 0 ? D - d : 1));  // 8 x 32 x 33
+    const int64_t q = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+    for (int i = threadIdx.x; i < D - d; i += blockDim.x) qs[i] = qp[q * D + d + i];
+    __syncthreads();
+    const uint64_t base = f1_off[q];
+    const int n2 = (int)f2_cnt[q];
+    float *tile = tiles + warp * 32 * 33;
+    for (int e0 = warp * 32; e0 < n2; e0 += nwarps * 32) {
+        const int e = e0 + lane;
+        const bool valid = e < n2;
+        const uint32_t slot = valid ? f2_pos[base + e] : 0u;
+        double acc = valid ? f2_head[base + e] : 0.0;
+        if (D > d) acc = warp_rows_sqdist(tails, D - d, 0, slot, valid, D - d, qs, acc, tile);
+        if (valid) f2_exact[base + e] = acc;
+    }
+}
+
+// ======================================================================= a8
+// Per-query top-K (Alg.2 L15-L16): the K smallest (exact, id) over
+// the distinct union S0 u S1 u F2; ids returned as the original int64 index,
+// distances rounded to fp32; padding id -1 / +inf.
+__global__ void __launch_bounds__(256) k_topk(int K, int Kp, const uint32_t *__restrict__ ids,
+                                              const uint32_t *__restrict__ s0_cnt, const uint32_t *__restrict__ s0_pos,
+                                              const double *__restrict__ s0_exact, const uint32_t *__restrict__ s1_cnt,
+                                              const uint32_t *__restrict__ s1_pos, const double *__restrict__ s1_exact,
+                                              const uint64_t *__restrict__ f1_off, const uint32_t *__restrict__ f2_cnt,
+                                              const uint32_t *__restrict__ f2_pos, const double *__restrict__ f2_exact,
+                                              int S, int64_t *__restrict__ out_ids, float *__restrict__ out_dist,
+                                              uint32_t *__restrict__ exact_cnt)
+{
+    extern __shared__ unsigned char ksm[];
+    uint32_t *sel = (uint32_t *)ksm;                         // 2 Kp slots of S0 u S1
+    SelItem *buf = (SelItem *)(((uintptr_t)(sel + 2 * Kp) + 15) & ~(uintptr_t)15);
+    __shared__ uint32_t sh_dup;
+    const int64_t q = blockIdx.x;
+    const int ns0 = (int)s0_cnt[q], ns1 = (int)s1_cnt[q], n2 = (int)f2_cnt[q];
+    const uint64_t base = f1_off[q];
+    for (int i = threadIdx.x; i < ns0; i += blockDim.x) sel[i] = s0_pos[q * Kp + i];
+    for (int i = threadIdx.x; i < ns1; i += blockDim.x) sel[ns0 + i] = s1_pos[q * Kp + i];
+    if (threadIdx.x == 0) sh_dup = 0;
+    __syncthreads();
+    const int nsel = ns0 + ns1;
+    auto member = [&](uint32_t slot, int upto) {
+        for (int t = 0; t < upto; t++)
+            if (sel[t] == slot) return true;
+        return false;
+    };
+    const int n = nsel + n2;
+    block_select(buf, S, K, n, [&](int i) {
+        SelItem s;
+        bool dup;
+        uint32_t slot;
+        double key;
+        if (i < ns0) {
+            slot = sel[i];
+            key = s0_exact[q * Kp + i];
+            dup = false;
+        } else if (i < nsel) {
+            slot = sel[i];
+            key = s1_exact[q * Kp + (i - ns0)];
+            dup = member(slot, ns0);
+        } else {
+            slot = f2_pos[base + (i - nsel)];
+            key = f2_exact[base + (i - nsel)];
+            dup = member(slot, nsel);
+        }
+        if (dup) {
+            atomicAdd(&sh_dup, 1u);
+            return sel_inf();
+        }
+        s.key = key;
+        s.id = ids[slot];
+        s.pay = slot;
+        return s;
+    });
+    for (int i = threadIdx.x; i < K; i += blockDim.x) {
+        const bool ok = buf[i].id != 0xFFFFFFFFu;
+        out_ids[q * K + i] = ok ? (int64_t)buf[i].id : (int64_t)-1;
+        out_dist[q * K + i] = ok ? (float)buf[i].key : __int_as_float(0x7f800000);
+    }
+    if (threadIdx.x == 0) exact_cnt[q] = (uint32_t)n - sh_dup;
+}
+
+// ================================================================ launchers
+template <int W>
+static void launch_seed_w(const LaunchSeed &a, cudaStream_t st)
+{
+    k_seed<W><<<a.nq, 256, a.smem, st>>>(a.probe, a.np, a.K, a.Kp, a.D, a.d, a.npad, a.list_off, a.list_size, a.ids,
+                                          a.codes, a.f1, a.f2, a.f3, a.heads, a.tails, a.planes, a.qconst, a.qp,
+                                          a.eps_r, a.isd, a.pool_cap, a.S, a.pool, a.s0_cnt, a.s0_pos, a.s0_exact,
+                                          a.tau0);
+}
+
+void launch_seed(int W, const LaunchSeed &a, cudaStream_t st)
+{
+    switch (W) {
+    case 1: launch_seed_w<1>(a, st); break;
+    case 2: launch_seed_w<2>(a, st); break;
+    case 3: launch_seed_w<3>(a, st); break;
+    case 4: launch_seed_w<4>(a, st); break;
+    case 8: launch_seed_w<8>(a, st); break;
+    case 16: launch_seed_w<16>(a, st); break;
+    default: break;
+    }
+}
+
+template <int W>
+static void launch_scan_w(const LaunchScan &a, cudaStream_t st)
+{
+    k_scan<W><<<a.nq, 256, a.smem, st>>>(a.probe, a.np, a.npad, a.list_off, a.list_size, a.codes, a.f1, a.f2, a.f3,
+                                          a.planes, a.qconst, a.eps_r, a.tau0, a.isd, a.f1_off, a.f1_cnt, a.f1_pos);
+}
+
+void launch_scan(int W, const LaunchScan &a, cudaStream_t st)
+{
+    switch (W) {
+    case 1: launch_scan_w<1>(a, st); break;
+    case 2: launch_scan_w<2>(a, st); break;
+    case 3: launch_scan_w<3>(a, st); break;
+    case 4: launch_scan_w<4>(a, st); break;
+    case 8: launch_scan_w<8>(a, st); break;
+    case 16: launch_scan_w<16>(a, st); break;
+    default: break;
+    }
+}
+
+bool supported_W(int W) { return W == 1 || W == 2 || W == 3 || W == 4 || W == 8 || W == 16; }
+
+int mrq_seed_smem_attr(int W, size_t bytes)
+{
+    if (bytes <= 48 * 1024) return MRQ_OK;
+    cudaError_t e = cudaSuccess;
+    switch (W) {
+    case 1: e = cudaFuncSetAttribute(k_seed<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes); break;
+    case 2: e = cudaFuncSetAttribute(k_seed<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes); break;
+    case 3: e = cudaFuncSetAttribute(k_seed<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes); break;
+    case 4: e = cudaFuncSetAttribute(k_seed<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes); break;
+    case 8: e = cudaFuncSetAttribute(k_seed<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes); break;
+    case 16: e = cudaFuncSetAttribute(k_seed<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes); break;
+    default: break;
+    }
+    if (e != cudaSuccess) {
+        mrq_set_error("cudaFuncSetAttribute(k_seed): %s", cudaGetErrorString(e));
+        return MRQ_ECUDA;
+    }
+    return MRQ_OK;
+}
+
+// Test hook (mrq_debug_set "dump_dis"): dis' and LB1 of every scanned
+// candidate, in probe order then slot order -- the oracle's scan order --
+// written at f1_off[q] + i.  Uses the same epilogue as k_scan.
+template <int W>
+__global__ void k_scan_dbg(const uint32_t *__restrict__ probe, int np, int64_t npad,
+                           const uint32_t *__restrict__ list_off, const uint32_t *__restrict__ list_size,
+                           const uint32_t *__restrict__ codes, const float *__restrict__ f1,
+                           const float *__restrict__ f2, const float *__restrict__ f3,
+                           const uint32_t *__restrict__ planes, const double *__restrict__ qconst,
+                           const double *__restrict__ eps_r_arr, double isd, const uint64_t *__restrict__ f1_off,
+                           double *__restrict__ dis_out, double *__restrict__ lb1_out)
+{
+    const int64_t q = blockIdx.x;
+    uint64_t at = f1_off[q];
+    const double eps_r = eps_r_arr[q];
+    for (int p = 0; p < np; p++) {
+        const uint32_t c = probe[q * np + p];
+        if (c == 0xFFFFFFFFu) continue;
+        const uint32_t off = list_off[c], sz = list_size[c];
+        const uint32_t *pl = planes + (q * np + p) * (MRQ_BQ * W);
+        const double *qc = qconst + (q * np + p) * 8;
+        for (uint32_t e = threadIdx.x; e < sz; e += blockDim.x) {
+            const uint32_t slot = off + e;
+            uint32_t code[W];
+#pragma unroll
+            for (int w = 0; w < W; w++) code[w] = codes[(int64_t)w * npad + slot];
+            double dis;
+            const double lb1 = mrq_lb1<W>(code, pl, qc, isd, eps_r, f1[slot], f2[slot], f3[slot], &dis);
+            dis_out[at + e] = dis;
+            lb1_out[at + e] = lb1;
+        }
+        at += sz;
+    }
+}
+
+void launch_scan_dbg(int W, const LaunchScan &a, double *dis, double *lb1, cudaStream_t st)
+{
+#define MRQ_DBG(WW)                                                                                           \
+    k_scan_dbg<WW><<<a.nq, 256, 0, st>>>(a.probe, a.np, a.npad, a.list_off, a.list_size, a.codes, a.f1, a.f2, \
+                                         a.f3, a.planes, a.qconst, a.eps_r, a.isd, a.f1_off, dis, lb1)
+    switch (W) {
+    case 1: MRQ_DBG(1); break;
+    case 2: MRQ_DBG(2); break;
+    case 3: MRQ_DBG(3); break;
+    case 4: MRQ_DBG(4); break;
+    case 8: MRQ_DBG(8); break;
+    case 16: MRQ_DBG(16); break;
+    default: break;
+    }
+#undef MRQ_DBG
+}

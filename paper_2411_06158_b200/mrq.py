@@ -1,0 +1,179 @@
+"""ctypes binding of libmrq with the C ABI's names (include/mrq.h).
+
+Argument marshalling only.  Host arrays are numpy; device arrays are torch
+CUDA tensors (PyTorch supplies device memory and streams: plumbing).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmrq.so")
+
+MRQ_MODES = {"FULL": 0, "STAGE1_ONLY": 1, "EXACT": 2}
+ERRORS = {-1: "EINVAL", -2: "EDIM", -3: "EFORMAT", -4: "EVERSION", -5: "EDEGENERATE", -6: "ECUDA",
+          -7: "ENOMEM", -8: "ENCCL", -9: "EIO"}
+
+
+class MRQError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__("%s (%d): %s" % (ERRORS.get(code, "?"), code, msg))
+        self.code = code
+
+
+class DistCfg(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("device", C.c_int32), ("nccl_unique_id", C.c_void_p)]
+
+
+class SearchParams(C.Structure):
+    _fields_ = [("K", C.c_int32), ("nprobe", C.c_int32), ("eps0", C.c_double), ("m", C.c_double),
+                ("mode", C.c_int32), ("tau_schedule", C.c_int32), ("seed_mult", C.c_int32),
+                ("resid_scale", C.c_double)]
+
+    @classmethod
+    def make(cls, K=10, nprobe=16, eps0=1.9, m=4.0, mode="FULL", tau_schedule="TIGHT", seed_mult=2,
+             resid_scale=2.0):
+        return cls(K, nprobe, eps0, m, MRQ_MODES[mode] if isinstance(mode, str) else mode,
+                   0 if tau_schedule in ("TIGHT", 0) else 1, seed_mult, resid_scale)
+
+
+class Stats(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in ("scanned", "stage1_pass", "stage2_pass", "exact", "seeds")] + \
+               [(n, C.c_double) for n in ("ms_total", "ms_qprep", "ms_probe", "ms_quant", "ms_seed", "ms_scan",
+                                          "ms_stage2", "ms_rerank", "ms_topk", "ms_comm")]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+_lib = None
+
+
+def lib():
+    """Load libmrq.so; fails loudly when the CUDA extension is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError("libmrq.so not built (run __graft_entry__.build()); there is no CPU fallback")
+        L = C.CDLL(LIB_PATH)
+        L.mrq_last_error.restype = C.c_char_p
+        for f in ("mrq_index_load", "mrq_search_batch", "mrq_search_batch_device", "mrq_debug_fetch",
+                  "mrq_index_info"):
+            getattr(L, f).restype = C.c_int
+        L.mrq_index_load.argtypes = [C.c_char_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p,
+                                     C.POINTER(C.c_void_p)]
+        L.mrq_search_batch.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(SearchParams), C.c_void_p,
+                                       C.c_void_p, C.c_void_p]
+        L.mrq_search_batch_device.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(SearchParams),
+                                              C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.mrq_free.argtypes = [C.c_void_p]
+        L.mrq_free.restype = None
+        L.mrq_debug_fetch.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t)]
+        L.mrq_index_info.argtypes = [C.c_void_p] + [C.c_void_p] * 5
+        L.mrq_debug_set.restype = C.c_int
+        L.mrq_debug_set.argtypes = [C.c_void_p, C.c_char_p, C.c_int64]
+        _lib = L
+    return _lib
+
+
+def mrq_last_error() -> str:
+    return lib().mrq_last_error().decode()
+
+
+def _check(rc):
+    if rc != 0:
+        raise MRQError(rc, mrq_last_error())
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        return C.c_void_p(a.data_ptr())
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def mrq_index_load(build_file: str, base: np.ndarray, d: int, rank=0, world=1, device=-1, nccl_unique_id=None):
+    base = np.ascontiguousarray(base, dtype=np.float32)
+    n, D = base.shape
+    h = C.c_void_p()
+    uid = None
+    if nccl_unique_id is not None:
+        uid = C.create_string_buffer(bytes(nccl_unique_id), 128)
+    cfg = DistCfg(rank, world, device, C.cast(uid, C.c_void_p) if uid is not None else None)
+    _check(lib().mrq_index_load(build_file.encode(), _ptr(base), n, D, d, C.byref(cfg), C.byref(h)))
+    return h
+
+
+def mrq_search_batch(h, queries: np.ndarray, params: SearchParams, with_stats=True):
+    q = np.ascontiguousarray(queries, dtype=np.float32)
+    nq = q.shape[0]
+    ids = np.empty((nq, params.K), np.int64)
+    dist = np.empty((nq, params.K), np.float32)
+    st = Stats()
+    _check(lib().mrq_search_batch(h, _ptr(q), nq, C.byref(params), _ptr(ids), _ptr(dist),
+                                  C.byref(st) if with_stats else None))
+    return ids, dist, st
+
+
+def mrq_search_batch_device(h, d_queries, params: SearchParams, d_ids, d_dist, stats: Stats | None = None,
+                            stream=None):
+    nq = d_queries.shape[0]
+    s = C.c_void_p(stream) if stream else None
+    _check(lib().mrq_search_batch_device(h, _ptr(d_queries), nq, C.byref(params), _ptr(d_ids), _ptr(d_dist),
+                                         C.byref(stats) if stats is not None else None, s))
+
+
+def mrq_free(h):
+    if h:
+        lib().mrq_free(h)
+
+
+def mrq_index_info(h):
+    n, npad = C.c_int64(), C.c_int64()
+    D, d, k = C.c_int32(), C.c_int32(), C.c_int32()
+    _check(lib().mrq_index_info(h, C.byref(n), C.byref(D), C.byref(d), C.byref(k), C.byref(npad)))
+    return {"n": n.value, "D": D.value, "d": d.value, "k": k.value, "npad": npad.value}
+
+
+_DT = {"u32": np.uint32, "u64": np.uint64, "f32": np.float32, "f64": np.float64}
+
+
+def mrq_debug_set(h, name: str, value: int):
+    _check(lib().mrq_debug_set(h, name.encode(), value))
+
+
+def mrq_debug_fetch(h, name: str, dtype: str):
+    need = C.c_size_t()
+    _check(lib().mrq_debug_fetch(h, name.encode(), None, 0, C.byref(need)))
+    out = np.empty(need.value // np.dtype(_DT[dtype]).itemsize, _DT[dtype])
+    _check(lib().mrq_debug_fetch(h, name.encode(), _ptr(out), out.nbytes, C.byref(need)))
+    return out
+
+
+class Index:
+    """Convenience owner of an mrq_index handle."""
+
+    def __init__(self, build_file, base, d, **kw):
+        self.h = mrq_index_load(build_file, base, d, **kw)
+        self.info = mrq_index_info(self.h)
+
+    def search(self, queries, K=10, nprobe=16, **kw):
+        return mrq_search_batch(self.h, queries, SearchParams.make(K=K, nprobe=nprobe, **kw))
+
+    def fetch(self, name, dtype):
+        return mrq_debug_fetch(self.h, name, dtype)
+
+    def close(self):
+        mrq_free(self.h)
+        self.h = None
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                self.close()
+        except Exception:
+            pass

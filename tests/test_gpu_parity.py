@@ -1,0 +1,220 @@
+"""GPU <-> oracle parity, stage by stage, through the C ABI (-m gpu).
+
+Both sides read the same oracle build file (BASELINE.json north_star) and the
+same seeded base/queries.  Bar: codes, bit-planes,
+probe lists, flag sets (F1, F2, S0, S1) and returned ids are compared
+bit-exactly; because both sides follow the canonical fp64 order, the fp64
+intermediates (q_p, constants, dis', LB1, tau0, tau1, exact distances) are
+also compared bit-exactly, which is stricter than north_star's 1e-4
+relative distance tolerance (asserted as well, separately).
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from oracle import build as B
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+pytestmark = pytest.mark.gpu
+
+
+def _gpu():
+    import paper_2411_06158_b200 as m
+    return m
+
+
+CASES = {
+    # name: (config, N, Q, D, d, k, nprobe list, committed build file or None)
+    "tiny": ("tiny", None, None, None, 16, 16, (1, 4, 16), "data/tiny/build_d16.mrqb"),
+    "sift50k": ("sift", 50_000, 64, 128, 64, 256, (8, 32), None),
+    "deep_d48": ("deep", 20_000, 48, 96, 48, 64, (5, 16), None),
+    "gist_small": ("gist", 8_000, 24, 960, 128, 32, (4,), None),
+}
+
+
+@pytest.fixture(scope="module", params=list(CASES))
+def case(request, tmp_path_factory):
+    name = request.param
+    cfgname, N, Q, D, d, k, nps, bfile = CASES[name]
+    cfg = synth.config_by_name(cfgname)
+    X, Qv = synth.generate(cfg, N=N, Q=Q, D=D)
+    if bfile:
+        path = os.path.join(ROOT, bfile)
+        bf = B.read(path)
+    else:
+        bf = B.build(X, d, k)
+        path = str(tmp_path_factory.mktemp("bf") / (name + ".mrqb"))
+        B.write(path, bf)
+    ox = oracle.Index(bf, X)
+    m = _gpu()
+    gx = m.Index(path, X, d)
+    yield dict(name=name, X=X, Q=Qv, bf=bf, ox=ox, gx=gx, d=d, nprobe=nps, m=m)
+    gx.close()
+
+
+def _slot_to_id(gx):
+    return gx.fetch("ids", "u32").astype(np.int64)
+
+
+def test_encode_bit_exact(case):
+    """a0: Alg.1 L3-L8 on the GPU equals the oracle bit for bit."""
+    gx, ox, d = case["gx"], case["ox"], case["d"]
+    ids = _slot_to_id(gx)
+    npad = gx.info["npad"]
+    W = (d + 31) // 32
+    valid = ids != 0xFFFFFFFF
+    sid = ids[valid]
+    codes = gx.fetch("codes", "u32").reshape(W, npad)[:, valid].T
+    assert np.array_equal(codes, ox.code[sid])
+    for nm, ref in (("f1", ox.f1), ("f2", ox.f2), ("f3", ox.f3), ("xr2", ox.xr2f)):
+        got = gx.fetch(nm, "f32")[valid]
+        assert np.array_equal(got.view(np.uint32), ref[sid].view(np.uint32)), nm
+    heads = gx.fetch("heads", "f32").reshape(npad, d)[valid]
+    assert np.array_equal(heads, ox.head[sid])
+    D = ox.D
+    if D > d:
+        tails = gx.fetch("tails", "f32").reshape(npad, D - d)[valid]
+        assert np.array_equal(tails, ox.tail[sid])
+    # inverted lists: same members, ascending ids inside each list (A-28)
+    off = gx.fetch("list_off", "u32").astype(np.int64)
+    size = gx.fetch("list_size", "u32").astype(np.int64)
+    for c in range(ox.k):
+        got = ids[off[c]:off[c] + size[c]]
+        assert np.array_equal(got, ox.list_ids[ox.list_off[c]:ox.list_off[c + 1]])
+        assert off[c] % 4 == 0
+    assert np.array_equal(gx.fetch("Rc", "f64").reshape(ox.k, d), ox.Rc)
+
+
+def _search_both(case, nprobe, K=10, mode="FULL", tau="TIGHT"):
+    gx, ox, Q = case["gx"], case["ox"], case["Q"]
+    m = case["m"]
+    m.mrq_debug_set(gx.h, "dump_dis", 1)
+    gi, gd, gst = gx.search(Q, K=K, nprobe=nprobe, mode=mode, tau_schedule=tau)
+    oi, od, ost, dp = ox.search(Q, K=K, nprobe=nprobe, mode=mode, tau_schedule=tau, dump=True)
+    return gi, gd, gst, oi, od, ost, dp
+
+
+def _segments(gx, nq, cnt_name, pos_name, extra=None):
+    off = gx.fetch("f1_off", "u64").astype(np.int64)
+    cnt = gx.fetch(cnt_name, "u32").astype(np.int64)
+    pos = gx.fetch(pos_name, "u32").astype(np.int64)
+    ex = gx.fetch(extra, "f64") if extra else None
+    ids = _slot_to_id(gx)
+    out = []
+    for q in range(nq):
+        sl = pos[off[q]:off[q] + cnt[q]]
+        v = ex[off[q]:off[q] + cnt[q]] if ex is not None else None
+        out.append((ids[sl], v))
+    return out
+
+
+@pytest.mark.parametrize("tau", ["TIGHT", "LOOSE"])
+def test_stagewise_parity(case, tau):
+    gx, ox, Q = case["gx"], case["ox"], case["Q"]
+    nq, D, d = Q.shape[0], ox.D, case["d"]
+    for npb in case["nprobe"]:
+        gi, gd, gst, oi, od, ost, dp = _search_both(case, npb, tau=tau)
+        npe = min(npb, ox.k)
+        # a1 query projection, residual constants
+        assert np.array_equal(gx.fetch("qp", "f64").reshape(nq, D), dp["qp"])
+        assert np.array_equal(gx.fetch("qr2", "f64"), dp["qr2"])
+        assert np.array_equal(gx.fetch("eps_r", "f64"), dp["eps_r"])
+        # a2 probe: identical lists in identical order, bit-exact ||q_d - c||^2
+        assert np.array_equal(gx.fetch("probe", "u32").reshape(nq, npe).astype(np.int64), dp["probe"])
+        assert np.array_equal(gx.fetch("probe_qn2", "f64").reshape(nq, npe), dp["probe_qn2"])
+        # a3 quantization: bit-planes reproduce the oracle's levels; constants bit-exact
+        W = (d + 31) // 32
+        planes = gx.fetch("planes", "u32").reshape(nq, npe, 4, W)
+        j = np.arange(d)
+        lev = np.zeros((nq, npe, d), np.int64)
+        for b in range(4):
+            lev += (((planes[:, :, b, j // 32] >> (j % 32).astype(np.uint32)) & 1).astype(np.int64)) << b
+        assert np.array_equal(lev, dp["levels"].astype(np.int64))
+        qc = gx.fetch("qconst", "f64").reshape(nq, npe, 8)[:, :, :5]
+        assert np.array_equal(qc, dp["qconst"])
+        # a5 scan: dis' and LB1 of every candidate bit-exact (and within 1e-4 rel), tau0, F1 sets
+        off = gx.fetch("f1_off", "u64").astype(np.int64)
+        dis = gx.fetch("dbg_dis", "f64")
+        lb1 = gx.fetch("dbg_lb1", "f64")
+        for q in range(nq):
+            n = dp["scan_cnt"][q]
+            assert off[q + 1] - off[q] == n
+            assert np.array_equal(dis[off[q]:off[q] + n], dp["scan_dis"][q, :n])
+            assert np.array_equal(lb1[off[q]:off[q] + n], dp["scan_lb1"][q, :n])
+            rel = np.abs(dis[off[q]:off[q] + n] - dp["scan_dis"][q, :n]) / np.maximum(np.abs(dp["scan_dis"][q, :n]), 1e-30)
+            assert np.all(rel <= 1e-4)
+        assert np.array_equal(gx.fetch("tau0", "f64"), dp["tau0"])
+        f1 = _segments(gx, nq, "f1_cnt", "f1_pos")
+        for q in range(nq):
+            assert sorted(f1[q][0].tolist()) == sorted(dp["f1_ids"][q, :dp["f1_cnt"][q]].tolist())
+        # a4 seeds
+        s0c = gx.fetch("s0_cnt", "u32")
+        Kp = 20
+        s0p = gx.fetch("s0_pos", "u32").reshape(nq, Kp)
+        ids = _slot_to_id(gx)
+        for q in range(nq):
+            assert s0c[q] == dp["s0_cnt"][q]
+            assert sorted(ids[s0p[q, :s0c[q]]].tolist()) == sorted(dp["s0_ids"][q, :s0c[q]].tolist())
+        # a6 stage 2: tau1 and F2 sets
+        assert np.array_equal(gx.fetch("tau1", "f64"), dp["tau1"])
+        f2 = _segments(gx, nq, "f2_cnt", "f2_pos", "f2_exact")
+        for q in range(nq):
+            oid = dp["f2_ids"][q, :dp["f2_cnt"][q]]
+            oex = dp["f2_exact"][q, :dp["f2_cnt"][q]]
+            gid, gex = f2[q]
+            assert sorted(gid.tolist()) == sorted(oid.tolist())
+            # a7 exact distances bit-exact
+            o = dict(zip(oid.tolist(), oex.tolist()))
+            assert all(o[i] == v for i, v in zip(gid.tolist(), gex.tolist()))
+        # a8 top-K: identical ids and fp32 distances
+        assert np.array_equal(gi, oi)
+        assert np.array_equal(gd.view(np.uint32), od.view(np.uint32))
+        assert gst.scanned == ost["scanned"]
+        assert gst.stage1_pass == ost["f1"] and gst.stage2_pass == ost["f2"] and gst.exact == ost["exact"]
+
+
+@pytest.mark.parametrize("mode", ["STAGE1_ONLY", "EXACT"])
+def test_modes_parity(case, mode):
+    npb = case["nprobe"][-1]
+    gi, gd, gst, oi, od, ost, dp = _search_both(case, npb, mode=mode)
+    assert np.array_equal(gi, oi)
+    assert np.array_equal(gd.view(np.uint32), od.view(np.uint32))
+    assert gst.exact == ost["exact"]
+
+
+@pytest.mark.parametrize("K", [1, 100])
+def test_k_edge_parity(case, K):
+    gi, gd, gst, oi, od, ost, dp = _search_both(case, case["nprobe"][0], K=K)
+    assert np.array_equal(gi, oi)
+    assert np.array_equal(gd.view(np.uint32), od.view(np.uint32))
+
+
+def test_probe_all_lists_and_padding(case):
+    """nprobe = k (every list) and K larger than the candidate count (-1/+inf padding)."""
+    ox = case["ox"]
+    k = min(ox.k, 1024)
+    gi, gd, gst, oi, od, ost, dp = _search_both(case, k, K=10)
+    assert np.array_equal(gi, oi)
+    small = case["Q"][:3]
+    for mode in ("EXACT", "FULL"):
+        g = case["gx"].search(small, K=1024, nprobe=1, mode=mode)
+        o = ox.search(small, K=1024, nprobe=1, mode=mode)
+        assert np.array_equal(g[0], o[0])
+        assert np.array_equal(g[1].view(np.uint32), o[1].view(np.uint32))
+        pad = g[0] < 0
+        assert pad.any() and np.all(np.isinf(g[1][pad]))
+
+
+def test_empty_batch_and_errors(case):
+    m, gx = case["m"], case["gx"]
+    ids, dist, st = gx.search(np.zeros((0, case["ox"].D), np.float32), K=10, nprobe=4)
+    assert ids.shape == (0, 10)
+    with pytest.raises(m.MRQError) as e:
+        gx.search(case["Q"][:2], K=0, nprobe=4)
+    assert e.value.code == -1
+    with pytest.raises(m.MRQError) as e:
+        gx.search(case["Q"][:2], K=10, nprobe=case["ox"].k + 1)
+    assert e.value.code == -1
