@@ -477,6 +477,18 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
     SCR("f2_exact", double, total, f2_exact);
     if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[3], st));
 
+    StageArgs sa;
+    memset(&sa, 0, sizeof sa);
+    sa.nq = nq; sa.np = np; sa.K = K; sa.Kp = Kp; sa.D = D; sa.d = d; sa.mode = mode; sa.tight = tight;
+    sa.npad = ix->npad; sa.isd = isd; sa.probe = probe; sa.list_off = ix->list_off; sa.list_size = ix->list_size;
+    sa.ids = ix->ids; sa.codes = ix->codes; sa.planes = planes; sa.f1 = ix->f1; sa.f2 = ix->f2; sa.f3 = ix->f3;
+    sa.heads = ix->heads; sa.tails = ix->tails; sa.xr2 = ix->xr2; sa.qconst = qconst; sa.qp = qp; sa.qr2 = qr2;
+    sa.eps_r = eps_r; sa.s0_cnt = s0_cnt; sa.s0_pos = s0_pos; sa.s1_cnt = s1_cnt; sa.s1_pos = s1_pos;
+    sa.f1_cnt = f1_cnt; sa.f1_pos = f1_pos; sa.f2_cnt = f2_cnt; sa.f2_pos = f2_pos; sa.exact_cnt = exact_cnt;
+    sa.s0_exact = s0_exact; sa.s1_exact = s1_exact; sa.tau0 = tau0; sa.tau1 = tau1; sa.f1_head = f1_head;
+    sa.f1_diso = f1_diso; sa.f2_head = f2_head; sa.f2_exact = f2_exact; sa.f1_off = f1_off;
+    sa.out_ids = d_ids; sa.out_dist = d_dist;
+
     // ---- a4: seeds S0 and tau0 (decision T); EXACT mode scans everything
     if (mode == 2) {
         std::vector<double> inf(nq, INFINITY);
@@ -484,21 +496,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
         MRQ_CUDA_TRY(cudaMemsetAsync(s0_cnt, 0, nq * 4, st));
         MRQ_CUDA_TRY(cudaStreamSynchronize(st));
     } else {
-        const int pool_cap = Kp + (int)ix->max_list;
-        SelItem *pool;
-        SCR("pool", SelItem, nq * pool_cap, pool);
-        const int S = pow2_at_least(std::max(Kp + 256, 512));
-        LaunchSeed a;
-        a.nq = nq;
-        a.smem = (size_t)D * 8 + 8 * 32 * 33 * 4 + (size_t)S * sizeof(SelItem);
-        a.probe = probe; a.np = np; a.K = K; a.Kp = Kp; a.D = D; a.d = d; a.npad = ix->npad;
-        a.list_off = ix->list_off; a.list_size = ix->list_size; a.ids = ix->ids; a.codes = ix->codes;
-        a.f1 = ix->f1; a.f2 = ix->f2; a.f3 = ix->f3; a.heads = ix->heads; a.tails = ix->tails;
-        a.planes = planes; a.qconst = qconst; a.qp = qp; a.eps_r = eps_r; a.isd = isd;
-        a.pool_cap = pool_cap; a.S = S; a.pool = pool; a.s0_cnt = s0_cnt; a.s0_pos = s0_pos;
-        a.s0_exact = s0_exact; a.tau0 = tau0;
-        TRY(mrq_seed_smem_attr(W, a.smem));
-        launch_seed(W, a, st);
+        TRY(launch_seed_w(W, sa, st));
         if (ix->world > 1) TRY(mrq_comm_seeds(ix, nq, K, Kp, s0_cnt, s0_pos, s0_exact, tau0, st));
     }
     if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[4], st));
@@ -522,35 +520,17 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
     if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[5], st));
 
     // ---- a6: stage 2 -> F2 (and S1, tau1)
-    {
-        const int S = pow2_at_least(std::max(std::max(Kp, 2 * Kp) + 256, 512));
-        const size_t smem = (size_t)D * 8 + 8 * 32 * 33 * 4 + (size_t)S * sizeof(SelItem);
-        TRY(set_smem((const void *)k_stage2, smem));
-        k_stage2<<<(unsigned)nq, 256, smem, st>>>(mode, tight, K, Kp, D, d, ix->ids, ix->heads, ix->tails, ix->xr2, qp,
-                                                  qr2, eps_r, tau0, f1_off, f1_cnt, f1_pos, f1_head, f1_diso, s0_cnt,
-                                                  s0_pos, s0_exact, s1_cnt, s1_pos, s1_exact, S, tau1, f2_cnt, f2_pos,
-                                                  f2_head);
-        if (ix->world > 1 && mode == 0 && tight)
-            TRY(mrq_comm_tau1(ix, nq, K, Kp, s0_cnt, s0_pos, s0_exact, s1_cnt, s1_pos, s1_exact, tau1, st));
-    }
+    TRY(launch_stage2_w(sa, st));
+    if (ix->world > 1 && mode == 0 && tight)
+        TRY(mrq_comm_tau1(ix, nq, K, Kp, s0_cnt, s0_pos, s0_exact, s1_cnt, s1_pos, s1_exact, tau1, st));
     if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[6], st));
 
     // ---- a7: exact re-rank of F2
-    {
-        const size_t smem = (size_t)std::max(D - d, 1) * 8 + 8 * 32 * 33 * 4;
-        TRY(set_smem((const void *)k_rerank, smem));
-        k_rerank<<<(unsigned)nq, 256, smem, st>>>(D, d, ix->tails, qp, f1_off, f2_cnt, f2_pos, f2_head, f2_exact);
-    }
+    TRY(launch_rerank_w(sa, st));
     if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[7], st));
 
     // ---- a8: per-query top-K
-    {
-        const int S = pow2_at_least(std::max(K + 256, 512));
-        const size_t smem = (size_t)2 * Kp * 4 + 16 + (size_t)S * sizeof(SelItem);
-        TRY(set_smem((const void *)k_topk, smem));
-        k_topk<<<(unsigned)nq, 256, smem, st>>>(K, Kp, ix->ids, s0_cnt, s0_pos, s0_exact, s1_cnt, s1_pos, s1_exact,
-                                                f1_off, f2_cnt, f2_pos, f2_exact, S, d_ids, d_dist, exact_cnt);
-    }
+    TRY(launch_topk_w(sa, st));
     if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[8], st));
     // ---- a9: multi-GPU merge (NCCL all-gather of per-rank top-K)
     if (ix->world > 1) TRY(mrq_comm_merge(ix, nq, K, d_ids, d_dist, st));

@@ -12,4 +12,3 @@ int mrq_comm_tau1(mrq_index *ix, int64_t nq, int K, int Kp, const uint32_t *s0_c
                   const double *s0_exact, const uint32_t *s1_cnt, const uint32_t *s1_pos, const double *s1_exact,
                   double *tau1, cudaStream_t st);
 int mrq_comm_merge(mrq_index *ix, int64_t nq, int K, int64_t *d_ids, float *d_dist, cudaStream_t st);
-int mrq_seed_smem_attr(int W, size_t bytes);

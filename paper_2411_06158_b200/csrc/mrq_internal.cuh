@@ -157,19 +157,45 @@ __device__ __forceinline__ float key2f(uint32_t k)
 
 // Warp-cooperative sequential squared distance over row segments.  Each lane
 // owns one row (slot_lane, valid): acc += sum_{e=0}^{len-1} ((double)row[off+e]
-// - q[e])^2, left to right (the oracle's order), with the rows staged through
-// shared memory tile[32][33] so global loads are 128-byte coalesced.
+// - q[e])^2, left to right (the oracle's order).  Rows are staged 32 columns
+// at a time through shared memory tile[32][33]: when stride, off and len are
+// multiples of 4 floats, each lane issues 8 independent 16-byte loads (8 lanes
+// cover one 128-byte row segment, a warp instruction covers 4 rows) before the
+// first store, so a warp keeps 8 x 512 B of gathers in flight.
 __device__ __forceinline__ double warp_rows_sqdist(const float *__restrict__ base, int64_t stride, int off,
                                                    uint32_t slot_lane, bool valid, int len,
                                                    const double *q, double acc, float *tile)
 {
     const int lane = threadIdx.x & 31;
+    const bool vec = ((stride | off | len) & 3) == 0;
+    const int rs = lane >> 3, cq = lane & 7;
     for (int c0 = 0; c0 < len; c0 += 32) {
         const int cl = min(32, len - c0);
-        for (int r = 0; r < 32; r++) {
-            uint32_t s = __shfl_sync(0xffffffffu, slot_lane, r);
-            int v = __shfl_sync(0xffffffffu, (int)valid, r);
-            if (v && lane < cl) tile[r * 33 + lane] = __ldg(base + (int64_t)s * stride + off + c0 + lane);
+        if (vec) {
+            float4 v[8];
+#pragma unroll
+            for (int it = 0; it < 8; it++) {
+                const int r = it * 4 + rs;
+                const uint32_t s = __shfl_sync(0xffffffffu, slot_lane, r);
+                const int ok = __shfl_sync(0xffffffffu, (int)valid, r);
+                const int col = cq * 4;
+                v[it] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (ok && col < cl) v[it] = __ldg((const float4 *)(base + (int64_t)s * stride + off + c0 + col));
+            }
+#pragma unroll
+            for (int it = 0; it < 8; it++) {
+                float *t = tile + (it * 4 + rs) * 33 + cq * 4;
+                t[0] = v[it].x;
+                t[1] = v[it].y;
+                t[2] = v[it].z;
+                t[3] = v[it].w;
+            }
+        } else {
+            for (int r = 0; r < 32; r++) {
+                const uint32_t s = __shfl_sync(0xffffffffu, slot_lane, r);
+                const int ok = __shfl_sync(0xffffffffu, (int)valid, r);
+                if (ok && lane < cl) tile[r * 33 + lane] = __ldg(base + (int64_t)s * stride + off + c0 + lane);
+            }
         }
         __syncwarp();
         if (valid) {
@@ -182,3 +208,92 @@ __device__ __forceinline__ double warp_rows_sqdist(const float *__restrict__ bas
     }
     return acc;
 }
+
+// Warp-level streaming top-L (L smallest (key, id)) kept sorted in shared
+// memory a[0..L).  Every lane offers one item per call; the warp inserts the
+// survivors one by one (position = number of smaller entries, found with
+// ballots; entries shift up by one).  An item equal to an entry (same key and
+// id) is a duplicate and is dropped, so the list holds distinct items.
+struct WarpTop {
+    SelItem *a;
+    int L;
+
+    __device__ __forceinline__ void init(SelItem *buf, int L_)
+    {
+        a = buf;
+        L = L_;
+        const int lane = threadIdx.x & 31;
+        for (int j = lane; j < L; j += 32) a[j] = sel_inf();
+        __syncwarp();
+    }
+
+    __device__ __forceinline__ void offer(const SelItem &it, bool valid)
+    {
+        const int lane = threadIdx.x & 31;
+        unsigned m = __ballot_sync(0xffffffffu, valid && sel_less(it, a[L - 1]));
+        while (m) {
+            const int src = __ffs(m) - 1;
+            m &= m - 1;
+            SelItem x;
+            x.key = __shfl_sync(0xffffffffu, it.key, src);
+            x.id = __shfl_sync(0xffffffffu, it.id, src);
+            x.pay = __shfl_sync(0xffffffffu, it.pay, src);
+            if (!sel_less(x, a[L - 1])) continue;                 // warp-uniform
+            int pos = 0;
+            bool dup = false;
+            for (int j0 = 0; j0 < L; j0 += 32) {
+                const int j = j0 + lane;
+                const bool in = j < L;
+                const SelItem e = in ? a[j] : sel_inf();
+                pos += __popc(__ballot_sync(0xffffffffu, in && sel_less(e, x)));
+                dup |= __any_sync(0xffffffffu, in && e.key == x.key && e.id == x.id);
+            }
+            if (dup) continue;                                     // warp-uniform
+            for (int j0 = ((L - 1) / 32) * 32; j0 >= 0; j0 -= 32) {
+                const int j = j0 + lane;
+                const bool mv = j >= pos && j < L - 1;
+                SelItem v;
+                if (mv) v = a[j];
+                __syncwarp();
+                if (mv) a[j + 1] = v;
+                __syncwarp();
+            }
+            if (lane == 0) a[pos] = x;
+            __syncwarp();
+        }
+    }
+};
+
+// ================================================================ a4 / a5
+// The scan epilogue shared by the seed pass and the scan (Eq.4
+// with A-1; Eq.5 P:255 with A-2/A-6; Alg.2 L12 P:314):
+//   S = sum_b 2^b popc(code & p_b) = sum_{bit_j=1} L_j,  pop = popc(code)
+//   ip = ((A pop + Bc S) - C0) / sqrt(d)        = <x_hat, r_bar>
+//   dis' = (f1 + g1) - 2 (f2 ip)
+//   LB1 = (dis' - eb f3) - eps_r
+template <int W>
+__device__ __forceinline__ double mrq_lb1(const uint32_t *code, const uint32_t *pl, const double *qc, double isd,
+                                          double eps_r, float f1, float f2, float f3, double *dis_out)
+{
+    int pop = 0;
+#pragma unroll
+    for (int w = 0; w < W; w++) pop += __popc(code[w]);
+    int S = 0;
+#pragma unroll
+    for (int b = 0; b < MRQ_BQ; b++) {
+        int s = 0;
+#pragma unroll
+        for (int w = 0; w < W; w++) s += __popc(code[w] & pl[b * W + w]);
+        S += s << b;
+    }
+    const double t1 = qc[0] * (double)pop;
+    const double t2 = qc[1] * (double)S;
+    const double t4 = (t1 + t2) - qc[2];
+    const double ip = t4 * isd;
+    const double t5 = (double)f1 + qc[3];
+    const double t6 = (double)f2 * ip;
+    const double dis = t5 - 2.0 * t6;
+    *dis_out = dis;
+    return (dis - qc[4] * (double)f3) - eps_r;
+}
+

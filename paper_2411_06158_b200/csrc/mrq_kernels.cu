@@ -413,129 +413,6 @@ __global__ void k_exclusive_scan(const uint64_t *__restrict__ in, int64_t n, uin
     if (threadIdx.x == 0) out[n] = carry;
 }
 
-// ================================================================ a4 / a5
-// The scan epilogue shared by the seed pass and the scan (Eq.4
-// with A-1; Eq.5 P:255 with A-2/A-6; Alg.2 L12 P:314):
-//   S = sum_b 2^b popc(code & p_b) = sum_{bit_j=1} L_j,  pop = popc(code)
-//   ip = ((A pop + Bc S) - C0) / sqrt(d)        = <x_hat, r_bar>
-//   dis' = (f1 + g1) - 2 (f2 ip)
-//   LB1 = (dis' - eb f3) - eps_r
-template <int W>
-__device__ __forceinline__ double mrq_lb1(const uint32_t *code, const uint32_t *pl, const double *qc, double isd,
-                                          double eps_r, float f1, float f2, float f3, double *dis_out)
-{
-    int pop = 0;
-#pragma unroll
-    for (int w = 0; w < W; w++) pop += __popc(code[w]);
-    int S = 0;
-#pragma unroll
-    for (int b = 0; b < MRQ_BQ; b++) {
-        int s = 0;
-#pragma unroll
-        for (int w = 0; w < W; w++) s += __popc(code[w] & pl[b * W + w]);
-        S += s << b;
-    }
-    const double t1 = qc[0] * (double)pop;
-    const double t2 = qc[1] * (double)S;
-    const double t4 = (t1 + t2) - qc[2];
-    const double ip = t4 * isd;
-    const double t5 = (double)f1 + qc[3];
-    const double t6 = (double)f2 * ip;
-    const double dis = t5 - 2.0 * t6;
-    *dis_out = dis;
-    return (dis - qc[4] * (double)f3) - eps_r;
-}
-
-// Seeds S0 and tau0 (decision T of DESIGN.md, replacing "tau <- threshold of
-// the result queue", Alg.2 L9 P:311): the probed lists in probe order until
-// they hold >= K' candidates form the pool; S0 = the K' smallest (dis', id)
-// of the pool; their exact distances ||x_p - q_p||^2 (Alg.2 L14 P:316);
-// tau0 = K-th smallest exact over S0 (+inf if |S0| < K).  Block per query.
-template <int W>
-__global__ void __launch_bounds__(256) k_seed(
-    const uint32_t *__restrict__ probe, int np, int K, int Kp, int D, int d, int64_t npad,
-    const uint32_t *__restrict__ list_off, const uint32_t *__restrict__ list_size,
-    const uint32_t *__restrict__ ids, const uint32_t *__restrict__ codes, const float *__restrict__ f1,
-    const float *__restrict__ f2, const float *__restrict__ f3, const float *__restrict__ heads,
-    const float *__restrict__ tails, const uint32_t *__restrict__ planes, const double *__restrict__ qconst,
-    const double *__restrict__ qp, const double *__restrict__ eps_r_arr, double isd, int pool_cap, int S,
-    SelItem *__restrict__ pool, uint32_t *__restrict__ s0_cnt, uint32_t *__restrict__ s0_pos,
-    double *__restrict__ s0_exact, double *__restrict__ tau0)
-{
-    extern __shared__ unsigned char ssm[];
-    double *qs = (double *)ssm;                              // D
-    float *tiles = (float *)(qs + D);                        // 8 warps x 32 x 33
-    SelItem *buf = (SelItem *)(tiles + 8 * 32 * 33);         // S
-    __shared__ int sh_npool, sh_lists;
-    const int64_t q = blockIdx.x;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const double eps_r = eps_r_arr[q];
-    for (int i = threadIdx.x; i < D; i += blockDim.x) qs[i] = qp[q * D + i];
-    if (threadIdx.x == 0) {
-        int cum = 0, p = 0;
-        while (p < np && cum < Kp) {
-            uint32_t c = probe[q * np + p];
-            if (c != 0xFFFFFFFFu) cum += list_size[c];
-            p++;
-        }
-        sh_npool = cum;
-        sh_lists = p;
-    }
-    __syncthreads();
-    SelItem *qpool = pool + q * pool_cap;
-    // dis' of the pool, in probe order
-    int at = 0;
-    for (int p = 0; p < sh_lists; p++) {
-        const uint32_t c = probe[q * np + p];
-        if (c == 0xFFFFFFFFu) continue;
-        const uint32_t off = list_off[c], sz = list_size[c];
-        const uint32_t *pl = planes + (q * np + p) * (MRQ_BQ * W);
-        const double *qc = qconst + (q * np + p) * 8;
-        for (uint32_t e = threadIdx.x; e < sz; e += blockDim.x) {
-            const uint32_t slot = off + e;
-            uint32_t code[W];
-#pragma unroll
-            for (int w = 0; w < W; w++) code[w] = codes[(int64_t)w * npad + slot];
-            double dis;
-            mrq_lb1<W>(code, pl, qc, isd, eps_r, f1[slot], f2[slot], f3[slot], &dis);
-            SelItem s;
-            s.key = dis;
-            s.id = ids[slot];
-            s.pay = slot;
-            qpool[at + e] = s;
-        }
-        at += sz;
-    }
-    __syncthreads();
-    const int ns0 = block_select(buf, S, Kp, sh_npool, [&](int i) { return qpool[i]; });
-    // exact distances of S0: warp w handles entries w*32 .. (chunks of 32)
-    float *tile = tiles + warp * 32 * 33;
-    for (int e0 = warp * 32; e0 < ns0; e0 += 8 * 32) {
-        const int e = e0 + lane;
-        const bool valid = e < ns0;
-        const uint32_t slot = valid ? buf[e].pay : 0u;
-        double acc = warp_rows_sqdist(heads, d, 0, slot, valid, d, qs, 0.0, tile);
-        if (D > d) acc = warp_rows_sqdist(tails, D - d, 0, slot, valid, D - d, qs + d, acc, tile);
-        if (valid) {
-            s0_pos[q * Kp + e] = slot;
-            s0_exact[q * Kp + e] = acc;
-        }
-    }
-    __syncthreads();
-    // tau0 = K-th smallest exact over S0 (ids are distinct)
-    block_select(buf, S, K, ns0, [&](int i) {
-        SelItem s;
-        s.key = s0_exact[q * Kp + i];
-        s.id = ids[s0_pos[q * Kp + i]];
-        s.pay = i;
-        return s;
-    });
-    if (threadIdx.x == 0) {
-        s0_cnt[q] = ns0;
-        tau0[q] = ns0 >= K ? buf[K - 1].key : __longlong_as_double(0x7ff0000000000000ll);
-    }
-}
-
 // The code scan (hot loop of Alg.2 L7-L12): block per query, every
 // warp streams (list, 128-slot chunk) tiles of the query's probed lists.  Each
 // lane reads 4 consecutive slots with 128-bit loads: W code words (word-major
@@ -625,248 +502,7 @@ __global__ void __launch_bounds__(256) k_scan(
     if (threadIdx.x == 0) f1_cnt[q] = sh_cnt;
 }
 
-// ======================================================================= a6
-// Stage 2 (Alg.2 L13 P:315; "Optimization" P:327 read as A-7): for every F1
-// entry HEAD = ||x_d - q_d||^2 (left to right over i < d) and
-// dis_o' = (HEAD + ||x_r||^2) + ||q_r||^2.  TIGHT: S1 = the K' smallest
-// (dis_o', id) of F1, their exact distances (HEAD continued over the tail),
-// tau1 = K-th smallest distinct exact over S0 u S1; LOOSE: tau1 = tau0.
-// F2 = {e in F1 : dis_o' - eps_r < tau1} (FULL) or F1 (STAGE1_ONLY / EXACT).
-__global__ void __launch_bounds__(256) k_stage2(
-    int mode, int tight, int K, int Kp, int D, int d, const uint32_t *__restrict__ ids,
-    const float *__restrict__ heads, const float *__restrict__ tails, const float *__restrict__ xr2,
-    const double *__restrict__ qp, const double *__restrict__ qr2_arr, const double *__restrict__ eps_r_arr,
-    const double *__restrict__ tau0_arr, const uint64_t *__restrict__ f1_off, const uint32_t *__restrict__ f1_cnt,
-    const uint32_t *__restrict__ f1_pos, double *__restrict__ f1_head, double *__restrict__ f1_diso,
-    const uint32_t *__restrict__ s0_cnt, const uint32_t *__restrict__ s0_pos, const double *__restrict__ s0_exact,
-    uint32_t *__restrict__ s1_cnt, uint32_t *__restrict__ s1_pos, double *__restrict__ s1_exact, int S,
-    double *__restrict__ tau1_arr, uint32_t *__restrict__ f2_cnt, uint32_t *__restrict__ f2_pos,
-    double *__restrict__ f2_head)
-{
-    extern __shared__ unsigned char tsm[];
-    double *qs = (double *)tsm;                              // D
-    float *tiles = (float *)(qs + D);                        // 8 x 32 x 33
-    SelItem *buf = (SelItem *)(tiles + 8 * 32 * 33);         // S
-    __shared__ uint32_t sh_cnt;
-    __shared__ double sh_tau1;
-    __shared__ uint32_t sh_dups;
-    const int64_t q = blockIdx.x;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nwarps = blockDim.x >> 5;
-    for (int i = threadIdx.x; i < D; i += blockDim.x) qs[i] = qp[q * D + i];
-    if (threadIdx.x == 0) sh_cnt = 0;
-    __syncthreads();
-    const uint64_t base = f1_off[q];
-    const int n1 = (int)f1_cnt[q];
-    const double qr2 = qr2_arr[q], eps_r = eps_r_arr[q];
-    float *tile = tiles + warp * 32 * 33;
-    for (int e0 = warp * 32; e0 < n1; e0 += nwarps * 32) {
-        const int e = e0 + lane;
-        const bool valid = e < n1;
-        const uint32_t slot = valid ? f1_pos[base + e] : 0u;
-        const double head = warp_rows_sqdist(heads, d, 0, slot, valid, d, qs, 0.0, tile);
-        if (valid) {
-            f1_head[base + e] = head;
-            f1_diso[base + e] = (head + (double)xr2[slot]) + qr2;
-        }
-    }
-    __syncthreads();
-    double tau1 = tau0_arr[q];
-    if (mode == 0 && tight) {
-        const int ns1 = block_select(buf, S, Kp, n1, [&](int i) {
-            SelItem s;
-            s.key = f1_diso[base + i];
-            s.id = ids[f1_pos[base + i]];
-            s.pay = (uint32_t)i;
-            return s;
-        });
-        for (int e0 = warp * 32; e0 < ns1; e0 += nwarps * 32) {
-            const int e = e0 + lane;
-            const bool valid = e < ns1;
-            const uint32_t ent = valid ? buf[e].pay : 0u;
-            const uint32_t slot = valid ? f1_pos[base + ent] : 0u;
-            double acc = valid ? f1_head[base + ent] : 0.0;
-            if (D > d) acc = warp_rows_sqdist(tails, D - d, 0, slot, valid, D - d, qs + d, acc, tile);
-            if (valid) {
-                s1_pos[q * Kp + e] = slot;
-                s1_exact[q * Kp + e] = acc;
-            }
-        }
-        __syncthreads();
-        const int ns0 = (int)s0_cnt[q];
-        if (threadIdx.x == 0) sh_dups = 0;
-        __syncthreads();
-        for (int j = threadIdx.x; j < ns1; j += blockDim.x) {
-            const uint32_t sl = s1_pos[q * Kp + j];
-            bool dup = false;
-            for (int t = 0; t < ns0; t++) dup |= (s0_pos[q * Kp + t] == sl);
-            if (dup) atomicAdd(&sh_dups, 1u);
-        }
-        __syncthreads();
-        const int distinct = ns0 + ns1 - (int)sh_dups;
-        // K-th smallest distinct exact over S0 u S1 (S1 members already in S0 are skipped)
-        block_select(buf, S, K, ns0 + ns1, [&](int i) {
-            SelItem s;
-            if (i < ns0) {
-                s.key = s0_exact[q * Kp + i];
-                s.id = ids[s0_pos[q * Kp + i]];
-            } else {
-                const int j = i - ns0;
-                const uint32_t sl = s1_pos[q * Kp + j];
-                bool dup = false;
-                for (int t = 0; t < ns0; t++) dup |= (s0_pos[q * Kp + t] == sl);
-                s.key = dup ? __longlong_as_double(0x7ff0000000000000ll) : s1_exact[q * Kp + j];
-                s.id = dup ? 0xFFFFFFFFu : ids[sl];
-            }
-            s.pay = i;
-            return s;
-        });
-        if (threadIdx.x == 0) {
-            sh_tau1 = distinct >= K ? buf[K - 1].key : __longlong_as_double(0x7ff0000000000000ll);
-            s1_cnt[q] = ns1;
-        }
-        __syncthreads();
-        tau1 = sh_tau1;
-    } else if (threadIdx.x == 0) {
-        s1_cnt[q] = 0;
-    }
-    if (threadIdx.x == 0) tau1_arr[q] = tau1;
-    // F2
-    for (int e0 = 0; e0 < n1; e0 += blockDim.x) {
-        const int e = e0 + threadIdx.x;
-        bool pass = false;
-        if (e < n1) pass = (mode != 0) || (f1_diso[base + e] - eps_r < tau1);
-        const unsigned bal = __ballot_sync(0xffffffffu, pass);
-        uint32_t wb = 0;
-        if (lane == 0 && bal) wb = atomicAdd(&sh_cnt, (uint32_t)__popc(bal));
-        wb = __shfl_sync(0xffffffffu, wb, 0);
-        if (pass) {
-            const uint32_t at = wb + __popc(bal & ((1u << lane) - 1u));
-            f2_pos[base + at] = f1_pos[base + e];
-            f2_head[base + at] = f1_head[base + e];
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) f2_cnt[q] = sh_cnt;
-}
-
-// ======================================================================= a7
-// Exact re-rank of F2 (Alg.2 L14 P:316): exact = HEAD continued over the
-// tail, i.e. ||x_p - q_p||^2 left to right over i = 0..D-1 (A-8).
-__global__ void __launch_bounds__(256) k_rerank(int D, int d, const float *__restrict__ tails,
-                                                const double *__restrict__ qp, const uint64_t *__restrict__ f1_off,
-                                                const uint32_t *__restrict__ f2_cnt, const uint32_t *__restrict__ f2_pos,
-                                                const double *__restrict__ f2_head, double *__restrict__ f2_exact)
-{
-    extern __shared__ unsigned char rsm[];
-    double *qs = (double *)rsm;                              // D - d
-    float *tiles = (float *)(qs + (D - d > 0 ? D - d : 1));  // 8 x 32 x 33
-    const int64_t q = blockIdx.x;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-    for (int i = threadIdx.x; i < D - d; i += blockDim.x) qs[i] = qp[q * D + d + i];
-    __syncthreads();
-    const uint64_t base = f1_off[q];
-    const int n2 = (int)f2_cnt[q];
-    float *tile = tiles + warp * 32 * 33;
-    for (int e0 = warp * 32; e0 < n2; e0 += nwarps * 32) {
-        const int e = e0 + lane;
-        const bool valid = e < n2;
-        const uint32_t slot = valid ? f2_pos[base + e] : 0u;
-        double acc = valid ? f2_head[base + e] : 0.0;
-        if (D > d) acc = warp_rows_sqdist(tails, D - d, 0, slot, valid, D - d, qs, acc, tile);
-        if (valid) f2_exact[base + e] = acc;
-    }
-}
-
-// ======================================================================= a8
-// Per-query top-K (Alg.2 L15-L16): the K smallest (exact, id) over
-// the distinct union S0 u S1 u F2; ids returned as the original int64 index,
-// distances rounded to fp32; padding id -1 / +inf.
-__global__ void __launch_bounds__(256) k_topk(int K, int Kp, const uint32_t *__restrict__ ids,
-                                              const uint32_t *__restrict__ s0_cnt, const uint32_t *__restrict__ s0_pos,
-                                              const double *__restrict__ s0_exact, const uint32_t *__restrict__ s1_cnt,
-                                              const uint32_t *__restrict__ s1_pos, const double *__restrict__ s1_exact,
-                                              const uint64_t *__restrict__ f1_off, const uint32_t *__restrict__ f2_cnt,
-                                              const uint32_t *__restrict__ f2_pos, const double *__restrict__ f2_exact,
-                                              int S, int64_t *__restrict__ out_ids, float *__restrict__ out_dist,
-                                              uint32_t *__restrict__ exact_cnt)
-{
-    extern __shared__ unsigned char ksm[];
-    uint32_t *sel = (uint32_t *)ksm;                         // 2 Kp slots of S0 u S1
-    SelItem *buf = (SelItem *)(((uintptr_t)(sel + 2 * Kp) + 15) & ~(uintptr_t)15);
-    __shared__ uint32_t sh_dup;
-    const int64_t q = blockIdx.x;
-    const int ns0 = (int)s0_cnt[q], ns1 = (int)s1_cnt[q], n2 = (int)f2_cnt[q];
-    const uint64_t base = f1_off[q];
-    for (int i = threadIdx.x; i < ns0; i += blockDim.x) sel[i] = s0_pos[q * Kp + i];
-    for (int i = threadIdx.x; i < ns1; i += blockDim.x) sel[ns0 + i] = s1_pos[q * Kp + i];
-    if (threadIdx.x == 0) sh_dup = 0;
-    __syncthreads();
-    const int nsel = ns0 + ns1;
-    auto member = [&](uint32_t slot, int upto) {
-        for (int t = 0; t < upto; t++)
-            if (sel[t] == slot) return true;
-        return false;
-    };
-    const int n = nsel + n2;
-    block_select(buf, S, K, n, [&](int i) {
-        SelItem s;
-        bool dup;
-        uint32_t slot;
-        double key;
-        if (i < ns0) {
-            slot = sel[i];
-            key = s0_exact[q * Kp + i];
-            dup = false;
-        } else if (i < nsel) {
-            slot = sel[i];
-            key = s1_exact[q * Kp + (i - ns0)];
-            dup = member(slot, ns0);
-        } else {
-            slot = f2_pos[base + (i - nsel)];
-            key = f2_exact[base + (i - nsel)];
-            dup = member(slot, nsel);
-        }
-        if (dup) {
-            atomicAdd(&sh_dup, 1u);
-            return sel_inf();
-        }
-        s.key = key;
-        s.id = ids[slot];
-        s.pay = slot;
-        return s;
-    });
-    for (int i = threadIdx.x; i < K; i += blockDim.x) {
-        const bool ok = buf[i].id != 0xFFFFFFFFu;
-        out_ids[q * K + i] = ok ? (int64_t)buf[i].id : (int64_t)-1;
-        out_dist[q * K + i] = ok ? (float)buf[i].key : __int_as_float(0x7f800000);
-    }
-    if (threadIdx.x == 0) exact_cnt[q] = (uint32_t)n - sh_dup;
-}
-
 // ================================================================ launchers
-template <int W>
-static void launch_seed_w(const LaunchSeed &a, cudaStream_t st)
-{
-    k_seed<W><<<a.nq, 256, a.smem, st>>>(a.probe, a.np, a.K, a.Kp, a.D, a.d, a.npad, a.list_off, a.list_size, a.ids,
-                                          a.codes, a.f1, a.f2, a.f3, a.heads, a.tails, a.planes, a.qconst, a.qp,
-                                          a.eps_r, a.isd, a.pool_cap, a.S, a.pool, a.s0_cnt, a.s0_pos, a.s0_exact,
-                                          a.tau0);
-}
-
-void launch_seed(int W, const LaunchSeed &a, cudaStream_t st)
-{
-    switch (W) {
-    case 1: launch_seed_w<1>(a, st); break;
-    case 2: launch_seed_w<2>(a, st); break;
-    case 3: launch_seed_w<3>(a, st); break;
-    case 4: launch_seed_w<4>(a, st); break;
-    case 8: launch_seed_w<8>(a, st); break;
-    case 16: launch_seed_w<16>(a, st); break;
-    default: break;
-    }
-}
-
 template <int W>
 static void launch_scan_w(const LaunchScan &a, cudaStream_t st)
 {
@@ -888,26 +524,6 @@ void launch_scan(int W, const LaunchScan &a, cudaStream_t st)
 }
 
 bool supported_W(int W) { return W == 1 || W == 2 || W == 3 || W == 4 || W == 8 || W == 16; }
-
-int mrq_seed_smem_attr(int W, size_t bytes)
-{
-    if (bytes <= 48 * 1024) return MRQ_OK;
-    cudaError_t e = cudaSuccess;
-    switch (W) {
-    case 1: e = cudaFuncSetAttribute(k_seed<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes); break;
-    case 2: e = cudaFuncSetAttribute(k_seed<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes); break;
-    case 3: e = cudaFuncSetAttribute(k_seed<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes); break;
-    case 4: e = cudaFuncSetAttribute(k_seed<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes); break;
-    case 8: e = cudaFuncSetAttribute(k_seed<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes); break;
-    case 16: e = cudaFuncSetAttribute(k_seed<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes); break;
-    default: break;
-    }
-    if (e != cudaSuccess) {
-        mrq_set_error("cudaFuncSetAttribute(k_seed): %s", cudaGetErrorString(e));
-        return MRQ_ECUDA;
-    }
-    return MRQ_OK;
-}
 
 // Test hook (mrq_debug_set "dump_dis"): dis' and LB1 of every scanned
 // candidate, in probe order then slot order -- the oracle's scan order --

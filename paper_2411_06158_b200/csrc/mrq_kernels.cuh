@@ -20,37 +20,25 @@ __global__ void k_quant(const uint32_t *probe, const double *probe_qn2, int64_t 
                         double *qconst);
 __global__ void k_cand_count(const uint32_t *probe, int64_t nq, int np, const uint32_t *list_size, uint64_t *cnt);
 __global__ void k_exclusive_scan(const uint64_t *in, int64_t n, uint64_t *out);
-__global__ void k_stage2(int mode, int tight, int K, int Kp, int D, int d, const uint32_t *ids, const float *heads,
-                         const float *tails, const float *xr2, const double *qp, const double *qr2_arr,
-                         const double *eps_r_arr, const double *tau0_arr, const uint64_t *f1_off,
-                         const uint32_t *f1_cnt, const uint32_t *f1_pos, double *f1_head, double *f1_diso,
-                         const uint32_t *s0_cnt, const uint32_t *s0_pos, const double *s0_exact, uint32_t *s1_cnt,
-                         uint32_t *s1_pos, double *s1_exact, int S, double *tau1_arr, uint32_t *f2_cnt,
-                         uint32_t *f2_pos, double *f2_head);
-__global__ void k_rerank(int D, int d, const float *tails, const double *qp, const uint64_t *f1_off,
-                         const uint32_t *f2_cnt, const uint32_t *f2_pos, const double *f2_head, double *f2_exact);
-__global__ void k_topk(int K, int Kp, const uint32_t *ids, const uint32_t *s0_cnt, const uint32_t *s0_pos,
-                       const double *s0_exact, const uint32_t *s1_cnt, const uint32_t *s1_pos,
-                       const double *s1_exact, const uint64_t *f1_off, const uint32_t *f2_cnt,
-                       const uint32_t *f2_pos, const double *f2_exact, int S, int64_t *out_ids, float *out_dist,
-                       uint32_t *exact_cnt);
-
-struct LaunchSeed {
+struct StageArgs {
     int64_t nq;
-    size_t smem;
-    const uint32_t *probe;
-    int np, K, Kp, D, d;
+    int np, K, Kp, D, d, mode, tight;
     int64_t npad;
-    const uint32_t *list_off, *list_size, *ids, *codes;
-    const float *f1, *f2, *f3, *heads, *tails;
-    const uint32_t *planes;
-    const double *qconst, *qp, *eps_r;
     double isd;
-    int pool_cap, S;
-    SelItem *pool;
-    uint32_t *s0_cnt, *s0_pos;
-    double *s0_exact, *tau0;
+    const uint32_t *probe, *list_off, *list_size, *ids, *codes, *planes;
+    const float *f1, *f2, *f3, *heads, *tails, *xr2;
+    const double *qconst, *qp, *qr2, *eps_r;
+    uint32_t *s0_cnt, *s0_pos, *s1_cnt, *s1_pos, *f1_cnt, *f1_pos, *f2_cnt, *f2_pos, *exact_cnt;
+    double *s0_exact, *s1_exact, *tau0, *tau1, *f1_head, *f1_diso, *f2_head, *f2_exact;
+    const uint64_t *f1_off;
+    int64_t *out_ids;
+    float *out_dist;
 };
+
+int launch_seed_w(int W, const StageArgs &a, cudaStream_t st);
+int launch_stage2_w(const StageArgs &a, cudaStream_t st);
+int launch_rerank_w(const StageArgs &a, cudaStream_t st);
+int launch_topk_w(const StageArgs &a, cudaStream_t st);
 
 struct LaunchScan {
     int64_t nq;
@@ -67,7 +55,6 @@ struct LaunchScan {
     uint32_t *f1_cnt, *f1_pos;
 };
 
-void launch_seed(int W, const LaunchSeed &a, cudaStream_t st);
 void launch_scan(int W, const LaunchScan &a, cudaStream_t st);
 bool supported_W(int W);
 void launch_scan_dbg(int W, const LaunchScan &a, double *dis, double *lb1, cudaStream_t st);
