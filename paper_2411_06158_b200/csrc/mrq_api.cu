@@ -446,12 +446,11 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
             k_probe_approx<<<grid, 256, 8 * d * sizeof(float), st>>>(qd32, nq, d, k, ix->C32T, approx);
             kappa = std::ldexp(1.0, -24) * (2.0 * d + 8.0);
         }
-        const int cap = std::min(k, std::max(4 * np + 256, 1024));
-        const int S = pow2_at_least(np + 256);
-        const size_t smem = (size_t)k * 4 + (size_t)cap * 4 + 16 + (size_t)d * 8 + (size_t)S * sizeof(SelItem);
-        TRY(set_smem((const void *)k_probe_select, smem));
-        k_probe_select<<<(unsigned)nq, 256, smem, st>>>(approx, nq, k, d, np, qp, D, ix->C, qnorm, ix->cmax, kappa,
-                                                        cap, S, probe, probe_qn2, fallback);
+        uint32_t *cand, *ncand;
+        SCR("probe_cand", uint32_t, nq * k, cand);
+        SCR("probe_ncand", uint32_t, nq, ncand);
+        TRY(launch_probe_select_w(approx, nq, k, d, np, qp, D, ix->C, qnorm, ix->cmax, kappa, cand, probe, probe_qn2,
+                                  ncand, st));
     }
     if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[2], st));
 
@@ -480,6 +479,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
     StageArgs sa;
     memset(&sa, 0, sizeof sa);
     sa.nq = nq; sa.np = np; sa.K = K; sa.Kp = Kp; sa.D = D; sa.d = d; sa.mode = mode; sa.tight = tight;
+    sa.aligned = (D % 4 == 0) && (d % 4 == 0);
     sa.npad = ix->npad; sa.isd = isd; sa.probe = probe; sa.list_off = ix->list_off; sa.list_size = ix->list_size;
     sa.ids = ix->ids; sa.codes = ix->codes; sa.planes = planes; sa.f1 = ix->f1; sa.f2 = ix->f2; sa.f3 = ix->f3;
     sa.heads = ix->heads; sa.tails = ix->tails; sa.xr2 = ix->xr2; sa.qconst = qconst; sa.qp = qp; sa.qr2 = qr2;
@@ -682,7 +682,7 @@ extern "C" int mrq_debug_fetch(mrq_index *ix, const char *name, void *dst, size_
             {"f1_pos", (size_t)ix->last_total * 4}, {"f1_head", (size_t)ix->last_total * 8},
             {"f1_diso", (size_t)ix->last_total * 8}, {"f2_pos", (size_t)ix->last_total * 4},
             {"f2_head", (size_t)ix->last_total * 8}, {"f2_exact", (size_t)ix->last_total * 8},
-            {"fallback", 4}, {"approx", (size_t)nq * k * 4},
+            {"fallback", 4}, {"approx", (size_t)nq * k * 4}, {"probe_ncand", (size_t)nq * 4},
             {"dbg_dis", (size_t)ix->last_total * 8}, {"dbg_lb1", (size_t)ix->last_total * 8},
         };
         for (auto &e : per)

@@ -297,3 +297,110 @@ __device__ __forceinline__ double mrq_lb1(const uint32_t *code, const uint32_t *
     return (dis - qc[4] * (double)f3) - eps_r;
 }
 
+
+// -------------------------------------------------------------------------
+// Pipelined warp row gather (cp.async, double-buffered).  A warp processes
+// entries 0..n-1 in groups of 32 (lane = entry within the group); for each
+// group it streams the columns [off, off + len) of every lane's row through
+// shared memory in chunks of up to CH floats, while the next (group, chunk)
+// job's 16-byte cp.async copies are already in flight.  Each lane sums its
+// own row left to right in fp64:  acc = init(e); acc += ((double)x - q)^2 ...
+// then done(e, valid, acc) is called by the whole warp.
+// Requirements: row stride, off and len multiples of 4 floats (16-B copies).
+#define MRQ_RG_CH 64
+#define MRQ_RG_STRIDE (MRQ_RG_CH + 4)          // = 4 (mod 8): conflict-free 16-B row reads
+#define MRQ_RG_FLOATS (2 * 32 * MRQ_RG_STRIDE)  // per-warp smem (floats)
+
+__device__ __forceinline__ void cp_async16(void *smem_dst, const void *gmem_src)
+{
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+template <class SlotOf, class Init, class Done>
+__device__ __forceinline__ void warp_gather_rows(const float *__restrict__ base, int64_t stride, int off, int len,
+                                                 const double *__restrict__ q, int n, float *sbuf, SlotOf slot_of,
+                                                 Init init, Done done)
+{
+    const int lane = threadIdx.x & 31;
+    const int nchunk = (len + MRQ_RG_CH - 1) / MRQ_RG_CH;
+    const int ngroup = (n + 31) / 32;
+    const int njobs = ngroup * nchunk;
+    if (njobs == 0) return;
+    auto issue = [&](int job) {
+        const int g = job / nchunk, c = job % nchunk;
+        const int e = g * 32 + lane;
+        const bool v = e < n;
+        const uint32_t slot = v ? slot_of(e) : 0u;
+        const int c0 = c * MRQ_RG_CH;
+        const int nu = (min(MRQ_RG_CH, len - c0)) >> 2;       // 16-B units per row segment
+        float *dst = sbuf + (job & 1) * (32 * MRQ_RG_STRIDE);
+        for (int j = lane; j < 32 * nu; j += 32) {
+            const int r = j / nu, u = j - r * nu;
+            const uint32_t s = __shfl_sync(0xffffffffu, slot, r);
+            const int ok = __shfl_sync(0xffffffffu, (int)v, r);
+            if (ok) cp_async16(dst + r * MRQ_RG_STRIDE + 4 * u, base + (int64_t)s * stride + off + c0 + 4 * u);
+        }
+        cp_async_commit();
+    };
+    issue(0);
+    double acc = 0.0;
+    for (int job = 0; job < njobs; job++) {
+        if (job + 1 < njobs) {
+            issue(job + 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncwarp();
+        const int g = job / nchunk, c = job % nchunk;
+        const int e = g * 32 + lane;
+        const bool v = e < n;
+        if (c == 0) acc = v ? init(e) : 0.0;
+        const int c0 = c * MRQ_RG_CH;
+        const int cl = min(MRQ_RG_CH, len - c0);
+        const float *row = sbuf + (job & 1) * (32 * MRQ_RG_STRIDE) + lane * MRQ_RG_STRIDE;
+        const double *qq = q + c0;
+        if (v) {
+            for (int u = 0; u < cl; u += 4) {
+                const float4 x = *(const float4 *)(row + u);
+                const double2 qa = *(const double2 *)(qq + u);
+                const double2 qb = *(const double2 *)(qq + u + 2);
+                const double t0 = (double)x.x - qa.x, t1 = (double)x.y - qa.y;
+                const double t2 = (double)x.z - qb.x, t3 = (double)x.w - qb.y;
+                const double s0 = t0 * t0, s1 = t1 * t1, s2 = t2 * t2, s3 = t3 * t3;
+                acc = acc + s0;
+                acc = acc + s1;
+                acc = acc + s2;
+                acc = acc + s3;
+            }
+        }
+        __syncwarp();
+        if (c == nchunk - 1) done(e, v, acc);
+    }
+}
+
+// Row gather dispatcher: the pipelined cp.async path when the shapes allow
+// 16-byte copies, else the register-staged path (same arithmetic, same order).
+template <class SlotOf, class Init, class Done>
+__device__ __forceinline__ void warp_rows(bool aligned, const float *__restrict__ base, int64_t stride, int off,
+                                          int len, const double *__restrict__ q, int n, float *sbuf, SlotOf slot_of,
+                                          Init init, Done done)
+{
+    if (aligned) {
+        warp_gather_rows(base, stride, off, len, q, n, sbuf, slot_of, init, done);
+        return;
+    }
+    const int lane = threadIdx.x & 31;
+    for (int g = 0; g < n; g += 32) {
+        const int e = g + lane;
+        const bool v = e < n;
+        const uint32_t slot = v ? slot_of(e) : 0u;
+        double acc = v ? init(e) : 0.0;
+        acc = warp_rows_sqdist(base, stride, off, slot, v, len, q, acc, sbuf);
+        done(e, v, acc);
+    }
+}

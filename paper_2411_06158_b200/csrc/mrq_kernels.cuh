@@ -22,7 +22,7 @@ __global__ void k_cand_count(const uint32_t *probe, int64_t nq, int np, const ui
 __global__ void k_exclusive_scan(const uint64_t *in, int64_t n, uint64_t *out);
 struct StageArgs {
     int64_t nq;
-    int np, K, Kp, D, d, mode, tight;
+    int np, K, Kp, D, d, mode, tight, aligned;
     int64_t npad;
     double isd;
     const uint32_t *probe, *list_off, *list_size, *ids, *codes, *planes;
@@ -58,3 +58,6 @@ struct LaunchScan {
 void launch_scan(int W, const LaunchScan &a, cudaStream_t st);
 bool supported_W(int W);
 void launch_scan_dbg(int W, const LaunchScan &a, double *dis, double *lb1, cudaStream_t st);
+int launch_probe_select_w(const float *approx, int64_t nq, int k, int d, int np, const double *qp, int D,
+                          const double *C, const double *qnorm, double cmax, double kappa, uint32_t *cand,
+                          uint32_t *probe, double *probe_qn2, uint32_t *ncand, cudaStream_t st);

@@ -15,7 +15,7 @@
 // smallest exact over S0 (+inf if |S0| < K).
 template <int W>
 __global__ void __launch_bounds__(256) k_seed_w(
-    int64_t nq, const uint32_t *__restrict__ probe, int np, int K, int Kp, int D, int d, int64_t npad,
+    int64_t nq, int aligned, const uint32_t *__restrict__ probe, int np, int K, int Kp, int D, int d, int64_t npad,
     const uint32_t *__restrict__ list_off, const uint32_t *__restrict__ list_size, const uint32_t *__restrict__ ids,
     const uint32_t *__restrict__ codes, const float *__restrict__ f1, const float *__restrict__ f2,
     const float *__restrict__ f3, const float *__restrict__ heads, const float *__restrict__ tails,
@@ -27,8 +27,8 @@ __global__ void __launch_bounds__(256) k_seed_w(
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
     const int64_t q = (int64_t)blockIdx.x * wpb + warp;
     if (q >= nq) return;
-    float *tile = (float *)wsm + warp * (32 * 33);
-    SelItem *lst = (SelItem *)((float *)wsm + wpb * (32 * 33)) + (size_t)warp * Kp;
+    float *tile = (float *)wsm + warp * MRQ_RG_FLOATS;
+    SelItem *lst = (SelItem *)((float *)wsm + wpb * MRQ_RG_FLOATS) + (size_t)warp * Kp;
     WarpTop top;
     top.init(lst, Kp);
     const double eps_r = eps_r_arr[q];
@@ -60,18 +60,20 @@ __global__ void __launch_bounds__(256) k_seed_w(
         npool += sz;
     }
     const int ns0 = npool < Kp ? npool : Kp;
-    // exact distances of S0 (groups of 32)
-    for (int g = 0; g < ns0; g += 32) {
-        const int e = g + lane;
-        const bool v = e < ns0;
-        const uint32_t slot = v ? lst[e].pay : 0u;
-        double acc = warp_rows_sqdist(heads, d, 0, slot, v, d, qrow, 0.0, tile);
-        if (D > d) acc = warp_rows_sqdist(tails, D - d, 0, slot, v, D - d, qrow + d, acc, tile);
-        if (v) {
-            s0_pos[q * Kp + e] = slot;
-            s0_exact[q * Kp + e] = acc;
-        }
-    }
+    // exact distances of S0: HEAD over the head rows, then continued over the tail rows
+    warp_rows(aligned, heads, d, 0, d, qrow, ns0, tile, [&](int e) { return lst[e].pay; },
+              [&](int) { return 0.0; }, [&](int e, bool v, double acc) {
+                  if (v) {
+                      s0_pos[q * Kp + e] = lst[e].pay;
+                      s0_exact[q * Kp + e] = acc;
+                  }
+              });
+    __syncwarp();
+    if (D > d)
+        warp_rows(aligned, tails, D - d, 0, D - d, qrow + d, ns0, tile, [&](int e) { return s0_pos[q * Kp + e]; },
+                  [&](int e) { return s0_exact[q * Kp + e]; }, [&](int e, bool v, double acc) {
+                      if (v) s0_exact[q * Kp + e] = acc;
+                  });
     __syncwarp();
     // tau0 = K-th smallest exact over S0
     top.init(lst, K);
@@ -100,7 +102,7 @@ __global__ void __launch_bounds__(256) k_seed_w(
 // tau1 = K-th smallest distinct exact over S0 u S1; LOOSE: tau1 = tau0.
 // F2 = {e in F1 : dis_o' - eps_r < tau1} (FULL), F1 (STAGE1_ONLY / EXACT).
 __global__ void __launch_bounds__(256) k_stage2_w(
-    int64_t nq, int mode, int tight, int K, int Kp, int D, int d, const uint32_t *__restrict__ ids,
+    int64_t nq, int aligned, int mode, int tight, int K, int Kp, int D, int d, const uint32_t *__restrict__ ids,
     const float *__restrict__ heads, const float *__restrict__ tails, const float *__restrict__ xr2,
     const double *__restrict__ qp, const double *__restrict__ qr2_arr, const double *__restrict__ eps_r_arr,
     const double *__restrict__ tau0_arr, const uint64_t *__restrict__ f1_off, const uint32_t *__restrict__ f1_cnt,
@@ -114,8 +116,8 @@ __global__ void __launch_bounds__(256) k_stage2_w(
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
     const int64_t q = (int64_t)blockIdx.x * wpb + warp;
     if (q >= nq) return;
-    float *tile = (float *)wsm + warp * (32 * 33);
-    SelItem *lst = (SelItem *)((float *)wsm + wpb * (32 * 33)) + (size_t)warp * Kp;
+    float *tile = (float *)wsm + warp * MRQ_RG_FLOATS;
+    SelItem *lst = (SelItem *)((float *)wsm + wpb * MRQ_RG_FLOATS) + (size_t)warp * Kp;
     const bool sel1 = mode == 0 && tight;
     WarpTop top;
     top.init(lst, Kp);
@@ -123,38 +125,35 @@ __global__ void __launch_bounds__(256) k_stage2_w(
     const int n1 = (int)f1_cnt[q];
     const double qr2 = qr2_arr[q], eps_r = eps_r_arr[q];
     const double *qrow = qp + q * D;
-    for (int g = 0; g < n1; g += 32) {
-        const int e = g + lane;
-        const bool v = e < n1;
-        const uint32_t slot = v ? f1_pos[base + e] : 0u;
-        const double head = warp_rows_sqdist(heads, d, 0, slot, v, d, qrow, 0.0, tile);
-        SelItem it = sel_inf();
-        if (v) {
-            const double diso = (head + (double)xr2[slot]) + qr2;
-            f1_head[base + e] = head;
-            f1_diso[base + e] = diso;
-            it.key = diso;
-            it.id = ids[slot];
-            it.pay = (uint32_t)e;
-        }
-        if (sel1) top.offer(it, v);
-    }
+    warp_rows(aligned, heads, d, 0, d, qrow, n1, tile, [&](int e) { return f1_pos[base + e]; },
+              [&](int) { return 0.0; }, [&](int e, bool v, double head) {
+                  SelItem it = sel_inf();
+                  if (v) {
+                      const uint32_t slot = f1_pos[base + e];
+                      const double diso = (head + (double)xr2[slot]) + qr2;
+                      f1_head[base + e] = head;
+                      f1_diso[base + e] = diso;
+                      it.key = diso;
+                      it.id = ids[slot];
+                      it.pay = (uint32_t)e;
+                  }
+                  if (sel1) top.offer(it, v);
+              });
     __syncwarp();
     double tau1 = tau0_arr[q];
     if (sel1) {
         const int ns1 = n1 < Kp ? n1 : Kp;
-        for (int g = 0; g < ns1; g += 32) {
-            const int e = g + lane;
-            const bool v = e < ns1;
-            const uint32_t ent = v ? lst[e].pay : 0u;
-            const uint32_t slot = v ? f1_pos[base + ent] : 0u;
-            double acc = v ? f1_head[base + ent] : 0.0;
-            if (D > d) acc = warp_rows_sqdist(tails, D - d, 0, slot, v, D - d, qrow + d, acc, tile);
-            if (v) {
-                s1_pos[q * Kp + e] = slot;
-                s1_exact[q * Kp + e] = acc;
-            }
-        }
+        for (int e = lane; e < ns1; e += 32) s1_pos[q * Kp + e] = f1_pos[base + lst[e].pay];
+        __syncwarp();
+        auto s1_init = [&](int e) { return f1_head[base + lst[e].pay]; };
+        auto s1_done = [&](int e, bool v, double acc) {
+            if (v) s1_exact[q * Kp + e] = acc;
+        };
+        if (D > d)
+            warp_rows(aligned, tails, D - d, 0, D - d, qrow + d, ns1, tile, [&](int e) { return s1_pos[q * Kp + e]; },
+                      s1_init, s1_done);
+        else
+            for (int e = lane; e < ns1; e += 32) s1_exact[q * Kp + e] = s1_init(e);
         __syncwarp();
         // tau1 = K-th smallest distinct exact over S0 u S1 (duplicates dropped by WarpTop)
         top.init(lst, K);
@@ -198,7 +197,7 @@ __global__ void __launch_bounds__(256) k_stage2_w(
 // ----------------------------------------------------------------------- a7
 // Exact re-rank of F2 (Alg.2 L14 P:316): exact = HEAD continued over the
 // tail = ||x_p - q_p||^2 left to right over i = 0..D-1 (A-8).
-__global__ void __launch_bounds__(256) k_rerank_w(int64_t nq, int D, int d, const float *__restrict__ tails,
+__global__ void __launch_bounds__(256) k_rerank_w(int64_t nq, int aligned, int D, int d, const float *__restrict__ tails,
                                                   const double *__restrict__ qp, const uint64_t *__restrict__ f1_off,
                                                   const uint32_t *__restrict__ f2_cnt,
                                                   const uint32_t *__restrict__ f2_pos,
@@ -208,18 +207,17 @@ __global__ void __launch_bounds__(256) k_rerank_w(int64_t nq, int D, int d, cons
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
     const int64_t q = (int64_t)blockIdx.x * wpb + warp;
     if (q >= nq) return;
-    float *tile = (float *)wsm + warp * (32 * 33);
+    float *tile = (float *)wsm + warp * MRQ_RG_FLOATS;
     const uint64_t base = f1_off[q];
     const int n2 = (int)f2_cnt[q];
     const double *qt = qp + q * D + d;
-    for (int g = 0; g < n2; g += 32) {
-        const int e = g + lane;
-        const bool v = e < n2;
-        const uint32_t slot = v ? f2_pos[base + e] : 0u;
-        double acc = v ? f2_head[base + e] : 0.0;
-        if (D > d) acc = warp_rows_sqdist(tails, D - d, 0, slot, v, D - d, qt, acc, tile);
-        if (v) f2_exact[base + e] = acc;
-    }
+    if (D > d)
+        warp_rows(aligned, tails, D - d, 0, D - d, qt, n2, tile, [&](int e) { return f2_pos[base + e]; },
+                  [&](int e) { return f2_head[base + e]; }, [&](int e, bool v, double acc) {
+                      if (v) f2_exact[base + e] = acc;
+                  });
+    else
+        for (int e = lane; e < n2; e += 32) f2_exact[base + e] = f2_head[base + e];
 }
 
 // ----------------------------------------------------------------------- a8
@@ -293,8 +291,8 @@ __global__ void __launch_bounds__(256) k_topk_w(
 // ---------------------------------------------------------------- launchers
 static int warps_for(size_t per_warp)
 {
-    int w = 8;
-    while (w > 1 && per_warp * w > 160 * 1024) w >>= 1;
+    int w = 4;
+    while (w > 1 && per_warp * w > 100 * 1024) w >>= 1;
     return w;
 }
 
@@ -312,7 +310,7 @@ static int set_attr(const void *fn, size_t smem)
 
 int launch_seed_w(int W, const StageArgs &a, cudaStream_t st)
 {
-    const size_t per = 32 * 33 * 4 + (size_t)a.Kp * sizeof(SelItem);
+    const size_t per = MRQ_RG_FLOATS * 4 + (size_t)a.Kp * sizeof(SelItem);
     const int wpb = warps_for(per);
     const size_t smem = per * wpb;
     const unsigned grid = (unsigned)((a.nq + wpb - 1) / wpb);
@@ -320,7 +318,7 @@ int launch_seed_w(int W, const StageArgs &a, cudaStream_t st)
     do {                                                                                                            \
         int rc = set_attr((const void *)k_seed_w<WW>, smem);                                                        \
         if (rc) return rc;                                                                                          \
-        k_seed_w<WW><<<grid, wpb * 32, smem, st>>>(a.nq, a.probe, a.np, a.K, a.Kp, a.D, a.d, a.npad, a.list_off,   \
+        k_seed_w<WW><<<grid, wpb * 32, smem, st>>>(a.nq, a.aligned, a.probe, a.np, a.K, a.Kp, a.D, a.d, a.npad, a.list_off,   \
                                                    a.list_size, a.ids, a.codes, a.f1, a.f2, a.f3, a.heads, a.tails, \
                                                    a.planes, a.qconst, a.qp, a.eps_r, a.isd, a.s0_cnt, a.s0_pos,    \
                                                    a.s0_exact, a.tau0);                                             \
@@ -340,13 +338,13 @@ int launch_seed_w(int W, const StageArgs &a, cudaStream_t st)
 
 int launch_stage2_w(const StageArgs &a, cudaStream_t st)
 {
-    const size_t per = 32 * 33 * 4 + (size_t)a.Kp * sizeof(SelItem);
+    const size_t per = MRQ_RG_FLOATS * 4 + (size_t)a.Kp * sizeof(SelItem);
     const int wpb = warps_for(per);
     const size_t smem = per * wpb;
     int rc = set_attr((const void *)k_stage2_w, smem);
     if (rc) return rc;
     k_stage2_w<<<(unsigned)((a.nq + wpb - 1) / wpb), wpb * 32, smem, st>>>(
-        a.nq, a.mode, a.tight, a.K, a.Kp, a.D, a.d, a.ids, a.heads, a.tails, a.xr2, a.qp, a.qr2, a.eps_r, a.tau0,
+        a.nq, a.aligned, a.mode, a.tight, a.K, a.Kp, a.D, a.d, a.ids, a.heads, a.tails, a.xr2, a.qp, a.qr2, a.eps_r, a.tau0,
         a.f1_off, a.f1_cnt, a.f1_pos, a.f1_head, a.f1_diso, a.s0_cnt, a.s0_pos, a.s0_exact, a.s1_cnt, a.s1_pos,
         a.s1_exact, a.tau1, a.f2_cnt, a.f2_pos, a.f2_head);
     return MRQ_OK;
@@ -354,9 +352,11 @@ int launch_stage2_w(const StageArgs &a, cudaStream_t st)
 
 int launch_rerank_w(const StageArgs &a, cudaStream_t st)
 {
-    const int wpb = 8;
-    const size_t smem = (size_t)wpb * 32 * 33 * 4;
-    k_rerank_w<<<(unsigned)((a.nq + wpb - 1) / wpb), wpb * 32, smem, st>>>(a.nq, a.D, a.d, a.tails, a.qp, a.f1_off,
+    const int wpb = 4;
+    const size_t smem = (size_t)wpb * MRQ_RG_FLOATS * 4;
+    int rc = set_attr((const void *)k_rerank_w, smem);
+    if (rc) return rc;
+    k_rerank_w<<<(unsigned)((a.nq + wpb - 1) / wpb), wpb * 32, smem, st>>>(a.nq, a.aligned, a.D, a.d, a.tails, a.qp, a.f1_off,
                                                                          a.f2_cnt, a.f2_pos, a.f2_head, a.f2_exact);
     return MRQ_OK;
 }
@@ -371,5 +371,91 @@ int launch_topk_w(const StageArgs &a, cudaStream_t st)
     k_topk_w<<<(unsigned)((a.nq + wpb - 1) / wpb), wpb * 32, smem, st>>>(
         a.nq, a.K, a.Kp, a.ids, a.s0_cnt, a.s0_pos, a.s0_exact, a.s1_cnt, a.s1_pos, a.s1_exact, a.f1_off, a.f2_cnt,
         a.f2_pos, a.f2_exact, a.out_ids, a.out_dist, a.exact_cnt);
+    return MRQ_OK;
+}
+
+// ----------------------------------------------------------------------- a2
+// Exact top-nprobe from a screened distance row (Alg.2 L7), warp per
+// query.  Every screen value a_c is within delta_q of an exact-order key
+// (||q_d - c||^2 for the CUDA-core screen, ||q_d - c||^2 - ||q_d||^2 for the
+// tensor-core screen; the shift is the same for every c), so every member of
+// the exact top-np has a_c <= a_(np) + 2 delta_q with a_(np) the np-th
+// smallest screen value.  Pass 1 finds a_(np)
+// (WarpTop over the row), pass 2 collects {c : a_c <= a_(np) + 2 delta_q},
+// pass 3 rescores them in fp64 left to right over i and keeps the np
+// smallest (qn2, c).
+__global__ void __launch_bounds__(128) k_probe_select_w(
+    const float *__restrict__ approx, int64_t nq, int k, int d, int np, const double *__restrict__ qp, int D,
+    const double *__restrict__ C, const double *__restrict__ qnorm, double cmax, double kappa,
+    uint32_t *__restrict__ cand, uint32_t *__restrict__ probe, double *__restrict__ probe_qn2,
+    uint32_t *__restrict__ ncand_out)
+{
+    extern __shared__ unsigned char wsm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+    const int64_t q = (int64_t)blockIdx.x * wpb + warp;
+    if (q >= nq) return;
+    SelItem *lst = (SelItem *)wsm + (size_t)warp * np;
+    const float *row = approx + q * k;
+    WarpTop top;
+    top.init(lst, np);
+    for (int c0 = 0; c0 < k; c0 += 32) {
+        const int c = c0 + lane;
+        SelItem it = sel_inf();
+        if (c < k) {
+            it.key = (double)row[c];
+            it.id = (uint32_t)c;
+            it.pay = (uint32_t)c;
+        }
+        top.offer(it, c < k);
+    }
+    const double g = qnorm[q] + cmax;
+    const double thr = lst[np - 1].key + 2.0 * (kappa * (g * g));
+    uint32_t *cq = cand + q * k;
+    uint32_t nc = 0;
+    for (int c0 = 0; c0 < k; c0 += 32) {
+        const int c = c0 + lane;
+        const bool in = c < k && (double)row[c] <= thr;
+        const unsigned bal = __ballot_sync(0xffffffffu, in);
+        if (in) cq[nc + __popc(bal & ((1u << lane) - 1u))] = (uint32_t)c;
+        nc += __popc(bal);
+    }
+    __syncwarp();
+    const double *qd = qp + q * D;
+    top.init(lst, np);
+    for (uint32_t e0 = 0; e0 < nc; e0 += 32) {
+        const uint32_t e = e0 + lane;
+        SelItem it = sel_inf();
+        if (e < nc) {
+            const uint32_t c = cq[e];
+            const double *cr = C + (int64_t)c * d;
+            double acc = 0.0;
+            for (int j = 0; j < d; j++) {
+                const double t = qd[j] - cr[j];
+                acc = acc + t * t;
+            }
+            it.key = acc;
+            it.id = c;
+            it.pay = c;
+        }
+        top.offer(it, e < nc);
+    }
+    for (int p = lane; p < np; p += 32) {
+        const bool ok = lst[p].id != 0xFFFFFFFFu;
+        probe[q * np + p] = ok ? lst[p].id : 0xFFFFFFFFu;
+        probe_qn2[q * np + p] = ok ? lst[p].key : __longlong_as_double(0x7ff0000000000000ll);
+    }
+    if (lane == 0) ncand_out[q] = nc;
+}
+
+int launch_probe_select_w(const float *approx, int64_t nq, int k, int d, int np, const double *qp, int D,
+                          const double *C, const double *qnorm, double cmax, double kappa, uint32_t *cand,
+                          uint32_t *probe, double *probe_qn2, uint32_t *ncand, cudaStream_t st)
+{
+    const int wpb = 4;
+    const size_t smem = (size_t)wpb * np * sizeof(SelItem);
+    int rc = set_attr((const void *)k_probe_select_w, smem);
+    if (rc) return rc;
+    k_probe_select_w<<<(unsigned)((nq + wpb - 1) / wpb), wpb * 32, smem, st>>>(
+        approx, nq, k, d, np, qp, D, C, qnorm, cmax, kappa, cand, probe, probe_qn2, ncand);
     return MRQ_OK;
 }
