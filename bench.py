@@ -287,7 +287,7 @@ def main():
             cpu = {"value": None, "unit": "queries/s", "cores": os.cpu_count(), "kind": "oracle",
                    "sample": "failed: %s" % e}
 
-    launches_per_step = 12 + (3 if world > 1 else 0)
+    launches_per_step = 12 + (4 if world > 1 else 0)   # + 3 k_xmerge + k_f2_w when sharded
     out = {
         "metric": METRIC,
         "value": round(nq / (ms * 1e-3), 1),

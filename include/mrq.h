@@ -43,14 +43,23 @@ typedef enum {
     MRQ_EIO = -9          /* cannot open/read the build file                             */
 } mrq_err;
 
-/* Multi-GPU placement.  NULL, or world == 1, means one GPU (the current device
- * when device < 0).  With world > 1 every rank calls every function with
- * identical arguments; IVF lists are sharded across ranks (greedy by size) and
- * results are merged with an NCCL all-gather (nccl_unique_id: 128 bytes, the
- * same on all ranks). */
+/* Host all-gather used in place of NCCL (tests, virtual ranks): gathers
+ * `bytes` from every rank's `send` into `recv` (world * bytes, rank-major).
+ * Returns 0 on success.  Called from the thread that called the search. */
+typedef int (*mrq_allgather_fn)(const void *send, void *recv, size_t bytes, void *ctx);
+
+/* Multi-GPU placement.  NULL, or world == 1, means
+ * one GPU (the current device when device < 0).  With world > 1 every rank
+ * calls every function with identical arguments; IVF lists are sharded across
+ * ranks (mrq_shard_plan) and the decision-T seed sets and the per-rank top-K
+ * are exchanged with an all-gather: NCCL when nccl_unique_id (128 bytes from
+ * mrq_nccl_unique_id, the same on all ranks) is non-NULL, else the host
+ * callback host_allgather(ctx).  Results are identical for every world size. */
 typedef struct {
     int32_t rank, world, device;
     const void *nccl_unique_id;
+    mrq_allgather_fn host_allgather;
+    void *host_ctx;
 } mrq_dist_cfg;
 
 /* Search parameters (Alg.2 inputs N^probe, eps0, m). */
@@ -66,7 +75,8 @@ typedef struct {
     double resid_scale;   /* eps_r = (resid_scale * m) * sigma; 2 = distance domain (default) */
 } mrq_search_params;
 
-/* Per-call counters (summed over queries) and per-stage device milliseconds
+/* Per-call counters (summed over queries; at world > 1 over this rank's lists
+ * only -- "seeds" counts the owned members of the global S0/S1) and per-stage device milliseconds
  * (CUDA events on the library's stream; filled only when stats != NULL, which
  * makes the call synchronous). */
 typedef struct {
@@ -112,6 +122,22 @@ int mrq_search_batch(mrq_index *idx, const float *queries, int64_t nq, const mrq
 int mrq_search_batch_device(mrq_index *idx, const float *d_queries, int64_t nq, const mrq_search_params *p,
                             int64_t *d_out_ids, float *d_out_dist, mrq_stats *stats, void *stream);
 
+/*
+ * Multi-GPU bootstrap: writes a fresh 128-byte NCCL unique id to out (rank 0
+ * calls it and broadcasts the bytes).  NCCL is loaded at run time
+ * (libnccl.so.2); errors: MRQ_EINVAL (out NULL or bytes < 128), MRQ_ENCCL.
+ */
+int mrq_nccl_unique_id(void *out, size_t bytes);
+
+/*
+ * The list -> rank plan used by mrq_index_load at world > 1 (host only, no
+ * GPU needed): greedy longest-processing-time on list size -- lists by size
+ * descending (ties by list id) each go to the least-loaded rank (ties by
+ * rank).  sizes: host u32[k]; owner: host u32[k] written with ranks in
+ * [0, world).  Errors: MRQ_EINVAL (NULL, k < 1, world < 1).
+ */
+int mrq_shard_plan(const uint32_t *sizes, int32_t k, int32_t world, uint32_t *owner);
+
 /* Free the index (NULL-safe): device memory, streams, NCCL communicator. */
 void mrq_free(mrq_index *idx);
 
@@ -132,8 +158,8 @@ int mrq_index_info(const mrq_index *idx, int64_t *n, int32_t *D, int32_t *d, int
  * "probe" u32[nq][np], "probe_qn2" f64[nq][np], "planes" u32[nq][np][4][W],
  * "qconst" f64[nq][np][8], "f1_off" u64[nq], "f1_cnt" u32[nq], "f1_pos" u32[..],
  * "f1_diso" f64[..], "f2_cnt" u32[nq], "f2_pos" u32[..], "f2_exact" f64[..],
- * "s0_cnt" u32[nq], "s0_pos" u32[nq][Kp], "s0_exact" f64[nq][Kp], "s1_cnt",
- * "s1_pos", "s1_exact".
+ * "s0_cnt" u32[nq], "s0_pos" u32[nq][Kp], "s0_id" u32[nq][Kp],
+ * "s0_exact" f64[nq][Kp], "s1_cnt", "s1_pos", "s1_id", "s1_exact".
  * Errors: MRQ_EINVAL (unknown name, dst too small), MRQ_ECUDA.
  */
 int mrq_debug_fetch(mrq_index *idx, const char *name, void *dst, size_t dst_bytes, size_t *bytes_needed);
@@ -142,7 +168,9 @@ int mrq_debug_fetch(mrq_index *idx, const char *name, void *dst, size_t dst_byte
  * Test hook: set a debug switch of the index.  "dump_dis" = 1 makes every
  * later search also write dis' and LB1 of every scanned candidate (debug
  * buffers "dbg_dis", "dbg_lb1" f64, per query at f1_off[q] in probe order,
- * then slot order).  Errors: MRQ_EINVAL (unknown name).
+ * then slot order).  "force_exchange" = 1 makes a world-1 index run the
+ * multi-rank path (exchange buffers, device-copy all-gather, k_xmerge).
+ * Errors: MRQ_EINVAL (unknown name).
  */
 int mrq_debug_set(mrq_index *idx, const char *name, int64_t value);
 

@@ -35,7 +35,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
     cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "--fmad=false",
            "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-o", LIB + ".tmp"] + SRC
     if inc:
-        cmd += ["-DMRQ_HAVE_NCCL=1", "-I", inc, "-L", lib, "-lnccl", "-Xlinker", "-rpath=" + lib]
+        # headers only: NCCL itself is dlopen'ed at run time (csrc/mrq_comm.cu)
+        cmd += ["-DMRQ_HAVE_NCCL=1", "-I", inc, '-DMRQ_NCCL_LIB="%s"' % os.path.join(lib, "libnccl.so.2")]
+    cmd += ["-ldl"]
     if verbose:
         cmd += ["-Xptxas", "-v"]
     subprocess.check_call(cmd)

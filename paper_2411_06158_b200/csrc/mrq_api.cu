@@ -197,7 +197,7 @@ static int load_impl(mrq_index *ix, const char *build_file, const float *base, i
         std::vector<uint32_t> owner;
         mrq_shard_lists(cnt, ix->world, owner);
         for (int c = 0; c < k; c++) own[c] = owner[c] == (uint32_t)ix->rank;
-        TRY(mrq_comm_init(ix, dist->nccl_unique_id));
+        TRY(mrq_comm_init(ix, dist));
     }
     // list slots: owned lists only, each start aligned to MRQ_SLOT_ALIGN
     ix->h_list_off.assign(k + 1, 0);
@@ -256,6 +256,7 @@ static int load_impl(mrq_index *ix, const char *build_file, const float *base, i
     TRY(upload(ix, &ix->cn32, cn32.data(), cn32.size()));
     TRY(upload(ix, &ix->list_off, ix->h_list_off.data(), k + 1));
     TRY(upload(ix, &ix->list_size, ix->h_list_size.data(), k));
+    TRY(upload(ix, &ix->list_size_g, cnt.data(), k));
     TRY(upload(ix, &ix->ids, ids.data(), npad));
     TRY(dalloc(ix, (void **)&ix->Rc, (size_t)k * d * 8));
     k_rc<<<(k + 7) / 8, 256, 0, ix->stream>>>(ix->C, ix->RT, k, d, W, ix->Rc);
@@ -419,6 +420,16 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
     SCR("s1_cnt", uint32_t, nq, s1_cnt);
     SCR("s1_pos", uint32_t, nq * Kp, s1_pos);
     SCR("s1_exact", double, nq * Kp, s1_exact);
+    uint32_t *s0_id, *s1_id;
+    SCR("s0_id", uint32_t, nq * Kp, s0_id);
+    SCR("s1_id", uint32_t, nq * Kp, s1_id);
+    const bool sharded = ix->world > 1 || ix->force_exchange;
+    const int Lx = std::max(Kp, K);
+    XItem *xsend = nullptr, *xrecv = nullptr;
+    if (sharded) {
+        SCR("xsend", XItem, nq * Lx, xsend);
+        SCR("xrecv", XItem, (size_t)nq * Lx * ix->world, xrecv);
+    }
     SCR("f1_cnt", uint32_t, nq, f1_cnt);
     SCR("f2_cnt", uint32_t, nq, f2_cnt);
     SCR("exact_cnt", uint32_t, nq, exact_cnt);
@@ -488,6 +499,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
     sa.s0_exact = s0_exact; sa.s1_exact = s1_exact; sa.tau0 = tau0; sa.tau1 = tau1; sa.f1_head = f1_head;
     sa.f1_diso = f1_diso; sa.f2_head = f2_head; sa.f2_exact = f2_exact; sa.f1_off = f1_off;
     sa.out_ids = d_ids; sa.out_dist = d_dist;
+    sa.list_size_g = ix->list_size_g; sa.s0_id = s0_id; sa.s1_id = s1_id; sa.xout = nullptr;
 
     // ---- a4: seeds S0 and tau0 (decision T); EXACT mode scans everything
     if (mode == 2) {
@@ -496,8 +508,15 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
         MRQ_CUDA_TRY(cudaMemsetAsync(s0_cnt, 0, nq * 4, st));
         MRQ_CUDA_TRY(cudaStreamSynchronize(st));
     } else {
-        TRY(launch_seed_w(W, sa, st));
-        if (ix->world > 1) TRY(mrq_comm_seeds(ix, nq, K, Kp, s0_cnt, s0_pos, s0_exact, tau0, st));
+        if (sharded) {   // local part of S0 -> all-gather -> global S0, tau0
+            StageArgs sx = sa;
+            sx.xout = xsend;
+            TRY(launch_seed_w(W, sx, st));
+            TRY(mrq_allgather(ix, xsend, xrecv, (size_t)nq * Kp * sizeof(XItem), st));
+            TRY(launch_xmerge(0, sa, ix->world, ix->rank, xrecv, st));
+        } else {
+            TRY(launch_seed_w(W, sa, st));
+        }
     }
     if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[4], st));
 
@@ -520,9 +539,16 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
     if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[5], st));
 
     // ---- a6: stage 2 -> F2 (and S1, tau1)
-    TRY(launch_stage2_w(sa, st));
-    if (ix->world > 1 && mode == 0 && tight)
-        TRY(mrq_comm_tau1(ix, nq, K, Kp, s0_cnt, s0_pos, s0_exact, s1_cnt, s1_pos, s1_exact, tau1, st));
+    if (sharded && mode == 0 && tight) {   // local S1 -> all-gather -> global S1, tau1 -> F2
+        StageArgs sx = sa;
+        sx.xout = xsend;
+        TRY(launch_stage2_w(sx, st));
+        TRY(mrq_allgather(ix, xsend, xrecv, (size_t)nq * Kp * sizeof(XItem), st));
+        TRY(launch_xmerge(1, sa, ix->world, ix->rank, xrecv, st));
+        TRY(launch_f2_w(sa, st));
+    } else {
+        TRY(launch_stage2_w(sa, st));
+    }
     if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[6], st));
 
     // ---- a7: exact re-rank of F2
@@ -530,10 +556,19 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
     if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[7], st));
 
     // ---- a8: per-query top-K
-    TRY(launch_topk_w(sa, st));
+    if (sharded) {
+        StageArgs sx = sa;
+        sx.xout = xsend;
+        TRY(launch_topk_w(sx, st));
+    } else {
+        TRY(launch_topk_w(sa, st));
+    }
     if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[8], st));
-    // ---- a9: multi-GPU merge (NCCL all-gather of per-rank top-K)
-    if (ix->world > 1) TRY(mrq_comm_merge(ix, nq, K, d_ids, d_dist, st));
+    // ---- a9: multi-GPU merge (all-gather of the per-rank top-K)
+    if (sharded) {
+        TRY(mrq_allgather(ix, xsend, xrecv, (size_t)nq * K * sizeof(XItem), st));
+        TRY(launch_xmerge(2, sa, ix->world, ix->rank, xrecv, st));
+    }
     if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[9], st));
     MRQ_CUDA_TRY(cudaGetLastError());
 
@@ -679,6 +714,7 @@ extern "C" int mrq_debug_fetch(mrq_index *ix, const char *name, void *dst, size_
             {"s1_cnt", (size_t)nq * 4},        {"exact_cnt", (size_t)nq * 4},
             {"s0_pos", (size_t)nq * Kp * 4},   {"s0_exact", (size_t)nq * Kp * 8},
             {"s1_pos", (size_t)nq * Kp * 4},   {"s1_exact", (size_t)nq * Kp * 8},
+            {"s0_id", (size_t)nq * Kp * 4},    {"s1_id", (size_t)nq * Kp * 4},
             {"f1_pos", (size_t)ix->last_total * 4}, {"f1_head", (size_t)ix->last_total * 8},
             {"f1_diso", (size_t)ix->last_total * 8}, {"f2_pos", (size_t)ix->last_total * 4},
             {"f2_head", (size_t)ix->last_total * 8}, {"f2_exact", (size_t)ix->last_total * 8},
@@ -717,6 +753,10 @@ extern "C" int mrq_debug_set(mrq_index *ix, const char *name, int64_t value)
     }
     if (std::string(name) == "dump_dis") {
         ix->dbg_dump_dis = (int)value;
+        return MRQ_OK;
+    }
+    if (std::string(name) == "force_exchange") {   // world 1 runs the sharded (exchange + merge) path
+        ix->force_exchange = (int)value;
         return MRQ_OK;
     }
     mrq_set_error("unknown debug switch '%s'", name);

@@ -1,8 +1,21 @@
-// mrq_comm.cu -- list sharding across ranks and NCCL exchanges.
+// mrq_comm.cu -- list sharding across ranks and the all-gather exchanges of
+// the multi-GPU path.
+//
+// NCCL is resolved at run time (dlopen "libnccl.so.2", the library torch
+// ships), so libmrq loads on hosts without NCCL; a world > 1 index fails
+// loudly (MRQ_ENCCL) if NCCL cannot be loaded.
+#include <dlfcn.h>
+#include <string.h>
+
 #include <algorithm>
+#include <mutex>
 #include <numeric>
 
 #include "mrq_comm.cuh"
+
+#if MRQ_HAVE_NCCL
+#include <nccl.h>
+#endif
 
 // Greedy longest-processing-time assignment of lists to ranks: lists by size
 // descending (ties by id), each to the currently least-loaded rank (ties by
@@ -24,19 +37,164 @@ void mrq_shard_lists(const std::vector<uint32_t> &sizes, int world, std::vector<
     }
 }
 
-int mrq_comm_init(mrq_index *, const void *)
+extern "C" int mrq_shard_plan(const uint32_t *sizes, int32_t k, int32_t world, uint32_t *owner)
 {
-    mrq_set_error("multi-GPU (NCCL) path not built in this library");
-    return MRQ_ENCCL;
+    if (!sizes || !owner || k < 1 || world < 1) {
+        mrq_set_error("InvalidConfig: mrq_shard_plan needs sizes, owner, k >= 1, world >= 1");
+        return MRQ_EINVAL;
+    }
+    std::vector<uint32_t> s(sizes, sizes + k), o;
+    mrq_shard_lists(s, world, o);
+    memcpy(owner, o.data(), (size_t)k * 4);
+    return MRQ_OK;
 }
-void mrq_comm_free(mrq_index *) {}
-int mrq_comm_seeds(mrq_index *, int64_t, int, int, uint32_t *, uint32_t *, double *, double *, cudaStream_t)
+
+#if MRQ_HAVE_NCCL
+namespace {
+struct NcclApi {
+    bool ok = false;
+    char err[256] = "";
+    ncclResult_t (*getUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*allGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    const char *(*getErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi &nccl()
 {
-    return MRQ_ENCCL;
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+#ifdef MRQ_NCCL_LIB
+        if (!h) h = dlopen(MRQ_NCCL_LIB, RTLD_NOW | RTLD_GLOBAL);
+#endif
+        if (!h) {
+            snprintf(api.err, sizeof api.err, "cannot load libnccl.so.2: %s", dlerror());
+            return;
+        }
+        api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");
+        api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
+        api.allGather = (decltype(api.allGather))dlsym(h, "ncclAllGather");
+        api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
+        api.getErrorString = (decltype(api.getErrorString))dlsym(h, "ncclGetErrorString");
+        api.ok = api.getUniqueId && api.commInitRank && api.allGather && api.commDestroy && api.getErrorString;
+        if (!api.ok) snprintf(api.err, sizeof api.err, "libnccl.so.2 lacks a required symbol");
+    });
+    return api;
 }
-int mrq_comm_tau1(mrq_index *, int64_t, int, int, const uint32_t *, const uint32_t *, const double *,
-                  const uint32_t *, const uint32_t *, const double *, double *, cudaStream_t)
+}  // namespace
+#endif
+
+extern "C" int mrq_nccl_unique_id(void *out, size_t bytes)
 {
+    if (!out || bytes < 128) {
+        mrq_set_error("InvalidConfig: mrq_nccl_unique_id needs a 128-byte buffer");
+        return MRQ_EINVAL;
+    }
+#if MRQ_HAVE_NCCL
+    NcclApi &a = nccl();
+    if (!a.ok) {
+        mrq_set_error("%s", a.err);
+        return MRQ_ENCCL;
+    }
+    ncclUniqueId id;
+    ncclResult_t r = a.getUniqueId(&id);
+    if (r != ncclSuccess) {
+        mrq_set_error("ncclGetUniqueId: %s", a.getErrorString(r));
+        return MRQ_ENCCL;
+    }
+    static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id is 128 bytes");
+    memcpy(out, &id, 128);
+    return MRQ_OK;
+#else
+    mrq_set_error("libmrq was built without nccl.h");
     return MRQ_ENCCL;
+#endif
 }
-int mrq_comm_merge(mrq_index *, int64_t, int, int64_t *, float *, cudaStream_t) { return MRQ_ENCCL; }
+
+int mrq_comm_init(mrq_index *ix, const mrq_dist_cfg *dist)
+{
+    if (dist->nccl_unique_id) {
+#if MRQ_HAVE_NCCL
+        NcclApi &a = nccl();
+        if (!a.ok) {
+            mrq_set_error("%s", a.err);
+            return MRQ_ENCCL;
+        }
+        ncclUniqueId id;
+        memcpy(&id, dist->nccl_unique_id, sizeof id);
+        ncclComm_t comm = nullptr;
+        ncclResult_t r = a.commInitRank(&comm, ix->world, id, ix->rank);
+        if (r != ncclSuccess) {
+            mrq_set_error("ncclCommInitRank(world=%d, rank=%d): %s", ix->world, ix->rank, a.getErrorString(r));
+            return MRQ_ENCCL;
+        }
+        ix->nccl_comm = comm;
+        return MRQ_OK;
+#else
+        mrq_set_error("libmrq was built without nccl.h");
+        return MRQ_ENCCL;
+#endif
+    }
+    if (dist->host_allgather) {
+        ix->host_ag = dist->host_allgather;
+        ix->host_ctx = dist->host_ctx;
+        return MRQ_OK;
+    }
+    mrq_set_error("InvalidConfig: world=%d needs nccl_unique_id or host_allgather", ix->world);
+    return MRQ_EINVAL;
+}
+
+void mrq_comm_free(mrq_index *ix)
+{
+#if MRQ_HAVE_NCCL
+    if (ix->nccl_comm) nccl().commDestroy((ncclComm_t)ix->nccl_comm);
+#endif
+    ix->nccl_comm = nullptr;
+    if (ix->xhost) cudaFreeHost(ix->xhost);
+    ix->xhost = nullptr;
+    ix->xhost_bytes = 0;
+}
+
+int mrq_allgather(mrq_index *ix, const void *send, void *recv, size_t bytes, cudaStream_t st)
+{
+    if (ix->world == 1) {
+        MRQ_CUDA_TRY(cudaMemcpyAsync(recv, send, bytes, cudaMemcpyDeviceToDevice, st));
+        return MRQ_OK;
+    }
+#if MRQ_HAVE_NCCL
+    if (ix->nccl_comm) {
+        NcclApi &a = nccl();
+        ncclResult_t r = a.allGather(send, recv, bytes, ncclUint8, (ncclComm_t)ix->nccl_comm, st);
+        if (r != ncclSuccess) {
+            mrq_set_error("ncclAllGather(%zu B): %s", bytes, a.getErrorString(r));
+            return MRQ_ENCCL;
+        }
+        return MRQ_OK;
+    }
+#endif
+    if (!ix->host_ag) {
+        mrq_set_error("no exchange configured for world=%d", ix->world);
+        return MRQ_ENCCL;
+    }
+    const size_t need = bytes * (size_t)(ix->world + 1);
+    MRQ_CUDA_TRY(cudaStreamSynchronize(st));
+    if (ix->xhost_bytes < need) {
+        if (ix->xhost) cudaFreeHost(ix->xhost);
+        ix->xhost = nullptr;
+        ix->xhost_bytes = 0;
+        MRQ_CUDA_TRY(cudaMallocHost(&ix->xhost, need));
+        ix->xhost_bytes = need;
+    }
+    char *h = (char *)ix->xhost;
+    MRQ_CUDA_TRY(cudaMemcpyAsync(h, send, bytes, cudaMemcpyDeviceToHost, st));
+    MRQ_CUDA_TRY(cudaStreamSynchronize(st));
+    if (ix->host_ag(h, h + bytes, bytes, ix->host_ctx) != 0) {
+        mrq_set_error("host all-gather callback failed");
+        return MRQ_ENCCL;
+    }
+    MRQ_CUDA_TRY(cudaMemcpyAsync(recv, h + bytes, bytes * (size_t)ix->world, cudaMemcpyHostToDevice, st));
+    return MRQ_OK;
+}

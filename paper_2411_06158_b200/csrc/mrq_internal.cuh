@@ -48,7 +48,12 @@ struct mrq_index {
     int64_t N = 0, npad = 0;
     int D = 0, d = 0, k = 0, W = 0;
     int rank = 0, world = 1;
-    void *nccl_comm = nullptr;
+    void *nccl_comm = nullptr;                 // ncclComm_t (NCCL loaded at run time)
+    mrq_allgather_fn host_ag = nullptr;        // host exchange (tests / virtual ranks)
+    void *host_ctx = nullptr;
+    void *xhost = nullptr;                     // pinned staging of the host exchange
+    size_t xhost_bytes = 0;
+    int force_exchange = 0;                    // mrq_debug_set("force_exchange"): world-1 runs the sharded path
     int sm_count = 148;
 
     // host mirrors
@@ -62,7 +67,8 @@ struct mrq_index {
     float *C32T = nullptr;                                                // C32T[i][k] fp32 centroids, transposed
     float *C32 = nullptr;                                                 // C32[k][d] fp32 centroids (GEMM B operand)
     float *cn32 = nullptr;                                                // ||c||^2 fp32 (GEMM epilogue)
-    uint32_t *list_off = nullptr, *list_size = nullptr;                   // [k+1], [k]
+    uint32_t *list_off = nullptr, *list_size = nullptr;                   // [k+1], [k] (owned lists; 0 if not owned)
+    uint32_t *list_size_g = nullptr;                                      // [k] global list sizes (seed pool, decision T)
     uint32_t *ids = nullptr;                                              // [npad] global id of each slot
     uint32_t *codes = nullptr;                                            // [W][npad]
     float *f1 = nullptr, *f2 = nullptr, *f3 = nullptr, *xr2 = nullptr;    // [npad]
@@ -80,6 +86,16 @@ struct mrq_index {
 
 // helpers in mrq_api.cu
 int mrq_scratch(mrq_index *ix, const char *name, size_t bytes, void **out);
+
+// Item of the multi-rank exchanges: selection key (dis',
+// dis_o' or exact), exact distance, global id, local slot (PAD on the
+// receiving side when the item belongs to another rank).
+struct XItem {
+    double key;
+    double exact;
+    uint32_t id;
+    uint32_t slot;
+};
 
 // ---------------------------------------------------------- device helpers
 struct SelItem {

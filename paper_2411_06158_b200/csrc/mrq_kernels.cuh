@@ -28,7 +28,10 @@ struct StageArgs {
     const uint32_t *probe, *list_off, *list_size, *ids, *codes, *planes;
     const float *f1, *f2, *f3, *heads, *tails, *xr2;
     const double *qconst, *qp, *qr2, *eps_r;
+    const uint32_t *list_size_g;
     uint32_t *s0_cnt, *s0_pos, *s1_cnt, *s1_pos, *f1_cnt, *f1_pos, *f2_cnt, *f2_pos, *exact_cnt;
+    uint32_t *s0_id, *s1_id;
+    XItem *xout;   // sharded exchange send buffer (NULL = single-rank fast path)
     double *s0_exact, *s1_exact, *tau0, *tau1, *f1_head, *f1_diso, *f2_head, *f2_exact;
     const uint64_t *f1_off;
     int64_t *out_ids;
@@ -39,6 +42,8 @@ int launch_seed_w(int W, const StageArgs &a, cudaStream_t st);
 int launch_stage2_w(const StageArgs &a, cudaStream_t st);
 int launch_rerank_w(const StageArgs &a, cudaStream_t st);
 int launch_topk_w(const StageArgs &a, cudaStream_t st);
+int launch_f2_w(const StageArgs &a, cudaStream_t st);
+int launch_xmerge(int kind, const StageArgs &a, int world, int rank, const XItem *recv, cudaStream_t st);
 
 struct LaunchScan {
     int64_t nq;

@@ -4,6 +4,8 @@
 // warp once; rows are gathered through a 32x33 shared tile so global loads
 // stay 128-byte coalesced and each lane sums its own row left to right (the
 // canonical order of DESIGN.md).
+#include <algorithm>
+
 #include "mrq_internal.cuh"
 #include "mrq_kernels.cuh"
 
@@ -21,7 +23,8 @@ __global__ void __launch_bounds__(256) k_seed_w(
     const float *__restrict__ f3, const float *__restrict__ heads, const float *__restrict__ tails,
     const uint32_t *__restrict__ planes, const double *__restrict__ qconst, const double *__restrict__ qp,
     const double *__restrict__ eps_r_arr, double isd, uint32_t *__restrict__ s0_cnt, uint32_t *__restrict__ s0_pos,
-    double *__restrict__ s0_exact, double *__restrict__ tau0)
+    double *__restrict__ s0_exact, double *__restrict__ tau0, const uint32_t *__restrict__ list_size_g,
+    uint32_t *__restrict__ s0_id, XItem *__restrict__ xout)
 {
     extern __shared__ unsigned char wsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
@@ -33,10 +36,14 @@ __global__ void __launch_bounds__(256) k_seed_w(
     top.init(lst, Kp);
     const double eps_r = eps_r_arr[q];
     const double *qrow = qp + q * D;
-    int npool = 0;
+    // the pool is defined on GLOBAL list sizes (decision T); a rank scans only
+    // the lists it owns (list_size = 0 for the others)
+    int64_t npool = 0;
+    int nloc = 0;
     for (int p = 0; p < np && npool < Kp; p++) {
         const uint32_t c = probe[q * np + p];
         if (c == 0xFFFFFFFFu) continue;
+        npool += list_size_g[c];
         const uint32_t off = list_off[c], sz = list_size[c];
         const uint32_t *pl = planes + (q * np + p) * (MRQ_BQ * W);
         const double *qc = qconst + (q * np + p) * 8;
@@ -57,14 +64,15 @@ __global__ void __launch_bounds__(256) k_seed_w(
             }
             top.offer(it, v);
         }
-        npool += sz;
+        nloc += (int)sz;
     }
-    const int ns0 = npool < Kp ? npool : Kp;
+    const int ns0 = nloc < Kp ? nloc : Kp;
     // exact distances of S0: HEAD over the head rows, then continued over the tail rows
     warp_rows(aligned, heads, d, 0, d, qrow, ns0, tile, [&](int e) { return lst[e].pay; },
               [&](int) { return 0.0; }, [&](int e, bool v, double acc) {
                   if (v) {
                       s0_pos[q * Kp + e] = lst[e].pay;
+                      s0_id[q * Kp + e] = lst[e].id;
                       s0_exact[q * Kp + e] = acc;
                   }
               });
@@ -75,6 +83,17 @@ __global__ void __launch_bounds__(256) k_seed_w(
                       if (v) s0_exact[q * Kp + e] = acc;
                   });
     __syncwarp();
+    if (xout) {   // sharded: this rank's part of S0 goes to the exchange (k_xmerge makes S0, tau0)
+        for (int e = lane; e < Kp; e += 32) {
+            XItem x;
+            x.key = e < ns0 ? lst[e].key : __longlong_as_double(0x7ff0000000000000ll);
+            x.exact = e < ns0 ? s0_exact[q * Kp + e] : x.key;
+            x.id = e < ns0 ? lst[e].id : MRQ_PAD_ID;
+            x.slot = e < ns0 ? lst[e].pay : MRQ_PAD_ID;
+            xout[q * Kp + e] = x;
+        }
+        return;
+    }
     // tau0 = K-th smallest exact over S0
     top.init(lst, K);
     for (int g = 0; g < ns0; g += 32) {
@@ -83,7 +102,7 @@ __global__ void __launch_bounds__(256) k_seed_w(
         SelItem it = sel_inf();
         if (v) {
             it.key = s0_exact[q * Kp + e];
-            it.id = ids[s0_pos[q * Kp + e]];
+            it.id = s0_id[q * Kp + e];
             it.pay = e;
         }
         top.offer(it, v);
@@ -95,22 +114,47 @@ __global__ void __launch_bounds__(256) k_seed_w(
 }
 
 // ----------------------------------------------------------------------- a6
-// Stage 2 (Alg.2 L13 P:315; "Optimization" P:327, reading A-7): for every F1
+// F2 = {e in F1 : dis_o' - eps_r < tau1} (FULL), all of F1 otherwise:
+// ordered warp compaction (no atomics) of the query's F1 segment.
+__device__ __forceinline__ void f2_compact(int64_t q, int mode, int n1, uint64_t base, double eps_r, double tau1,
+                                           const uint32_t *__restrict__ f1_pos, const double *__restrict__ f1_head,
+                                           const double *__restrict__ f1_diso, uint32_t *__restrict__ f2_cnt,
+                                           uint32_t *__restrict__ f2_pos, double *__restrict__ f2_head)
+{
+    const int lane = threadIdx.x & 31;
+    uint32_t at = 0;
+    for (int g = 0; g < n1; g += 32) {
+        const int e = g + lane;
+        bool pass = false;
+        if (e < n1) pass = (mode != 0) || (f1_diso[base + e] - eps_r < tau1);
+        const unsigned bal = __ballot_sync(0xffffffffu, pass);
+        if (pass) {
+            const uint32_t o = at + __popc(bal & ((1u << lane) - 1u));
+            f2_pos[base + o] = f1_pos[base + e];
+            f2_head[base + o] = f1_head[base + e];
+        }
+        at += __popc(bal);
+    }
+    if (lane == 0) f2_cnt[q] = at;
+}
+
+// Stage 2 (Alg.2 L13 P:315; "Optimization" P:327, reading R-6): for every F1
 // entry HEAD = ||x_d - q_d||^2 (left to right over i < d) and
 // dis_o' = (HEAD + ||x_r||^2) + ||q_r||^2.  TIGHT: S1 = the K' smallest
 // (dis_o', id) of F1, their exact distances (HEAD continued over the tail),
 // tau1 = K-th smallest distinct exact over S0 u S1; LOOSE: tau1 = tau0.
-// F2 = {e in F1 : dis_o' - eps_r < tau1} (FULL), F1 (STAGE1_ONLY / EXACT).
+// F2 as in f2_compact.  Sharded TIGHT (xout != NULL): the local S1 goes to
+// the exchange and k_xmerge / k_f2_w finish tau1 and F2.
 __global__ void __launch_bounds__(256) k_stage2_w(
     int64_t nq, int aligned, int mode, int tight, int K, int Kp, int D, int d, const uint32_t *__restrict__ ids,
     const float *__restrict__ heads, const float *__restrict__ tails, const float *__restrict__ xr2,
     const double *__restrict__ qp, const double *__restrict__ qr2_arr, const double *__restrict__ eps_r_arr,
     const double *__restrict__ tau0_arr, const uint64_t *__restrict__ f1_off, const uint32_t *__restrict__ f1_cnt,
     const uint32_t *__restrict__ f1_pos, double *__restrict__ f1_head, double *__restrict__ f1_diso,
-    const uint32_t *__restrict__ s0_cnt, const uint32_t *__restrict__ s0_pos, const double *__restrict__ s0_exact,
-    uint32_t *__restrict__ s1_cnt, uint32_t *__restrict__ s1_pos, double *__restrict__ s1_exact,
-    double *__restrict__ tau1_arr, uint32_t *__restrict__ f2_cnt, uint32_t *__restrict__ f2_pos,
-    double *__restrict__ f2_head)
+    const uint32_t *__restrict__ s0_cnt, const uint32_t *__restrict__ s0_id, const double *__restrict__ s0_exact,
+    uint32_t *__restrict__ s1_cnt, uint32_t *__restrict__ s1_pos, uint32_t *__restrict__ s1_id,
+    double *__restrict__ s1_exact, double *__restrict__ tau1_arr, uint32_t *__restrict__ f2_cnt,
+    uint32_t *__restrict__ f2_pos, double *__restrict__ f2_head, XItem *__restrict__ xout)
 {
     extern __shared__ unsigned char wsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
@@ -143,7 +187,10 @@ __global__ void __launch_bounds__(256) k_stage2_w(
     double tau1 = tau0_arr[q];
     if (sel1) {
         const int ns1 = n1 < Kp ? n1 : Kp;
-        for (int e = lane; e < ns1; e += 32) s1_pos[q * Kp + e] = f1_pos[base + lst[e].pay];
+        for (int e = lane; e < ns1; e += 32) {
+            s1_pos[q * Kp + e] = f1_pos[base + lst[e].pay];
+            s1_id[q * Kp + e] = lst[e].id;
+        }
         __syncwarp();
         auto s1_init = [&](int e) { return f1_head[base + lst[e].pay]; };
         auto s1_done = [&](int e, bool v, double acc) {
@@ -155,6 +202,17 @@ __global__ void __launch_bounds__(256) k_stage2_w(
         else
             for (int e = lane; e < ns1; e += 32) s1_exact[q * Kp + e] = s1_init(e);
         __syncwarp();
+        if (xout) {   // sharded TIGHT: exchange the local S1
+            for (int e = lane; e < Kp; e += 32) {
+                XItem x;
+                x.key = e < ns1 ? lst[e].key : __longlong_as_double(0x7ff0000000000000ll);
+                x.exact = e < ns1 ? s1_exact[q * Kp + e] : x.key;
+                x.id = e < ns1 ? lst[e].id : MRQ_PAD_ID;
+                x.slot = e < ns1 ? s1_pos[q * Kp + e] : MRQ_PAD_ID;
+                xout[q * Kp + e] = x;
+            }
+            return;
+        }
         // tau1 = K-th smallest distinct exact over S0 u S1 (duplicates dropped by WarpTop)
         top.init(lst, K);
         const int ns0 = (int)s0_cnt[q];
@@ -164,10 +222,9 @@ __global__ void __launch_bounds__(256) k_stage2_w(
             SelItem it = sel_inf();
             if (v) {
                 const bool a0 = e < ns0;
-                const uint32_t slot = a0 ? s0_pos[q * Kp + e] : s1_pos[q * Kp + (e - ns0)];
                 it.key = a0 ? s0_exact[q * Kp + e] : s1_exact[q * Kp + (e - ns0)];
-                it.id = ids[slot];
-                it.pay = slot;
+                it.id = a0 ? s0_id[q * Kp + e] : s1_id[q * Kp + (e - ns0)];
+                it.pay = (uint32_t)e;
             }
             top.offer(it, v);
         }
@@ -177,21 +234,21 @@ __global__ void __launch_bounds__(256) k_stage2_w(
         s1_cnt[q] = 0;
     }
     if (lane == 0) tau1_arr[q] = tau1;
-    // F2: ordered compaction (warp-local, no atomics)
-    uint32_t at = 0;
-    for (int g = 0; g < n1; g += 32) {
-        const int e = g + lane;
-        bool pass = false;
-        if (e < n1) pass = (mode != 0) || (f1_diso[base + e] - eps_r < tau1);
-        const unsigned bal = __ballot_sync(0xffffffffu, pass);
-        if (pass) {
-            const uint32_t o = at + __popc(bal & ((1u << lane) - 1u));
-            f2_pos[base + o] = f1_pos[base + e];
-            f2_head[base + o] = f1_head[base + e];
-        }
-        at += __popc(bal);
-    }
-    if (lane == 0) f2_cnt[q] = at;
+    f2_compact(q, mode, n1, base, eps_r, tau1, f1_pos, f1_head, f1_diso, f2_cnt, f2_pos, f2_head);
+}
+
+// F2 after a sharded tau1 exchange (warp per query).
+__global__ void __launch_bounds__(256) k_f2_w(int64_t nq, int mode, const double *__restrict__ eps_r_arr,
+                                              const double *__restrict__ tau1_arr, const uint64_t *__restrict__ f1_off,
+                                              const uint32_t *__restrict__ f1_cnt, const uint32_t *__restrict__ f1_pos,
+                                              const double *__restrict__ f1_head, const double *__restrict__ f1_diso,
+                                              uint32_t *__restrict__ f2_cnt, uint32_t *__restrict__ f2_pos,
+                                              double *__restrict__ f2_head)
+{
+    const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (q >= nq) return;
+    f2_compact(q, mode, (int)f1_cnt[q], f1_off[q], eps_r_arr[q], tau1_arr[q], f1_pos, f1_head, f1_diso, f2_cnt,
+               f2_pos, f2_head);
 }
 
 // ----------------------------------------------------------------------- a7
@@ -222,15 +279,20 @@ __global__ void __launch_bounds__(256) k_rerank_w(int64_t nq, int aligned, int D
 
 // ----------------------------------------------------------------------- a8
 // Per-query top-K (Alg.2 L15-L16): the K smallest (exact, id) over
-// the distinct union S0 u S1 u F2 (a candidate in several sets has the same
-// exact value in each, so WarpTop drops the copies); ids returned as the
-// original int64 index, distances rounded to fp32; padding id -1 / +inf.
+// the distinct union S0 u S1 u F2 restricted to this rank's slots (a
+// candidate in several sets has the same exact value in each, so WarpTop
+// drops the copies; members of the global S0/S1 owned by another rank carry
+// slot PAD and are skipped).  ids are returned as the original int64 index,
+// distances rounded to fp32, padding id -1 / +inf.  Sharded (xout != NULL):
+// the local top-K (exact fp64, id) goes to the exchange and k_xmerge writes
+// the outputs.
 __global__ void __launch_bounds__(256) k_topk_w(
     int64_t nq, int K, int Kp, const uint32_t *__restrict__ ids, const uint32_t *__restrict__ s0_cnt,
-    const uint32_t *__restrict__ s0_pos, const double *__restrict__ s0_exact, const uint32_t *__restrict__ s1_cnt,
-    const uint32_t *__restrict__ s1_pos, const double *__restrict__ s1_exact, const uint64_t *__restrict__ f1_off,
-    const uint32_t *__restrict__ f2_cnt, const uint32_t *__restrict__ f2_pos, const double *__restrict__ f2_exact,
-    int64_t *__restrict__ out_ids, float *__restrict__ out_dist, uint32_t *__restrict__ exact_cnt)
+    const uint32_t *__restrict__ s0_pos, const uint32_t *__restrict__ s0_id, const double *__restrict__ s0_exact,
+    const uint32_t *__restrict__ s1_cnt, const uint32_t *__restrict__ s1_pos, const uint32_t *__restrict__ s1_id,
+    const double *__restrict__ s1_exact, const uint64_t *__restrict__ f1_off, const uint32_t *__restrict__ f2_cnt,
+    const uint32_t *__restrict__ f2_pos, const double *__restrict__ f2_exact, int64_t *__restrict__ out_ids,
+    float *__restrict__ out_dist, uint32_t *__restrict__ exact_cnt, XItem *__restrict__ xout)
 {
     extern __shared__ unsigned char wsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
@@ -244,48 +306,151 @@ __global__ void __launch_bounds__(256) k_topk_w(
     const int n = ns0 + ns1 + n2;
     for (int g = 0; g < n; g += 32) {
         const int e = g + lane;
-        const bool v = e < n;
+        bool v = e < n;
         SelItem it = sel_inf();
         if (v) {
             uint32_t slot;
             if (e < ns0) {
                 slot = s0_pos[q * Kp + e];
                 it.key = s0_exact[q * Kp + e];
+                it.id = s0_id[q * Kp + e];
             } else if (e < ns0 + ns1) {
                 slot = s1_pos[q * Kp + (e - ns0)];
                 it.key = s1_exact[q * Kp + (e - ns0)];
+                it.id = s1_id[q * Kp + (e - ns0)];
             } else {
                 slot = f2_pos[base + (e - ns0 - ns1)];
                 it.key = f2_exact[base + (e - ns0 - ns1)];
+                it.id = ids[slot];
             }
-            it.id = ids[slot];
             it.pay = slot;
+            v = slot != MRQ_PAD_ID;
+            if (!v) it = sel_inf();
         }
         top.offer(it, v);
     }
-    for (int i = lane; i < K; i += 32) {
-        const bool ok = lst[i].id != 0xFFFFFFFFu;
-        out_ids[q * K + i] = ok ? (int64_t)lst[i].id : (int64_t)-1;
-        out_dist[q * K + i] = ok ? (float)lst[i].key : __int_as_float(0x7f800000);
-    }
-    // distinct exact computations = |S0 u S1 u F2| (S1 and F2 are subsets of F1; S0 may overlap both)
-    if (lane == 0) exact_cnt[q] = 0;
-    __syncwarp();
-    uint32_t dup = 0;
-    for (int g = ns0; g < n; g += 32) {
-        const int e = g + lane;
-        if (e < n) {
-            const uint32_t slot = e < ns0 + ns1 ? s1_pos[q * Kp + (e - ns0)] : f2_pos[base + (e - ns0 - ns1)];
-            bool d0 = false;
-            for (int t = 0; t < ns0; t++) d0 |= s0_pos[q * Kp + t] == slot;
-            bool d1 = false;
-            if (e >= ns0 + ns1)
-                for (int t = 0; t < ns1; t++) d1 |= s1_pos[q * Kp + t] == slot;
-            dup += (d0 || d1) ? 1u : 0u;
+    if (xout) {
+        for (int i = lane; i < K; i += 32) {
+            XItem x;
+            x.key = lst[i].key;
+            x.exact = lst[i].key;
+            x.id = lst[i].id;
+            x.slot = lst[i].pay;
+            xout[q * K + i] = x;
+        }
+    } else {
+        for (int i = lane; i < K; i += 32) {
+            const bool ok = lst[i].id != 0xFFFFFFFFu;
+            out_ids[q * K + i] = ok ? (int64_t)lst[i].id : (int64_t)-1;
+            out_dist[q * K + i] = ok ? (float)lst[i].key : __int_as_float(0x7f800000);
         }
     }
-    for (int o = 16; o > 0; o >>= 1) dup += __shfl_xor_sync(0xffffffffu, dup, o);
-    if (lane == 0) exact_cnt[q] = (uint32_t)n - dup;
+    // distinct exact computations on this rank = |(S0 u S1 u F2) n owned|
+    // (S1 and F2 are subsets of F1; S0 may overlap both)
+    uint32_t cnt = 0;
+    for (int g = 0; g < n; g += 32) {
+        const int e = g + lane;
+        if (e < n) {
+            const uint32_t slot = e < ns0 ? s0_pos[q * Kp + e]
+                                  : e < ns0 + ns1 ? s1_pos[q * Kp + (e - ns0)] : f2_pos[base + (e - ns0 - ns1)];
+            bool dup = slot == MRQ_PAD_ID;
+            if (e >= ns0)
+                for (int t = 0; t < ns0 && !dup; t++) dup = s0_pos[q * Kp + t] == slot;
+            if (e >= ns0 + ns1)
+                for (int t = 0; t < ns1 && !dup; t++) dup = s1_pos[q * Kp + t] == slot;
+            cnt += dup ? 0u : 1u;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (lane == 0) exact_cnt[q] = cnt;
+}
+
+// ----------------------------------------------------------------------- a9
+// Merge of an all-gather, warp per query.  recv holds, rank
+// major, every rank's L items of every query: recv[(r * nq + q) * L + j].
+// The L smallest (key, id) of the union are kept (ids are distinct across
+// ranks: each vector lives on one rank).
+//   kind 0 (seeds):  global S0 (key = dis') and tau0 = K-th smallest exact
+//   kind 1 (S1):     global S1 (key = dis_o') and tau1 = K-th smallest
+//                    distinct exact over S0 u S1
+//   kind 2 (final):  top-K (key = exact) -> out_ids / out_dist
+// Slots of items that came from another rank become PAD.
+__global__ void __launch_bounds__(128) k_xmerge(int kind, int64_t nq, int world, int rank, int L, int K, int Kp,
+                                                const XItem *__restrict__ recv, uint32_t *__restrict__ s_cnt,
+                                                uint32_t *__restrict__ s_pos, uint32_t *__restrict__ s_id,
+                                                double *__restrict__ s_exact, double *__restrict__ tau,
+                                                const uint32_t *__restrict__ s0_cnt, const uint32_t *__restrict__ s0_id,
+                                                const double *__restrict__ s0_exact, int64_t *__restrict__ out_ids,
+                                                float *__restrict__ out_dist)
+{
+    extern __shared__ unsigned char wsm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+    const int64_t q = (int64_t)blockIdx.x * wpb + warp;
+    if (q >= nq) return;
+    SelItem *lst = (SelItem *)wsm + (size_t)warp * L;
+    WarpTop top;
+    top.init(lst, L);
+    for (int r = 0; r < world; r++) {
+        const XItem *src = recv + ((int64_t)r * nq + q) * L;
+        for (int j0 = 0; j0 < L; j0 += 32) {
+            const int j = j0 + lane;
+            SelItem it = sel_inf();
+            bool v = false;
+            if (j < L) {
+                const XItem x = src[j];
+                v = x.id != MRQ_PAD_ID;
+                if (v) {
+                    it.key = x.key;
+                    it.id = x.id;
+                    it.pay = (uint32_t)(r * L + j);
+                }
+            }
+            top.offer(it, v);
+        }
+    }
+    if (kind == 2) {
+        for (int i = lane; i < K; i += 32) {
+            const bool ok = lst[i].id != MRQ_PAD_ID;
+            double ex = 0.0;
+            if (ok) {
+                const uint32_t pay = lst[i].pay;
+                ex = recv[((int64_t)(pay / L) * nq + q) * L + pay % L].exact;
+            }
+            out_ids[q * K + i] = ok ? (int64_t)lst[i].id : (int64_t)-1;
+            out_dist[q * K + i] = ok ? (float)ex : __int_as_float(0x7f800000);
+        }
+        return;
+    }
+    int n = 0;
+    for (int j0 = 0; j0 < L; j0 += 32) n += __popc(__ballot_sync(0xffffffffu, j0 + lane < L && lst[j0 + lane].id != MRQ_PAD_ID));
+    for (int e = lane; e < n; e += 32) {
+        const uint32_t pay = lst[e].pay;
+        const int r = (int)(pay / L);
+        const XItem x = recv[((int64_t)r * nq + q) * L + pay % L];
+        s_exact[q * Kp + e] = x.exact;
+        s_id[q * Kp + e] = x.id;
+        s_pos[q * Kp + e] = r == rank ? x.slot : MRQ_PAD_ID;
+    }
+    __syncwarp();
+    // tau = K-th smallest distinct exact over S0 (kind 0) or S0 u S1 (kind 1)
+    top.init(lst, K);
+    const int n0 = kind == 1 ? (int)s0_cnt[q] : 0;
+    for (int g = 0; g < n0 + n; g += 32) {
+        const int e = g + lane;
+        const bool v = e < n0 + n;
+        SelItem it = sel_inf();
+        if (v) {
+            const bool a0 = e < n0;
+            it.key = a0 ? s0_exact[q * Kp + e] : s_exact[q * Kp + (e - n0)];
+            it.id = a0 ? s0_id[q * Kp + e] : s_id[q * Kp + (e - n0)];
+            it.pay = (uint32_t)e;
+        }
+        top.offer(it, v);
+    }
+    if (lane == 0) {
+        s_cnt[q] = (uint32_t)n;
+        tau[q] = lst[K - 1].key;
+    }
 }
 
 // ---------------------------------------------------------------- launchers
@@ -321,7 +486,7 @@ int launch_seed_w(int W, const StageArgs &a, cudaStream_t st)
         k_seed_w<WW><<<grid, wpb * 32, smem, st>>>(a.nq, a.aligned, a.probe, a.np, a.K, a.Kp, a.D, a.d, a.npad, a.list_off,   \
                                                    a.list_size, a.ids, a.codes, a.f1, a.f2, a.f3, a.heads, a.tails, \
                                                    a.planes, a.qconst, a.qp, a.eps_r, a.isd, a.s0_cnt, a.s0_pos,    \
-                                                   a.s0_exact, a.tau0);                                             \
+                                                   a.s0_exact, a.tau0, a.list_size_g, a.s0_id, a.xout);             \
     } while (0)
     switch (W) {
     case 1: MRQ_SEED(1); break;
@@ -345,8 +510,34 @@ int launch_stage2_w(const StageArgs &a, cudaStream_t st)
     if (rc) return rc;
     k_stage2_w<<<(unsigned)((a.nq + wpb - 1) / wpb), wpb * 32, smem, st>>>(
         a.nq, a.aligned, a.mode, a.tight, a.K, a.Kp, a.D, a.d, a.ids, a.heads, a.tails, a.xr2, a.qp, a.qr2, a.eps_r, a.tau0,
-        a.f1_off, a.f1_cnt, a.f1_pos, a.f1_head, a.f1_diso, a.s0_cnt, a.s0_pos, a.s0_exact, a.s1_cnt, a.s1_pos,
-        a.s1_exact, a.tau1, a.f2_cnt, a.f2_pos, a.f2_head);
+        a.f1_off, a.f1_cnt, a.f1_pos, a.f1_head, a.f1_diso, a.s0_cnt, a.s0_id, a.s0_exact, a.s1_cnt, a.s1_pos, a.s1_id,
+        a.s1_exact, a.tau1, a.f2_cnt, a.f2_pos, a.f2_head, a.xout);
+    return MRQ_OK;
+}
+
+int launch_f2_w(const StageArgs &a, cudaStream_t st)
+{
+    k_f2_w<<<(unsigned)((a.nq + 7) / 8), 256, 0, st>>>(a.nq, a.mode, a.eps_r, a.tau1, a.f1_off, a.f1_cnt, a.f1_pos,
+                                                       a.f1_head, a.f1_diso, a.f2_cnt, a.f2_pos, a.f2_head);
+    return MRQ_OK;
+}
+
+int launch_xmerge(int kind, const StageArgs &a, int world, int rank, const XItem *recv, cudaStream_t st)
+{
+    const int L = kind == 2 ? a.K : a.Kp;
+    const size_t per = (size_t)std::max(L, a.K) * sizeof(SelItem);
+    const int wpb = warps_for(per);
+    const size_t smem = per * wpb;
+    int rc = set_attr((const void *)k_xmerge, smem);
+    if (rc) return rc;
+    uint32_t *cnt = kind == 0 ? a.s0_cnt : a.s1_cnt;
+    uint32_t *pos = kind == 0 ? a.s0_pos : a.s1_pos;
+    uint32_t *sid = kind == 0 ? a.s0_id : a.s1_id;
+    double *ex = kind == 0 ? a.s0_exact : a.s1_exact;
+    double *tau = kind == 0 ? a.tau0 : a.tau1;
+    k_xmerge<<<(unsigned)((a.nq + wpb - 1) / wpb), wpb * 32, smem, st>>>(kind, a.nq, world, rank, L, a.K, a.Kp, recv,
+                                                                        cnt, pos, sid, ex, tau, a.s0_cnt, a.s0_id,
+                                                                        a.s0_exact, a.out_ids, a.out_dist);
     return MRQ_OK;
 }
 
@@ -369,8 +560,8 @@ int launch_topk_w(const StageArgs &a, cudaStream_t st)
     int rc = set_attr((const void *)k_topk_w, smem);
     if (rc) return rc;
     k_topk_w<<<(unsigned)((a.nq + wpb - 1) / wpb), wpb * 32, smem, st>>>(
-        a.nq, a.K, a.Kp, a.ids, a.s0_cnt, a.s0_pos, a.s0_exact, a.s1_cnt, a.s1_pos, a.s1_exact, a.f1_off, a.f2_cnt,
-        a.f2_pos, a.f2_exact, a.out_ids, a.out_dist, a.exact_cnt);
+        a.nq, a.K, a.Kp, a.ids, a.s0_cnt, a.s0_pos, a.s0_id, a.s0_exact, a.s1_cnt, a.s1_pos, a.s1_id, a.s1_exact,
+        a.f1_off, a.f2_cnt, a.f2_pos, a.f2_exact, a.out_ids, a.out_dist, a.exact_cnt, a.xout);
     return MRQ_OK;
 }
 

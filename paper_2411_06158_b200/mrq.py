@@ -24,8 +24,12 @@ class MRQError(RuntimeError):
         self.code = code
 
 
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
+
+
 class DistCfg(C.Structure):
-    _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("device", C.c_int32), ("nccl_unique_id", C.c_void_p)]
+    _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("device", C.c_int32), ("nccl_unique_id", C.c_void_p),
+                ("host_allgather", ALLGATHER_FN), ("host_ctx", C.c_void_p)]
 
 
 class SearchParams(C.Structure):
@@ -75,6 +79,10 @@ def lib():
         L.mrq_index_info.argtypes = [C.c_void_p] + [C.c_void_p] * 5
         L.mrq_debug_set.restype = C.c_int
         L.mrq_debug_set.argtypes = [C.c_void_p, C.c_char_p, C.c_int64]
+        L.mrq_nccl_unique_id.restype = C.c_int
+        L.mrq_nccl_unique_id.argtypes = [C.c_void_p, C.c_size_t]
+        L.mrq_shard_plan.restype = C.c_int
+        L.mrq_shard_plan.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]
         _lib = L
     return _lib
 
@@ -96,16 +104,55 @@ def _ptr(a):
     return a.ctypes.data_as(C.c_void_p)
 
 
-def mrq_index_load(build_file: str, base: np.ndarray, d: int, rank=0, world=1, device=-1, nccl_unique_id=None):
+_CALLBACKS = {}   # handle value -> ctypes callback (kept alive while the index lives)
+
+
+def host_allgather_callback(fn):
+    """Wraps fn(send: bytes, world_bytes_out: memoryview) ... as the C callback:
+    fn(send_bytes) must return the rank-major concatenation of every rank's
+    bytes (len = world * len(send_bytes))."""
+    def cb(send, recv, nbytes, ctx):
+        try:
+            data = fn(C.string_at(send, nbytes))
+            C.memmove(recv, data, len(data))
+            return 0
+        except Exception:  # pragma: no cover - reported as MRQ_ENCCL by the library
+            return 1
+    return ALLGATHER_FN(cb)
+
+
+def mrq_index_load(build_file: str, base: np.ndarray, d: int, rank=0, world=1, device=-1, nccl_unique_id=None,
+                   host_allgather=None):
+    """host_allgather: optional python callable send_bytes -> all ranks' bytes
+    (rank-major), used in place of NCCL when nccl_unique_id is None."""
     base = np.ascontiguousarray(base, dtype=np.float32)
     n, D = base.shape
     h = C.c_void_p()
     uid = None
     if nccl_unique_id is not None:
         uid = C.create_string_buffer(bytes(nccl_unique_id), 128)
-    cfg = DistCfg(rank, world, device, C.cast(uid, C.c_void_p) if uid is not None else None)
+    cb = host_allgather_callback(host_allgather) if host_allgather is not None else ALLGATHER_FN()
+    cfg = DistCfg(rank, world, device, C.cast(uid, C.c_void_p) if uid is not None else None, cb, None)
     _check(lib().mrq_index_load(build_file.encode(), _ptr(base), n, D, d, C.byref(cfg), C.byref(h)))
+    if host_allgather is not None:
+        _CALLBACKS[h.value] = cb
     return h
+
+
+def mrq_nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib().mrq_nccl_unique_id(buf, 128))
+    return buf.raw
+
+
+nccl_unique_id = mrq_nccl_unique_id
+
+
+def mrq_shard_plan(sizes, world: int) -> np.ndarray:
+    s = np.ascontiguousarray(sizes, dtype=np.uint32)
+    owner = np.empty(s.shape[0], np.uint32)
+    _check(lib().mrq_shard_plan(_ptr(s), s.shape[0], world, _ptr(owner)))
+    return owner
 
 
 def mrq_search_batch(h, queries: np.ndarray, params: SearchParams, with_stats=True):
@@ -130,6 +177,7 @@ def mrq_search_batch_device(h, d_queries, params: SearchParams, d_ids, d_dist, s
 def mrq_free(h):
     if h:
         lib().mrq_free(h)
+        _CALLBACKS.pop(getattr(h, "value", h), None)
 
 
 def mrq_index_info(h):

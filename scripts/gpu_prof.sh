@@ -9,6 +9,6 @@ echo "plain rc $rc"
 if [ $rc -ne 0 ]; then tail -20 gpurun_out/plain.log; exit 1; fi
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
 echo "ncu launches rc $?"
-ncu --set full --clock-control none --import-source on -k "regex:${KREGEX:-k_stage2_w|k_scan|k_probe_select|k_probe_approx}" -s ${SKIP:-40} -c ${COUNT:-4} -o gpurun_out/prof $CMD > gpurun_out/ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on -k "regex:${KREGEX:-k_stage2_w|k_scan|k_probe_select_w|k_probe_approx|k_seed_w}" -s ${SKIP:-25} -c ${COUNT:-5} -o gpurun_out/prof $CMD > gpurun_out/ncu_full.log 2>&1
 echo "ncu full rc $?"
 tail -3 gpurun_out/ncu_full.log
