@@ -170,6 +170,8 @@ int mrq_debug_fetch(mrq_index *idx, const char *name, void *dst, size_t dst_byte
  * buffers "dbg_dis", "dbg_lb1" f64, per query at f1_off[q] in probe order,
  * then slot order).  "force_exchange" = 1 makes a world-1 index run the
  * multi-rank path (exchange buffers, device-copy all-gather, k_xmerge).
+ * "cuda_core_probe" = 1 screens the probe on CUDA cores (fp32) instead of
+ * the tcgen05 tf32 GEMM (the exact fp64 selection is the same).
  * Errors: MRQ_EINVAL (unknown name).
  */
 int mrq_debug_set(mrq_index *idx, const char *name, int64_t value);

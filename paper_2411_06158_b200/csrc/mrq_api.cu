@@ -372,19 +372,6 @@ extern "C" int mrq_index_info(const mrq_index *ix, int64_t *n, int32_t *D, int32
 }
 
 // ------------------------------------------------------------------ search
-static int pow2_at_least(int x)
-{
-    int s = 1;
-    while (s < x) s <<= 1;
-    return s;
-}
-
-static int set_smem(const void *fn, size_t bytes)
-{
-    if (bytes > 48 * 1024) MRQ_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    return MRQ_OK;
-}
-
 static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_search_params *p, int64_t *d_ids,
                        float *d_dist, mrq_stats *stats, cudaStream_t st)
 {
@@ -485,6 +472,8 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
     SCR("f2_pos", uint32_t, total, f2_pos);
     SCR("f2_head", double, total, f2_head);
     SCR("f2_exact", double, total, f2_exact);
+    uint32_t *f1_id;
+    SCR("f1_id", uint32_t, total, f1_id);
     if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[3], st));
 
     StageArgs sa;
@@ -499,6 +488,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
     sa.s0_exact = s0_exact; sa.s1_exact = s1_exact; sa.tau0 = tau0; sa.tau1 = tau1; sa.f1_head = f1_head;
     sa.f1_diso = f1_diso; sa.f2_head = f2_head; sa.f2_exact = f2_exact; sa.f1_off = f1_off;
     sa.out_ids = d_ids; sa.out_dist = d_dist;
+    sa.f1_id = f1_id;
     sa.list_size_g = ix->list_size_g; sa.s0_id = s0_id; sa.s1_id = s1_id; sa.xout = nullptr;
 
     // ---- a4: seeds S0 and tau0 (decision T); EXACT mode scans everything
@@ -757,6 +747,10 @@ extern "C" int mrq_debug_set(mrq_index *ix, const char *name, int64_t value)
     }
     if (std::string(name) == "force_exchange") {   // world 1 runs the sharded (exchange + merge) path
         ix->force_exchange = (int)value;
+        return MRQ_OK;
+    }
+    if (std::string(name) == "cuda_core_probe") {  // probe screen on CUDA cores instead of tcgen05
+        ix->force_cuda_core_probe = (int)value;
         return MRQ_OK;
     }
     mrq_set_error("unknown debug switch '%s'", name);

@@ -54,6 +54,8 @@ struct mrq_index {
     void *xhost = nullptr;                     // pinned staging of the host exchange
     size_t xhost_bytes = 0;
     int force_exchange = 0;                    // mrq_debug_set("force_exchange"): world-1 runs the sharded path
+    void *probe_tc = nullptr;                  // tcgen05 probe state (mrq_probe_tc.cu)
+    int force_cuda_core_probe = 0;             // mrq_debug_set("cuda_core_probe"): CUDA-core screen instead
     int sm_count = 148;
 
     // host mirrors
@@ -280,6 +282,98 @@ struct WarpTop {
     }
 };
 
+// Register-resident variant for L <= 32: lane i holds the i-th smallest
+// item; an insertion is one ballot (position) and one shuffle-up (shift).
+struct WarpTopReg {
+    double key;
+    uint32_t id, pay;
+    int L;
+
+    __device__ __forceinline__ void init(int L_)
+    {
+        L = L_;
+        const SelItem z = sel_inf();
+        key = z.key;
+        id = z.id;
+        pay = z.pay;
+    }
+
+    __device__ __forceinline__ void offer(const SelItem &it, bool valid)
+    {
+        const int lane = threadIdx.x & 31;
+        double tk = __shfl_sync(0xffffffffu, key, L - 1);
+        uint32_t ti = __shfl_sync(0xffffffffu, id, L - 1);
+        unsigned m = __ballot_sync(0xffffffffu, valid && (it.key < tk || (it.key == tk && it.id < ti)));
+        while (m) {
+            const int src = __ffs(m) - 1;
+            m &= m - 1;
+            const double xk = __shfl_sync(0xffffffffu, it.key, src);
+            const uint32_t xi = __shfl_sync(0xffffffffu, it.id, src);
+            const uint32_t xp = __shfl_sync(0xffffffffu, it.pay, src);
+            if (!(xk < tk || (xk == tk && xi < ti))) continue;                      // warp-uniform
+            const bool mine = lane < L;
+            if (__any_sync(0xffffffffu, mine && key == xk && id == xi)) continue;    // duplicate
+            const int pos = __popc(__ballot_sync(0xffffffffu, mine && (key < xk || (key == xk && id < xi))));
+            const double uk = __shfl_up_sync(0xffffffffu, key, 1);
+            const uint32_t ui = __shfl_up_sync(0xffffffffu, id, 1);
+            const uint32_t up = __shfl_up_sync(0xffffffffu, pay, 1);
+            if (lane > pos) {
+                key = uk;
+                id = ui;
+                pay = up;
+            } else if (lane == pos) {
+                key = xk;
+                id = xi;
+                pay = xp;
+            }
+            tk = __shfl_sync(0xffffffffu, key, L - 1);
+            ti = __shfl_sync(0xffffffffu, id, L - 1);
+        }
+    }
+};
+
+// Selection of the L smallest distinct (key, id): registers for L <= 32,
+// the shared-memory list otherwise.  After finish() the sorted items are in
+// buf[0 .. L) either way.
+struct WarpSel {
+    WarpTop sm;
+    WarpTopReg rg;
+    bool reg;
+
+    __device__ __forceinline__ void init(SelItem *buf, int L)
+    {
+        reg = L <= 32;
+        sm.a = buf;
+        sm.L = L;
+        if (reg)
+            rg.init(L);
+        else
+            sm.init(buf, L);
+    }
+    __device__ __forceinline__ void offer(const SelItem &it, bool valid)
+    {
+        if (reg)
+            rg.offer(it, valid);
+        else
+            sm.offer(it, valid);
+    }
+    __device__ __forceinline__ void finish()
+    {
+        if (reg) {
+            const int lane = threadIdx.x & 31;
+            __syncwarp();
+            if (lane < rg.L) {
+                SelItem x;
+                x.key = rg.key;
+                x.id = rg.id;
+                x.pay = rg.pay;
+                sm.a[lane] = x;
+            }
+        }
+        __syncwarp();
+    }
+};
+
 // ================================================================ a4 / a5
 // The scan epilogue shared by the seed pass and the scan (Eq.4
 // with A-1; Eq.5 P:255 with A-2/A-6; Alg.2 L12 P:314):
@@ -315,87 +409,111 @@ __device__ __forceinline__ double mrq_lb1(const uint32_t *code, const uint32_t *
 
 
 // -------------------------------------------------------------------------
-// Pipelined warp row gather (cp.async, double-buffered).  A warp processes
-// entries 0..n-1 in groups of 32 (lane = entry within the group); for each
-// group it streams the columns [off, off + len) of every lane's row through
-// shared memory in chunks of up to CH floats, while the next (group, chunk)
-// job's 16-byte cp.async copies are already in flight.  Each lane sums its
-// own row left to right in fp64:  acc = init(e); acc += ((double)x - q)^2 ...
-// then done(e, valid, acc) is called by the whole warp.
+// Staged warp row gather.  A warp processes entries 0..n-1 in groups of 32
+// (lane = entry within the group).  Each group's rows are copied, one
+// MRQ_RG_CH-float column batch of [off, off + len) at a time, into the warp's
+// shared-memory stage with coalesced 16-byte cp.async (8 lanes cover one
+// 128-byte row segment, an instruction covers 4 rows); two stages, so batch
+// j+1 is in flight while batch j is consumed.  Each lane then sums its own
+// row from shared memory left to right in fp64 (the canonical order,
+// DESIGN.md §4):  acc = init(e, slot); acc += ((double)x - q)^2 ...  and
+// done(e, valid, acc) is called by the whole warp after the row's last batch.
+// Shared-memory reads are conflict-free (row stride CH + 4 floats).
+// (A per-lane cp.async.bulk of each row was tried: its operands must be
+// warp-uniform, so the compiler serializes the 32 lanes' copies.)
+// Per-warp shared memory: MRQ_RG_FLOATS floats.
 // Requirements: row stride, off and len multiples of 4 floats (16-B copies).
-#define MRQ_RG_CH 64
-#define MRQ_RG_STRIDE (MRQ_RG_CH + 4)          // = 4 (mod 8): conflict-free 16-B row reads
-#define MRQ_RG_FLOATS (2 * 32 * MRQ_RG_STRIDE)  // per-warp smem (floats)
+#define MRQ_RG_CH 32
+#define MRQ_RG_STRIDE (MRQ_RG_CH + 4)
+#define MRQ_RG_STAGE (32 * MRQ_RG_STRIDE)
+#define MRQ_RG_FLOATS (2 * MRQ_RG_STAGE)       // >= 32 * 33 (the unaligned fallback's tile)
 
-__device__ __forceinline__ void cp_async16(void *smem_dst, const void *gmem_src)
-{
-    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 template <class SlotOf, class Init, class Done>
 __device__ __forceinline__ void warp_gather_rows(const float *__restrict__ base, int64_t stride, int off, int len,
                                                  const double *__restrict__ q, int n, float *sbuf, SlotOf slot_of,
-                                                 Init init, Done done)
+                                                 Init init, Done done, int g0 = 0, int gs = 1)
 {
+    // groups g0, g0 + gs, g0 + 2 gs, ... of 32 entries (several warps can split one list)
     const int lane = threadIdx.x & 31;
     const int nchunk = (len + MRQ_RG_CH - 1) / MRQ_RG_CH;
-    const int ngroup = (n + 31) / 32;
-    const int njobs = ngroup * nchunk;
+    const int ngroups = (n + 31) / 32;
+    const int mygroups = ngroups > g0 ? (ngroups - g0 + gs - 1) / gs : 0;
+    const int njobs = mygroups * nchunk;
     if (njobs == 0) return;
-    auto issue = [&](int job) {
-        const int g = job / nchunk, c = job % nchunk;
+    uint32_t slot_cur = 0;
+    // job (g, c): 32 rows x MRQ_RG_CH floats; lane copies 16-B unit (lane & 7)
+    // of rows (lane >> 3) + 4 i, i = 0..7 (one 128-B row segment per 8 lanes).
+    auto issue = [&](int job, int g, int c) {
         const int e = g * 32 + lane;
-        const bool v = e < n;
-        const uint32_t slot = v ? slot_of(e) : 0u;
         const int c0 = c * MRQ_RG_CH;
-        const int nu = (min(MRQ_RG_CH, len - c0)) >> 2;       // 16-B units per row segment
-        float *dst = sbuf + (job & 1) * (32 * MRQ_RG_STRIDE);
-        for (int j = lane; j < 32 * nu; j += 32) {
-            const int r = j / nu, u = j - r * nu;
-            const uint32_t s = __shfl_sync(0xffffffffu, slot, r);
-            const int ok = __shfl_sync(0xffffffffu, (int)v, r);
-            if (ok) cp_async16(dst + r * MRQ_RG_STRIDE + 4 * u, base + (int64_t)s * stride + off + c0 + 4 * u);
+        const int nu = min(MRQ_RG_CH, len - c0) >> 2;
+        const int st = job & 1;
+        if (c == 0 && e < n) slot_cur = slot_of(e);
+        const int cnt = min(32, n - g * 32);
+        const int u = lane & 7;
+        float *dst0 = sbuf + st * MRQ_RG_STAGE + 4 * u;
+        const float *src0 = base + off + c0 + 4 * u;
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            const int r = (lane >> 3) + 4 * i;
+            const uint32_t s = __shfl_sync(0xffffffffu, slot_cur, r);
+            if (r < cnt && u < nu) {
+                const unsigned d = smem_u32(dst0 + r * MRQ_RG_STRIDE);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src0 + (int64_t)s * stride)
+                             : "memory");
+            }
         }
-        cp_async_commit();
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
-    issue(0);
+    issue(0, g0, 0);
     double acc = 0.0;
+    uint32_t slot_row = slot_cur;
+    int g = g0, c = 0;           // current job
+    int gi = g0, ci = 0;         // last issued job
     for (int job = 0; job < njobs; job++) {
-        if (job + 1 < njobs) {
-            issue(job + 1);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        __syncwarp();
-        const int g = job / nchunk, c = job % nchunk;
         const int e = g * 32 + lane;
         const bool v = e < n;
-        if (c == 0) acc = v ? init(e) : 0.0;
+        if (c == 0) slot_row = slot_cur;
+        if (job + 1 < njobs) {
+            if (++ci == nchunk) {
+                ci = 0;
+                gi += gs;
+            }
+            issue(job + 1, gi, ci);
+        }
+        const int st = job & 1;
+        if (c == 0 && v) acc = init(e, slot_row);
+        if (job + 1 < njobs)
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        else
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        __syncwarp();
         const int c0 = c * MRQ_RG_CH;
         const int cl = min(MRQ_RG_CH, len - c0);
-        const float *row = sbuf + (job & 1) * (32 * MRQ_RG_STRIDE) + lane * MRQ_RG_STRIDE;
+        const float *row = sbuf + st * MRQ_RG_STAGE + lane * MRQ_RG_STRIDE;
         const double *qq = q + c0;
         if (v) {
+#pragma unroll 4
             for (int u = 0; u < cl; u += 4) {
                 const float4 x = *(const float4 *)(row + u);
                 const double2 qa = *(const double2 *)(qq + u);
                 const double2 qb = *(const double2 *)(qq + u + 2);
                 const double t0 = (double)x.x - qa.x, t1 = (double)x.y - qa.y;
                 const double t2 = (double)x.z - qb.x, t3 = (double)x.w - qb.y;
-                const double s0 = t0 * t0, s1 = t1 * t1, s2 = t2 * t2, s3 = t3 * t3;
-                acc = acc + s0;
-                acc = acc + s1;
-                acc = acc + s2;
-                acc = acc + s3;
+                acc = acc + t0 * t0;
+                acc = acc + t1 * t1;
+                acc = acc + t2 * t2;
+                acc = acc + t3 * t3;
             }
         }
-        __syncwarp();
+        __syncwarp();   // the stage is refilled by the next issue
         if (c == nchunk - 1) done(e, v, acc);
+        if (++c == nchunk) {
+            c = 0;
+            g += gs;
+        }
     }
 }
 
@@ -404,18 +522,18 @@ __device__ __forceinline__ void warp_gather_rows(const float *__restrict__ base,
 template <class SlotOf, class Init, class Done>
 __device__ __forceinline__ void warp_rows(bool aligned, const float *__restrict__ base, int64_t stride, int off,
                                           int len, const double *__restrict__ q, int n, float *sbuf, SlotOf slot_of,
-                                          Init init, Done done)
+                                          Init init, Done done, int g0 = 0, int gs = 1)
 {
     if (aligned) {
-        warp_gather_rows(base, stride, off, len, q, n, sbuf, slot_of, init, done);
+        warp_gather_rows(base, stride, off, len, q, n, sbuf, slot_of, init, done, g0, gs);
         return;
     }
     const int lane = threadIdx.x & 31;
-    for (int g = 0; g < n; g += 32) {
+    for (int g = g0 * 32; g < n; g += 32 * gs) {
         const int e = g + lane;
         const bool v = e < n;
         const uint32_t slot = v ? slot_of(e) : 0u;
-        double acc = v ? init(e) : 0.0;
+        double acc = v ? init(e, slot) : 0.0;
         acc = warp_rows_sqdist(base, stride, off, slot, v, len, q, acc, sbuf);
         done(e, v, acc);
     }

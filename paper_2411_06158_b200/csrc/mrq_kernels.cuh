@@ -33,6 +33,7 @@ struct StageArgs {
     uint32_t *s0_id, *s1_id;
     XItem *xout;   // sharded exchange send buffer (NULL = single-rank fast path)
     double *s0_exact, *s1_exact, *tau0, *tau1, *f1_head, *f1_diso, *f2_head, *f2_exact;
+    uint32_t *f1_id;
     const uint64_t *f1_off;
     int64_t *out_ids;
     float *out_dist;

@@ -1,13 +1,339 @@
-// mrq_probe_tc.cu -- tcgen05 tensor-core probe screen (placeholder until the
-// UMMA kernel lands: the CUDA-core fp32 screen in mrq_kernels.cu is used).
+// mrq_probe_tc.cu -- the probe screen (Alg.2 L7, on the projected
+// centroids of Alg.1 L6 P:286 / Exp-2 P:2405-2408) as a tcgen05 tensor-core
+// GEMM on sm_100a.
+//
+//   approx[q][c] = ||c||^2 - 2 <q_d, c>        (fp32; the q-only term ||q_d||^2 is dropped)
+//
+// A = q_d (fp32 [nq][d], K-major), B = centroids (fp32 [k][d], K-major);
+// kind::tf32 MMAs (M = 128 queries, N = 256 centroids, K = 8) accumulate in
+// TMEM.  Warp roles (one CTA = one 128-query block x a range of 256-centroid
+// tiles):
+//   warp 0  TMA producer: 2-D tensor-map loads of A and B k-blocks (32 fp32 =
+//           128 B rows, 128-byte swizzle) into a 4-stage smem ring;
+//   warp 1  TMEM allocator + MMA issuer (one elected thread);
+//   warps 2-5  epilogue: tcgen05.ld of the 128 x 256 accumulator (each thread
+//           owns one query row), ||c||^2 - 2 acc, fp32 stores.
+// Two TMEM accumulators (2 x 256 columns) let the epilogue of tile j overlap
+// the MMAs of tile j+1.  Out-of-range rows/columns/k are zero-filled by TMA.
+//
+// Exactness (DESIGN.md §4 "probe exactness"): tf32 keeps 10 mantissa bits of
+// each fp32 input (relative error <= 2^-10 whether truncated or rounded), the
+// fp32 accumulation of d products adds <= d 2^-23 sum|q_i c_i|, and ||c||^2,
+// q_d, c are fp32 roundings of fp64 values; with sum|q_i c_i| <= ||q|| ||c||
+// and 2 ||q|| ||c|| <= (||q|| + ||c||)^2 / 2 ... the screen is within
+//   delta_q = kappa (||q_d|| + max ||c||)^2,  kappa = 2^-9 + d 2^-22 + 2^-20
+// of the exact key ||c||^2 - 2 <q_d, c> (a generous bound: each term is at
+// least 2x the derivation).  k_probe_select_w then rescores every centroid
+// within 2 delta_q of the np-th smallest screen value in canonical fp64.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cmath>
+
 #include "mrq_probe_tc.cuh"
 
-int mrq_probe_tc_init(mrq_index *) { return MRQ_OK; }
-void mrq_probe_tc_free(mrq_index *) {}
-bool mrq_probe_tc_enabled(const mrq_index *) { return false; }
-double mrq_probe_tc_kappa(const mrq_index *) { return 0.0; }
-int mrq_probe_tc_run(mrq_index *, const float *, int64_t, float *, cudaStream_t)
+#define TC_BM 128
+#define TC_BN 256
+#define TC_BK 32                       // fp32 elements per 128-byte swizzle row
+#define TC_STAGES 4
+#define TC_A_BYTES (TC_BM * TC_BK * 4) // 16 KB
+#define TC_B_BYTES (TC_BN * TC_BK * 4) // 32 KB
+#define TC_STAGE_BYTES (TC_A_BYTES + TC_B_BYTES)
+#define TC_THREADS 192
+#define TC_SMEM (TC_STAGES * TC_STAGE_BYTES + 1024 + 256)
+
+struct ProbeTC {
+    bool enabled = false;
+    CUtensorMap mapB;                  // centroids
+    PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+};
+
+// ------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t n)
 {
-    mrq_set_error("tcgen05 probe not available");
-    return MRQ_ECUDA;
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(b)), "r"(n));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *b)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity)
+{
+    uint32_t ok = 0;
+    do {
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                     : "=r"(ok)
+                     : "r"(su32(b)), "r"(parity)
+                     : "memory");
+    } while (!ok);
+}
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+            su32(dst)),
+        "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(su32(bar))
+        : "memory");
+}
+// K-major, 128-byte-swizzled operand: 8-row core groups 1024 B apart (SBO),
+// LBO unused for swizzled K-major (1), descriptor version 1 (sm_100),
+// layout type 2 = SWIZZLE_128B.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr)
+{
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;
+    d |= (uint64_t)(1024 >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)2 << 61;
+    return d;
+}
+// kind::tf32 instruction descriptor: D fp32, A/B tf32, both K-major, N, M.
+__host__ __device__ constexpr uint32_t tf32_idesc(int M, int N)
+{
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__global__ void __launch_bounds__(TC_THREADS, 1) k_probe_tc(const __grid_constant__ CUtensorMap mapA,
+                                                            const __grid_constant__ CUtensorMap mapB, int nq, int k,
+                                                            int d, int tiles_per_cta, const float *__restrict__ cn32,
+                                                            float *__restrict__ approx)
+{
+    extern __shared__ __align__(1024) unsigned char tsm[];
+    unsigned char *ring = (unsigned char *)(((uintptr_t)tsm + 1023) & ~(uintptr_t)1023);
+    uint64_t *full = (uint64_t *)(ring + TC_STAGES * TC_STAGE_BYTES);
+    uint64_t *empty = full + TC_STAGES;
+    uint64_t *tfull = empty + TC_STAGES;    // [2]
+    uint64_t *tempty = tfull + 2;           // [2]
+    uint32_t *tmem_slot = (uint32_t *)(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m0 = blockIdx.x * TC_BM;
+    const int ntiles = (k + TC_BN - 1) / TC_BN;
+    const int t_begin = blockIdx.y * tiles_per_cta;
+    const int t_end = min(ntiles, t_begin + tiles_per_cta);
+    const int kb_n = (d + TC_BK - 1) / TC_BK;
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < TC_STAGES; s++) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, 1);
+        }
+        for (int b = 0; b < 2; b++) {
+            mbar_init(tfull + b, 1);
+            mbar_init(tempty + b, 4);       // one arrival per epilogue warp
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"((uint64_t)&mapA) : "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"((uint64_t)&mapB) : "memory");
+    }
+    if (warp == 1) {   // TMEM: 2 accumulators x 256 fp32 columns
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(su32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {   // ---------------- TMA producer
+            int s = 0;
+            uint32_t ph = 0;
+            for (int t = t_begin; t < t_end; t++) {
+                for (int kb = 0; kb < kb_n; kb++) {
+                    mbar_wait(empty + s, ph ^ 1u);
+                    unsigned char *sa = ring + s * TC_STAGE_BYTES;
+                    mbar_expect_tx(full + s, TC_STAGE_BYTES);
+                    tma_load_2d(sa, &mapA, full + s, kb * TC_BK, m0);
+                    tma_load_2d(sa + TC_A_BYTES, &mapB, full + s, kb * TC_BK, t * TC_BN);
+                    if (++s == TC_STAGES) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {   // ---------------- MMA issuer
+            constexpr uint32_t idesc = tf32_idesc(TC_BM, TC_BN);
+            int s = 0;
+            uint32_t ph = 0;
+            int it = 0;
+            for (int t = t_begin; t < t_end; t++, it++) {
+                const int b = it & 1;
+                mbar_wait(tempty + b, (((uint32_t)it >> 1) & 1u) ^ 1u);
+                asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+                const uint32_t dt = tmem + (uint32_t)(b * TC_BN);
+                for (int kb = 0; kb < kb_n; kb++) {
+                    mbar_wait(full + s, ph);
+                    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+                    const uint32_t sa = su32(ring + s * TC_STAGE_BYTES);
+                    const uint32_t sb = sa + TC_A_BYTES;
+#pragma unroll
+                    for (int kk = 0; kk < TC_BK / 8; kk++) {
+                        const uint64_t da = sw128_desc(sa + kk * 32);
+                        const uint64_t db = sw128_desc(sb + kk * 32);
+                        const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
+                        asm volatile(
+                            "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                            " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(dt),
+                            "l"(da), "l"(db), "r"(idesc), "r"(acc)
+                            : "memory");
+                    }
+                    // frees the smem stage once these MMAs have read it
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                                     su32(empty + s))
+                                 : "memory");
+                    if (++s == TC_STAGES) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                                 su32(tfull + b))
+                             : "memory");
+            }
+        }
+    } else {   // ---------------------------- epilogue warps 2..5
+        const int quad = warp & 3;            // TMEM lanes 32 quad .. 32 quad + 31
+        const int row = m0 + quad * 32 + lane;
+        int it = 0;
+        for (int t = t_begin; t < t_end; t++, it++) {
+            const int b = it & 1;
+            mbar_wait(tfull + b, ((uint32_t)it >> 1) & 1u);
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            const int n0 = t * TC_BN;
+#pragma unroll 1
+            for (int c = 0; c < TC_BN; c += 32) {
+                uint32_t v[32];
+                const uint32_t ta = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * TC_BN + c);
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                      "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                      "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+                      "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+                      "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                    : "r"(ta));
+                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+                if (row < nq) {
+                    float *dst = approx + (int64_t)row * k + n0 + c;
+                    if (n0 + c + 32 <= k && (k & 3) == 0) {
+#pragma unroll
+                        for (int j = 0; j < 32; j += 4) {
+                            const float4 cn = __ldg((const float4 *)(cn32 + n0 + c + j));
+                            float4 o;
+                            o.x = cn.x - 2.0f * __uint_as_float(v[j]);
+                            o.y = cn.y - 2.0f * __uint_as_float(v[j + 1]);
+                            o.z = cn.z - 2.0f * __uint_as_float(v[j + 2]);
+                            o.w = cn.w - 2.0f * __uint_as_float(v[j + 3]);
+                            *(float4 *)(dst + j) = o;
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; j++)
+                            if (n0 + c + j < k) dst[j] = cn32[n0 + c + j] - 2.0f * __uint_as_float(v[j]);
+                    }
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty + b);
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+}
+
+// ------------------------------------------------------------------ host
+static int make_map(ProbeTC *tc, CUtensorMap *map, const float *ptr, int rows, int d, int box_rows)
+{
+    cuuint64_t gdim[2] = {(cuuint64_t)d, (cuuint64_t)rows};
+    cuuint64_t gstride[1] = {(cuuint64_t)d * 4};
+    cuuint32_t box[2] = {TC_BK, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = tc->encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)ptr, gdim, gstride, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        mrq_set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+        return MRQ_ECUDA;
+    }
+    return MRQ_OK;
+}
+
+int mrq_probe_tc_init(mrq_index *ix)
+{
+    ix->probe_tc = nullptr;
+    // TMA needs 16-byte row strides; the tensor-core screen is used when d % 4 == 0
+    if (ix->d % 4 != 0) return MRQ_OK;
+    ProbeTC *tc = new ProbeTC();
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) != cudaSuccess || !fn ||
+        qr != cudaDriverEntryPointSuccess) {
+        delete tc;
+        mrq_set_error("cuTensorMapEncodeTiled unavailable");
+        return MRQ_ECUDA;
+    }
+    tc->encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    int rc = make_map(tc, &tc->mapB, ix->C32, ix->k, ix->d, TC_BN);
+    if (rc != MRQ_OK) {
+        delete tc;
+        return rc;
+    }
+    cudaError_t e = cudaFuncSetAttribute(k_probe_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
+    if (e != cudaSuccess) {
+        delete tc;
+        mrq_set_error("k_probe_tc smem attribute: %s", cudaGetErrorString(e));
+        return MRQ_ECUDA;
+    }
+    tc->enabled = true;
+    ix->probe_tc = tc;
+    return MRQ_OK;
+}
+
+void mrq_probe_tc_free(mrq_index *ix)
+{
+    delete (ProbeTC *)ix->probe_tc;
+    ix->probe_tc = nullptr;
+}
+
+bool mrq_probe_tc_enabled(const mrq_index *ix)
+{
+    return ix->probe_tc && ((const ProbeTC *)ix->probe_tc)->enabled && !ix->force_cuda_core_probe;
+}
+
+double mrq_probe_tc_kappa(const mrq_index *ix)
+{
+    return std::ldexp(1.0, -9) + (double)ix->d * std::ldexp(1.0, -22) + std::ldexp(1.0, -20);
+}
+
+int mrq_probe_tc_run(mrq_index *ix, const float *qd32, int64_t nq, float *approx, cudaStream_t st)
+{
+    ProbeTC *tc = (ProbeTC *)ix->probe_tc;
+    CUtensorMap mapA;
+    int rc = make_map(tc, &mapA, qd32, (int)nq, ix->d, TC_BM);
+    if (rc != MRQ_OK) return rc;
+    const int mblocks = (int)((nq + TC_BM - 1) / TC_BM);
+    const int ntiles = (ix->k + TC_BN - 1) / TC_BN;
+    // split the centroid tiles so the grid covers the SMs about once
+    int gy = (ix->sm_count + mblocks - 1) / mblocks;
+    gy = std::max(1, std::min(gy, ntiles));
+    const int per = (ntiles + gy - 1) / gy;
+    gy = (ntiles + per - 1) / per;
+    k_probe_tc<<<dim3(mblocks, gy), TC_THREADS, TC_SMEM, st>>>(mapA, tc->mapB, (int)nq, ix->k, ix->d, per, ix->cn32,
+                                                                approx);
+    MRQ_CUDA_TRY(cudaGetLastError());
+    return MRQ_OK;
 }

@@ -1,8 +1,8 @@
 // mrq_stages.cu -- seeds (a4), stage 2 (a6), exact re-rank (a7) and top-K
 // (a8): one warp per query.  The selections keep a warp-private sorted top-L
 // list in shared memory (WarpTop), so a query's candidates stream through the
-// warp once; rows are gathered through a 32x33 shared tile so global loads
-// stay 128-byte coalesced and each lane sums its own row left to right (the
+// warp once; rows are gathered through per-warp shared-memory stages
+// (warp_gather_rows) and each lane sums its own row left to right (the
 // canonical order of DESIGN.md).
 #include <algorithm>
 
@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(256) k_seed_w(
     if (q >= nq) return;
     float *tile = (float *)wsm + warp * MRQ_RG_FLOATS;
     SelItem *lst = (SelItem *)((float *)wsm + wpb * MRQ_RG_FLOATS) + (size_t)warp * Kp;
-    WarpTop top;
+    WarpSel top;
     top.init(lst, Kp);
     const double eps_r = eps_r_arr[q];
     const double *qrow = qp + q * D;
@@ -66,10 +66,11 @@ __global__ void __launch_bounds__(256) k_seed_w(
         }
         nloc += (int)sz;
     }
+    top.finish();
     const int ns0 = nloc < Kp ? nloc : Kp;
     // exact distances of S0: HEAD over the head rows, then continued over the tail rows
     warp_rows(aligned, heads, d, 0, d, qrow, ns0, tile, [&](int e) { return lst[e].pay; },
-              [&](int) { return 0.0; }, [&](int e, bool v, double acc) {
+              [&](int, uint32_t) { return 0.0; }, [&](int e, bool v, double acc) {
                   if (v) {
                       s0_pos[q * Kp + e] = lst[e].pay;
                       s0_id[q * Kp + e] = lst[e].id;
@@ -79,7 +80,7 @@ __global__ void __launch_bounds__(256) k_seed_w(
     __syncwarp();
     if (D > d)
         warp_rows(aligned, tails, D - d, 0, D - d, qrow + d, ns0, tile, [&](int e) { return s0_pos[q * Kp + e]; },
-                  [&](int e) { return s0_exact[q * Kp + e]; }, [&](int e, bool v, double acc) {
+                  [&](int e, uint32_t) { return s0_exact[q * Kp + e]; }, [&](int e, bool v, double acc) {
                       if (v) s0_exact[q * Kp + e] = acc;
                   });
     __syncwarp();
@@ -107,6 +108,7 @@ __global__ void __launch_bounds__(256) k_seed_w(
         }
         top.offer(it, v);
     }
+    top.finish();
     if (lane == 0) {
         s0_cnt[q] = ns0;
         tau0[q] = lst[K - 1].key;    // +inf while fewer than K distinct seeds
@@ -123,34 +125,76 @@ __device__ __forceinline__ void f2_compact(int64_t q, int mode, int n1, uint64_t
 {
     const int lane = threadIdx.x & 31;
     uint32_t at = 0;
-    for (int g = 0; g < n1; g += 32) {
-        const int e = g + lane;
-        bool pass = false;
-        if (e < n1) pass = (mode != 0) || (f1_diso[base + e] - eps_r < tau1);
-        const unsigned bal = __ballot_sync(0xffffffffu, pass);
-        if (pass) {
-            const uint32_t o = at + __popc(bal & ((1u << lane) - 1u));
-            f2_pos[base + o] = f1_pos[base + e];
-            f2_head[base + o] = f1_head[base + e];
+    for (int g0 = 0; g0 < n1; g0 += 128) {
+        double dv[4];
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const int e = g0 + 32 * j + lane;
+            dv[j] = e < n1 ? f1_diso[base + e] : 0.0;
         }
-        at += __popc(bal);
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const int e = g0 + 32 * j + lane;
+            bool pass = false;
+            if (e < n1) pass = (mode != 0) || (dv[j] - eps_r < tau1);
+            const unsigned bal = __ballot_sync(0xffffffffu, pass);
+            if (pass) {
+                const uint32_t o = at + __popc(bal & ((1u << lane) - 1u));
+                f2_pos[base + o] = f1_pos[base + e];
+                f2_head[base + o] = f1_head[base + e];
+            }
+            at += __popc(bal);
+        }
     }
     if (lane == 0) f2_cnt[q] = at;
 }
 
-// Stage 2 (Alg.2 L13 P:315; "Optimization" P:327, reading R-6): for every F1
-// entry HEAD = ||x_d - q_d||^2 (left to right over i < d) and
-// dis_o' = (HEAD + ||x_r||^2) + ||q_r||^2.  TIGHT: S1 = the K' smallest
+// Stage 2, gather half (Alg.2 L13 P:315; "Optimization" P:327, reading R-6):
+// block per query, its warps split the query's F1 entries in 32-row groups;
+// for every F1 entry HEAD = ||x_d - q_d||^2 (left to right over i < d),
+// dis_o' = (HEAD + ||x_r||^2) + ||q_r||^2, and the global id, written to the
+// entry's F1 slot (f1_head, f1_diso, f1_id).
+__global__ void __launch_bounds__(256) k_head_b(
+    int aligned, int D, int d, const uint32_t *__restrict__ ids, const float *__restrict__ heads,
+    const float *__restrict__ xr2, const double *__restrict__ qp, const double *__restrict__ qr2_arr,
+    const uint64_t *__restrict__ f1_off, const uint32_t *__restrict__ f1_cnt, const uint32_t *__restrict__ f1_pos,
+    double *__restrict__ f1_head, double *__restrict__ f1_diso, uint32_t *__restrict__ f1_id)
+{
+    extern __shared__ unsigned char wsm[];
+    const int warp = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+    const int64_t q = blockIdx.x;
+    float *tile = (float *)wsm + warp * MRQ_RG_FLOATS;
+    const uint64_t base = f1_off[q];
+    const int n1 = (int)f1_cnt[q];
+    const double qr2 = qr2_arr[q];
+    float xr2v = 0.f;   // ||x_r||^2 and id of the lane's row, loaded while the row is in flight
+    uint32_t idv = 0;
+    warp_rows(aligned, heads, d, 0, d, qp + q * D, n1, tile, [&](int e) { return f1_pos[base + e]; },
+              [&](int, uint32_t slot) {
+                  xr2v = xr2[slot];
+                  idv = ids[slot];
+                  return 0.0;
+              },
+              [&](int e, bool v, double head) {
+                  if (v) {
+                      f1_head[base + e] = head;
+                      f1_diso[base + e] = (head + (double)xr2v) + qr2;
+                      f1_id[base + e] = idv;
+                  }
+              },
+              warp, wpb);
+}
+
+// Stage 2, decision half, warp per query.  TIGHT: S1 = the K' smallest
 // (dis_o', id) of F1, their exact distances (HEAD continued over the tail),
 // tau1 = K-th smallest distinct exact over S0 u S1; LOOSE: tau1 = tau0.
 // F2 as in f2_compact.  Sharded TIGHT (xout != NULL): the local S1 goes to
 // the exchange and k_xmerge / k_f2_w finish tau1 and F2.
 __global__ void __launch_bounds__(256) k_stage2_w(
-    int64_t nq, int aligned, int mode, int tight, int K, int Kp, int D, int d, const uint32_t *__restrict__ ids,
-    const float *__restrict__ heads, const float *__restrict__ tails, const float *__restrict__ xr2,
-    const double *__restrict__ qp, const double *__restrict__ qr2_arr, const double *__restrict__ eps_r_arr,
-    const double *__restrict__ tau0_arr, const uint64_t *__restrict__ f1_off, const uint32_t *__restrict__ f1_cnt,
-    const uint32_t *__restrict__ f1_pos, double *__restrict__ f1_head, double *__restrict__ f1_diso,
+    int64_t nq, int aligned, int mode, int tight, int K, int Kp, int D, int d, const float *__restrict__ tails,
+    const double *__restrict__ qp, const double *__restrict__ eps_r_arr, const double *__restrict__ tau0_arr,
+    const uint64_t *__restrict__ f1_off, const uint32_t *__restrict__ f1_cnt, const uint32_t *__restrict__ f1_pos,
+    const double *__restrict__ f1_head, const double *__restrict__ f1_diso, const uint32_t *__restrict__ f1_id,
     const uint32_t *__restrict__ s0_cnt, const uint32_t *__restrict__ s0_id, const double *__restrict__ s0_exact,
     uint32_t *__restrict__ s1_cnt, uint32_t *__restrict__ s1_pos, uint32_t *__restrict__ s1_id,
     double *__restrict__ s1_exact, double *__restrict__ tau1_arr, uint32_t *__restrict__ f2_cnt,
@@ -163,36 +207,41 @@ __global__ void __launch_bounds__(256) k_stage2_w(
     float *tile = (float *)wsm + warp * MRQ_RG_FLOATS;
     SelItem *lst = (SelItem *)((float *)wsm + wpb * MRQ_RG_FLOATS) + (size_t)warp * Kp;
     const bool sel1 = mode == 0 && tight;
-    WarpTop top;
-    top.init(lst, Kp);
     const uint64_t base = f1_off[q];
     const int n1 = (int)f1_cnt[q];
-    const double qr2 = qr2_arr[q], eps_r = eps_r_arr[q];
+    const double eps_r = eps_r_arr[q];
     const double *qrow = qp + q * D;
-    warp_rows(aligned, heads, d, 0, d, qrow, n1, tile, [&](int e) { return f1_pos[base + e]; },
-              [&](int) { return 0.0; }, [&](int e, bool v, double head) {
-                  SelItem it = sel_inf();
-                  if (v) {
-                      const uint32_t slot = f1_pos[base + e];
-                      const double diso = (head + (double)xr2[slot]) + qr2;
-                      f1_head[base + e] = head;
-                      f1_diso[base + e] = diso;
-                      it.key = diso;
-                      it.id = ids[slot];
-                      it.pay = (uint32_t)e;
-                  }
-                  if (sel1) top.offer(it, v);
-              });
-    __syncwarp();
     double tau1 = tau0_arr[q];
     if (sel1) {
+        WarpSel top;
+        top.init(lst, Kp);
+        for (int g0 = 0; g0 < n1; g0 += 128) {
+            double kv[4];
+            uint32_t iv[4];
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const int e = g0 + 32 * j + lane;
+                kv[j] = e < n1 ? f1_diso[base + e] : 0.0;
+                iv[j] = e < n1 ? f1_id[base + e] : 0u;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const int e = g0 + 32 * j + lane;
+                SelItem it;
+                it.key = kv[j];
+                it.id = iv[j];
+                it.pay = (uint32_t)e;
+                top.offer(it, e < n1);
+            }
+        }
+        top.finish();
         const int ns1 = n1 < Kp ? n1 : Kp;
         for (int e = lane; e < ns1; e += 32) {
             s1_pos[q * Kp + e] = f1_pos[base + lst[e].pay];
             s1_id[q * Kp + e] = lst[e].id;
         }
         __syncwarp();
-        auto s1_init = [&](int e) { return f1_head[base + lst[e].pay]; };
+        auto s1_init = [&](int e, uint32_t) { return f1_head[base + lst[e].pay]; };
         auto s1_done = [&](int e, bool v, double acc) {
             if (v) s1_exact[q * Kp + e] = acc;
         };
@@ -200,7 +249,7 @@ __global__ void __launch_bounds__(256) k_stage2_w(
             warp_rows(aligned, tails, D - d, 0, D - d, qrow + d, ns1, tile, [&](int e) { return s1_pos[q * Kp + e]; },
                       s1_init, s1_done);
         else
-            for (int e = lane; e < ns1; e += 32) s1_exact[q * Kp + e] = s1_init(e);
+            for (int e = lane; e < ns1; e += 32) s1_exact[q * Kp + e] = s1_init(e, 0u);
         __syncwarp();
         if (xout) {   // sharded TIGHT: exchange the local S1
             for (int e = lane; e < Kp; e += 32) {
@@ -213,7 +262,7 @@ __global__ void __launch_bounds__(256) k_stage2_w(
             }
             return;
         }
-        // tau1 = K-th smallest distinct exact over S0 u S1 (duplicates dropped by WarpTop)
+        // tau1 = K-th smallest distinct exact over S0 u S1 (duplicates dropped by the selection)
         top.init(lst, K);
         const int ns0 = (int)s0_cnt[q];
         for (int g = 0; g < ns0 + ns1; g += 32) {
@@ -228,6 +277,7 @@ __global__ void __launch_bounds__(256) k_stage2_w(
             }
             top.offer(it, v);
         }
+        top.finish();
         tau1 = lst[K - 1].key;
         if (lane == 0) s1_cnt[q] = ns1;
     } else if (lane == 0) {
@@ -270,7 +320,7 @@ __global__ void __launch_bounds__(256) k_rerank_w(int64_t nq, int aligned, int D
     const double *qt = qp + q * D + d;
     if (D > d)
         warp_rows(aligned, tails, D - d, 0, D - d, qt, n2, tile, [&](int e) { return f2_pos[base + e]; },
-                  [&](int e) { return f2_head[base + e]; }, [&](int e, bool v, double acc) {
+                  [&](int e, uint32_t) { return f2_head[base + e]; }, [&](int e, bool v, double acc) {
                       if (v) f2_exact[base + e] = acc;
                   });
     else
@@ -299,7 +349,7 @@ __global__ void __launch_bounds__(256) k_topk_w(
     const int64_t q = (int64_t)blockIdx.x * wpb + warp;
     if (q >= nq) return;
     SelItem *lst = (SelItem *)wsm + (size_t)warp * K;
-    WarpTop top;
+    WarpSel top;
     top.init(lst, K);
     const int ns0 = (int)s0_cnt[q], ns1 = (int)s1_cnt[q], n2 = (int)f2_cnt[q];
     const uint64_t base = f1_off[q];
@@ -329,6 +379,7 @@ __global__ void __launch_bounds__(256) k_topk_w(
         }
         top.offer(it, v);
     }
+    top.finish();
     if (xout) {
         for (int i = lane; i < K; i += 32) {
             XItem x;
@@ -388,7 +439,7 @@ __global__ void __launch_bounds__(128) k_xmerge(int kind, int64_t nq, int world,
     const int64_t q = (int64_t)blockIdx.x * wpb + warp;
     if (q >= nq) return;
     SelItem *lst = (SelItem *)wsm + (size_t)warp * L;
-    WarpTop top;
+    WarpSel top;
     top.init(lst, L);
     for (int r = 0; r < world; r++) {
         const XItem *src = recv + ((int64_t)r * nq + q) * L;
@@ -408,6 +459,7 @@ __global__ void __launch_bounds__(128) k_xmerge(int kind, int64_t nq, int world,
             top.offer(it, v);
         }
     }
+    top.finish();
     if (kind == 2) {
         for (int i = lane; i < K; i += 32) {
             const bool ok = lst[i].id != MRQ_PAD_ID;
@@ -447,6 +499,7 @@ __global__ void __launch_bounds__(128) k_xmerge(int kind, int64_t nq, int world,
         }
         top.offer(it, v);
     }
+    top.finish();
     if (lane == 0) {
         s_cnt[q] = (uint32_t)n;
         tau[q] = lst[K - 1].key;
@@ -503,14 +556,22 @@ int launch_seed_w(int W, const StageArgs &a, cudaStream_t st)
 
 int launch_stage2_w(const StageArgs &a, cudaStream_t st)
 {
-    const size_t per = MRQ_RG_FLOATS * 4 + (size_t)a.Kp * sizeof(SelItem);
+    {   // gather half: block per query, 8 warps split the F1 rows
+        const int wpb = 8;
+        const size_t smem = (size_t)wpb * MRQ_RG_FLOATS * 4;
+        int rc = set_attr((const void *)k_head_b, smem);
+        if (rc) return rc;
+        k_head_b<<<(unsigned)a.nq, wpb * 32, smem, st>>>(a.aligned, a.D, a.d, a.ids, a.heads, a.xr2, a.qp, a.qr2,
+                                                          a.f1_off, a.f1_cnt, a.f1_pos, a.f1_head, a.f1_diso, a.f1_id);
+    }
+    const size_t per = MRQ_RG_FLOATS * 4 + (size_t)std::max(a.Kp, a.K) * sizeof(SelItem);
     const int wpb = warps_for(per);
     const size_t smem = per * wpb;
     int rc = set_attr((const void *)k_stage2_w, smem);
     if (rc) return rc;
     k_stage2_w<<<(unsigned)((a.nq + wpb - 1) / wpb), wpb * 32, smem, st>>>(
-        a.nq, a.aligned, a.mode, a.tight, a.K, a.Kp, a.D, a.d, a.ids, a.heads, a.tails, a.xr2, a.qp, a.qr2, a.eps_r, a.tau0,
-        a.f1_off, a.f1_cnt, a.f1_pos, a.f1_head, a.f1_diso, a.s0_cnt, a.s0_id, a.s0_exact, a.s1_cnt, a.s1_pos, a.s1_id,
+        a.nq, a.aligned, a.mode, a.tight, a.K, a.Kp, a.D, a.d, a.tails, a.qp, a.eps_r, a.tau0, a.f1_off, a.f1_cnt,
+        a.f1_pos, a.f1_head, a.f1_diso, a.f1_id, a.s0_cnt, a.s0_id, a.s0_exact, a.s1_cnt, a.s1_pos, a.s1_id,
         a.s1_exact, a.tau1, a.f2_cnt, a.f2_pos, a.f2_head, a.xout);
     return MRQ_OK;
 }
@@ -587,7 +648,7 @@ __global__ void __launch_bounds__(128) k_probe_select_w(
     if (q >= nq) return;
     SelItem *lst = (SelItem *)wsm + (size_t)warp * np;
     const float *row = approx + q * k;
-    WarpTop top;
+    WarpSel top;
     top.init(lst, np);
     for (int c0 = 0; c0 < k; c0 += 32) {
         const int c = c0 + lane;
@@ -599,6 +660,7 @@ __global__ void __launch_bounds__(128) k_probe_select_w(
         }
         top.offer(it, c < k);
     }
+    top.finish();
     const double g = qnorm[q] + cmax;
     const double thr = lst[np - 1].key + 2.0 * (kappa * (g * g));
     uint32_t *cq = cand + q * k;
@@ -630,6 +692,7 @@ __global__ void __launch_bounds__(128) k_probe_select_w(
         }
         top.offer(it, e < nc);
     }
+    top.finish();
     for (int p = lane; p < np; p += 32) {
         const bool ok = lst[p].id != 0xFFFFFFFFu;
         probe[q * np + p] = ok ? lst[p].id : 0xFFFFFFFFu;

@@ -218,3 +218,29 @@ def test_empty_batch_and_errors(case):
     with pytest.raises(m.MRQError) as e:
         gx.search(case["Q"][:2], K=10, nprobe=case["ox"].k + 1)
     assert e.value.code == -1
+
+
+def test_probe_tensor_core_screen_bound(case):
+    """The tcgen05 tf32 screen a_c = ||c||^2 - 2<q_d, c> stays within the proven
+    delta_q = kappa (||q_d|| + max||c||)^2 of the exact key, and
+    the CUDA-core screen gives the same probe lists (both are rescored exactly)."""
+    gx, bf = case["gx"], case["bf"]
+    d, k = case["d"], bf.k
+    Q = case["Q"]
+    np_ = min(case["nprobe"][-1], k)
+    g1 = gx.search(Q, K=10, nprobe=np_)
+    approx = gx.fetch("approx", "f32").reshape(Q.shape[0], k).astype(np.float64)
+    qp = gx.fetch("qp", "f64").reshape(Q.shape[0], -1)[:, :d]
+    C = bf.C.astype(np.float64)
+    key = (C * C).sum(1)[None, :] - 2.0 * qp @ C.T
+    cmax = np.sqrt((C * C).sum(1).max())
+    kappa = 2.0 ** -9 + d * 2.0 ** -22 + 2.0 ** -20
+    bound = kappa * (np.sqrt((qp * qp).sum(1)) + cmax) ** 2
+    err = np.abs(approx - key)
+    assert np.all(err <= bound[:, None]), float((err / bound[:, None]).max())
+    probe_tc = gx.fetch("probe", "u32").copy()
+    case["m"].mrq_debug_set(gx.h, "cuda_core_probe", 1)
+    g2 = gx.search(Q, K=10, nprobe=np_)
+    case["m"].mrq_debug_set(gx.h, "cuda_core_probe", 0)
+    assert np.array_equal(probe_tc, gx.fetch("probe", "u32"))
+    assert np.array_equal(g1[0], g2[0]) and np.array_equal(g1[1], g2[1])
