@@ -454,9 +454,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
 
     // ---- a3: per-(query, list) quantization into bit-planes
     {
-        const int64_t warps = nq * np;
-        k_quant<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(probe, probe_qn2, nq, np, d, W, r0, ix->Rc, qr2, p->eps0,
-                                                             planes, qconst);
+        launch_quant(probe, probe_qn2, nq, np, d, W, r0, ix->Rc, qr2, p->eps0, planes, qconst, st);
         k_cand_count<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(probe, nq, np, ix->list_size, cand_cnt);
         k_exclusive_scan<<<1, 1024, 0, st>>>(cand_cnt, nq, f1_off);
     }

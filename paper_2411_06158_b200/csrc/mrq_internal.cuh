@@ -332,41 +332,134 @@ struct WarpTopReg {
     }
 };
 
+// Register-resident warp select for streams of DISTINCT items, L <= 32
+// (bitonic, in the manner of warp-select top-k): the warp keeps its 32
+// smallest items sorted across lanes; a batch with any item below the L-th
+// smallest is sorted descending (bitonic sort over lanes), merged by an
+// elementwise min (a bitonic sequence holding the 32 smallest of both) and
+// re-sorted ascending by a bitonic merge -- 20 compare-exchange steps per
+// useful batch, independent of how many of its items enter.
+struct WarpTopBitonic {
+    double key;
+    uint32_t id, pay;
+    int L;
+
+    __device__ __forceinline__ static bool lt(double ak, uint32_t ai, double bk, uint32_t bi)
+    {
+        return ak < bk || (ak == bk && ai < bi);
+    }
+    // compare-exchange with lane ^ j; keep the smaller item iff `keep_min`
+    __device__ __forceinline__ static void cx(double &k, uint32_t &i, uint32_t &p, int j, bool keep_min)
+    {
+        const double ok = __shfl_xor_sync(0xffffffffu, k, j);
+        const uint32_t oi = __shfl_xor_sync(0xffffffffu, i, j);
+        const uint32_t op = __shfl_xor_sync(0xffffffffu, p, j);
+        const bool other_less = lt(ok, oi, k, i);
+        if (other_less == keep_min) {
+            k = ok;
+            i = oi;
+            p = op;
+        }
+    }
+    __device__ __forceinline__ void init(int L_)
+    {
+        L = L_;
+        key = __longlong_as_double(0x7ff0000000000000ll);
+        id = 0xFFFFFFFFu;
+        pay = 0xFFFFFFFFu;
+    }
+    __device__ __forceinline__ void offer(const SelItem &it, bool valid)
+    {
+        const int lane = threadIdx.x & 31;
+        const double tk = __shfl_sync(0xffffffffu, key, L - 1);
+        const uint32_t ti = __shfl_sync(0xffffffffu, id, L - 1);
+        const bool pass = valid && lt(it.key, it.id, tk, ti);
+        if (!__any_sync(0xffffffffu, pass)) return;
+        double xk = pass ? it.key : __longlong_as_double(0x7ff0000000000000ll);
+        uint32_t xi = pass ? it.id : 0xFFFFFFFFu, xp = pass ? it.pay : 0xFFFFFFFFu;
+        // bitonic sort of the batch, descending across lanes
+#pragma unroll
+        for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                const bool up = (lane & k) != 0;           // k = 32: all descending
+                const bool lower = (lane & j) == 0;
+                cx(xk, xi, xp, j, lower == up);
+            }
+        }
+        // elementwise min with the ascending list: bitonic, holds the 32 smallest
+        if (lt(xk, xi, key, id)) {
+            key = xk;
+            id = xi;
+            pay = xp;
+        }
+        // bitonic merge, ascending
+#pragma unroll
+        for (int j = 16; j > 0; j >>= 1) cx(key, id, pay, j, (lane & j) == 0);
+    }
+};
+
+// The L-th smallest (L <= 32) of the 32 lane values v (bitonic sort across
+// lanes).  Used as a selection pre-threshold: if every lane's v is the
+// minimum of its share of a stream, at least L stream items are <= the result.
+__device__ __forceinline__ double warp_kth_smallest(double v, int L)
+{
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            const double o = __shfl_xor_sync(0xffffffffu, v, j);
+            const bool up = (lane & k) == 0;
+            const bool lower = (lane & j) == 0;
+            const bool keep_min = lower == up;
+            v = keep_min ? fmin(v, o) : fmax(v, o);
+        }
+    }
+    return __shfl_sync(0xffffffffu, v, L - 1);
+}
+
 // Selection of the L smallest distinct (key, id): registers for L <= 32,
 // the shared-memory list otherwise.  After finish() the sorted items are in
 // buf[0 .. L) either way.
 struct WarpSel {
     WarpTop sm;
     WarpTopReg rg;
-    bool reg;
+    WarpTopBitonic bt;
+    int mode;   // 0 shared-memory list, 1 register insertion (dedup), 2 register bitonic (distinct items)
 
-    __device__ __forceinline__ void init(SelItem *buf, int L)
+    // distinct: the caller guarantees no (key, id) is offered twice
+    __device__ __forceinline__ void init(SelItem *buf, int L, bool distinct = false)
     {
-        reg = L <= 32;
+        mode = L > 32 ? 0 : (distinct ? 2 : 1);
         sm.a = buf;
         sm.L = L;
-        if (reg)
+        if (mode == 2)
+            bt.init(L);
+        else if (mode == 1)
             rg.init(L);
         else
             sm.init(buf, L);
     }
     __device__ __forceinline__ void offer(const SelItem &it, bool valid)
     {
-        if (reg)
+        if (mode == 2)
+            bt.offer(it, valid);
+        else if (mode == 1)
             rg.offer(it, valid);
         else
             sm.offer(it, valid);
     }
     __device__ __forceinline__ void finish()
     {
-        if (reg) {
+        if (mode != 0) {
             const int lane = threadIdx.x & 31;
             __syncwarp();
-            if (lane < rg.L) {
+            if (lane < sm.L) {
                 SelItem x;
-                x.key = rg.key;
-                x.id = rg.id;
-                x.pay = rg.pay;
+                x.key = mode == 2 ? bt.key : rg.key;
+                x.id = mode == 2 ? bt.id : rg.id;
+                x.pay = mode == 2 ? bt.pay : rg.pay;
                 sm.a[lane] = x;
             }
         }

@@ -196,171 +196,110 @@ __global__ void __launch_bounds__(256) k_probe_approx(const float *__restrict__ 
         if (q0 + b < nq) approx[(q0 + b) * k + c] = acc[b];
 }
 
-// Exact top-nprobe from a screened distance row (Alg.2 L7).  The
-// screen value a_c of every centroid is within delta_q of the exact
-// ||q_d - c||^2 (bound derived in DESIGN.md "probe exactness"), so every
-// member of the exact top-np has a_c <= a_(np) + 2 delta_q, where a_(np) is the
-// np-th smallest screen value.  Those candidates are rescored in fp64 (left
-// to right over i) and the np smallest (qn2, c) are kept.  If the candidate
-// set exceeds `cap`, all k centroids are rescored.
-//
-// Screens: kind 0 = fp32 direct difference (k_probe_approx), kind 1 =
-// ||c||^2 - 2<q,c> from the tf32 tensor-core GEMM (q-independent ||q||^2
-// omitted; the bound is the same shift-free form).
-__global__ void __launch_bounds__(256) k_probe_select(const float *__restrict__ approx, int64_t nq, int k, int d,
-                                                      int np, const double *__restrict__ qp, int D,
-                                                      const double *__restrict__ C, const double *__restrict__ qnorm,
-                                                      double cmax, double kappa, int cap, int S,
-                                                      uint32_t *__restrict__ probe, double *__restrict__ probe_qn2,
-                                                      uint32_t *__restrict__ fallback_cnt)
-{
-    extern __shared__ unsigned char psm[];
-    uint32_t *keys = (uint32_t *)psm;                            // k
-    uint32_t *cand = keys + k;                                   // cap
-    double *qs = (double *)(((uintptr_t)(cand + cap) + 15) & ~(uintptr_t)15);   // d
-    SelItem *buf = (SelItem *)(qs + d);                          // S
-    __shared__ uint32_t hist[256];
-    __shared__ uint32_t sh_sel, sh_rem, sh_n;
-    const int64_t q = blockIdx.x;
-    const float *row = approx + q * k;
-    for (int i = threadIdx.x; i < k; i += blockDim.x) keys[i] = f2key(row[i]);
-    for (int i = threadIdx.x; i < d; i += blockDim.x) qs[i] = qp[q * D + i];
-    if (threadIdx.x == 0) sh_n = 0;
-    __syncthreads();
-    // radix select of the np-th smallest key
-    uint32_t prefix = 0, mask = 0;
-    uint32_t rem = (uint32_t)np;
-    for (int shift = 24; shift >= 0; shift -= 8) {
-        for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
-        __syncthreads();
-        for (int i = threadIdx.x; i < k; i += blockDim.x) {
-            uint32_t key = keys[i];
-            if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            uint32_t cum = 0, sel = 255;
-            for (int b = 0; b < 256; b++) {
-                if (cum + hist[b] >= rem) { sel = b; break; }
-                cum += hist[b];
-            }
-            sh_sel = sel;
-            sh_rem = rem - cum;
-        }
-        __syncthreads();
-        prefix |= sh_sel << shift;
-        mask |= 0xFFu << shift;
-        rem = sh_rem;
-        __syncthreads();
-    }
-    const double a_np = (double)key2f(prefix);
-    const double g = qnorm[q] + cmax;
-    const double thr = a_np + 2.0 * (kappa * (g * g));
-    for (int i = threadIdx.x; i < k; i += blockDim.x) {
-        if ((double)row[i] <= thr) {
-            uint32_t at = atomicAdd(&sh_n, 1u);
-            if (at < (uint32_t)cap) cand[at] = i;
-        }
-    }
-    __syncthreads();
-    const bool all = sh_n > (uint32_t)cap;
-    const int nc = all ? k : (int)sh_n;
-    if (all && threadIdx.x == 0) atomicAdd(fallback_cnt, 1u);
-    auto get = [&](int i) -> SelItem {
-        const uint32_t c = all ? (uint32_t)i : cand[i];
-        const double *cr = C + (int64_t)c * d;
-        double acc = 0.0;
-        for (int j = 0; j < d; j++) {
-            double t = qs[j] - cr[j];
-            acc = acc + t * t;
-        }
-        SelItem s;
-        s.key = acc;
-        s.id = c;
-        s.pay = c;
-        return s;
-    };
-    const int L = min(np, nc);
-    block_select(buf, S, np, nc, get);
-    for (int p = threadIdx.x; p < np; p += blockDim.x) {
-        probe[q * np + p] = p < L ? buf[p].id : 0xFFFFFFFFu;
-        probe_qn2[q * np + p] = p < L ? buf[p].key : __longlong_as_double(0x7ff0000000000000ll);
-    }
-}
-
 // ======================================================================= a3
-// Per (query, probed list), warp-wide (Alg.2 L4-L5; readings
-// A-12/A-13/A-27): r = R q_d - R c (unnormalized), lo/hi = min/max r,
+// Per (query, probed list) (Alg.2 L4-L5; readings R-7): r = R q_d - R c (unnormalized), lo/hi = min/max r,
 // delta = (hi - lo)/15, L_j = clamp(floor((r_j - lo)/delta + 0.5), 0, 15)
 // (all 0 when delta = 0), bit-planes p_b = {j : bit b of L_j}, and the
 // constants of the scan epilogue:
 //   A = 2 lo, Bc = 2 delta, C0 = d lo + delta sum L, g1 = ||q_d-c||^2 + ||q_r||^2,
-//   eb = (2 eps0) ||q_d - c||          (Eq.5 distance-domain scale, A-6)
-__global__ void k_quant(const uint32_t *__restrict__ probe, const double *__restrict__ probe_qn2, int64_t nq,
-                        int np, int d, int W, const double *__restrict__ r0, const double *__restrict__ Rc,
-                        const double *__restrict__ qr2, double eps0, uint32_t *__restrict__ planes,
-                        double *__restrict__ qconst)
+//   eb = (2 eps0) ||q_d - c||          (Eq.5 distance-domain scale, R-5)
+// G lanes per (query, list) pair (32 / G pairs per warp): lane s of a pair
+// holds the E consecutive coordinates j = s E .. s E + E - 1 (E = 8 for d <= 256, 16 up to 512; G = the power of two >= d / E).  min/max
+// and sum L reduce over the G lanes (exact: fmin/fmax and integers), the
+// level expression is the same per coordinate, and a plane word (32 bits)
+// is assembled from 32 / E lanes.
+template <int E>
+__global__ void __launch_bounds__(256) k_quant_g(const uint32_t *__restrict__ probe,
+                                                 const double *__restrict__ probe_qn2, int64_t npairs, int np, int d,
+                                                 int W, int G, const double *__restrict__ r0,
+                                                 const double *__restrict__ Rc, const double *__restrict__ qr2,
+                                                 double eps0, uint32_t *__restrict__ planes,
+                                                 double *__restrict__ qconst)
 {
-    const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
-    if (gw >= nq * np) return;
-    const int64_t q = gw / np;
-    const uint32_t c = probe[gw];
-    uint32_t *pl = planes + gw * (MRQ_BQ * W);
-    double *qc = qconst + gw * 8;
-    if (c == 0xFFFFFFFFu) {          // fewer than np lists exist
-        for (int i = lane; i < MRQ_BQ * W; i += 32) pl[i] = 0;
-        if (lane < 8) qc[lane] = 0.0;
-        return;
-    }
-    const double qn2 = probe_qn2[gw];
-    double lo = __longlong_as_double(0x7ff0000000000000ll), hi = -lo;
-    double rv[16];
+    const int P = 32 / G;
+    const int sub = lane / G, s = lane - sub * G;
+    const int64_t gw = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * P + sub;
+    const bool pv = gw < npairs;
+    const int64_t q = pv ? gw / np : 0;
+    const uint32_t c = pv ? probe[gw] : 0xFFFFFFFFu;
+    const bool ok = c != 0xFFFFFFFFu;
+    const double INF = __longlong_as_double(0x7ff0000000000000ll);
+    double rv[E];
+    double lo = INF, hi = -INF;
 #pragma unroll
-    for (int w = 0; w < 16; w++) {
-        if (w < W) {
-            const int j = w * 32 + lane;
-            if (j < d) {
-                rv[w] = r0[q * d + j] - Rc[(int64_t)c * d + j];
-                lo = fmin(lo, rv[w]);
-                hi = fmax(hi, rv[w]);
-            }
+    for (int t = 0; t < E; t++) {
+        const int j = s * E + t;
+        rv[t] = 0.0;
+        if (ok && j < d) {
+            rv[t] = r0[q * d + j] - Rc[(int64_t)c * d + j];
+            lo = fmin(lo, rv[t]);
+            hi = fmax(hi, rv[t]);
         }
     }
-    for (int o = 16; o > 0; o >>= 1) {
-        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    for (int o = G >> 1; o > 0; o >>= 1) {
+        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o, G));
+        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o, G));
     }
     const double delta = (hi - lo) / 15.0;
     int sumL = 0;
+    uint32_t bits[MRQ_BQ] = {0u, 0u, 0u, 0u};
 #pragma unroll
-    for (int w = 0; w < 16; w++) {
-        if (w < W) {
-            const int j = w * 32 + lane;
-            int v = 0;
-            if (j < d && delta > 0.0) {
-                double f = floor((rv[w] - lo) / delta + 0.5);
-                v = f < 0.0 ? 0 : (f > 15.0 ? 15 : (int)f);
-            }
-            sumL += v;
+    for (int t = 0; t < E; t++) {
+        const int j = s * E + t;
+        int v = 0;
+        if (ok && j < d && delta > 0.0) {
+            const double f = floor((rv[t] - lo) / delta + 0.5);
+            v = f < 0.0 ? 0 : (f > 15.0 ? 15 : (int)f);
+        }
+        sumL += v;
 #pragma unroll
-            for (int b = 0; b < MRQ_BQ; b++) {
-                unsigned word = __ballot_sync(0xffffffffu, j < d && ((v >> b) & 1));
-                if (lane == 0) pl[b * W + w] = word;
-            }
+        for (int b = 0; b < MRQ_BQ; b++) bits[b] |= (uint32_t)((v >> b) & 1) << t;
+    }
+    for (int o = G >> 1; o > 0; o >>= 1) sumL += __shfl_xor_sync(0xffffffffu, sumL, o, G);
+    const int L = 32 / E;                     // lanes per plane word
+    const int Lg = L < G ? L : G;
+    const int w = s / L;
+#pragma unroll
+    for (int b = 0; b < MRQ_BQ; b++) {
+        uint32_t x = bits[b] << ((s % L) * E);
+        for (int o = 1; o < Lg; o <<= 1) x |= __shfl_xor_sync(0xffffffffu, x, o, G);
+        if (pv && s % L == 0 && w < W) planes[gw * (MRQ_BQ * W) + b * W + w] = ok ? x : 0u;
+    }
+    if (pv && s == 0) {
+        double *qc = qconst + gw * 8;
+        if (!ok) {
+            for (int i = 0; i < 8; i++) qc[i] = 0.0;
+        } else {
+            const double qn2 = probe_qn2[gw];
+            qc[0] = 2.0 * lo;                                  // A
+            qc[1] = 2.0 * delta;                               // Bc
+            qc[2] = (double)d * lo + delta * (double)sumL;     // C0
+            qc[3] = qn2 + qr2[q];                              // g1
+            qc[4] = (2.0 * eps0) * sqrt(qn2);                  // eb
+            qc[5] = lo;
+            qc[6] = delta;
+            qc[7] = (double)sumL;
         }
     }
-    for (int o = 16; o > 0; o >>= 1) sumL += __shfl_xor_sync(0xffffffffu, sumL, o);
-    if (lane == 0) {
-        qc[0] = 2.0 * lo;                                  // A
-        qc[1] = 2.0 * delta;                               // Bc
-        qc[2] = (double)d * lo + delta * (double)sumL;     // C0
-        qc[3] = qn2 + qr2[q];                              // g1
-        qc[4] = (2.0 * eps0) * sqrt(qn2);                  // eb
-        qc[5] = lo;
-        qc[6] = delta;
-        qc[7] = (double)sumL;
-    }
+}
+
+void launch_quant(const uint32_t *probe, const double *probe_qn2, int64_t nq, int np, int d, int W,
+                  const double *r0, const double *Rc, const double *qr2, double eps0, uint32_t *planes,
+                  double *qconst, cudaStream_t st)
+{
+    const int64_t npairs = nq * np;
+    const int E = d <= 256 ? 8 : 16;
+    int G = 1;
+    while (G * E < d) G <<= 1;
+    if (G > 32) G = 32;
+    const int P = 32 / G;
+    const int64_t warps = (npairs + P - 1) / P;
+    const unsigned grid = (unsigned)((warps + 7) / 8);
+    if (E == 8)
+        k_quant_g<8><<<grid, 256, 0, st>>>(probe, probe_qn2, npairs, np, d, W, G, r0, Rc, qr2, eps0, planes, qconst);
+    else
+        k_quant_g<16><<<grid, 256, 0, st>>>(probe, probe_qn2, npairs, np, d, W, G, r0, Rc, qr2, eps0, planes, qconst);
 }
 
 // Candidate count per query (sum of its probed list sizes) ...

@@ -12,12 +12,9 @@ __global__ void k_qtail(const double *qp, int64_t nq, int D, int d, int W, const
                         double rscale, double m, double *qr2o, double *eps_r, double *r0, float *qd32,
                         double *qnorm);
 __global__ void k_probe_approx(const float *qd32, int64_t nq, int d, int k, const float *C32T, float *approx);
-__global__ void k_probe_select(const float *approx, int64_t nq, int k, int d, int np, const double *qp, int D,
-                               const double *C, const double *qnorm, double cmax, double kappa, int cap, int S,
-                               uint32_t *probe, double *probe_qn2, uint32_t *fallback_cnt);
-__global__ void k_quant(const uint32_t *probe, const double *probe_qn2, int64_t nq, int np, int d, int W,
-                        const double *r0, const double *Rc, const double *qr2, double eps0, uint32_t *planes,
-                        double *qconst);
+void launch_quant(const uint32_t *probe, const double *probe_qn2, int64_t nq, int np, int d, int W,
+                  const double *r0, const double *Rc, const double *qr2, double eps0, uint32_t *planes,
+                  double *qconst, cudaStream_t st);
 __global__ void k_cand_count(const uint32_t *probe, int64_t nq, int np, const uint32_t *list_size, uint64_t *cnt);
 __global__ void k_exclusive_scan(const uint64_t *in, int64_t n, uint64_t *out);
 struct StageArgs {

@@ -32,39 +32,55 @@ __global__ void __launch_bounds__(256) k_seed_w(
     if (q >= nq) return;
     float *tile = (float *)wsm + warp * MRQ_RG_FLOATS;
     SelItem *lst = (SelItem *)((float *)wsm + wpb * MRQ_RG_FLOATS) + (size_t)warp * Kp;
-    WarpSel top;
-    top.init(lst, Kp);
     const double eps_r = eps_r_arr[q];
     const double *qrow = qp + q * D;
     // the pool is defined on GLOBAL list sizes (decision T); a rank scans only
-    // the lists it owns (list_size = 0 for the others)
-    int64_t npool = 0;
+    // the lists it owns (list_size = 0 for the others).  each(it, valid) sees
+    // every pool item (dis', id, slot) of this rank, 32 at a time.
     int nloc = 0;
-    for (int p = 0; p < np && npool < Kp; p++) {
-        const uint32_t c = probe[q * np + p];
-        if (c == 0xFFFFFFFFu) continue;
-        npool += list_size_g[c];
-        const uint32_t off = list_off[c], sz = list_size[c];
-        const uint32_t *pl = planes + (q * np + p) * (MRQ_BQ * W);
-        const double *qc = qconst + (q * np + p) * 8;
-        for (uint32_t e0 = 0; e0 < sz; e0 += 32) {
-            const uint32_t e = e0 + lane;
-            const bool v = e < sz;
-            SelItem it = sel_inf();
-            if (v) {
-                const uint32_t slot = off + e;
-                uint32_t code[W];
+    auto scan_pool = [&](auto each) {
+        int64_t npool = 0;
+        nloc = 0;
+        for (int p = 0; p < np && npool < Kp; p++) {
+            const uint32_t c = probe[q * np + p];
+            if (c == 0xFFFFFFFFu) continue;
+            npool += list_size_g[c];
+            const uint32_t off = list_off[c], sz = list_size[c];
+            const uint32_t *pl = planes + (q * np + p) * (MRQ_BQ * W);
+            const double *qc = qconst + (q * np + p) * 8;
+            for (uint32_t e0 = 0; e0 < sz; e0 += 32) {
+                const uint32_t e = e0 + lane;
+                const bool v = e < sz;
+                SelItem it = sel_inf();
+                if (v) {
+                    const uint32_t slot = off + e;
+                    uint32_t code[W];
 #pragma unroll
-                for (int w = 0; w < W; w++) code[w] = codes[(int64_t)w * npad + slot];
-                double dis;
-                mrq_lb1<W>(code, pl, qc, isd, eps_r, f1[slot], f2[slot], f3[slot], &dis);
-                it.key = dis;
-                it.id = ids[slot];
-                it.pay = slot;
+                    for (int w = 0; w < W; w++) code[w] = codes[(int64_t)w * npad + slot];
+                    double dis;
+                    mrq_lb1<W>(code, pl, qc, isd, eps_r, f1[slot], f2[slot], f3[slot], &dis);
+                    it.key = dis;
+                    it.id = ids[slot];
+                    it.pay = slot;
+                }
+                each(it, v);
             }
-            top.offer(it, v);
+            nloc += (int)sz;
         }
-        nloc += (int)sz;
+    };
+    WarpSel top;
+    top.init(lst, Kp);
+    if (Kp <= 32) {
+        // two passes: U = Kp-th smallest lane minimum bounds the Kp-th smallest
+        // dis' from above, so only items <= U can enter S0
+        double mn = __longlong_as_double(0x7ff0000000000000ll);
+        scan_pool([&](const SelItem &it, bool v) {
+            if (v) mn = fmin(mn, it.key);
+        });
+        const double U = warp_kth_smallest(mn, Kp);
+        scan_pool([&](const SelItem &it, bool v) { top.offer(it, v && it.key <= U); });
+    } else {
+        scan_pool([&](const SelItem &it, bool v) { top.offer(it, v); });
     }
     top.finish();
     const int ns0 = nloc < Kp ? nloc : Kp;
@@ -215,24 +231,37 @@ __global__ void __launch_bounds__(256) k_stage2_w(
     if (sel1) {
         WarpSel top;
         top.init(lst, Kp);
-        for (int g0 = 0; g0 < n1; g0 += 128) {
-            double kv[4];
-            uint32_t iv[4];
+        // each(it, valid) over F1: (dis_o', id, entry), 128 entries per round
+        auto scan_f1 = [&](auto each) {
+            for (int g0 = 0; g0 < n1; g0 += 128) {
+                double kv[4];
+                uint32_t iv[4];
 #pragma unroll
-            for (int j = 0; j < 4; j++) {
-                const int e = g0 + 32 * j + lane;
-                kv[j] = e < n1 ? f1_diso[base + e] : 0.0;
-                iv[j] = e < n1 ? f1_id[base + e] : 0u;
-            }
+                for (int j = 0; j < 4; j++) {
+                    const int e = g0 + 32 * j + lane;
+                    kv[j] = e < n1 ? f1_diso[base + e] : 0.0;
+                    iv[j] = e < n1 ? f1_id[base + e] : 0u;
+                }
 #pragma unroll
-            for (int j = 0; j < 4; j++) {
-                const int e = g0 + 32 * j + lane;
-                SelItem it;
-                it.key = kv[j];
-                it.id = iv[j];
-                it.pay = (uint32_t)e;
-                top.offer(it, e < n1);
+                for (int j = 0; j < 4; j++) {
+                    const int e = g0 + 32 * j + lane;
+                    SelItem it;
+                    it.key = kv[j];
+                    it.id = iv[j];
+                    it.pay = (uint32_t)e;
+                    each(it, e < n1);
+                }
             }
+        };
+        if (Kp <= 32) {   // two passes, as for S0
+            double mn = __longlong_as_double(0x7ff0000000000000ll);
+            scan_f1([&](const SelItem &it, bool v) {
+                if (v) mn = fmin(mn, it.key);
+            });
+            const double U = warp_kth_smallest(mn, Kp);
+            scan_f1([&](const SelItem &it, bool v) { top.offer(it, v && it.key <= U); });
+        } else {
+            scan_f1([&](const SelItem &it, bool v) { top.offer(it, v); });
         }
         top.finish();
         const int ns1 = n1 < Kp ? n1 : Kp;
@@ -440,7 +469,7 @@ __global__ void __launch_bounds__(128) k_xmerge(int kind, int64_t nq, int world,
     if (q >= nq) return;
     SelItem *lst = (SelItem *)wsm + (size_t)warp * L;
     WarpSel top;
-    top.init(lst, L);
+    top.init(lst, L, true);
     for (int r = 0; r < world; r++) {
         const XItem *src = recv + ((int64_t)r * nq + q) * L;
         for (int j0 = 0; j0 < L; j0 += 32) {
@@ -631,11 +660,16 @@ int launch_topk_w(const StageArgs &a, cudaStream_t st)
 // query.  Every screen value a_c is within delta_q of an exact-order key
 // (||q_d - c||^2 for the CUDA-core screen, ||q_d - c||^2 - ||q_d||^2 for the
 // tensor-core screen; the shift is the same for every c), so every member of
-// the exact top-np has a_c <= a_(np) + 2 delta_q with a_(np) the np-th
-// smallest screen value.  Pass 1 finds a_(np)
-// (WarpTop over the row), pass 2 collects {c : a_c <= a_(np) + 2 delta_q},
-// pass 3 rescores them in fp64 left to right over i and keeps the np
-// smallest (qn2, c).
+// the exact top-np has a_c <= a_(np) + 2 delta_q, where a_(np) is the np-th
+// smallest screen value.
+//   1. Each lane keeps the M = ceil(np/32) smallest of its strided share of
+//      the row (registers).  U = the np-th smallest of these 32 M values
+//      (radix select on order-preserving u32 keys, ballot counts) is >= a_(np):
+//      at least np row values are <= U.
+//   2. C = {c : a_c <= U + 2 delta_q} is a superset of the margin set
+//      {c : a_c <= a_(np) + 2 delta_q} (ballot compaction into cand[q]).
+//   3. C is rescored in fp64 left to right over i; the np smallest (qn2, c) are kept.
+template <int M>
 __global__ void __launch_bounds__(128) k_probe_select_w(
     const float *__restrict__ approx, int64_t nq, int k, int d, int np, const double *__restrict__ qp, int D,
     const double *__restrict__ C, const double *__restrict__ qnorm, double cmax, double kappa,
@@ -648,33 +682,62 @@ __global__ void __launch_bounds__(128) k_probe_select_w(
     if (q >= nq) return;
     SelItem *lst = (SelItem *)wsm + (size_t)warp * np;
     const float *row = approx + q * k;
-    WarpSel top;
-    top.init(lst, np);
-    for (int c0 = 0; c0 < k; c0 += 32) {
-        const int c = c0 + lane;
-        SelItem it = sel_inf();
-        if (c < k) {
-            it.key = (double)row[c];
-            it.id = (uint32_t)c;
-            it.pay = (uint32_t)c;
+    const float FINF = __int_as_float(0x7f800000);
+    // 1. lane-local M smallest (sorted ascending in registers)
+    float loc[M];
+#pragma unroll
+    for (int j = 0; j < M; j++) loc[j] = FINF;
+    for (int c0 = 0; c0 < k; c0 += 128) {
+        float v[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const int c = c0 + 32 * u + lane;
+            v[u] = c < k ? __ldg(row + c) : FINF;
         }
-        top.offer(it, c < k);
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            float x = v[u];
+            if (x < loc[M - 1]) {
+#pragma unroll
+                for (int j = 0; j < M; j++) {   // insertion by compare-exchange
+                    const float lo = fminf(loc[j], x);
+                    x = fmaxf(loc[j], x);
+                    loc[j] = lo;
+                }
+            }
+        }
     }
-    top.finish();
+    // np-th smallest key of the 32 M lane-local values
+    uint32_t key[M];
+#pragma unroll
+    for (int j = 0; j < M; j++) key[j] = f2key(loc[j]);
+    uint32_t res = 0;
+    for (int bit = 31; bit >= 0; bit--) {
+        const uint32_t t = res | (1u << bit);
+        int cnt = 0;
+#pragma unroll
+        for (int j = 0; j < M; j++) cnt += __popc(__ballot_sync(0xffffffffu, key[j] < t));
+        if (cnt < np) res = t;
+    }
+    const float U = key2f(res);
     const double g = qnorm[q] + cmax;
-    const double thr = lst[np - 1].key + 2.0 * (kappa * (g * g));
+    const double margin = 2.0 * (kappa * (g * g));
+    // 2. C
     uint32_t *cq = cand + q * k;
+    const double t1 = (double)U + margin;
     uint32_t nc = 0;
     for (int c0 = 0; c0 < k; c0 += 32) {
         const int c = c0 + lane;
-        const bool in = c < k && (double)row[c] <= thr;
+        const bool in = c < k && (double)__ldg(row + c) <= t1;
         const unsigned bal = __ballot_sync(0xffffffffu, in);
         if (in) cq[nc + __popc(bal & ((1u << lane) - 1u))] = (uint32_t)c;
         nc += __popc(bal);
     }
     __syncwarp();
+    WarpSel top;
+    // 3. canonical fp64 rescore of C and the np smallest (qn2, c)
     const double *qd = qp + q * D;
-    top.init(lst, np);
+    top.init(lst, np, true);
     for (uint32_t e0 = 0; e0 < nc; e0 += 32) {
         const uint32_t e = e0 + lane;
         SelItem it = sel_inf();
@@ -707,9 +770,21 @@ int launch_probe_select_w(const float *approx, int64_t nq, int k, int d, int np,
 {
     const int wpb = 4;
     const size_t smem = (size_t)wpb * np * sizeof(SelItem);
-    int rc = set_attr((const void *)k_probe_select_w, smem);
-    if (rc) return rc;
-    k_probe_select_w<<<(unsigned)((nq + wpb - 1) / wpb), wpb * 32, smem, st>>>(
-        approx, nq, k, d, np, qp, D, C, qnorm, cmax, kappa, cand, probe, probe_qn2, ncand);
+    const int m = (np + 31) / 32;
+    const unsigned grid = (unsigned)((nq + wpb - 1) / wpb);
+#define MRQ_PSEL(MM)                                                                                          \
+    do {                                                                                                      \
+        int rc = set_attr((const void *)k_probe_select_w<MM>, smem);                                          \
+        if (rc) return rc;                                                                                    \
+        k_probe_select_w<MM><<<grid, wpb * 32, smem, st>>>(approx, nq, k, d, np, qp, D, C, qnorm, cmax, kappa, \
+                                                           cand, probe, probe_qn2, ncand);                    \
+    } while (0)
+    if (m <= 1) MRQ_PSEL(1);
+    else if (m <= 2) MRQ_PSEL(2);
+    else if (m <= 4) MRQ_PSEL(4);
+    else if (m <= 8) MRQ_PSEL(8);
+    else if (m <= 16) MRQ_PSEL(16);
+    else MRQ_PSEL(32);
+#undef MRQ_PSEL
     return MRQ_OK;
 }
