@@ -399,6 +399,8 @@ struct WarpTopBitonic {
     }
 };
 
+#define MRQ_SELQ 64   // items of a WarpSel compaction queue
+
 // The L-th smallest (L <= 32) of the 32 lane values v (bitonic sort across
 // lanes).  Used as a selection pre-threshold: if every lane's v is the
 // minimum of its share of a stream, at least L stream items are <= the result.
@@ -426,14 +428,20 @@ struct WarpSel {
     WarpTop sm;
     WarpTopReg rg;
     WarpTopBitonic bt;
-    int mode;   // 0 shared-memory list, 1 register insertion (dedup), 2 register bitonic (distinct items)
+    SelItem *qbuf;   // mode 2: compaction queue of MRQ_SELQ items
+    int qn;
+    int mode;        // 0 shared-memory list, 1 register insertion (dedup), 2 register bitonic (distinct items)
 
-    // distinct: the caller guarantees no (key, id) is offered twice
-    __device__ __forceinline__ void init(SelItem *buf, int L, bool distinct = false)
+    // distinct: the caller guarantees no (key, id) is offered twice; then
+    // qbuf (MRQ_SELQ items of shared memory) queues the items that pass the
+    // current threshold and full batches of 32 go through one bitonic merge.
+    __device__ __forceinline__ void init(SelItem *buf, int L, bool distinct = false, SelItem *queue = nullptr)
     {
-        mode = L > 32 ? 0 : (distinct ? 2 : 1);
+        mode = L > 32 ? 0 : (distinct && queue ? 2 : 1);
         sm.a = buf;
         sm.L = L;
+        qbuf = queue;
+        qn = 0;
         if (mode == 2)
             bt.init(L);
         else if (mode == 1)
@@ -441,17 +449,48 @@ struct WarpSel {
         else
             sm.init(buf, L);
     }
+    __device__ __forceinline__ void flush(int n)
+    {
+        const int lane = threadIdx.x & 31;
+        __syncwarp();
+        SelItem x = sel_inf();
+        if (lane < n) x = qbuf[lane];
+        __syncwarp();
+        bt.offer(x, lane < n);
+    }
     __device__ __forceinline__ void offer(const SelItem &it, bool valid)
     {
-        if (mode == 2)
-            bt.offer(it, valid);
-        else if (mode == 1)
+        if (mode == 2) {
+            const int lane = threadIdx.x & 31;
+            const double tk = __shfl_sync(0xffffffffu, bt.key, bt.L - 1);
+            const uint32_t ti = __shfl_sync(0xffffffffu, bt.id, bt.L - 1);
+            const bool pass = valid && WarpTopBitonic::lt(it.key, it.id, tk, ti);
+            const unsigned m = __ballot_sync(0xffffffffu, pass);
+            if (!m) return;
+            if (pass) qbuf[qn + __popc(m & ((1u << lane) - 1u))] = it;
+            qn += __popc(m);
+            if (qn >= 32) {
+                flush(32);
+                const int rest = qn - 32;
+                SelItem y;
+                if (lane < rest) y = qbuf[32 + lane];
+                __syncwarp();
+                if (lane < rest) qbuf[lane] = y;
+                __syncwarp();
+                qn = rest;
+            }
+        } else if (mode == 1) {
             rg.offer(it, valid);
-        else
+        } else {
             sm.offer(it, valid);
+        }
     }
     __device__ __forceinline__ void finish()
     {
+        if (mode == 2 && qn > 0) {
+            flush(qn);
+            qn = 0;
+        }
         if (mode != 0) {
             const int lane = threadIdx.x & 31;
             __syncwarp();

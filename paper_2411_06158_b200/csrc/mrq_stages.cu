@@ -31,7 +31,8 @@ __global__ void __launch_bounds__(256) k_seed_w(
     const int64_t q = (int64_t)blockIdx.x * wpb + warp;
     if (q >= nq) return;
     float *tile = (float *)wsm + warp * MRQ_RG_FLOATS;
-    SelItem *lst = (SelItem *)((float *)wsm + wpb * MRQ_RG_FLOATS) + (size_t)warp * Kp;
+    SelItem *lst = (SelItem *)((float *)wsm + wpb * MRQ_RG_FLOATS) + (size_t)warp * (Kp + MRQ_SELQ);
+    SelItem *queue = lst + Kp;
     const double eps_r = eps_r_arr[q];
     const double *qrow = qp + q * D;
     // the pool is defined on GLOBAL list sizes (decision T); a rank scans only
@@ -78,6 +79,7 @@ __global__ void __launch_bounds__(256) k_seed_w(
             if (v) mn = fmin(mn, it.key);
         });
         const double U = warp_kth_smallest(mn, Kp);
+        top.init(lst, Kp, true, queue);
         scan_pool([&](const SelItem &it, bool v) { top.offer(it, v && it.key <= U); });
     } else {
         scan_pool([&](const SelItem &it, bool v) { top.offer(it, v); });
@@ -111,8 +113,8 @@ __global__ void __launch_bounds__(256) k_seed_w(
         }
         return;
     }
-    // tau0 = K-th smallest exact over S0
-    top.init(lst, K);
+    // tau0 = K-th smallest exact over S0 (distinct items)
+    top.init(lst, K, true, queue);
     for (int g = 0; g < ns0; g += 32) {
         const int e = g + lane;
         const bool v = e < ns0;
@@ -221,7 +223,8 @@ __global__ void __launch_bounds__(256) k_stage2_w(
     const int64_t q = (int64_t)blockIdx.x * wpb + warp;
     if (q >= nq) return;
     float *tile = (float *)wsm + warp * MRQ_RG_FLOATS;
-    SelItem *lst = (SelItem *)((float *)wsm + wpb * MRQ_RG_FLOATS) + (size_t)warp * Kp;
+    SelItem *lst = (SelItem *)((float *)wsm + wpb * MRQ_RG_FLOATS) + (size_t)warp * (Kp + MRQ_SELQ);
+    SelItem *queue = lst + Kp;
     const bool sel1 = mode == 0 && tight;
     const uint64_t base = f1_off[q];
     const int n1 = (int)f1_cnt[q];
@@ -259,6 +262,7 @@ __global__ void __launch_bounds__(256) k_stage2_w(
                 if (v) mn = fmin(mn, it.key);
             });
             const double U = warp_kth_smallest(mn, Kp);
+            top.init(lst, Kp, true, queue);
             scan_f1([&](const SelItem &it, bool v) { top.offer(it, v && it.key <= U); });
         } else {
             scan_f1([&](const SelItem &it, bool v) { top.offer(it, v); });
@@ -467,9 +471,10 @@ __global__ void __launch_bounds__(128) k_xmerge(int kind, int64_t nq, int world,
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
     const int64_t q = (int64_t)blockIdx.x * wpb + warp;
     if (q >= nq) return;
-    SelItem *lst = (SelItem *)wsm + (size_t)warp * L;
+    SelItem *lst = (SelItem *)wsm + (size_t)warp * (L + MRQ_SELQ);
+    SelItem *queue = lst + L;
     WarpSel top;
-    top.init(lst, L, true);
+    top.init(lst, L, true, queue);
     for (int r = 0; r < world; r++) {
         const XItem *src = recv + ((int64_t)r * nq + q) * L;
         for (int j0 = 0; j0 < L; j0 += 32) {
@@ -557,7 +562,7 @@ static int set_attr(const void *fn, size_t smem)
 
 int launch_seed_w(int W, const StageArgs &a, cudaStream_t st)
 {
-    const size_t per = MRQ_RG_FLOATS * 4 + (size_t)a.Kp * sizeof(SelItem);
+    const size_t per = MRQ_RG_FLOATS * 4 + (size_t)(a.Kp + MRQ_SELQ) * sizeof(SelItem);
     const int wpb = warps_for(per);
     const size_t smem = per * wpb;
     const unsigned grid = (unsigned)((a.nq + wpb - 1) / wpb);
@@ -593,7 +598,7 @@ int launch_stage2_w(const StageArgs &a, cudaStream_t st)
         k_head_b<<<(unsigned)a.nq, wpb * 32, smem, st>>>(a.aligned, a.D, a.d, a.ids, a.heads, a.xr2, a.qp, a.qr2,
                                                           a.f1_off, a.f1_cnt, a.f1_pos, a.f1_head, a.f1_diso, a.f1_id);
     }
-    const size_t per = MRQ_RG_FLOATS * 4 + (size_t)std::max(a.Kp, a.K) * sizeof(SelItem);
+    const size_t per = MRQ_RG_FLOATS * 4 + (size_t)(std::max(a.Kp, a.K) + MRQ_SELQ) * sizeof(SelItem);
     const int wpb = warps_for(per);
     const size_t smem = per * wpb;
     int rc = set_attr((const void *)k_stage2_w, smem);
@@ -615,7 +620,7 @@ int launch_f2_w(const StageArgs &a, cudaStream_t st)
 int launch_xmerge(int kind, const StageArgs &a, int world, int rank, const XItem *recv, cudaStream_t st)
 {
     const int L = kind == 2 ? a.K : a.Kp;
-    const size_t per = (size_t)std::max(L, a.K) * sizeof(SelItem);
+    const size_t per = (size_t)(std::max(L, a.K) + MRQ_SELQ) * sizeof(SelItem);
     const int wpb = warps_for(per);
     const size_t smem = per * wpb;
     int rc = set_attr((const void *)k_xmerge, smem);
@@ -680,7 +685,8 @@ __global__ void __launch_bounds__(128) k_probe_select_w(
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
     const int64_t q = (int64_t)blockIdx.x * wpb + warp;
     if (q >= nq) return;
-    SelItem *lst = (SelItem *)wsm + (size_t)warp * np;
+    SelItem *lst = (SelItem *)wsm + (size_t)warp * (np + MRQ_SELQ);
+    SelItem *queue = lst + np;
     const float *row = approx + q * k;
     const float FINF = __int_as_float(0x7f800000);
     // 1. lane-local M smallest (sorted ascending in registers)
@@ -737,7 +743,7 @@ __global__ void __launch_bounds__(128) k_probe_select_w(
     WarpSel top;
     // 3. canonical fp64 rescore of C and the np smallest (qn2, c)
     const double *qd = qp + q * D;
-    top.init(lst, np, true);
+    top.init(lst, np, true, queue);
     for (uint32_t e0 = 0; e0 < nc; e0 += 32) {
         const uint32_t e = e0 + lane;
         SelItem it = sel_inf();
@@ -769,7 +775,7 @@ int launch_probe_select_w(const float *approx, int64_t nq, int k, int d, int np,
                           uint32_t *probe, double *probe_qn2, uint32_t *ncand, cudaStream_t st)
 {
     const int wpb = 4;
-    const size_t smem = (size_t)wpb * np * sizeof(SelItem);
+    const size_t smem = (size_t)wpb * (np + MRQ_SELQ) * sizeof(SelItem);
     const int m = (np + 31) / 32;
     const unsigned grid = (unsigned)((nq + wpb - 1) / wpb);
 #define MRQ_PSEL(MM)                                                                                          \
