@@ -119,6 +119,17 @@ def read_build_header(path):
     return dict(D=D, d=d, k=k, N=N, sha=h[40:104].decode())
 
 
+def ncu_traffic(cfg_name, nprobe):
+    """dram__bytes_read + dram__bytes_write per launch of each kernel from the
+    committed ncu --set full summary of this workload (profiles/), or {}."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic_%s_np%d.json" % (cfg_name, nprobe))
+    try:
+        with open(path) as f:
+            return {k: v["dram_bytes_per_launch"] for k, v in json.load(f)["kernels"].items()}
+    except Exception:
+        return {}
+
+
 def recall_at_k(found, gt, K):
     f = np.asarray(found)[:, :K]
     g = np.asarray(gt)[:, :K]
@@ -252,13 +263,30 @@ def main():
     rc = recall_at_k(found, gt, 10) if gt is not None else None
 
     scanned = int(np.mean([s.scanned for s in sts]))
+    f1 = float(np.mean([s.stage1_pass for s in sts]))
     ms_scan = float(np.mean([s.ms_scan for s in sts]))
-    bcode = 4 * ((d + 31) // 32) + 12
+    ms_head = float(np.mean([s.ms_head for s in sts]))
     hbm, peak_kind = peaks()
-    achieved = scanned * bcode / (ms_scan * 1e-3) / 1e9
+    traffic = ncu_traffic(cfg_name, nprobe)
+    # algorithmic bytes per unit: scan = one scanned code (W code
+    # words + f1/f2/f3); head gather = one F1 survivor (fp32 head row, ||x_r||^2,
+    # id, its F1 slot read, f1_head/f1_diso/f1_id written)
+    bcode = 4 * ((d + 31) // 32) + 12
+    bhead = 4 * d + 32
+    kern = {
+        "k_scan": {"unit": "scanned code", "bytes_per_unit": bcode, "units_per_launch": scanned, "ms": ms_scan},
+        "k_head_b": {"unit": "F1 survivor", "bytes_per_unit": bhead, "units_per_launch": int(f1), "ms": ms_head},
+    }
+    for nm, kk in kern.items():
+        kk["achieved_gbs"] = round(kk["bytes_per_unit"] * kk["units_per_launch"] / (kk["ms"] * 1e-3) / 1e9, 1)
+        kk["frac"] = round(kk["achieved_gbs"] / hbm, 4)
+        kk["ms"] = round(kk["ms"], 4)
+        kk["traffic"] = traffic.get(nm)
+    dom = max(kern, key=lambda n: kern[n]["ms"])
+    achieved = kern[dom]["achieved_gbs"]
     stage_ms = {k: round(float(np.mean([getattr(s, k) for s in sts])), 4)
-                for k in ("ms_qprep", "ms_probe", "ms_quant", "ms_seed", "ms_scan", "ms_stage2", "ms_rerank",
-                          "ms_topk", "ms_comm")}
+                for k in ("ms_qprep", "ms_probe", "ms_quant", "ms_seed", "ms_scan", "ms_stage2", "ms_head",
+                          "ms_rerank", "ms_topk", "ms_comm")}
 
     # e2e through the host-buffer call (pinned host queries; H2D + D2H inside the timed region)
     hq = torch.from_numpy(Q).pin_memory().numpy()
@@ -308,10 +336,11 @@ def main():
                    "parallelism": "lists sharded over %d GPU(s)" % world, "base_sha_match": sha_ok,
                    "scanned_per_step": scanned, "exact_per_query": round(float(np.mean([s.exact for s in sts])) / nq, 2),
                    "stage_ms": stage_ms, "sweep": sweep, "index_load_s": round(load_s, 2)},
-        "roofline": {"bound": "hbm", "kernel": "k_scan", "achieved": round(achieved, 1), "peak": hbm,
-                     "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": None,
-                     "algorithmic_bytes_per_code": bcode,
-                     "codes_per_s_per_gpu": round(scanned / (ms_scan * 1e-3), 1)},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "peak_kind": peak_kind,
+                     "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": kern[dom]["traffic"],
+                     "bytes_per_unit": kern[dom]["bytes_per_unit"], "unit_kind": kern[dom]["unit"],
+                     "kernels": kern, "codes_per_s_per_gpu": round(scanned / (ms_scan * 1e-3), 1),
+                     "scan_frac_of_hbm": kern["k_scan"]["frac"]},
         "e2e": {"value": round(nq / e2e_s, 1), "unit": "queries/s", "h2d_bytes_per_step": int(nq * X.shape[1] * 4),
                 "d2h_bytes_per_step": int(nq * K * 12)},
         "gpu_launches": launches_per_step * args.steps,

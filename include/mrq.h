@@ -86,6 +86,7 @@ typedef struct {
     uint64_t exact;        /* distinct exact distances computed (F2 u S0 u S1)  */
     uint64_t seeds;        /* |S0| + |S1|                                        */
     double ms_total, ms_qprep, ms_probe, ms_quant, ms_seed, ms_scan, ms_stage2, ms_rerank, ms_topk, ms_comm;
+    double ms_head;        /* the stage-2 head gather alone (part of ms_stage2)  */
 } mrq_stats;
 
 /*

@@ -434,21 +434,35 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
 
     // ---- a2: probe (Alg.2 L7): screen + exact selection
     {
-        SCR("approx", float, nq * k, approx);
-        double kappa;
-        if (mrq_probe_tc_enabled(ix)) {
-            TRY(mrq_probe_tc_run(ix, qd32, nq, approx, st));
-            kappa = mrq_probe_tc_kappa(ix);
-        } else {
-            dim3 grid((k + 255) / 256, (unsigned)((nq + 7) / 8));
-            k_probe_approx<<<grid, 256, 8 * d * sizeof(float), st>>>(qd32, nq, d, k, ix->C32T, approx);
-            kappa = std::ldexp(1.0, -24) * (2.0 * d + 8.0);
-        }
         uint32_t *cand, *ncand;
         SCR("probe_cand", uint32_t, nq * k, cand);
         SCR("probe_ncand", uint32_t, nq, ncand);
-        TRY(launch_probe_select_w(approx, nq, k, d, np, qp, D, ix->C, qnorm, ix->cmax, kappa, cand, probe, probe_qn2,
-                                  ncand, st));
+        if (mrq_probe_tc_fusable(ix, np)) {   // tcgen05 screen with the running top-np in its epilogue
+            const int P = mrq_probe_tc_parts(ix, nq), capp = 256;
+            uint2 *cbuf;
+            uint32_t *ccnt;
+            float *kvbuf;
+            SCR("probe_cbuf", uint2, (size_t)nq * P * capp, cbuf);
+            SCR("probe_ccnt", uint32_t, (size_t)nq * P, ccnt);
+            SCR("probe_kv", float, (size_t)nq * P * 16, kvbuf);
+            const double kappa = mrq_probe_tc_kappa(ix);
+            TRY(mrq_probe_tc_run_fused(ix, qd32, nq, np, qnorm, kappa, cbuf, capp, ccnt, kvbuf, st));
+            TRY(launch_probe_finish_w(nq, k, d, np, qp, D, ix->C, qnorm, ix->cmax, kappa, cbuf, P, capp, ccnt, kvbuf,
+                                      cand, probe, probe_qn2, ncand, st));
+        } else {
+            SCR("approx", float, nq * k, approx);
+            double kappa;
+            if (mrq_probe_tc_enabled(ix)) {
+                TRY(mrq_probe_tc_run(ix, qd32, nq, approx, st));
+                kappa = mrq_probe_tc_kappa(ix);
+            } else {
+                dim3 grid((k + 255) / 256, (unsigned)((nq + 7) / 8));
+                k_probe_approx<<<grid, 256, 8 * d * sizeof(float), st>>>(qd32, nq, d, k, ix->C32T, approx);
+                kappa = std::ldexp(1.0, -24) * (2.0 * d + 8.0);
+            }
+            TRY(launch_probe_select_w(approx, nq, k, d, np, qp, D, ix->C, qnorm, ix->cmax, kappa, cand, probe,
+                                      probe_qn2, ncand, st));
+        }
     }
     if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[2], st));
 
@@ -530,12 +544,12 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
     if (sharded && mode == 0 && tight) {   // local S1 -> all-gather -> global S1, tau1 -> F2
         StageArgs sx = sa;
         sx.xout = xsend;
-        TRY(launch_stage2_w(sx, st));
+        TRY(launch_stage2_w(sx, st, timed ? ix->ev[10] : nullptr));
         TRY(mrq_allgather(ix, xsend, xrecv, (size_t)nq * Kp * sizeof(XItem), st));
         TRY(launch_xmerge(1, sa, ix->world, ix->rank, xrecv, st));
         TRY(launch_f2_w(sa, st));
     } else {
-        TRY(launch_stage2_w(sa, st));
+        TRY(launch_stage2_w(sa, st, timed ? ix->ev[10] : nullptr));
     }
     if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[6], st));
 
@@ -581,6 +595,9 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
         stats->ms_rerank = ms[7];
         stats->ms_topk = ms[8];
         stats->ms_comm = ms[9];
+        float mh = 0.f;
+        MRQ_CUDA_TRY(cudaEventElapsedTime(&mh, ix->ev[5], ix->ev[10]));
+        stats->ms_head = mh;
         std::vector<uint32_t> h(nq);
         auto sum32 = [&](const uint32_t *dv) -> uint64_t {
             if (cudaMemcpy(h.data(), dv, nq * 4, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
@@ -749,6 +766,10 @@ extern "C" int mrq_debug_set(mrq_index *ix, const char *name, int64_t value)
     }
     if (std::string(name) == "cuda_core_probe") {  // probe screen on CUDA cores instead of tcgen05
         ix->force_cuda_core_probe = (int)value;
+        return MRQ_OK;
+    }
+    if (std::string(name) == "probe_unfused") {    // screen to HBM + separate selection kernel
+        ix->force_probe_unfused = (int)value;
         return MRQ_OK;
     }
     mrq_set_error("unknown debug switch '%s'", name);

@@ -56,6 +56,7 @@ struct mrq_index {
     int force_exchange = 0;                    // mrq_debug_set("force_exchange"): world-1 runs the sharded path
     void *probe_tc = nullptr;                  // tcgen05 probe state (mrq_probe_tc.cu)
     int force_cuda_core_probe = 0;             // mrq_debug_set("cuda_core_probe"): CUDA-core screen instead
+    int force_probe_unfused = 0;               // mrq_debug_set("probe_unfused"): screen to HBM + k_probe_select_w
     int sm_count = 148;
 
     // host mirrors

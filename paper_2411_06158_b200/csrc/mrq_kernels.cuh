@@ -37,7 +37,7 @@ struct StageArgs {
 };
 
 int launch_seed_w(int W, const StageArgs &a, cudaStream_t st);
-int launch_stage2_w(const StageArgs &a, cudaStream_t st);
+int launch_stage2_w(const StageArgs &a, cudaStream_t st, cudaEvent_t after_gather = nullptr);
 int launch_rerank_w(const StageArgs &a, cudaStream_t st);
 int launch_topk_w(const StageArgs &a, cudaStream_t st);
 int launch_f2_w(const StageArgs &a, cudaStream_t st);
@@ -61,6 +61,10 @@ struct LaunchScan {
 void launch_scan(int W, const LaunchScan &a, cudaStream_t st);
 bool supported_W(int W);
 void launch_scan_dbg(int W, const LaunchScan &a, double *dis, double *lb1, cudaStream_t st);
+int launch_probe_finish_w(int64_t nq, int k, int d, int np, const double *qp, int D, const double *C,
+                          const double *qnorm, double cmax, double kappa, const uint2 *cbuf, int P, int capp,
+                          const uint32_t *ccnt, const float *kvbuf, uint32_t *cand, uint32_t *probe,
+                          double *probe_qn2, uint32_t *ncand, cudaStream_t st);
 int launch_probe_select_w(const float *approx, int64_t nq, int k, int d, int np, const double *qp, int D,
                           const double *C, const double *qnorm, double cmax, double kappa, uint32_t *cand,
                           uint32_t *probe, double *probe_qn2, uint32_t *ncand, cudaStream_t st);

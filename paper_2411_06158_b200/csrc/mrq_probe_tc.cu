@@ -39,8 +39,8 @@
 #define TC_A_BYTES (TC_BM * TC_BK * 4) // 16 KB
 #define TC_B_BYTES (TC_BN * TC_BK * 4) // 32 KB
 #define TC_STAGE_BYTES (TC_A_BYTES + TC_B_BYTES)
-#define TC_THREADS 192
-#define TC_SMEM (TC_STAGES * TC_STAGE_BYTES + 1024 + 256)
+#define TC_THREADS 320                 // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
+#define TC_SMEM (TC_STAGES * TC_STAGE_BYTES + 1024 + 256 + 256 * 33 * 4)
 
 struct ProbeTC {
     bool enabled = false;
@@ -100,10 +100,24 @@ __host__ __device__ constexpr uint32_t tf32_idesc(int M, int N)
     return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
+// Fused selection (FUSED = true, np <= TC_NPMAX).  A row's columns are split
+// into P = 2 gridDim.y parts (CTA column range x epilogue half); the thread
+// owning (row, part) keeps the 16 smallest screen values of its part sorted
+// in registers and appends every (a_c, c) with
+// a_c <= RU(its current np-th smallest + 2 delta_q) to the part's candidate
+// buffer.  A part's running np-th smallest never drops below the row's final
+// a_(np), so every member of the margin set {c : a_c <= a_(np) + 2 delta_q}
+// is appended by its part; the parts' 16 smallest go to kvbuf so that
+// k_probe_finish_w can form a_(np) and rescore the margin set.
+#define TC_NPMAX 16
+template <bool FUSED>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_probe_tc(const __grid_constant__ CUtensorMap mapA,
                                                             const __grid_constant__ CUtensorMap mapB, int nq, int k,
                                                             int d, int tiles_per_cta, const float *__restrict__ cn32,
-                                                            float *__restrict__ approx)
+                                                            float *__restrict__ approx, int np,
+                                                            const double *__restrict__ qnorm, double cmax,
+                                                            double kappa, uint2 *__restrict__ cbuf, int capp,
+                                                            uint32_t *__restrict__ ccnt, float *__restrict__ kvbuf)
 {
     extern __shared__ __align__(1024) unsigned char tsm[];
     unsigned char *ring = (unsigned char *)(((uintptr_t)tsm + 1023) & ~(uintptr_t)1023);
@@ -112,6 +126,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_probe_tc(const __grid_constan
     uint64_t *tfull = empty + TC_STAGES;    // [2]
     uint64_t *tempty = tfull + 2;           // [2]
     uint32_t *tmem_slot = (uint32_t *)(tempty + 2);
+    float *scratch = (float *)(tmem_slot + 4);   // FUSED: 256 x 33 floats (per-thread chunk staging)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m0 = blockIdx.x * TC_BM;
@@ -127,7 +142,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_probe_tc(const __grid_constan
         }
         for (int b = 0; b < 2; b++) {
             mbar_init(tfull + b, 1);
-            mbar_init(tempty + b, 4);       // one arrival per epilogue warp
+            mbar_init(tempty + b, 8);       // one arrival per epilogue warp
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         asm volatile("prefetch.tensormap [%0];\n" ::"l"((uint64_t)&mapA) : "memory");
@@ -203,7 +218,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_probe_tc(const __grid_constan
         }
     } else {   // ---------------------------- epilogue warps 2..5
         const int quad = warp & 3;            // TMEM lanes 32 quad .. 32 quad + 31
+        const int half = (warp - 2) >> 2;     // column chunks half, half + 2, ... of each tile
         const int row = m0 + quad * 32 + lane;
+        const int P = 2 * (int)gridDim.y, part = 2 * (int)blockIdx.y + half;
+        const float FINF = __int_as_float(0x7f800000);
+        float kv[TC_NPMAX];                   // FUSED: the np smallest screen values, ascending
+        float tf = FINF;                      // FUSED: append threshold RU(kv[np-1] + margin)
+        uint32_t cnt = 0;
+        double margin = 0.0;
+        uint2 *rb = nullptr;
+        if (FUSED) {
+            // kv holds 16 - np placeholders (-inf) followed by the np smallest
+            // values, so the running np-th smallest is always kv[TC_NPMAX - 1]
+#pragma unroll
+            for (int j = 0; j < TC_NPMAX; j++) kv[j] = j < TC_NPMAX - np ? -FINF : FINF;
+            if (row < nq) {
+                const double g = qnorm[row] + cmax;
+                margin = 2.0 * (kappa * (g * g));
+                rb = cbuf + ((int64_t)row * P + part) * capp;
+            }
+        }
         int it = 0;
         for (int t = t_begin; t < t_end; t++, it++) {
             const int b = it & 1;
@@ -211,7 +245,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_probe_tc(const __grid_constan
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
             const int n0 = t * TC_BN;
 #pragma unroll 1
-            for (int c = 0; c < TC_BN; c += 32) {
+            for (int c = half * 32; c < TC_BN; c += 64) {
                 uint32_t v[32];
                 const uint32_t ta = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * TC_BN + c);
                 asm volatile(
@@ -224,7 +258,47 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_probe_tc(const __grid_constan
                       "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
                     : "r"(ta));
                 asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-                if (row < nq) {
+                if (FUSED) {
+                    // screen values of the chunk; mask of those <= the append threshold
+                    float av[32];
+                    uint32_t mask = 0;
+#pragma unroll
+                    for (int j = 0; j < 32; j += 4) {
+                        const float4 cn = __ldg((const float4 *)(cn32 + n0 + c + j));
+                        av[j] = cn.x - 2.0f * __uint_as_float(v[j]);
+                        av[j + 1] = cn.y - 2.0f * __uint_as_float(v[j + 1]);
+                        av[j + 2] = cn.z - 2.0f * __uint_as_float(v[j + 2]);
+                        av[j + 3] = cn.w - 2.0f * __uint_as_float(v[j + 3]);
+                    }
+#pragma unroll
+                    for (int j = 0; j < 32; j++)
+                        mask |= (n0 + c + j < k && av[j] <= tf) ? (1u << j) : 0u;
+                    if (row >= nq) mask = 0;
+                    if (mask) {   // rare after warm-up: stage the chunk, walk the passing values
+                        float *sc = scratch + ((warp - 2) * 32 + lane) * 33;
+#pragma unroll
+                        for (int j = 0; j < 32; j++) sc[j] = av[j];
+                        while (mask) {
+                            const int j = __ffs(mask) - 1;
+                            mask &= mask - 1;
+                            const float a = sc[j];
+                            if (!(a <= tf)) continue;
+                            if (cnt < (uint32_t)capp) rb[cnt] = make_uint2(__float_as_uint(a), (uint32_t)(n0 + c + j));
+                            cnt++;
+                            if (a < kv[TC_NPMAX - 1]) {   // insertion (compare-exchange chain)
+                                float x = a;
+#pragma unroll
+                                for (int i = 0; i < TC_NPMAX; i++) {
+                                    const float lo = fminf(kv[i], x);
+                                    x = fmaxf(kv[i], x);
+                                    kv[i] = lo;
+                                }
+                                const float th = kv[TC_NPMAX - 1];
+                                tf = th == FINF ? FINF : __double2float_ru((double)th + margin);
+                            }
+                        }
+                    }
+                } else if (row < nq) {
                     float *dst = approx + (int64_t)row * k + n0 + c;
                     if (n0 + c + 32 <= k && (k & 3) == 0) {
 #pragma unroll
@@ -247,6 +321,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_probe_tc(const __grid_constan
             asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(tempty + b);
+        }
+        if (FUSED && row < nq) {
+            ccnt[(int64_t)row * P + part] = cnt;
+            float4 *kvo = (float4 *)(kvbuf + ((int64_t)row * P + part) * TC_NPMAX);
+#pragma unroll
+            for (int i = 0; i < TC_NPMAX; i += 4) {   // placeholders are not row values: +inf
+                float4 o = make_float4(kv[i], kv[i + 1], kv[i + 2], kv[i + 3]);
+                if (o.x == -FINF) o.x = FINF;
+                if (o.y == -FINF) o.y = FINF;
+                if (o.z == -FINF) o.z = FINF;
+                if (o.w == -FINF) o.w = FINF;
+                kvo[i / 4] = o;
+            }
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -292,7 +379,9 @@ int mrq_probe_tc_init(mrq_index *ix)
         delete tc;
         return rc;
     }
-    cudaError_t e = cudaFuncSetAttribute(k_probe_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
+    cudaError_t e = cudaFuncSetAttribute(k_probe_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_probe_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
     if (e != cudaSuccess) {
         delete tc;
         mrq_set_error("k_probe_tc smem attribute: %s", cudaGetErrorString(e));
@@ -332,8 +421,43 @@ int mrq_probe_tc_run(mrq_index *ix, const float *qd32, int64_t nq, float *approx
     gy = std::max(1, std::min(gy, ntiles));
     const int per = (ntiles + gy - 1) / gy;
     gy = (ntiles + per - 1) / per;
-    k_probe_tc<<<dim3(mblocks, gy), TC_THREADS, TC_SMEM, st>>>(mapA, tc->mapB, (int)nq, ix->k, ix->d, per, ix->cn32,
-                                                                approx);
+    k_probe_tc<false><<<dim3(mblocks, gy), TC_THREADS, TC_SMEM, st>>>(mapA, tc->mapB, (int)nq, ix->k, ix->d, per,
+                                                                       ix->cn32, approx, 0, nullptr, 0.0, 0.0,
+                                                                       nullptr, 0, nullptr, nullptr);
+    MRQ_CUDA_TRY(cudaGetLastError());
+    return MRQ_OK;
+}
+
+bool mrq_probe_tc_fusable(const mrq_index *ix, int np)
+{
+    return mrq_probe_tc_enabled(ix) && np <= TC_NPMAX && !ix->force_probe_unfused;
+}
+
+int mrq_probe_tc_parts(const mrq_index *ix, int64_t nq)
+{
+    const int mblocks = (int)((nq + TC_BM - 1) / TC_BM);
+    const int ntiles = (ix->k + TC_BN - 1) / TC_BN;
+    int gy = (ix->sm_count + mblocks - 1) / mblocks;
+    gy = std::max(1, std::min(std::min(gy, ntiles), 8));   // P = 2 gy <= 16 parts
+    const int per = (ntiles + gy - 1) / gy;
+    gy = (ntiles + per - 1) / per;
+    return 2 * gy;
+}
+
+int mrq_probe_tc_run_fused(mrq_index *ix, const float *qd32, int64_t nq, int np, const double *qnorm, double kappa,
+                           uint2 *cbuf, int capp, uint32_t *ccnt, float *kvbuf, cudaStream_t st)
+{
+    ProbeTC *tc = (ProbeTC *)ix->probe_tc;
+    CUtensorMap mapA;
+    int rc = make_map(tc, &mapA, qd32, (int)nq, ix->d, TC_BM);
+    if (rc != MRQ_OK) return rc;
+    const int mblocks = (int)((nq + TC_BM - 1) / TC_BM);
+    const int ntiles = (ix->k + TC_BN - 1) / TC_BN;
+    const int gy = mrq_probe_tc_parts(ix, nq) / 2;
+    const int per = (ntiles + gy - 1) / gy;
+    k_probe_tc<true><<<dim3(mblocks, gy), TC_THREADS, TC_SMEM, st>>>(mapA, tc->mapB, (int)nq, ix->k, ix->d, per,
+                                                                      ix->cn32, nullptr, np, qnorm, ix->cmax, kappa,
+                                                                      cbuf, capp, ccnt, kvbuf);
     MRQ_CUDA_TRY(cudaGetLastError());
     return MRQ_OK;
 }

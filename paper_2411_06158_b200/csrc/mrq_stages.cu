@@ -588,7 +588,7 @@ int launch_seed_w(int W, const StageArgs &a, cudaStream_t st)
     return MRQ_OK;
 }
 
-int launch_stage2_w(const StageArgs &a, cudaStream_t st)
+int launch_stage2_w(const StageArgs &a, cudaStream_t st, cudaEvent_t after_gather)
 {
     {   // gather half: block per query, 8 warps split the F1 rows
         const int wpb = 8;
@@ -598,6 +598,7 @@ int launch_stage2_w(const StageArgs &a, cudaStream_t st)
         k_head_b<<<(unsigned)a.nq, wpb * 32, smem, st>>>(a.aligned, a.D, a.d, a.ids, a.heads, a.xr2, a.qp, a.qr2,
                                                           a.f1_off, a.f1_cnt, a.f1_pos, a.f1_head, a.f1_diso, a.f1_id);
     }
+    if (after_gather) MRQ_CUDA_TRY(cudaEventRecord(after_gather, st));
     const size_t per = MRQ_RG_FLOATS * 4 + (size_t)(std::max(a.Kp, a.K) + MRQ_SELQ) * sizeof(SelItem);
     const int wpb = warps_for(per);
     const size_t smem = per * wpb;
@@ -768,6 +769,135 @@ __global__ void __launch_bounds__(128) k_probe_select_w(
         probe_qn2[q * np + p] = ok ? lst[p].key : __longlong_as_double(0x7ff0000000000000ll);
     }
     if (lane == 0) ncand_out[q] = nc;
+}
+
+// sum_{j<d} (q_j - c_j)^2 left to right (canonical), the row's loads issued
+// 8 at a time ahead of the dependent sum.
+__device__ __forceinline__ double sqdist_rows8(const double *__restrict__ cr, const double *__restrict__ qd, int d)
+{
+    double acc = 0.0;
+    int j = 0;
+    for (; j + 8 <= d; j += 8) {
+        double cv[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) cv[u] = __ldg(cr + j + u);
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            const double t = qd[j + u] - cv[u];
+            acc = acc + t * t;
+        }
+    }
+    for (; j < d; j++) {
+        const double t = qd[j] - cr[j];
+        acc = acc + t * t;
+    }
+    return acc;
+}
+
+// Finish of the fused tensor-core probe (k_probe_tc<true>), warp per query.
+// a_(np) = np-th smallest of the parts' 16 smallest screen values (their
+// union holds the row's 16 smallest, np <= 16; radix select on
+// order-preserving keys).  The margin set {(a, c) in the parts' candidate
+// buffers : a <= a_(np) + 2 delta_q} (every member was appended, see
+// mrq_probe_tc.cu) is rescored in fp64 left to right over i and the np
+// smallest (qn2, c) are kept.  If a buffer overflowed, all k centroids are
+// rescored.
+__global__ void __launch_bounds__(128) k_probe_finish_w(int64_t nq, int k, int d, int np, const double *__restrict__ qp,
+                                                        int D, const double *__restrict__ C,
+                                                        const double *__restrict__ qnorm, double cmax, double kappa,
+                                                        const uint2 *__restrict__ cbuf, int P, int capp,
+                                                        const uint32_t *__restrict__ ccnt,
+                                                        const float *__restrict__ kvbuf, uint32_t *__restrict__ cand,
+                                                        uint32_t *__restrict__ probe, double *__restrict__ probe_qn2,
+                                                        uint32_t *__restrict__ ncand_out)
+{
+    extern __shared__ unsigned char wsm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+    const int64_t q = (int64_t)blockIdx.x * wpb + warp;
+    if (q >= nq) return;
+    SelItem *lst = (SelItem *)wsm + (size_t)warp * (np + MRQ_SELQ);
+    SelItem *queue = lst + np;
+    // a_(np): the P * 16 part minima, up to 8 per lane (P <= 16)
+    const int nv = P * 16;
+    uint32_t key[8];
+    bool all = false;
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+        const int i = j * 32 + lane;
+        key[j] = i < nv ? f2key(kvbuf[q * nv + i]) : 0xFFFFFFFFu;
+    }
+    for (int pp = lane; pp < P; pp += 32) all |= ccnt[q * P + pp] > (uint32_t)capp;
+    all = __any_sync(0xffffffffu, all);
+    uint32_t res = 0;
+    for (int bit = 31; bit >= 0; bit--) {
+        const uint32_t t = res | (1u << bit);
+        int cnt = 0;
+#pragma unroll
+        for (int j = 0; j < 8; j++)
+            if (j * 32 < nv) cnt += __popc(__ballot_sync(0xffffffffu, key[j] < t));
+        if (cnt < np) res = t;
+    }
+    const double g = qnorm[q] + cmax;
+    const double thr = (double)key2f(res) + 2.0 * (kappa * (g * g));
+    uint32_t *cq = cand + q * k;
+    uint32_t nc = 0;
+    if (all) {
+        nc = (uint32_t)k;
+    } else {
+        for (int pp = 0; pp < P; pp++) {
+            const uint32_t n = ccnt[q * P + pp];
+            const uint2 *rb = cbuf + (q * P + pp) * capp;
+            for (uint32_t e0 = 0; e0 < n; e0 += 32) {
+                const uint32_t e = e0 + lane;
+                uint2 x = make_uint2(0u, 0u);
+                if (e < n) x = rb[e];
+                const bool in = e < n && (double)__uint_as_float(x.x) <= thr;
+                const unsigned bal = __ballot_sync(0xffffffffu, in);
+                if (in) cq[nc + __popc(bal & ((1u << lane) - 1u))] = x.y;
+                nc += __popc(bal);
+            }
+        }
+        __syncwarp();
+    }
+    const double *qd = qp + q * D;
+    WarpSel top;
+    top.init(lst, np, true, queue);
+    for (uint32_t e0 = 0; e0 < nc; e0 += 32) {
+        const uint32_t e = e0 + lane;
+        SelItem it = sel_inf();
+        if (e < nc) {
+            const uint32_t c = all ? e : cq[e];
+            it.key = sqdist_rows8(C + (int64_t)c * d, qd, d);
+            it.id = c;
+            it.pay = c;
+        }
+        top.offer(it, e < nc);
+    }
+    top.finish();
+    for (int p = lane; p < np; p += 32) {
+        const bool ok = lst[p].id != 0xFFFFFFFFu;
+        probe[q * np + p] = ok ? lst[p].id : 0xFFFFFFFFu;
+        probe_qn2[q * np + p] = ok ? lst[p].key : __longlong_as_double(0x7ff0000000000000ll);
+    }
+    if (lane == 0) ncand_out[q] = nc;
+}
+
+int launch_probe_finish_w(int64_t nq, int k, int d, int np, const double *qp, int D, const double *C,
+                          const double *qnorm, double cmax, double kappa, const uint2 *cbuf, int P, int capp,
+                          const uint32_t *ccnt, const float *kvbuf, uint32_t *cand, uint32_t *probe,
+                          double *probe_qn2, uint32_t *ncand, cudaStream_t st)
+{
+    if (P > 16) {
+        mrq_set_error("probe parts %d > 16", P);
+        return MRQ_EINVAL;
+    }
+    const int wpb = 4;
+    const size_t smem = (size_t)wpb * (np + MRQ_SELQ) * sizeof(SelItem);
+    int rc = set_attr((const void *)k_probe_finish_w, smem);
+    if (rc) return rc;
+    k_probe_finish_w<<<(unsigned)((nq + wpb - 1) / wpb), wpb * 32, smem, st>>>(
+        nq, k, d, np, qp, D, C, qnorm, cmax, kappa, cbuf, P, capp, ccnt, kvbuf, cand, probe, probe_qn2, ncand);
+    return MRQ_OK;
 }
 
 int launch_probe_select_w(const float *approx, int64_t nq, int k, int d, int np, const double *qp, int D,

@@ -47,7 +47,7 @@ class SearchParams(C.Structure):
 class Stats(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in ("scanned", "stage1_pass", "stage2_pass", "exact", "seeds")] + \
                [(n, C.c_double) for n in ("ms_total", "ms_qprep", "ms_probe", "ms_quant", "ms_seed", "ms_scan",
-                                          "ms_stage2", "ms_rerank", "ms_topk", "ms_comm")]
+                                          "ms_stage2", "ms_rerank", "ms_topk", "ms_comm", "ms_head")]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

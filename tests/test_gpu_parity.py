@@ -228,6 +228,8 @@ def test_probe_tensor_core_screen_bound(case):
     d, k = case["d"], bf.k
     Q = case["Q"]
     np_ = min(case["nprobe"][-1], k)
+    m = case["m"]
+    m.mrq_debug_set(gx.h, "probe_unfused", 1)     # the screen goes to HBM ("approx") for inspection
     g1 = gx.search(Q, K=10, nprobe=np_)
     approx = gx.fetch("approx", "f32").reshape(Q.shape[0], k).astype(np.float64)
     qp = gx.fetch("qp", "f64").reshape(Q.shape[0], -1)[:, :d]
@@ -239,8 +241,17 @@ def test_probe_tensor_core_screen_bound(case):
     err = np.abs(approx - key)
     assert np.all(err <= bound[:, None]), float((err / bound[:, None]).max())
     probe_tc = gx.fetch("probe", "u32").copy()
-    case["m"].mrq_debug_set(gx.h, "cuda_core_probe", 1)
+    m.mrq_debug_set(gx.h, "cuda_core_probe", 1)
     g2 = gx.search(Q, K=10, nprobe=np_)
-    case["m"].mrq_debug_set(gx.h, "cuda_core_probe", 0)
+    m.mrq_debug_set(gx.h, "cuda_core_probe", 0)
     assert np.array_equal(probe_tc, gx.fetch("probe", "u32"))
     assert np.array_equal(g1[0], g2[0]) and np.array_equal(g1[1], g2[1])
+    m.mrq_debug_set(gx.h, "probe_unfused", 0)     # fused screen + running top-np (np <= 16)
+    for npb in sorted({1, min(np_, 16), min(16, k)}):
+        m.mrq_debug_set(gx.h, "probe_unfused", 1)
+        gu = gx.search(Q, K=10, nprobe=npb)
+        pu = gx.fetch("probe", "u32").copy()
+        m.mrq_debug_set(gx.h, "probe_unfused", 0)
+        gf = gx.search(Q, K=10, nprobe=npb)
+        assert np.array_equal(pu, gx.fetch("probe", "u32")), npb
+        assert np.array_equal(gu[0], gf[0]) and np.array_equal(gu[1], gf[1])
