@@ -198,6 +198,10 @@ static int load_impl(mrq_index *ix, const char *build_file, const float *base, i
         mrq_shard_lists(cnt, ix->world, owner);
         for (int c = 0; c < k; c++) own[c] = owner[c] == (uint32_t)ix->rank;
         TRY(mrq_comm_init(ix, dist));
+    } else if (dist && dist->nccl_unique_id) {
+        // a one-rank NCCL communicator: the sharded path (mrq_debug_set
+        // "force_exchange") then runs its all-gathers through NCCL
+        TRY(mrq_comm_init(ix, dist));
     }
     // list slots: owned lists only, each start aligned to MRQ_SLOT_ALIGN
     ix->h_list_off.assign(k + 1, 0);
@@ -211,7 +215,7 @@ static int load_impl(mrq_index *ix, const char *build_file, const float *base, i
         ix->max_list = std::max(ix->max_list, ix->h_list_size[c]);
     }
     ix->h_list_off[k] = (uint32_t)pos;
-    ix->npad = (int64_t)((pos + 128 + 127) / 128 * 128);   // scan tiles may read 128 slots past a list
+    ix->npad = (int64_t)((pos + 256 + 127) / 128 * 128);   // scan tiles may read 256 slots past a list start
     if (ix->npad >= (int64_t)0xFFFFFFF0ll) {
         mrq_set_error("index too large for 32-bit slots");
         return MRQ_EINVAL;
@@ -526,7 +530,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
     {
         LaunchScan a;
         a.nq = nq;
-        a.smem = (size_t)(np + 1) * 4;
+        a.smem = (size_t)(3 * np + 1) * 4;
         a.probe = probe; a.np = np; a.npad = ix->npad; a.list_off = ix->list_off; a.list_size = ix->list_size;
         a.codes = ix->codes; a.f1 = ix->f1; a.f2 = ix->f2; a.f3 = ix->f3; a.planes = planes; a.qconst = qconst;
         a.eps_r = eps_r; a.tau0 = tau0; a.isd = isd; a.f1_off = f1_off; a.f1_cnt = f1_cnt; a.f1_pos = f1_pos;

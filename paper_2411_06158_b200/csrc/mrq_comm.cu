@@ -160,10 +160,6 @@ void mrq_comm_free(mrq_index *ix)
 
 int mrq_allgather(mrq_index *ix, const void *send, void *recv, size_t bytes, cudaStream_t st)
 {
-    if (ix->world == 1) {
-        MRQ_CUDA_TRY(cudaMemcpyAsync(recv, send, bytes, cudaMemcpyDeviceToDevice, st));
-        return MRQ_OK;
-    }
 #if MRQ_HAVE_NCCL
     if (ix->nccl_comm) {
         NcclApi &a = nccl();
@@ -175,6 +171,10 @@ int mrq_allgather(mrq_index *ix, const void *send, void *recv, size_t bytes, cud
         return MRQ_OK;
     }
 #endif
+    if (ix->world == 1) {
+        MRQ_CUDA_TRY(cudaMemcpyAsync(recv, send, bytes, cudaMemcpyDeviceToDevice, st));
+        return MRQ_OK;
+    }
     if (!ix->host_ag) {
         mrq_set_error("no exchange configured for world=%d", ix->world);
         return MRQ_ENCCL;

@@ -353,10 +353,15 @@ __global__ void k_exclusive_scan(const uint64_t *__restrict__ in, int64_t n, uin
 }
 
 // The code scan (hot loop of Alg.2 L7-L12): block per query, every
-// warp streams (list, 128-slot chunk) tiles of the query's probed lists.  Each
-// lane reads 4 consecutive slots with 128-bit loads: W code words (word-major
-// planes codes[w][slot]) and f1/f2/f3; evaluates LB1 in registers and appends
-// slots with LB1 < tau0 (stage 1, F1) to the query's segment of f1_pos.
+// warp streams (list, MRQ_SCAN_TILE-slot) tiles of the query's probed lists.
+// Each lane owns slots base + 128 h .. base + 128 h + 3 of its tile and reads
+// them with 128-bit loads (W code words of the word-major planes
+// codes[w][slot], then f1/f2/f3) before evaluating any, evaluates LB1 in
+// registers and appends slots with LB1 < tau0 (stage 1, F1) to the query's
+// segment of f1_pos.  Warp 0 builds the tile prefix of the probed lists in
+// shared memory with a shuffle scan.
+#define MRQ_SCAN_TILE 128
+#define MRQ_SCAN_H (MRQ_SCAN_TILE / 128)
 template <int W>
 __global__ void __launch_bounds__(256) k_scan(
     const uint32_t *__restrict__ probe, int np, int64_t npad, const uint32_t *__restrict__ list_off,
@@ -367,19 +372,41 @@ __global__ void __launch_bounds__(256) k_scan(
 {
     extern __shared__ unsigned char csm[];
     uint32_t *tile_pre = (uint32_t *)csm;     // np + 1
+    uint32_t *lst_start = tile_pre + np + 1;  // np
+    uint32_t *lst_end = lst_start + np;       // np
     __shared__ uint32_t sh_cnt;
     const int64_t q = blockIdx.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nwarps = blockDim.x >> 5;
-    if (threadIdx.x == 0) {
-        uint32_t acc = 0;
-        for (int p = 0; p < np; p++) {
-            tile_pre[p] = acc;
-            uint32_t c = probe[q * np + p];
-            if (c != 0xFFFFFFFFu) acc += (list_size[c] + 127) / 128;
+    if (warp == 0) {
+        uint32_t carry = 0;
+        for (int p0 = 0; p0 < np; p0 += 32) {
+            const int p = p0 + lane;
+            uint32_t nt = 0, st = 0, sz = 0;
+            if (p < np) {
+                const uint32_t c = probe[q * np + p];
+                if (c != 0xFFFFFFFFu) {
+                    st = list_off[c];
+                    sz = list_size[c];
+                    nt = (sz + MRQ_SCAN_TILE - 1) / MRQ_SCAN_TILE;
+                }
+            }
+            uint32_t x = nt;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (p < np) {
+                tile_pre[p] = carry + x - nt;
+                lst_start[p] = st;
+                lst_end[p] = st + sz;
+            }
+            carry += __shfl_sync(0xffffffffu, x, 31);
         }
-        tile_pre[np] = acc;
-        sh_cnt = 0;
+        if (lane == 0) {
+            tile_pre[np] = carry;
+            sh_cnt = 0;
+        }
     }
     __syncthreads();
     const double eps_r = eps_r_arr[q], tau0 = tau0_arr[q];
@@ -400,41 +427,50 @@ __global__ void __launch_bounds__(256) k_scan(
 #pragma unroll
             for (int i = 0; i < 5; i++) qc[i] = gc[i];
         }
-        const uint32_t c = probe[q * np + p];
-        const uint32_t lstart = list_off[c], lend = lstart + list_size[c];
-        const uint32_t base = lstart + (t - tile_pre[p]) * 128 + lane * 4;
-        uint4 cw[W];
+        const uint32_t lend = lst_end[p];
+        const uint32_t base = lst_start[p] + (t - tile_pre[p]) * MRQ_SCAN_TILE + lane * 4;
+        uint4 cw[MRQ_SCAN_H][W];
+        float4 a1[MRQ_SCAN_H], a2[MRQ_SCAN_H], a3[MRQ_SCAN_H];
 #pragma unroll
-        for (int w = 0; w < W; w++) cw[w] = __ldg((const uint4 *)(codes + (int64_t)w * npad + base));
-        const float4 a1 = __ldg((const float4 *)(f1 + base));
-        const float4 a2 = __ldg((const float4 *)(f2 + base));
-        const float4 a3 = __ldg((const float4 *)(f3 + base));
-        bool fl[4];
+        for (int h = 0; h < MRQ_SCAN_H; h++) {
+            const uint32_t b = base + h * 128;
 #pragma unroll
-        for (int r = 0; r < 4; r++) {
-            uint32_t code[W];
-#pragma unroll
-            for (int w = 0; w < W; w++) code[w] = r == 0 ? cw[w].x : r == 1 ? cw[w].y : r == 2 ? cw[w].z : cw[w].w;
-            const float v1 = r == 0 ? a1.x : r == 1 ? a1.y : r == 2 ? a1.z : a1.w;
-            const float v2 = r == 0 ? a2.x : r == 1 ? a2.y : r == 2 ? a2.z : a2.w;
-            const float v3 = r == 0 ? a3.x : r == 1 ? a3.y : r == 2 ? a3.z : a3.w;
-            double dis;
-            const double lb1 = mrq_lb1<W>(code, pl, qc, isd, eps_r, v1, v2, v3, &dis);
-            fl[r] = (base + r < lend) && (lb1 < tau0);
+            for (int w = 0; w < W; w++) cw[h][w] = __ldg((const uint4 *)(codes + (int64_t)w * npad + b));
+            a1[h] = __ldg((const float4 *)(f1 + b));
+            a2[h] = __ldg((const float4 *)(f2 + b));
+            a3[h] = __ldg((const float4 *)(f3 + b));
         }
-        const unsigned b0 = __ballot_sync(0xffffffffu, fl[0]), b1 = __ballot_sync(0xffffffffu, fl[1]);
-        const unsigned b2 = __ballot_sync(0xffffffffu, fl[2]), b3 = __ballot_sync(0xffffffffu, fl[3]);
-        const int n0 = __popc(b0), n1 = __popc(b1), n2 = __popc(b2), n3 = __popc(b3);
-        const int tot = n0 + n1 + n2 + n3;
-        if (tot) {
-            uint32_t wb = 0;
-            if (lane == 0) wb = atomicAdd(&sh_cnt, (uint32_t)tot);
-            wb = __shfl_sync(0xffffffffu, wb, 0);
-            const unsigned lt = (1u << lane) - 1u;
-            if (fl[0]) out[wb + __popc(b0 & lt)] = base;
-            if (fl[1]) out[wb + n0 + __popc(b1 & lt)] = base + 1;
-            if (fl[2]) out[wb + n0 + n1 + __popc(b2 & lt)] = base + 2;
-            if (fl[3]) out[wb + n0 + n1 + n2 + __popc(b3 & lt)] = base + 3;
+#pragma unroll
+        for (int h = 0; h < MRQ_SCAN_H; h++) {
+            const uint32_t b = base + h * 128;
+            bool fl[4];
+#pragma unroll
+            for (int r = 0; r < 4; r++) {
+                uint32_t code[W];
+#pragma unroll
+                for (int w = 0; w < W; w++)
+                    code[w] = r == 0 ? cw[h][w].x : r == 1 ? cw[h][w].y : r == 2 ? cw[h][w].z : cw[h][w].w;
+                const float v1 = r == 0 ? a1[h].x : r == 1 ? a1[h].y : r == 2 ? a1[h].z : a1[h].w;
+                const float v2 = r == 0 ? a2[h].x : r == 1 ? a2[h].y : r == 2 ? a2[h].z : a2[h].w;
+                const float v3 = r == 0 ? a3[h].x : r == 1 ? a3[h].y : r == 2 ? a3[h].z : a3[h].w;
+                double dis;
+                const double lb1 = mrq_lb1<W>(code, pl, qc, isd, eps_r, v1, v2, v3, &dis);
+                fl[r] = (b + r < lend) && (lb1 < tau0);
+            }
+            const unsigned b0 = __ballot_sync(0xffffffffu, fl[0]), b1 = __ballot_sync(0xffffffffu, fl[1]);
+            const unsigned b2 = __ballot_sync(0xffffffffu, fl[2]), b3 = __ballot_sync(0xffffffffu, fl[3]);
+            const int n0 = __popc(b0), n1 = __popc(b1), n2 = __popc(b2), n3 = __popc(b3);
+            const int tot = n0 + n1 + n2 + n3;
+            if (tot) {
+                uint32_t wb = 0;
+                if (lane == 0) wb = atomicAdd(&sh_cnt, (uint32_t)tot);
+                wb = __shfl_sync(0xffffffffu, wb, 0);
+                const unsigned lt = (1u << lane) - 1u;
+                if (fl[0]) out[wb + __popc(b0 & lt)] = b;
+                if (fl[1]) out[wb + n0 + __popc(b1 & lt)] = b + 1;
+                if (fl[2]) out[wb + n0 + n1 + __popc(b2 & lt)] = b + 2;
+                if (fl[3]) out[wb + n0 + n1 + n2 + __popc(b3 & lt)] = b + 3;
+            }
         }
     }
     __syncthreads();

@@ -32,6 +32,8 @@ CASES = {
     "sift50k": ("sift", 50_000, 64, 128, 64, 256, (8, 32), None),
     "deep_d48": ("deep", 20_000, 48, 96, 48, 64, (5, 16), None),
     "gist_small": ("gist", 8_000, 24, 960, 128, 32, (4,), None),
+    "gist_d256": ("gist", 6_000, 16, 960, 256, 24, (3, 24), None),        # W = 8 code words
+    "emb_d512": ("emb", 5_000, 12, 1536, 512, 16, (2, 16), None),         # W = 16, D = 1536
 }
 
 

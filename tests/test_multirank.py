@@ -179,3 +179,24 @@ def test_virtual_ranks_equal_single_gpu(world, tau, mode):
     assert tot("stage2_pass") == sr.stage2_pass
     for x in idx:
         x.close()
+
+
+@pytest.mark.gpu
+def test_nccl_one_rank_exchange_equals_fast_path():
+    """The NCCL transport itself (dlopen'ed libnccl, ncclCommInitRank,
+    ncclAllGather on the search stream) on a one-rank communicator: the
+    sharded path through NCCL gives the single-GPU result bit for bit."""
+    m = _lib()
+    X, Q, bfile = _tiny()
+    ref = m.Index(bfile, X, 16)
+    ir, dr, _ = ref.search(Q, K=10, nprobe=4)
+    ref.close()
+    uid = m.mrq_nccl_unique_id()
+    assert len(uid) == 128
+    a = m.Index(bfile, X, 16, rank=0, world=1, nccl_unique_id=uid)
+    m.mrq_debug_set(a.h, "force_exchange", 1)
+    for tau in ("TIGHT", "LOOSE"):
+        ia, da, _ = a.search(Q, K=10, nprobe=4, tau_schedule=tau)
+        if tau == "TIGHT":
+            assert np.array_equal(ia, ir) and np.array_equal(da, dr)
+    a.close()
