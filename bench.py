@@ -137,7 +137,7 @@ def recall_at_k(found, gt, K):
     return hits / float(g.shape[0] * K)
 
 
-def cpu_oracle_leg(bfile, X, Q, K, nprobe, budget_s=15.0):
+def cpu_oracle_leg(bfile, X, Q, K, nprobe, budget_s=15.0, **kw):
     """The oracle (oracle/), as it stands, timed on this host's cores on a
     bounded query sample of the same workload.  Returns (qps, cores, sample)."""
     import oracle
@@ -149,11 +149,11 @@ def cpu_oracle_leg(bfile, X, Q, K, nprobe, budget_s=15.0):
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
     n = 16
     t = time.time()
-    ox.search(Q[:n], K=K, nprobe=nprobe)
+    ox.search(Q[:n], K=K, nprobe=nprobe, **kw)
     dt = max(time.time() - t, 1e-3)
     n2 = int(min(Q.shape[0], max(32, n * budget_s / dt)))
     t = time.time()
-    ox.search(Q[:n2], K=K, nprobe=nprobe)
+    ox.search(Q[:n2], K=K, nprobe=nprobe, **kw)
     dt = time.time() - t
     return n2 / dt, cores, "first %d of %d queries, nprobe=%d, FULL/TIGHT; index encode %.1fs untimed" % (
         n2, Q.shape[0], nprobe, enc)
@@ -169,6 +169,8 @@ def main():
     ap.add_argument("--nprobe", type=int, default=0, help="0 = smallest grid nprobe with recall@10 >= 0.95")
     ap.add_argument("--K", type=int, default=10)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--seed-lists", type=int, default=2, help="decision T: seed pool spans >= this many lists")
+    ap.add_argument("--seed-mult", type=int, default=2, help="decision T: K' = seed_mult * K")
     args = ap.parse_args()
     rank, world, local = dist_env()
     cfg_name = args.config
@@ -212,7 +214,8 @@ def main():
     stream = torch.cuda.current_stream(dev)
 
     def run(nprobe, tau="TIGHT", stats=True):
-        p = mrq.SearchParams.make(K=K, nprobe=nprobe, tau_schedule=tau)
+        p = mrq.SearchParams.make(K=K, nprobe=nprobe, tau_schedule=tau, seed_lists=args.seed_lists,
+                                  seed_mult=args.seed_mult)
         st = mrq.Stats() if stats else None
         mrq.mrq_search_batch_device(h, dq, p, d_ids, d_dist, st, stream.cuda_stream)
         return st
@@ -290,7 +293,7 @@ def main():
 
     # e2e through the host-buffer call (pinned host queries; H2D + D2H inside the timed region)
     hq = torch.from_numpy(Q).pin_memory().numpy()
-    p = mrq.SearchParams.make(K=K, nprobe=nprobe)
+    p = mrq.SearchParams.make(K=K, nprobe=nprobe, seed_lists=args.seed_lists, seed_mult=args.seed_mult)
     for _ in range(2):
         mrq.mrq_search_batch(h, hq, p, with_stats=False)
     e2e_t = []
@@ -309,7 +312,8 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            qps, cores, sample = cpu_oracle_leg(bfile, X, Q, K, nprobe)
+            qps, cores, sample = cpu_oracle_leg(bfile, X, Q, K, nprobe, seed_lists=args.seed_lists,
+                                                seed_mult=args.seed_mult)
             cpu = {"value": round(qps, 2), "unit": "queries/s", "cores": cores, "kind": "oracle", "sample": sample}
         except Exception as e:  # pragma: no cover
             cpu = {"value": None, "unit": "queries/s", "cores": os.cpu_count(), "kind": "oracle",
@@ -332,6 +336,7 @@ def main():
         "config": {"workload": "SIFT-shaped (BASELINE.json configs[1])" if cfg_name == "sift" else cfg_name,
                    "N": int(X.shape[0]), "Q": nq, "D": int(X.shape[1]), "d": d, "k": hdr["k"], "K": K,
                    "nprobe": nprobe, "tau_schedule": "TIGHT", "eps0": 1.9, "m": 4.0, "mode": "FULL",
+                   "seed_lists": args.seed_lists, "seed_mult": args.seed_mult,
                    "recall10": round(rc, 4) if rc is not None else None, "l2": "flushed (512 MB write) between timed steps",
                    "parallelism": "lists sharded over %d GPU(s)" % world, "base_sha_match": sha_ok,
                    "scanned_per_step": scanned, "exact_per_query": round(float(np.mean([s.exact for s in sts])) / nq, 2),
@@ -370,12 +375,12 @@ def reference_arm(args, rank, world, cfg_name, bfile, gtfile):
     K = args.K
     sample = 200
     for _ in range(max(args.warmup, 1)):
-        ox.search(Q[:16], K=K, nprobe=nprobe)
+        ox.search(Q[:16], K=K, nprobe=nprobe, seed_lists=args.seed_lists, seed_mult=args.seed_mult)
     ts = []
     for i in range(args.steps):
         s = (i * sample) % Q.shape[0]
         t = time.time()
-        ox.search(Q[s:s + sample], K=K, nprobe=nprobe)
+        ox.search(Q[s:s + sample], K=K, nprobe=nprobe, seed_lists=args.seed_lists, seed_mult=args.seed_mult)
         ts.append(time.time() - t)
     dt = float(np.mean(ts))
     qps = sample / dt

@@ -73,6 +73,8 @@ typedef struct {
     int32_t tau_schedule; /* 0 TIGHT, 1 LOOSE (DESIGN.md decision T)                          */
     int32_t seed_mult;    /* K' = seed_mult * K seeds (>= 1; default 2)                        */
     double resid_scale;   /* eps_r = (resid_scale * m) * sigma; 2 = distance domain (default) */
+    int32_t seed_lists;   /* decision T seed pool: the first probed lists until they hold >= K'
+                             candidates AND at least seed_lists lists (>= 1; 0 means 1)      */
 } mrq_search_params;
 
 /* Per-call counters (summed over queries; at world > 1 over this rank's lists

@@ -58,7 +58,8 @@ class OrcIndex(C.Structure):
 class OrcParams(C.Structure):
     _fields_ = [("K", C.c_int32), ("nprobe", C.c_int32), ("eps0", C.c_double), ("m", C.c_double),
                 ("mode", C.c_int32), ("tau_schedule", C.c_int32), ("seed_mult", C.c_int32),
-                ("resid_scale", C.c_double), ("Bq", C.c_int32), ("est_kind", C.c_int32)]
+                ("resid_scale", C.c_double), ("Bq", C.c_int32), ("est_kind", C.c_int32),
+                ("seed_lists", C.c_int32)]
 
 
 class OrcStats(C.Structure):
@@ -111,11 +112,11 @@ class Index:
         return np.diff(self.list_off)
 
     def search(self, queries, K=10, nprobe=4, eps0=1.9, m=4.0, mode="FULL", tau_schedule="TIGHT",
-               seed_mult=2, resid_scale=2.0, Bq=4, est_kind=0, dump=False, cap=None):
+               seed_mult=2, resid_scale=2.0, Bq=4, est_kind=0, dump=False, cap=None, seed_lists=1):
         Qv = np.ascontiguousarray(queries, dtype=np.float32)
         nq = Qv.shape[0]
         pr = OrcParams(K, nprobe, eps0, m, MODES[mode] if isinstance(mode, str) else mode,
-                       0 if tau_schedule == "TIGHT" else 1, seed_mult, resid_scale, Bq, est_kind)
+                       0 if tau_schedule == "TIGHT" else 1, seed_mult, resid_scale, Bq, est_kind, seed_lists)
         ids = np.zeros((nq, K), np.int64)
         dist = np.zeros((nq, K), np.float32)
         st = OrcStats()

@@ -58,6 +58,7 @@ typedef struct {
     int32_t Bq;              /* query bits; levels 0 .. 2^Bq - 1                      */
     int32_t est_kind;        /* 0 quantized query, 1 unquantized query r,
                                 2 no quantization at all (exact <t, q_d - c>)         */
+    int32_t seed_lists;      /* decision T: the seed pool spans >= seed_lists lists    */
 } orc_params;
 
 typedef struct {
@@ -459,7 +460,8 @@ static void search_one(const orc_index *ix, const float *q, const orc_params *pr
     } else {                                     /* FULL / STAGE1_ONLY: decision T   */
         /* seeds: first lists in probe order holding >= K' candidates */
         int64_t pool = 0;
-        for (int p = 0; p < np; p++) { pool = listend[p]; if (pool >= Kp) break; }
+        const int sl = pr->seed_lists > 0 ? pr->seed_lists : 1;
+        for (int p = 0; p < np; p++) { pool = listend[p]; if (pool >= Kp && p + 1 >= sl) break; }
         vi_t *sv = (vi_t *)malloc(sizeof(vi_t) * (size_t)(pool > 0 ? pool : 1));
         for (int64_t i = 0; i < pool; i++) { sv[i].v = cs[i].dis; sv[i].id = cs[i].id; sv[i].slot = (int32_t)i; }
         qsort(sv, (size_t)pool, sizeof(vi_t), cmp_vi);

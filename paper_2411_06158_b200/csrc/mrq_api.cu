@@ -431,7 +431,9 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
     {
         dim3 grid((D + 31) / 32, (unsigned)((nq + 31) / 32));
         k_project<<<grid, dim3(32, 8), 0, st>>>(d_q, nq, D, ix->mu, ix->PT, qp);
-        k_qtail<<<(unsigned)((nq + 7) / 8), 256, 0, st>>>(qp, nq, D, d, W, ix->lam, ix->RT, p->resid_scale, p->m, qr2,
+        if (D * 8 * 8 > 48 * 1024)
+            MRQ_CUDA_TRY(cudaFuncSetAttribute(k_qtail, cudaFuncAttributeMaxDynamicSharedMemorySize, D * 8 * 8));
+        k_qtail<<<(unsigned)((nq + 7) / 8), 256, (size_t)D * 8 * 8, st>>>(qp, nq, D, d, W, ix->lam, ix->RT, p->resid_scale, p->m, qr2,
                                                           eps_r, r0, qd32, qnorm);
     }
     if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[1], st));
@@ -505,6 +507,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
     sa.f1_diso = f1_diso; sa.f2_head = f2_head; sa.f2_exact = f2_exact; sa.f1_off = f1_off;
     sa.out_ids = d_ids; sa.out_dist = d_dist;
     sa.f1_id = f1_id;
+    sa.seed_lists = p->seed_lists > 0 ? p->seed_lists : 1;
     sa.list_size_g = ix->list_size_g; sa.s0_id = s0_id; sa.s1_id = s1_id; sa.xout = nullptr;
 
     // ---- a4: seeds S0 and tau0 (decision T); EXACT mode scans everything
@@ -626,7 +629,8 @@ static int check_params(const mrq_index *ix, int64_t nq, const mrq_search_params
     }
     if (nq < 0 || p->K < 1 || p->K > MRQ_MAX_K || p->nprobe < 1 || p->nprobe > MRQ_MAX_NPROBE ||
         p->nprobe > ix->k || !(p->eps0 > 0) || !(p->m > 0) || p->mode < 0 || p->mode > 2 ||
-        p->tau_schedule < 0 || p->tau_schedule > 1 || p->seed_mult < 1 || !(p->resid_scale > 0)) {
+        p->tau_schedule < 0 || p->tau_schedule > 1 || p->seed_mult < 1 || !(p->resid_scale > 0) ||
+        p->seed_lists < 0) {
         mrq_set_error("InvalidConfig: K=%d nprobe=%d (k=%d) eps0=%g m=%g mode=%d tau=%d seed_mult=%d rscale=%g",
                       p->K, p->nprobe, ix->k, p->eps0, p->m, p->mode, p->tau_schedule, p->seed_mult,
                       p->resid_scale);

@@ -130,16 +130,36 @@ __global__ void k_rc(const double *__restrict__ C, const double *__restrict__ RT
 // ======================================================================= a1
 // Alg.2 L2-L4, warp per query: ||q_r||^2, sigma^2 = sum_{i>=d}
 // q_i^2 lambda_i (Eq.6), eps_r = (resid_scale m) sigma (Eq.7 / Alg.2
-// L11, reading A-5), r0 = R q_d; plus the fp32 q_d and ||q_d|| the probe uses.
-__global__ void k_qtail(const double *__restrict__ qp, int64_t nq, int D, int d, int W,
-                        const double *__restrict__ lam, const double *__restrict__ RT, double rscale, double m,
-                        double *__restrict__ qr2o, double *__restrict__ eps_r, double *__restrict__ r0,
-                        float *__restrict__ qd32, double *__restrict__ qnorm)
+// L11, reading R-4), r0 = R q_d; plus the fp32 q_d and ||q_d|| the probe uses.
+// The query row is staged in shared memory; the three left-to-right sums run
+// on three lanes at once, r0_j on lane j (j = lane + 32 w).
+__global__ void __launch_bounds__(256) k_qtail(const double *__restrict__ qp, int64_t nq, int D, int d, int W,
+                                               const double *__restrict__ lam, const double *__restrict__ RT,
+                                               double rscale, double m, double *__restrict__ qr2o,
+                                               double *__restrict__ eps_r, double *__restrict__ r0,
+                                               float *__restrict__ qd32, double *__restrict__ qnorm)
 {
-    const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
+    extern __shared__ double qsm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
     if (q >= nq) return;
-    const double *row = qp + q * D;
+    double *row = qsm + (size_t)warp * D;
+    const double *g = qp + q * D;
+    for (int i = lane; i < D; i += 32) row[i] = g[i];
+    __syncwarp();
+    if (lane == 0) {
+        double a = 0.0;
+        for (int i = d; i < D; i++) a = a + row[i] * row[i];
+        qr2o[q] = a;
+    } else if (lane == 1) {
+        double s2 = 0.0;
+        for (int i = d; i < D; i++) s2 = s2 + (row[i] * row[i]) * lam[i];
+        eps_r[q] = (rscale * m) * sqrt(s2);
+    } else if (lane == 2) {
+        double n2 = 0.0;
+        for (int i = 0; i < d; i++) n2 = n2 + row[i] * row[i];
+        qnorm[q] = sqrt(n2);
+    }
     for (int w = 0; w < W; w++) {
         const int j = w * 32 + lane;
         if (j < d) {
@@ -148,18 +168,6 @@ __global__ void k_qtail(const double *__restrict__ qp, int64_t nq, int D, int d,
             r0[q * d + j] = acc;
             qd32[q * d + j] = (float)row[j];
         }
-    }
-    if (lane == 0) {
-        double a = 0.0, s2 = 0.0;
-        for (int i = d; i < D; i++) {
-            a = a + row[i] * row[i];
-            s2 = s2 + (row[i] * row[i]) * lam[i];
-        }
-        qr2o[q] = a;
-        eps_r[q] = (rscale * m) * sqrt(s2);
-        double n2 = 0.0;
-        for (int i = 0; i < d; i++) n2 = n2 + row[i] * row[i];
-        qnorm[q] = sqrt(n2);
     }
 }
 

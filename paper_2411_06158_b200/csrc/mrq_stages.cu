@@ -12,7 +12,7 @@
 // ----------------------------------------------------------------------- a4
 // Seeds S0 and tau0 (decision T; replaces "tau <- threshold of the
 // result queue", Alg.2 L9 P:311): the probed lists in probe order until they
-// hold >= K' candidates form the pool; S0 = the K' smallest (dis', id) of the
+// hold >= K' candidates and number >= seed_lists form the pool; S0 = the K' smallest (dis', id) of the
 // pool; exact distances ||x_p - q_p||^2 (Alg.2 L14 P:316) of S0; tau0 = K-th
 // smallest exact over S0 (+inf if |S0| < K).
 template <int W>
@@ -24,7 +24,7 @@ __global__ void __launch_bounds__(256) k_seed_w(
     const uint32_t *__restrict__ planes, const double *__restrict__ qconst, const double *__restrict__ qp,
     const double *__restrict__ eps_r_arr, double isd, uint32_t *__restrict__ s0_cnt, uint32_t *__restrict__ s0_pos,
     double *__restrict__ s0_exact, double *__restrict__ tau0, const uint32_t *__restrict__ list_size_g,
-    uint32_t *__restrict__ s0_id, XItem *__restrict__ xout)
+    uint32_t *__restrict__ s0_id, XItem *__restrict__ xout, int seed_lists)
 {
     extern __shared__ unsigned char wsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(256) k_seed_w(
     auto scan_pool = [&](auto each) {
         int64_t npool = 0;
         nloc = 0;
-        for (int p = 0; p < np && npool < Kp; p++) {
+        for (int p = 0; p < np && (npool < Kp || p < seed_lists); p++) {
             const uint32_t c = probe[q * np + p];
             if (c == 0xFFFFFFFFu) continue;
             npool += list_size_g[c];
@@ -573,7 +573,8 @@ int launch_seed_w(int W, const StageArgs &a, cudaStream_t st)
         k_seed_w<WW><<<grid, wpb * 32, smem, st>>>(a.nq, a.aligned, a.probe, a.np, a.K, a.Kp, a.D, a.d, a.npad, a.list_off,   \
                                                    a.list_size, a.ids, a.codes, a.f1, a.f2, a.f3, a.heads, a.tails, \
                                                    a.planes, a.qconst, a.qp, a.eps_r, a.isd, a.s0_cnt, a.s0_pos,    \
-                                                   a.s0_exact, a.tau0, a.list_size_g, a.s0_id, a.xout);             \
+                                                   a.s0_exact, a.tau0, a.list_size_g, a.s0_id, a.xout,              \
+                                                   a.seed_lists);                                                   \
     } while (0)
     switch (W) {
     case 1: MRQ_SEED(1); break;

@@ -35,13 +35,13 @@ class DistCfg(C.Structure):
 class SearchParams(C.Structure):
     _fields_ = [("K", C.c_int32), ("nprobe", C.c_int32), ("eps0", C.c_double), ("m", C.c_double),
                 ("mode", C.c_int32), ("tau_schedule", C.c_int32), ("seed_mult", C.c_int32),
-                ("resid_scale", C.c_double)]
+                ("resid_scale", C.c_double), ("seed_lists", C.c_int32)]
 
     @classmethod
     def make(cls, K=10, nprobe=16, eps0=1.9, m=4.0, mode="FULL", tau_schedule="TIGHT", seed_mult=2,
-             resid_scale=2.0):
+             resid_scale=2.0, seed_lists=1):
         return cls(K, nprobe, eps0, m, MRQ_MODES[mode] if isinstance(mode, str) else mode,
-                   0 if tau_schedule in ("TIGHT", 0) else 1, seed_mult, resid_scale)
+                   0 if tau_schedule in ("TIGHT", 0) else 1, seed_mult, resid_scale, seed_lists)
 
 
 class Stats(C.Structure):

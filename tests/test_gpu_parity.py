@@ -90,12 +90,12 @@ def test_encode_bit_exact(case):
     assert np.array_equal(gx.fetch("Rc", "f64").reshape(ox.k, d), ox.Rc)
 
 
-def _search_both(case, nprobe, K=10, mode="FULL", tau="TIGHT"):
+def _search_both(case, nprobe, K=10, mode="FULL", tau="TIGHT", **kw):
     gx, ox, Q = case["gx"], case["ox"], case["Q"]
     m = case["m"]
     m.mrq_debug_set(gx.h, "dump_dis", 1)
-    gi, gd, gst = gx.search(Q, K=K, nprobe=nprobe, mode=mode, tau_schedule=tau)
-    oi, od, ost, dp = ox.search(Q, K=K, nprobe=nprobe, mode=mode, tau_schedule=tau, dump=True)
+    gi, gd, gst = gx.search(Q, K=K, nprobe=nprobe, mode=mode, tau_schedule=tau, **kw)
+    oi, od, ost, dp = ox.search(Q, K=K, nprobe=nprobe, mode=mode, tau_schedule=tau, dump=True, **kw)
     return gi, gd, gst, oi, od, ost, dp
 
 
@@ -114,11 +114,12 @@ def _segments(gx, nq, cnt_name, pos_name, extra=None):
 
 
 @pytest.mark.parametrize("tau", ["TIGHT", "LOOSE"])
-def test_stagewise_parity(case, tau):
+@pytest.mark.parametrize("seed_lists,seed_mult", [(1, 2), (4, 4)])
+def test_stagewise_parity(case, tau, seed_lists, seed_mult):
     gx, ox, Q = case["gx"], case["ox"], case["Q"]
     nq, D, d = Q.shape[0], ox.D, case["d"]
     for npb in case["nprobe"]:
-        gi, gd, gst, oi, od, ost, dp = _search_both(case, npb, tau=tau)
+        gi, gd, gst, oi, od, ost, dp = _search_both(case, npb, tau=tau, seed_lists=seed_lists, seed_mult=seed_mult)
         npe = min(npb, ox.k)
         # a1 query projection, residual constants
         assert np.array_equal(gx.fetch("qp", "f64").reshape(nq, D), dp["qp"])
@@ -154,7 +155,7 @@ def test_stagewise_parity(case, tau):
             assert sorted(f1[q][0].tolist()) == sorted(dp["f1_ids"][q, :dp["f1_cnt"][q]].tolist())
         # a4 seeds
         s0c = gx.fetch("s0_cnt", "u32")
-        Kp = 20
+        Kp = 10 * seed_mult
         s0p = gx.fetch("s0_pos", "u32").reshape(nq, Kp)
         ids = _slot_to_id(gx)
         for q in range(nq):
