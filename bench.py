@@ -43,38 +43,61 @@ def peaks():
 
 
 class Clocks:
-    """Samples nvidia-smi during the timed region (B200_PROFILING.md clocks line):
-    one single-shot query every ~100 ms from a thread (a looping nvidia-smi
-    block-buffers its pipe and loses samples on terminate)."""
+    """Samples the SM clock and the clock-event (throttle) reasons DURING the
+    timed region (B200_PROFILING.md clocks line) from a thread: NVML
+    (nvidia-ml-py) every ~2 ms, so a short timed region still gets samples;
+    nvidia-smi single shots if NVML is unavailable."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    NAMES = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+             ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+             ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+             ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+             ("hw_power_brake_slowdown", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
 
     def __init__(self, gpu=0):
         self.gpu = gpu
-        self.samples = []
+        self.samples = []      # (sm_mhz, max_mhz, [reasons])
         self.stop = threading.Event()
         self.err = None
+        self.nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(gpu)
+            self.nvml = pynvml
+        except Exception as e:  # pragma: no cover
+            self.err = "nvml: %s" % e
 
     def __enter__(self):
         self.t = threading.Thread(target=self._loop, daemon=True)
         self.t.start()
         return self
 
+    def _sample_nvml(self):
+        n = self.nvml
+        sm = n.nvmlDeviceGetClockInfo(self.h, n.NVML_CLOCK_SM)
+        mx = n.nvmlDeviceGetMaxClockInfo(self.h, n.NVML_CLOCK_SM)
+        r = n.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        reasons = [name for name, attr in self.NAMES if r & getattr(n, attr, 0)]
+        self.samples.append((float(sm), float(mx), reasons))
+
+    def _sample_smi(self):
+        f = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        r = subprocess.run(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + f, "--format=csv,noheader,nounits"],
+                           capture_output=True, text=True, timeout=5)
+        p = [x.strip() for x in r.stdout.strip().split(",")]
+        if len(p) >= 6:
+            reasons = [self.NAMES[i][0] for i in range(4) if p[2 + i].lower() == "active"]
+            self.samples.append((float(p[0]), float(p[1]), reasons))
+
     def _loop(self):
         while not self.stop.is_set():
             try:
-                r = subprocess.run(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.FIELDS,
-                                    "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                parts = [p.strip() for p in r.stdout.strip().split(",")]
-                if len(parts) >= 7:
-                    self.samples.append(parts)
-                elif self.err is None:
-                    self.err = (r.stdout + r.stderr).strip()[:200]
+                self._sample_nvml() if self.nvml else self._sample_smi()
             except Exception as e:  # pragma: no cover
                 self.err = str(e)
-            self.stop.wait(0.1)
+            self.stop.wait(0.002 if self.nvml else 0.1)
 
     def __exit__(self, *a):
         self.stop.set()
@@ -83,18 +106,10 @@ class Clocks:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "error": self.err}
-        def num(x):
-            try:
-                return float(x)
-            except ValueError:
-                return None
-        sm = [v for v in (num(s[0]) for s in self.samples) if v is not None]
-        mx = [v for v in (num(s[1]) for s in self.samples) if v is not None]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if s[3 + i].lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+        sm = [x[0] for x in self.samples]
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(x[1] for x in self.samples),
+                "reasons": sorted({r for x in self.samples for r in x[2]}), "samples": len(self.samples),
+                "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
 def dist_env():
@@ -211,7 +226,8 @@ def main():
     dq = torch.from_numpy(Q).to(dev)
     d_ids = torch.empty((nq, K), dtype=torch.int64, device=dev)
     d_dist = torch.empty((nq, K), dtype=torch.float32, device=dev)
-    stream = torch.cuda.current_stream(dev)
+    stream = torch.cuda.Stream(dev)          # a real stream: 0 would mean the library's own stream
+    torch.cuda.set_stream(stream)
 
     def run(nprobe, tau="TIGHT", stats=True):
         p = mrq.SearchParams.make(K=K, nprobe=nprobe, tau_schedule=tau, seed_lists=args.seed_lists,
@@ -251,11 +267,17 @@ def main():
         for i in range(args.steps):
             flush.fill_(float(i))                      # L2 flush between timed steps (not timed)
             ev[i][0].record(stream)
-            sts.append(run(nprobe))
+            run(nprobe, stats=False)                   # asynchronous: no host round trip inside the step
             ev[i][1].record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    # per-stage breakdown and counters: separate steps with stats (the stats
+    # call is synchronous and records the library's per-stage CUDA events)
+    for i in range(max(3, min(args.steps, 5))):
+        flush.fill_(float(i))
+        sts.append(run(nprobe))
+    torch.cuda.synchronize()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     ms = float(np.mean(step_ms))
     if world > 1:

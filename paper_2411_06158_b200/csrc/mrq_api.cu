@@ -5,6 +5,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <functional>
 #include <cmath>
 #include <vector>
 
@@ -215,6 +216,12 @@ static int load_impl(mrq_index *ix, const char *build_file, const float *base, i
         ix->max_list = std::max(ix->max_list, ix->h_list_size[c]);
     }
     ix->h_list_off[k] = (uint32_t)pos;
+    {
+        std::vector<uint32_t> srt(ix->h_list_size);
+        std::sort(srt.begin(), srt.end(), std::greater<uint32_t>());
+        ix->h_topsum.assign(k + 1, 0);
+        for (int c = 0; c < k; c++) ix->h_topsum[c + 1] = ix->h_topsum[c] + srt[c];
+    }
     ix->npad = (int64_t)((pos + 256 + 127) / 128 * 128);   // scan tiles may read 256 slots past a list start
     if (ix->npad >= (int64_t)0xFFFFFFF0ll) {
         mrq_set_error("index too large for 32-bit slots");
@@ -478,9 +485,15 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
         k_cand_count<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(probe, nq, np, ix->list_size, cand_cnt);
         k_exclusive_scan<<<1, 1024, 0, st>>>(cand_cnt, nq, f1_off);
     }
-    uint64_t total = 0;
-    MRQ_CUDA_TRY(cudaMemcpyAsync(&total, f1_off + nq, 8, cudaMemcpyDeviceToHost, st));
-    MRQ_CUDA_TRY(cudaStreamSynchronize(st));
+    // candidate-indexed scratch: sized by the host bound nq x (sum of the np
+    // largest lists) when that fits the budget, so the search never waits on
+    // the device; else by the exact total (one D2H + stream sync)
+    uint64_t total = (uint64_t)nq * ix->h_topsum[std::min(np, k)];
+    const uint64_t per_entry = 4 + 8 + 8 + 4 + 4 + 8 + 8;   // f1_pos/head/diso/id, f2_pos/head/exact
+    if (total * per_entry > ((uint64_t)8 << 30) || ix->dbg_dump_dis) {
+        MRQ_CUDA_TRY(cudaMemcpyAsync(&total, f1_off + nq, 8, cudaMemcpyDeviceToHost, st));
+        MRQ_CUDA_TRY(cudaStreamSynchronize(st));
+    }
     ix->last_total = total;
     uint32_t *f1_pos, *f2_pos;
     double *f1_head, *f1_diso, *f2_head, *f2_exact;
@@ -612,7 +625,9 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
             for (auto v : h) s += v;
             return s;
         };
-        stats->scanned = total;
+        uint64_t scanned = 0;
+        MRQ_CUDA_TRY(cudaMemcpy(&scanned, f1_off + nq, 8, cudaMemcpyDeviceToHost));
+        stats->scanned = scanned;
         stats->stage1_pass = sum32(f1_cnt);
         stats->stage2_pass = sum32(f2_cnt);
         stats->exact = sum32(exact_cnt);

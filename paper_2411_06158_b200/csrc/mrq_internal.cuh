@@ -61,6 +61,7 @@ struct mrq_index {
 
     // host mirrors
     std::vector<uint32_t> h_list_off, h_list_size;
+    std::vector<uint64_t> h_topsum;   // h_topsum[p] = sum of the p largest local list sizes
     uint32_t max_list = 0;
     double cmax = 0.0;           // max_j ||c_j|| (rounded up), probe error bound
 
@@ -508,8 +509,65 @@ struct WarpSel {
 };
 
 // ================================================================ a4 / a5
+// Weighted population counts with carry-save adders.  words[l] holds the
+// words of weight 2^l (counts n[l]); the result is sum_l 2^l sum_i popc(words).
+// At each weight the words are reduced with full adders (3 words -> sum at
+// this weight + carry at the next: popc(a)+popc(b)+popc(c) = popc(a^b^c) +
+// 2 popc(maj(a,b,c))) and half adders (2 -> 1 + carry) until one word is
+// left, which is counted with one POPC.  Exact integer identities; fewer
+// POPCs (quarter-rate on the SM) for a few more LOP3s: S over 4 planes x W
+// words needs 5 POPCs at W = 2 (not 8), 6 at W = 4 (not 16).
+template <int NMAX>
+struct CsaAcc {
+    uint32_t w[NMAX];
+    int n = 0;
+    __device__ __forceinline__ void push(uint32_t x) { w[n++] = x; }
+};
+
+__device__ __forceinline__ uint32_t lop_xor3(uint32_t a, uint32_t b, uint32_t c) { return a ^ b ^ c; }
+__device__ __forceinline__ uint32_t lop_maj(uint32_t a, uint32_t b, uint32_t c) { return (a & b) | (c & (a | b)); }
+
+// S = sum_b 2^b sum_w popc(x[b][w]) for NB planes of W words (all indices
+// compile-time, so the adder network is fully unrolled into registers).
+template <int NB, int W>
+__device__ __forceinline__ int csa_weighted_popc(const uint32_t (&x)[NB][W])
+{
+    int S = 0;
+    uint32_t carry[W + 2];
+    int nc = 0;
+#pragma unroll
+    for (int lvl = 0; lvl < NB + 8; lvl++) {
+        uint32_t cur[W + 2 + W];
+        int n = 0;
+#pragma unroll
+        for (int i = 0; i < W + 2; i++)
+            if (i < nc) cur[n++] = carry[i];
+        if (lvl < NB) {
+#pragma unroll
+            for (int i = 0; i < W; i++) cur[n++] = x[lvl][i];
+        }
+        nc = 0;
+#pragma unroll
+        for (int it = 0; it < 2 * W + 2; it++) {
+            if (n >= 3) {
+                const uint32_t a = cur[n - 1], b = cur[n - 2], c = cur[n - 3];
+                cur[n - 3] = lop_xor3(a, b, c);
+                carry[nc++] = lop_maj(a, b, c);
+                n -= 2;
+            } else if (n == 2) {
+                const uint32_t a = cur[0], b = cur[1];
+                cur[0] = a ^ b;
+                carry[nc++] = a & b;
+                n = 1;
+            }
+        }
+        if (n == 1) S += __popc(cur[0]) << lvl;
+    }
+    return S;
+}
+
 // The scan epilogue shared by the seed pass and the scan (Eq.4
-// with A-1; Eq.5 P:255 with A-2/A-6; Alg.2 L12 P:314):
+// with R-1; Eq.5 P:255 with R-2/R-5; Alg.2 L12 P:314):
 //   S = sum_b 2^b popc(code & p_b) = sum_{bit_j=1} L_j,  pop = popc(code)
 //   ip = ((A pop + Bc S) - C0) / sqrt(d)        = <x_hat, r_bar>
 //   dis' = (f1 + g1) - 2 (f2 ip)
@@ -518,17 +576,17 @@ template <int W>
 __device__ __forceinline__ double mrq_lb1(const uint32_t *code, const uint32_t *pl, const double *qc, double isd,
                                           double eps_r, float f1, float f2, float f3, double *dis_out)
 {
-    int pop = 0;
+    uint32_t cw[1][W];
 #pragma unroll
-    for (int w = 0; w < W; w++) pop += __popc(code[w]);
-    int S = 0;
+    for (int w = 0; w < W; w++) cw[0][w] = code[w];
+    const int pop = W <= 2 ? (W == 1 ? __popc(code[0]) : __popc(code[0]) + __popc(code[W - 1]))
+                           : csa_weighted_popc<1, W>(cw);
+    uint32_t x[MRQ_BQ][W];
 #pragma unroll
-    for (int b = 0; b < MRQ_BQ; b++) {
-        int s = 0;
+    for (int b = 0; b < MRQ_BQ; b++)
 #pragma unroll
-        for (int w = 0; w < W; w++) s += __popc(code[w] & pl[b * W + w]);
-        S += s << b;
-    }
+        for (int w = 0; w < W; w++) x[b][w] = code[w] & pl[b * W + w];
+    const int S = csa_weighted_popc<MRQ_BQ, W>(x);
     const double t1 = qc[0] * (double)pop;
     const double t2 = qc[1] * (double)S;
     const double t4 = (t1 + t2) - qc[2];
@@ -539,7 +597,6 @@ __device__ __forceinline__ double mrq_lb1(const uint32_t *code, const uint32_t *
     *dis_out = dis;
     return (dis - qc[4] * (double)f3) - eps_r;
 }
-
 
 // -------------------------------------------------------------------------
 // Staged warp row gather.  A warp processes entries 0..n-1 in groups of 32

@@ -371,7 +371,7 @@ __global__ void k_exclusive_scan(const uint64_t *__restrict__ in, int64_t n, uin
 #define MRQ_SCAN_TILE 128
 #define MRQ_SCAN_H (MRQ_SCAN_TILE / 128)
 template <int W>
-__global__ void __launch_bounds__(256) k_scan(
+__global__ void __launch_bounds__(256, (W <= 3 ? 4 : 1)) k_scan(
     const uint32_t *__restrict__ probe, int np, int64_t npad, const uint32_t *__restrict__ list_off,
     const uint32_t *__restrict__ list_size, const uint32_t *__restrict__ codes, const float *__restrict__ f1,
     const float *__restrict__ f2, const float *__restrict__ f3, const uint32_t *__restrict__ planes,
