@@ -29,6 +29,11 @@ MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
 METRIC = "QPS at recall@10>=0.95; scanned codes/s per GPU as % of HBM roofline"
 
 
+WORKLOADS = {"tiny": "Tiny (BASELINE.json configs[0])", "sift": "SIFT-shaped (BASELINE.json configs[1])",
+             "deep": "Deep-shaped (BASELINE.json configs[2])", "gist": "GIST-shaped (BASELINE.json configs[3])",
+             "emb": "Embedding-shaped (BASELINE.json configs[4])"}
+
+
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
@@ -180,7 +185,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="mrq", choices=["mrq", "reference"])
-    ap.add_argument("--config", default="sift")
+    ap.add_argument("--config", default="sift", help="tiny | sift (BASELINE.json configs[1], default) | gist")
+    ap.add_argument("--d", type=int, default=0, help="code length (build file build_d<d>.mrqb); 0 = config default")
     ap.add_argument("--nprobe", type=int, default=0, help="0 = smallest grid nprobe with recall@10 >= 0.95")
     ap.add_argument("--K", type=int, default=10)
     ap.add_argument("--no-cpu", action="store_true")
@@ -189,7 +195,8 @@ def main():
     args = ap.parse_args()
     rank, world, local = dist_env()
     cfg_name = args.config
-    bfile = os.path.join(ROOT, "data", cfg_name, "build_d%d.mrqb" % {"tiny": 16, "sift": 64}.get(cfg_name, 64))
+    dsel = args.d or {"tiny": 16, "sift": 64, "gist": 128, "deep": 64, "emb": 512}.get(cfg_name, 64)
+    bfile = os.path.join(ROOT, "data", cfg_name, "build_d%d.mrqb" % dsel)
     gtfile = os.path.join(ROOT, "data", cfg_name, "gt_k%d.npy" % args.K)
 
     if args.impl == "reference":
@@ -355,7 +362,7 @@ def main():
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": "SIFT-shaped (BASELINE.json configs[1])" if cfg_name == "sift" else cfg_name,
+        "config": {"workload": WORKLOADS.get(cfg_name, cfg_name),
                    "N": int(X.shape[0]), "Q": nq, "D": int(X.shape[1]), "d": d, "k": hdr["k"], "K": K,
                    "nprobe": nprobe, "tau_schedule": "TIGHT", "eps0": 1.9, "m": 4.0, "mode": "FULL",
                    "seed_lists": args.seed_lists, "seed_mult": args.seed_mult,
@@ -410,7 +417,7 @@ def reference_arm(args, rank, world, cfg_name, bfile, gtfile):
     out = {"impl": "reference", "metric": METRIC, "value": round(qps, 2), "unit": "queries/s", "n_gpus": world,
            "steps": args.steps, "warmup": max(args.warmup, 1), "ms_per_step": round(dt * 1e3, 3),
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": "SIFT-shaped (BASELINE.json configs[1])", "nprobe": nprobe, "K": K,
+           "config": {"workload": WORKLOADS.get(cfg_name, cfg_name), "nprobe": nprobe, "K": K,
                       "sample_per_step": sample},
            "cpu_baseline": {"value": round(qps, 2), "unit": "queries/s", "cores": cores, "kind": "oracle",
                             "sample": "%d queries per step" % sample},

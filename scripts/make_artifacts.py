@@ -5,7 +5,9 @@
   gt_k<K>.npy       exact KNN ids of the config's queries (fp64 ground truth)
 
 Calls nothing but ``synth`` (seeded inputs) and ``oracle`` -- no value here
-comes from the CUDA path.  Usage: python scripts/make_artifacts.py tiny sift
+comes from the CUDA path (``--cuda`` only runs the generator's elementwise
+loop on a GPU; its output is bit-identical).
+Usage: python scripts/make_artifacts.py tiny sift [--cuda] [--out=DIR]
 """
 import os
 import sys
@@ -21,13 +23,13 @@ import synth  # noqa: E402
 from oracle import build as B  # noqa: E402
 
 
-def main(names):
+def main(names, device=None, outroot=None):
     for name in names:
         cfg = synth.config_by_name(name)
-        out = os.path.join(ROOT, "data", name)
+        out = os.path.join(outroot or os.path.join(ROOT, "data"), name)
         os.makedirs(out, exist_ok=True)
         t = time.time()
-        X, Q = synth.generate(cfg)
+        X, Q = synth.generate(cfg, device=device)   # the device only runs the elementwise loop: same bits
         print(name, "generated", X.shape, Q.shape, "%.1fs" % (time.time() - t), flush=True)
         for d in cfg.d:
             p = os.path.join(out, "build_d%d.mrqb" % d)
@@ -48,4 +50,7 @@ def main(names):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["tiny", "sift"])
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    dev = "cuda" if "--cuda" in sys.argv else None
+    outroot = next((a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--out=")), None)
+    main(args or ["tiny", "sift"], dev, outroot)
