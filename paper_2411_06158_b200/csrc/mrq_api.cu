@@ -316,8 +316,7 @@ static int load_impl(mrq_index *ix, const char *build_file, const float *base, i
         MRQ_CUDA_TRY(cudaMemcpyAsync(dX, hx.data(), (size_t)m * D * 4, cudaMemcpyHostToDevice, ix->stream));
         MRQ_CUDA_TRY(cudaMemcpyAsync(dAssign, ha.data(), (size_t)m * 4, cudaMemcpyHostToDevice, ix->stream));
         MRQ_CUDA_TRY(cudaMemcpyAsync(dSlot, hs.data(), (size_t)m * 4, cudaMemcpyHostToDevice, ix->stream));
-        dim3 grid((D + 31) / 32, (unsigned)((m + 31) / 32));
-        k_project<<<grid, dim3(32, 8), 0, ix->stream>>>(dX, m, D, ix->mu, ix->PT, dXp);
+        launch_rowmat_f32(dX, m, D, D, ix->mu, ix->PT, D, dXp, D, ix->stream);
         k_encode_finish<<<(unsigned)((m + enc_warps - 1) / enc_warps), enc_warps * 32, enc_smem, ix->stream>>>(
             dXp, 0, m, D, d, W, dAssign, dSlot, ix->C, ix->RT, npad, ix->heads, ix->tails, ix->xr2, ix->codes, ix->f1,
             ix->f2, ix->f3);
@@ -436,12 +435,13 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
 
     // ---- a1: query projection (Alg.2 L1-L4)
     {
-        dim3 grid((D + 31) / 32, (unsigned)((nq + 31) / 32));
-        k_project<<<grid, dim3(32, 8), 0, st>>>(d_q, nq, D, ix->mu, ix->PT, qp);
-        if (D * 8 * 8 > 48 * 1024)
-            MRQ_CUDA_TRY(cudaFuncSetAttribute(k_qtail, cudaFuncAttributeMaxDynamicSharedMemorySize, D * 8 * 8));
-        k_qtail<<<(unsigned)((nq + 7) / 8), 256, (size_t)D * 8 * 8, st>>>(qp, nq, D, d, W, ix->lam, ix->RT, p->resid_scale, p->m, qr2,
-                                                          eps_r, r0, qd32, qnorm);
+        launch_rowmat_f32(d_q, nq, D, D, ix->mu, ix->PT, D, qp, D, st);             // q_p = P (q - mu)
+        const size_t qsmem = (size_t)D * 8 * 9;                                    // lambda + 8 query rows
+        if (qsmem > 48 * 1024)
+            MRQ_CUDA_TRY(cudaFuncSetAttribute(k_qtail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsmem));
+        k_qtail<<<(unsigned)((nq + 7) / 8), 256, qsmem, st>>>(qp, nq, D, d, W, ix->lam, ix->RT, p->resid_scale, p->m,
+                                                              qr2, eps_r, r0, qd32, qnorm);
+        launch_rowmat_f64(qp, nq, D, d, nullptr, ix->RT, d, r0, d, st);             // r0 = R q_d
     }
     if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[1], st));
 

@@ -9,44 +9,98 @@
 #include "mrq_comm.cuh"
 
 // ===================================================================== a0/a1
+// Row-matrix products in the canonical order:
+//   out[r][i] = sum_{j=0}^{Din-1} (x[r][j] - mu[j]) * MT[j][i]    (mu optional)
+// accumulated j ascending (acc = acc + u p, separately rounded).  Used for
 // x_p = P (x - mu) (Alg.1 L3 P:283 for base vectors, Alg.2 L1 P:303 for
-// queries).  Output r, dimension i: sum_{j=0}^{D-1} P[i][j] * (x[r][j] - mu[j])
-// accumulated j ascending.  Register-tiled across rows and outputs only (the
-// reduction order per output is untouched): a 32-output x 32-row tile per
-// 256-thread block, each P element read once per tile.
-__global__ void __launch_bounds__(256) k_project(const float *__restrict__ X, int64_t nrows, int D,
-                                                 const double *__restrict__ mu, const double *__restrict__ PT,
-                                                 double *__restrict__ out)
+// queries; MT = P^T) and for r0 = R q_d (Alg.2 L4 P:306; MT = R^T, mu = 0).
+// Register-tiled across rows and outputs only, which leaves each output's
+// reduction order untouched: a 64-row x 64-output tile per 256-thread block,
+// 4 x 4 outputs per thread, j in shared-memory chunks of 16 (8 shared loads
+// feed 16 products); the next chunk's global loads are issued before the
+// current chunk is consumed.  Padded j (beyond Din) contribute exact zeros,
+// which never change a sum that starts at +0.
+#define PJ_T 64
+#define PJ_K 16
+template <typename TIn>
+__global__ void __launch_bounds__(256) k_rowmat(const TIn *__restrict__ X, int64_t nrows, int ldx, int Din,
+                                                const double *__restrict__ mu, const double *__restrict__ MT,
+                                                int Dout, double *__restrict__ out, int ldo)
 {
-    __shared__ double us[32][33];
-    __shared__ double ps[32][33];
-    const int tx = threadIdx.x, ty = threadIdx.y;
-    const int i0 = blockIdx.x * 32;
-    const int64_t r0 = (int64_t)blockIdx.y * 32;
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int j0 = 0; j0 < D; j0 += 32) {
-        for (int rr = ty; rr < 32; rr += 8) {
-            int64_t r = r0 + rr;
-            int j = j0 + tx;
-            us[rr][tx] = (r < nrows && j < D) ? ((double)X[r * D + j] - mu[j]) : 0.0;
-            int jj = j0 + rr, i = i0 + tx;
-            ps[rr][tx] = (jj < D && i < D) ? PT[(int64_t)jj * D + i] : 0.0;
+    __shared__ double us[PJ_K][PJ_T + 1];
+    __shared__ double ps[PJ_K][PJ_T + 1];
+    const int tid = threadIdx.x;
+    const int tx = tid & 15, ty = tid >> 4;
+    const int i0 = blockIdx.x * PJ_T;
+    const int64_t r0 = (int64_t)blockIdx.y * PJ_T;
+    double acc[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; r++)
+#pragma unroll
+        for (int c = 0; c < 4; c++) acc[r][c] = 0.0;
+    double ur[4], pr[4];
+    auto fetch = [&](int j0) {
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const int t = tid + 256 * k;
+            const int rr = t / PJ_K, jj = t % PJ_K;
+            const int64_t r = r0 + rr;
+            const int j = j0 + jj;
+            ur[k] = 0.0;
+            if (r < nrows && j < Din) ur[k] = mu ? ((double)X[r * ldx + j] - mu[j]) : (double)X[r * ldx + j];
+            const int ii = t % PJ_T, jq = t / PJ_T;
+            const int i = i0 + ii, jp = j0 + jq;
+            pr[k] = (jp < Din && i < Dout) ? MT[(int64_t)jp * Dout + i] : 0.0;
+        }
+    };
+    fetch(0);
+    for (int j0 = 0; j0 < Din; j0 += PJ_K) {
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const int t = tid + 256 * k;
+            us[t % PJ_K][t / PJ_K] = ur[k];
+            ps[t / PJ_T][t % PJ_T] = pr[k];
         }
         __syncthreads();
-        const int jn = min(32, D - j0);
-        for (int jj = 0; jj < jn; jj++) {
-            const double p = ps[jj][tx];
+        if (j0 + PJ_K < Din) fetch(j0 + PJ_K);
 #pragma unroll
-            for (int q = 0; q < 4; q++) acc[q] = acc[q] + us[ty * 4 + q][jj] * p;
+        for (int jj = 0; jj < PJ_K; jj++) {
+            double a[4], b[4];
+#pragma unroll
+            for (int r = 0; r < 4; r++) a[r] = us[jj][ty + 16 * r];
+#pragma unroll
+            for (int c = 0; c < 4; c++) b[c] = ps[jj][tx + 16 * c];
+#pragma unroll
+            for (int r = 0; r < 4; r++)
+#pragma unroll
+                for (int c = 0; c < 4; c++) acc[r][c] = acc[r][c] + a[r] * b[c];
         }
         __syncthreads();
     }
 #pragma unroll
-    for (int q = 0; q < 4; q++) {
-        int64_t r = r0 + ty * 4 + q;
-        int i = i0 + tx;
-        if (r < nrows && i < D) out[r * D + i] = acc[q];
+    for (int r = 0; r < 4; r++) {
+        const int64_t row = r0 + ty + 16 * r;
+        if (row >= nrows) continue;
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+            const int i = i0 + tx + 16 * c;
+            if (i < Dout) out[row * ldo + i] = acc[r][c];
+        }
     }
+}
+
+void launch_rowmat_f32(const float *X, int64_t nrows, int ldx, int Din, const double *mu, const double *MT, int Dout,
+                       double *out, int ldo, cudaStream_t st)
+{
+    dim3 grid((Dout + PJ_T - 1) / PJ_T, (unsigned)((nrows + PJ_T - 1) / PJ_T));
+    k_rowmat<float><<<grid, 256, 0, st>>>(X, nrows, ldx, Din, mu, MT, Dout, out, ldo);
+}
+
+void launch_rowmat_f64(const double *X, int64_t nrows, int ldx, int Din, const double *mu, const double *MT,
+                       int Dout, double *out, int ldo, cudaStream_t st)
+{
+    dim3 grid((Dout + PJ_T - 1) / PJ_T, (unsigned)((nrows + PJ_T - 1) / PJ_T));
+    k_rowmat<double><<<grid, 256, 0, st>>>(X, nrows, ldx, Din, mu, MT, Dout, out, ldo);
 }
 
 // ======================================================================= a0
@@ -130,9 +184,9 @@ __global__ void k_rc(const double *__restrict__ C, const double *__restrict__ RT
 // ======================================================================= a1
 // Alg.2 L2-L4, warp per query: ||q_r||^2, sigma^2 = sum_{i>=d}
 // q_i^2 lambda_i (Eq.6), eps_r = (resid_scale m) sigma (Eq.7 / Alg.2
-// L11, reading R-4), r0 = R q_d; plus the fp32 q_d and ||q_d|| the probe uses.
-// The query row is staged in shared memory; the three left-to-right sums run
-// on three lanes at once, r0_j on lane j (j = lane + 32 w).
+// L11, reading R-4); plus the fp32 q_d and ||q_d|| the probe uses (r0 = R q_d
+// is k_rowmat).  The query row and lambda are staged in shared memory; the
+// three left-to-right sums run on three lanes at once.
 __global__ void __launch_bounds__(256) k_qtail(const double *__restrict__ qp, int64_t nq, int D, int d, int W,
                                                const double *__restrict__ lam, const double *__restrict__ RT,
                                                double rscale, double m, double *__restrict__ qr2o,
@@ -140,12 +194,16 @@ __global__ void __launch_bounds__(256) k_qtail(const double *__restrict__ qp, in
                                                float *__restrict__ qd32, double *__restrict__ qnorm)
 {
     extern __shared__ double qsm[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+    double *lams = qsm;                        // D
+    for (int i = threadIdx.x; i < D; i += blockDim.x) lams[i] = lam[i];
+    __syncthreads();
+    const int64_t q = (int64_t)blockIdx.x * wpb + warp;
     if (q >= nq) return;
-    double *row = qsm + (size_t)warp * D;
+    double *row = qsm + D + (size_t)warp * D;
     const double *g = qp + q * D;
     for (int i = lane; i < D; i += 32) row[i] = g[i];
+    for (int j = lane; j < d; j += 32) qd32[q * d + j] = (float)g[j];
     __syncwarp();
     if (lane == 0) {
         double a = 0.0;
@@ -153,21 +211,12 @@ __global__ void __launch_bounds__(256) k_qtail(const double *__restrict__ qp, in
         qr2o[q] = a;
     } else if (lane == 1) {
         double s2 = 0.0;
-        for (int i = d; i < D; i++) s2 = s2 + (row[i] * row[i]) * lam[i];
+        for (int i = d; i < D; i++) s2 = s2 + (row[i] * row[i]) * lams[i];
         eps_r[q] = (rscale * m) * sqrt(s2);
     } else if (lane == 2) {
         double n2 = 0.0;
         for (int i = 0; i < d; i++) n2 = n2 + row[i] * row[i];
         qnorm[q] = sqrt(n2);
-    }
-    for (int w = 0; w < W; w++) {
-        const int j = w * 32 + lane;
-        if (j < d) {
-            double acc = 0.0;
-            for (int i = 0; i < d; i++) acc = acc + RT[(int64_t)i * d + j] * row[i];
-            r0[q * d + j] = acc;
-            qd32[q * d + j] = (float)row[j];
-        }
     }
 }
 

@@ -2,7 +2,10 @@
 #pragma once
 #include "mrq_internal.cuh"
 
-__global__ void k_project(const float *X, int64_t nrows, int D, const double *mu, const double *PT, double *out);
+void launch_rowmat_f32(const float *X, int64_t nrows, int ldx, int Din, const double *mu, const double *MT, int Dout,
+                       double *out, int ldo, cudaStream_t st);
+void launch_rowmat_f64(const double *X, int64_t nrows, int ldx, int Din, const double *mu, const double *MT,
+                       int Dout, double *out, int ldo, cudaStream_t st);
 __global__ void k_encode_finish(const double *xp, int64_t n0, int64_t cnt, int D, int d, int W,
                                 const uint32_t *assign, const uint32_t *slot_of, const double *C, const double *RT,
                                 int64_t npad, float *heads, float *tails, float *xr2o, uint32_t *codes, float *f1,
