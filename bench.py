@@ -204,10 +204,18 @@ def main():
 
     import torch
     import torch.distributed as dist
+    # MRQ_BENCH_HOST_EXCHANGE=1 (a plumbing check on a one-GPU box, never a
+    # bench number): every rank on device 0, exchanges through gloo on the host
+    host_x = os.environ.get("MRQ_BENCH_HOST_EXCHANGE") == "1"
+    if host_x:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if host_x:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     import paper_2411_06158_b200 as mrq
     import synth
 
@@ -220,12 +228,20 @@ def main():
     nq = Q.shape[0]
 
     uid = None
-    if world > 1:
+    hx = None
+    if world > 1 and host_x:
+        def hx(b):
+            t = torch.frombuffer(bytearray(b), dtype=torch.uint8)
+            outs = [torch.empty_like(t) for _ in range(world)]
+            dist.all_gather(outs, t)
+            return b"".join(o.numpy().tobytes() for o in outs)
+    elif world > 1:
         obj = [mrq.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
     t0 = time.time()
-    h = mrq.mrq_index_load(bfile, X, d, rank=rank, world=world, device=local, nccl_unique_id=uid)
+    h = mrq.mrq_index_load(bfile, X, d, rank=rank, world=world, device=local, nccl_unique_id=uid,
+                           host_allgather=hx)
     load_s = time.time() - t0
     info = mrq.mrq_index_info(h)
     log("index loaded in %.2fs: %s (sha match %s)" % (load_s, info, sha_ok))
@@ -288,7 +304,7 @@ def main():
     step_ms = [a.elapsed_time(b) for a, b in ev]
     ms = float(np.mean(step_ms))
     if world > 1:
-        t = torch.tensor([ms], device=dev)
+        t = torch.tensor([ms], device="cpu" if host_x else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     found = d_ids.cpu().numpy()
@@ -334,7 +350,7 @@ def main():
         e2e_t.append(time.perf_counter() - t)
     e2e_s = float(np.mean(e2e_t))
     if world > 1:
-        t = torch.tensor([e2e_s], device=dev)
+        t = torch.tensor([e2e_s], device="cpu" if host_x else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
 
