@@ -515,7 +515,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
     sa.ids = ix->ids; sa.codes = ix->codes; sa.planes = planes; sa.f1 = ix->f1; sa.f2 = ix->f2; sa.f3 = ix->f3;
     sa.heads = ix->heads; sa.tails = ix->tails; sa.xr2 = ix->xr2; sa.qconst = qconst; sa.qp = qp; sa.qr2 = qr2;
     sa.eps_r = eps_r; sa.s0_cnt = s0_cnt; sa.s0_pos = s0_pos; sa.s1_cnt = s1_cnt; sa.s1_pos = s1_pos;
-    sa.f1_cnt = f1_cnt; sa.f1_pos = f1_pos; sa.f2_cnt = f2_cnt; sa.f2_pos = f2_pos; sa.exact_cnt = exact_cnt;
+    sa.f1_cnt = f1_cnt; sa.f1_pos = f1_pos; sa.f2_cnt = f2_cnt; sa.f2_pos = f2_pos; sa.exact_cnt = timed ? exact_cnt : nullptr;
     sa.s0_exact = s0_exact; sa.s1_exact = s1_exact; sa.tau0 = tau0; sa.tau1 = tau1; sa.f1_head = f1_head;
     sa.f1_diso = f1_diso; sa.f2_head = f2_head; sa.f2_exact = f2_exact; sa.f1_off = f1_off;
     sa.out_ids = d_ids; sa.out_dist = d_dist;
@@ -574,7 +574,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
     if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[6], st));
 
     // ---- a7: exact re-rank of F2
-    TRY(launch_rerank_w(sa, st));
+    // (a7, the exact re-rank of F2, runs inside the top-K kernel)
     if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[7], st));
 
     // ---- a8: per-query top-K

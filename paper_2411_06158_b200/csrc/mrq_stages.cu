@@ -334,34 +334,10 @@ __global__ void __launch_bounds__(256) k_f2_w(int64_t nq, int mode, const double
                f2_pos, f2_head);
 }
 
-// ----------------------------------------------------------------------- a7
-// Exact re-rank of F2 (Alg.2 L14 P:316): exact = HEAD continued over the
-// tail = ||x_p - q_p||^2 left to right over i = 0..D-1 (A-8).
-__global__ void __launch_bounds__(256) k_rerank_w(int64_t nq, int aligned, int D, int d, const float *__restrict__ tails,
-                                                  const double *__restrict__ qp, const uint64_t *__restrict__ f1_off,
-                                                  const uint32_t *__restrict__ f2_cnt,
-                                                  const uint32_t *__restrict__ f2_pos,
-                                                  const double *__restrict__ f2_head, double *__restrict__ f2_exact)
-{
-    extern __shared__ unsigned char wsm[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
-    const int64_t q = (int64_t)blockIdx.x * wpb + warp;
-    if (q >= nq) return;
-    float *tile = (float *)wsm + warp * MRQ_RG_FLOATS;
-    const uint64_t base = f1_off[q];
-    const int n2 = (int)f2_cnt[q];
-    const double *qt = qp + q * D + d;
-    if (D > d)
-        warp_rows(aligned, tails, D - d, 0, D - d, qt, n2, tile, [&](int e) { return f2_pos[base + e]; },
-                  [&](int e, uint32_t) { return f2_head[base + e]; }, [&](int e, bool v, double acc) {
-                      if (v) f2_exact[base + e] = acc;
-                  });
-    else
-        for (int e = lane; e < n2; e += 32) f2_exact[base + e] = f2_head[base + e];
-}
-
 // ----------------------------------------------------------------------- a8
-// Per-query top-K (Alg.2 L15-L16): the K smallest (exact, id) over
+// Exact re-rank of F2 (a7) and per-query top-K (Alg.2 L15-L16),
+// one warp per query: F2's tails are gathered first (f2_exact), then the K
+// smallest (exact, id) over
 // the distinct union S0 u S1 u F2 restricted to this rank's slots (a
 // candidate in several sets has the same exact value in each, so WarpTop
 // drops the copies; members of the global S0/S1 owned by another rank carry
@@ -374,18 +350,30 @@ __global__ void __launch_bounds__(256) k_topk_w(
     const uint32_t *__restrict__ s0_pos, const uint32_t *__restrict__ s0_id, const double *__restrict__ s0_exact,
     const uint32_t *__restrict__ s1_cnt, const uint32_t *__restrict__ s1_pos, const uint32_t *__restrict__ s1_id,
     const double *__restrict__ s1_exact, const uint64_t *__restrict__ f1_off, const uint32_t *__restrict__ f2_cnt,
-    const uint32_t *__restrict__ f2_pos, const double *__restrict__ f2_exact, int64_t *__restrict__ out_ids,
-    float *__restrict__ out_dist, uint32_t *__restrict__ exact_cnt, XItem *__restrict__ xout)
+    const uint32_t *__restrict__ f2_pos, double *__restrict__ f2_exact, int64_t *__restrict__ out_ids,
+    float *__restrict__ out_dist, uint32_t *__restrict__ exact_cnt, XItem *__restrict__ xout, int aligned, int D,
+    int d, const float *__restrict__ tails, const double *__restrict__ qp, const double *__restrict__ f2_head)
 {
     extern __shared__ unsigned char wsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
     const int64_t q = (int64_t)blockIdx.x * wpb + warp;
     if (q >= nq) return;
-    SelItem *lst = (SelItem *)wsm + (size_t)warp * K;
-    WarpSel top;
-    top.init(lst, K);
+    float *tile = (float *)wsm + warp * MRQ_RG_FLOATS;
+    SelItem *lst = (SelItem *)((float *)wsm + wpb * MRQ_RG_FLOATS) + (size_t)warp * K;
     const int ns0 = (int)s0_cnt[q], ns1 = (int)s1_cnt[q], n2 = (int)f2_cnt[q];
     const uint64_t base = f1_off[q];
+    // a7 exact re-rank of F2 (Alg.2 L14 P:316): exact = HEAD continued over
+    // the tail = ||x_p - q_p||^2 left to right over i = 0..D-1 (R-8)
+    if (D > d)
+        warp_rows(aligned, tails, D - d, 0, D - d, qp + q * D + d, n2, tile, [&](int e) { return f2_pos[base + e]; },
+                  [&](int e, uint32_t) { return f2_head[base + e]; }, [&](int e, bool v, double acc) {
+                      if (v) f2_exact[base + e] = acc;
+                  });
+    else
+        for (int e = lane; e < n2; e += 32) f2_exact[base + e] = f2_head[base + e];
+    __syncwarp();
+    WarpSel top;
+    top.init(lst, K);
     const int n = ns0 + ns1 + n2;
     for (int g = 0; g < n; g += 32) {
         const int e = g + lane;
@@ -430,7 +418,9 @@ __global__ void __launch_bounds__(256) k_topk_w(
         }
     }
     // distinct exact computations on this rank = |(S0 u S1 u F2) n owned|
-    // (S1 and F2 are subsets of F1; S0 may overlap both)
+    // (S1 and F2 are subsets of F1; S0 may overlap both): a statistic, only
+    // when the caller asked for stats (exact_cnt != NULL)
+    if (!exact_cnt) return;
     uint32_t cnt = 0;
     for (int g = 0; g < n; g += 32) {
         const int e = g + lane;
@@ -638,27 +628,17 @@ int launch_xmerge(int kind, const StageArgs &a, int world, int rank, const XItem
     return MRQ_OK;
 }
 
-int launch_rerank_w(const StageArgs &a, cudaStream_t st)
-{
-    const int wpb = 4;
-    const size_t smem = (size_t)wpb * MRQ_RG_FLOATS * 4;
-    int rc = set_attr((const void *)k_rerank_w, smem);
-    if (rc) return rc;
-    k_rerank_w<<<(unsigned)((a.nq + wpb - 1) / wpb), wpb * 32, smem, st>>>(a.nq, a.aligned, a.D, a.d, a.tails, a.qp, a.f1_off,
-                                                                         a.f2_cnt, a.f2_pos, a.f2_head, a.f2_exact);
-    return MRQ_OK;
-}
-
 int launch_topk_w(const StageArgs &a, cudaStream_t st)
 {
-    const size_t per = (size_t)a.K * sizeof(SelItem);
+    const size_t per = MRQ_RG_FLOATS * 4 + (size_t)a.K * sizeof(SelItem);
     const int wpb = warps_for(per);
     const size_t smem = per * wpb;
     int rc = set_attr((const void *)k_topk_w, smem);
     if (rc) return rc;
     k_topk_w<<<(unsigned)((a.nq + wpb - 1) / wpb), wpb * 32, smem, st>>>(
         a.nq, a.K, a.Kp, a.ids, a.s0_cnt, a.s0_pos, a.s0_id, a.s0_exact, a.s1_cnt, a.s1_pos, a.s1_id, a.s1_exact,
-        a.f1_off, a.f2_cnt, a.f2_pos, a.f2_exact, a.out_ids, a.out_dist, a.exact_cnt, a.xout);
+        a.f1_off, a.f2_cnt, a.f2_pos, a.f2_exact, a.out_ids, a.out_dist, a.exact_cnt, a.xout, a.aligned, a.D, a.d,
+        a.tails, a.qp, a.f2_head);
     return MRQ_OK;
 }
 
