@@ -71,19 +71,10 @@ __global__ void __launch_bounds__(256) k_seed_w(
     };
     WarpSel top;
     top.init(lst, Kp);
-    if (Kp <= 32) {
-        // two passes: U = Kp-th smallest lane minimum bounds the Kp-th smallest
-        // dis' from above, so only items <= U can enter S0
-        double mn = __longlong_as_double(0x7ff0000000000000ll);
-        scan_pool([&](const SelItem &it, bool v) {
-            if (v) mn = fmin(mn, it.key);
-        });
-        const double U = warp_kth_smallest(mn, Kp);
-        top.init(lst, Kp, true, queue);
-        scan_pool([&](const SelItem &it, bool v) { top.offer(it, v && it.key <= U); });
-    } else {
-        scan_pool([&](const SelItem &it, bool v) { top.offer(it, v); });
-    }
+    // one pass: items below the running K'-th smallest are queued and merged
+    // 32 at a time (bitonic) for K' <= 32; the shared-memory list otherwise
+    top.init(lst, Kp, true, queue);
+    scan_pool([&](const SelItem &it, bool v) { top.offer(it, v); });
     top.finish();
     const int ns0 = nloc < Kp ? nloc : Kp;
     // exact distances of S0: HEAD over the head rows, then continued over the tail rows
@@ -256,7 +247,9 @@ __global__ void __launch_bounds__(256) k_stage2_w(
                 }
             }
         };
-        if (Kp <= 32) {   // two passes, as for S0
+        if (Kp <= 32) {
+            // two passes: U = Kp-th smallest lane minimum bounds the Kp-th
+            // smallest dis_o' from above, so only items <= U can enter S1
             double mn = __longlong_as_double(0x7ff0000000000000ll);
             scan_f1([&](const SelItem &it, bool v) {
                 if (v) mn = fmin(mn, it.key);
@@ -758,6 +751,16 @@ __device__ __forceinline__ double sqdist_rows8(const double *__restrict__ cr, co
 {
     double acc = 0.0;
     int j = 0;
+    for (; j + 16 <= d; j += 16) {
+        double cv[16];
+#pragma unroll
+        for (int u = 0; u < 16; u++) cv[u] = __ldg(cr + j + u);
+#pragma unroll
+        for (int u = 0; u < 16; u++) {
+            const double t = qd[j + u] - cv[u];
+            acc = acc + t * t;
+        }
+    }
     for (; j + 8 <= d; j += 8) {
         double cv[8];
 #pragma unroll
@@ -825,16 +828,40 @@ __global__ void __launch_bounds__(128) k_probe_finish_w(int64_t nq, int k, int d
     if (all) {
         nc = (uint32_t)k;
     } else {
-        for (int pp = 0; pp < P; pp++) {
-            const uint32_t n = ccnt[q * P + pp];
-            const uint2 *rb = cbuf + (q * P + pp) * capp;
-            for (uint32_t e0 = 0; e0 < n; e0 += 32) {
-                const uint32_t e = e0 + lane;
-                uint2 x = make_uint2(0u, 0u);
-                if (e < n) x = rb[e];
-                const bool in = e < n && (double)__uint_as_float(x.x) <= thr;
-                const unsigned bal = __ballot_sync(0xffffffffu, in);
-                if (in) cq[nc + __popc(bal & ((1u << lane) - 1u))] = x.y;
+        // the parts' buffers as one flat index space (lane p holds part p's
+        // count and exclusive prefix), 4 batches of loads in flight
+        const uint32_t myc = lane < P ? ccnt[q * P + lane] : 0u;
+        uint32_t pre = myc;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, pre, o);
+            if (lane >= o) pre += y;
+        }
+        const uint32_t total = __shfl_sync(0xffffffffu, pre, 31);
+        pre -= myc;   // exclusive
+        for (uint32_t e0 = 0; e0 < total; e0 += 128) {
+            uint2 x[4];
+            bool in[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const uint32_t e = e0 + 32 * u + lane;
+                int part = 0;
+                uint32_t pbase = 0;
+                for (int pp = 1; pp < P; pp++) {   // last part whose prefix <= e
+                    const uint32_t b = __shfl_sync(0xffffffffu, pre, pp);
+                    if (b <= e) {
+                        part = pp;
+                        pbase = b;
+                    }
+                }
+                x[u] = make_uint2(0u, 0u);
+                if (e < total) x[u] = cbuf[(q * P + part) * capp + (e - pbase)];
+                in[u] = e < total;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const bool ok = in[u] && (double)__uint_as_float(x[u].x) <= thr;
+                const unsigned bal = __ballot_sync(0xffffffffu, ok);
+                if (ok) cq[nc + __popc(bal & ((1u << lane) - 1u))] = x[u].y;
                 nc += __popc(bal);
             }
         }
