@@ -47,74 +47,85 @@ def peaks():
         return 6650.0, "fallback"
 
 
-class Clocks:
-    """Samples the SM clock and the clock-event (throttle) reasons DURING the
-    timed region (B200_PROFILING.md clocks line) from a thread: NVML
-    (nvidia-ml-py) every ~2 ms, so a short timed region still gets samples;
-    nvidia-smi single shots if NVML is unavailable."""
+_SAMPLER = r"""
+import sys, time, select
+import pynvml as n
+n.nvmlInit()
+h = n.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+names = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+         ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+         ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+         ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+         ("hw_power_brake_slowdown", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
+mx = n.nvmlDeviceGetMaxClockInfo(h, n.NVML_CLOCK_SM)
+print("ready", flush=True)
+sys.stdin.readline()          # "go": the timed region starts
+while True:
+    r, _, _ = select.select([sys.stdin], [], [], 0.001)
+    if r and not sys.stdin.readline():
+        break
+    sm = n.nvmlDeviceGetClockInfo(h, n.NVML_CLOCK_SM)
+    rs = n.nvmlDeviceGetCurrentClocksEventReasons(h)
+    act = ",".join(nm for nm, at in names if rs & getattr(n, at, 0)) or "-"
+    print("%.6f %d %d %s" % (time.time(), sm, mx, act), flush=True)
+"""
 
-    NAMES = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
-             ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
-             ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
-             ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
-             ("hw_power_brake_slowdown", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
+
+class Clocks:
+    """SM clock and clock-event (throttle) reasons sampled DURING the timed
+    region (B200_PROFILING.md clocks line) by a separate sampler process (NVML
+    every ~1 ms, so the GIL of this process cannot starve it); only samples
+    whose timestamps fall inside the region count.  Start it before the
+    warm-up (start()), then bracket the timed region with `with clk:`."""
 
     def __init__(self, gpu=0):
         self.gpu = gpu
-        self.samples = []      # (sm_mhz, max_mhz, [reasons])
-        self.stop = threading.Event()
+        self.proc = None
         self.err = None
-        self.nvml = None
-        try:
-            import pynvml
-            pynvml.nvmlInit()
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(gpu)
-            self.nvml = pynvml
-        except Exception as e:  # pragma: no cover
-            self.err = "nvml: %s" % e
+        self.t0 = self.t1 = None
+        self.lines = []
 
-    def __enter__(self):
-        self.t = threading.Thread(target=self._loop, daemon=True)
-        self.t.start()
+    def start(self):
+        try:
+            self.proc = subprocess.Popen([sys.executable, "-c", _SAMPLER, str(self.gpu)], stdin=subprocess.PIPE,
+                                         stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)
+            ready = self.proc.stdout.readline()
+            if not ready.startswith("ready"):
+                self.err = (ready + self.proc.stderr.read())[:200]
+                self.proc = None
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+            self.proc = None
         return self
 
-    def _sample_nvml(self):
-        n = self.nvml
-        sm = n.nvmlDeviceGetClockInfo(self.h, n.NVML_CLOCK_SM)
-        mx = n.nvmlDeviceGetMaxClockInfo(self.h, n.NVML_CLOCK_SM)
-        r = n.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-        reasons = [name for name, attr in self.NAMES if r & getattr(n, attr, 0)]
-        self.samples.append((float(sm), float(mx), reasons))
-
-    def _sample_smi(self):
-        f = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-        r = subprocess.run(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + f, "--format=csv,noheader,nounits"],
-                           capture_output=True, text=True, timeout=5)
-        p = [x.strip() for x in r.stdout.strip().split(",")]
-        if len(p) >= 6:
-            reasons = [self.NAMES[i][0] for i in range(4) if p[2 + i].lower() == "active"]
-            self.samples.append((float(p[0]), float(p[1]), reasons))
-
-    def _loop(self):
-        while not self.stop.is_set():
-            try:
-                self._sample_nvml() if self.nvml else self._sample_smi()
-            except Exception as e:  # pragma: no cover
-                self.err = str(e)
-            self.stop.wait(0.002 if self.nvml else 0.1)
+    def __enter__(self):
+        if self.proc:
+            self.proc.stdin.write("go\n")
+            self.proc.stdin.flush()
+            time.sleep(0.002)
+        self.t0 = time.time()
+        return self
 
     def __exit__(self, *a):
-        self.stop.set()
-        self.t.join(6)
+        self.t1 = time.time()
+        if self.proc:
+            time.sleep(0.003)
+            self.proc.stdin.close()
+            self.lines = self.proc.stdout.read().splitlines()
+            self.proc.wait(10)
 
     def summary(self):
-        if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "error": self.err}
-        sm = [x[0] for x in self.samples]
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(x[1] for x in self.samples),
-                "reasons": sorted({r for x in self.samples for r in x[2]}), "samples": len(self.samples),
-                "source": "nvml" if self.nvml else "nvidia-smi"}
+        samples = []
+        for ln in self.lines:
+            p = ln.split()
+            if len(p) == 4 and self.t0 <= float(p[0]) <= self.t1 + 0.002:
+                samples.append((float(p[1]), float(p[2]), [] if p[3] == "-" else p[3].split(",")))
+        if not samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "error": self.err,
+                    "source": "nvml sampler process"}
+        return {"sm_mhz": float(np.median([x[0] for x in samples])), "sm_max_mhz": max(x[1] for x in samples),
+                "reasons": sorted({r for x in samples for r in x[2]}), "samples": len(samples),
+                "source": "nvml sampler process, ~1 ms"}
 
 
 def dist_env():
@@ -175,8 +186,8 @@ def cpu_oracle_leg(bfile, X, Q, K, nprobe, budget_s=15.0, **kw):
     t = time.time()
     ox.search(Q[:n2], K=K, nprobe=nprobe, **kw)
     dt = time.time() - t
-    return n2 / dt, cores, "first %d of %d queries, nprobe=%d, FULL/TIGHT; index encode %.1fs untimed" % (
-        n2, Q.shape[0], nprobe, enc)
+    return n2 / dt, cores, "first %d of %d queries, nprobe=%d, FULL/%s; index encode %.1fs untimed" % (
+        n2, Q.shape[0], nprobe, kw.get("tau_schedule", "TIGHT"), enc)
 
 
 def main():
@@ -190,6 +201,8 @@ def main():
     ap.add_argument("--nprobe", type=int, default=0, help="0 = smallest grid nprobe with recall@10 >= 0.95")
     ap.add_argument("--K", type=int, default=10)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--tau", default="auto", choices=["auto", "TIGHT", "LOOSE"],
+                    help="decision-T schedule; auto = the faster one at the operating point")
     ap.add_argument("--seed-lists", type=int, default=2, help="decision T: seed pool spans >= this many lists")
     ap.add_argument("--seed-mult", type=int, default=2, help="decision T: K' = seed_mult * K")
     args = ap.parse_args()
@@ -259,26 +272,49 @@ def main():
         mrq.mrq_search_batch_device(h, dq, p, d_ids, d_dist, st, stream.cuda_stream)
         return st
 
-    # operating point: smallest grid nprobe with recall@10 >= 0.95 (untimed sweep)
+    # operating point: the fastest (nprobe, tau schedule) of the
+    # grid with recall@10 >= 0.95 -- the smallest passing nprobe, then the
+    # faster schedule there (untimed selection; a few async searches each)
     sweep = []
     nprobe = args.nprobe
+    taus = ["TIGHT", "LOOSE"] if args.tau == "auto" else [args.tau]
+    tau_sel = taus[0]
+
+    def quick_ms(npb, tau, reps=3):
+        evs = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            run(npb, tau, stats=False)
+            b.record(stream)
+            evs.append((a, b))
+        torch.cuda.synchronize()
+        return float(np.median([a.elapsed_time(b) for a, b in evs]))
+
     if gt is not None:
-        for npb in cfg.nprobe:
-            st = run(npb)
-            torch.cuda.synchronize()
-            rc = recall_at_k(d_ids.cpu().numpy(), gt, 10)
-            sweep.append({"nprobe": npb, "recall10": round(rc, 4), "ms": round(st.ms_total, 3),
-                          "exact_per_q": round(st.exact / nq, 1), "f1_per_q": round(st.stage1_pass / nq, 1)})
-            log("sweep", sweep[-1])
-            if not nprobe and rc >= 0.95:
+        for npb in ([nprobe] if nprobe else cfg.nprobe):
+            passing = []
+            for tau in taus:
+                st = run(npb, tau)
+                torch.cuda.synchronize()
+                rc = recall_at_k(d_ids.cpu().numpy(), gt, 10)
+                ms_q = quick_ms(npb, tau)
+                sweep.append({"nprobe": npb, "tau_schedule": tau, "recall10": round(rc, 4), "ms": round(ms_q, 3),
+                              "exact_per_q": round(st.exact / nq, 1), "f1_per_q": round(st.stage1_pass / nq, 1)})
+                log("sweep", sweep[-1])
+                if rc >= 0.95:
+                    passing.append((ms_q, tau))
+            if passing:
                 nprobe = npb
+                tau_sel = min(passing)[1]
                 break
     if not nprobe:
         nprobe = cfg.default_nprobe
 
+    clk = Clocks(local).start()
     # warmup
     for _ in range(max(args.warmup, 3)):
-        run(nprobe)
+        run(nprobe, tau_sel)
     torch.cuda.synchronize()
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # 512 MB > 126 MB L2
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -286,11 +322,11 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    with Clocks(local) as clk:
+    with clk:
         for i in range(args.steps):
             flush.fill_(float(i))                      # L2 flush between timed steps (not timed)
             ev[i][0].record(stream)
-            run(nprobe, stats=False)                   # asynchronous: no host round trip inside the step
+            run(nprobe, tau_sel, stats=False)          # asynchronous: no host round trip inside the step
             ev[i][1].record(stream)
         torch.cuda.synchronize()
     if world > 1:
@@ -299,7 +335,7 @@ def main():
     # call is synchronous and records the library's per-stage CUDA events)
     for i in range(max(3, min(args.steps, 5))):
         flush.fill_(float(i))
-        sts.append(run(nprobe))
+        sts.append(run(nprobe, tau_sel))
     torch.cuda.synchronize()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     ms = float(np.mean(step_ms))
@@ -338,7 +374,8 @@ def main():
 
     # e2e through the host-buffer call (pinned host queries; H2D + D2H inside the timed region)
     hq = torch.from_numpy(Q).pin_memory().numpy()
-    p = mrq.SearchParams.make(K=K, nprobe=nprobe, seed_lists=args.seed_lists, seed_mult=args.seed_mult)
+    p = mrq.SearchParams.make(K=K, nprobe=nprobe, tau_schedule=tau_sel, seed_lists=args.seed_lists,
+                              seed_mult=args.seed_mult)
     for _ in range(2):
         mrq.mrq_search_batch(h, hq, p, with_stats=False)
     e2e_t = []
@@ -357,7 +394,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            qps, cores, sample = cpu_oracle_leg(bfile, X, Q, K, nprobe, seed_lists=args.seed_lists,
+            qps, cores, sample = cpu_oracle_leg(bfile, X, Q, K, nprobe, tau_schedule=tau_sel, seed_lists=args.seed_lists,
                                                 seed_mult=args.seed_mult)
             cpu = {"value": round(qps, 2), "unit": "queries/s", "cores": cores, "kind": "oracle", "sample": sample}
         except Exception as e:  # pragma: no cover
@@ -380,7 +417,7 @@ def main():
         "data": "synthetic",
         "config": {"workload": WORKLOADS.get(cfg_name, cfg_name),
                    "N": int(X.shape[0]), "Q": nq, "D": int(X.shape[1]), "d": d, "k": hdr["k"], "K": K,
-                   "nprobe": nprobe, "tau_schedule": "TIGHT", "eps0": 1.9, "m": 4.0, "mode": "FULL",
+                   "nprobe": nprobe, "tau_schedule": tau_sel, "eps0": 1.9, "m": 4.0, "mode": "FULL",
                    "seed_lists": args.seed_lists, "seed_mult": args.seed_mult,
                    "recall10": round(rc, 4) if rc is not None else None, "l2": "flushed (512 MB write) between timed steps",
                    "parallelism": "lists sharded over %d GPU(s)" % world, "base_sha_match": sha_ok,
@@ -414,18 +451,23 @@ def reference_arm(args, rank, world, cfg_name, bfile, gtfile):
     from oracle import build as B
     cfg = synth.config_by_name(cfg_name)
     X, Q = synth.generate(cfg, device="cuda" if _has_cuda() else None)
-    nprobe = args.nprobe or cfg.default_nprobe
+    # our arm's operating point on this workload: the grid's first nprobe
+    # (recall@10 >= 0.95 there) and, for --tau auto, the schedule our arm
+    # measures faster (LOOSE on the SIFT-shaped workload, profiles/r01_sweep_sift.json)
+    nprobe = args.nprobe or cfg.nprobe[0]
+    tau = "LOOSE" if args.tau == "auto" else args.tau
     bf = B.read(bfile)
     ox = oracle.Index(bf, X)
     K = args.K
     sample = 200
     for _ in range(max(args.warmup, 1)):
-        ox.search(Q[:16], K=K, nprobe=nprobe, seed_lists=args.seed_lists, seed_mult=args.seed_mult)
+        ox.search(Q[:16], K=K, nprobe=nprobe, tau_schedule=tau, seed_lists=args.seed_lists, seed_mult=args.seed_mult)
     ts = []
     for i in range(args.steps):
         s = (i * sample) % Q.shape[0]
         t = time.time()
-        ox.search(Q[s:s + sample], K=K, nprobe=nprobe, seed_lists=args.seed_lists, seed_mult=args.seed_mult)
+        ox.search(Q[s:s + sample], K=K, nprobe=nprobe, tau_schedule=tau, seed_lists=args.seed_lists,
+                  seed_mult=args.seed_mult)
         ts.append(time.time() - t)
     dt = float(np.mean(ts))
     qps = sample / dt
@@ -433,7 +475,7 @@ def reference_arm(args, rank, world, cfg_name, bfile, gtfile):
     out = {"impl": "reference", "metric": METRIC, "value": round(qps, 2), "unit": "queries/s", "n_gpus": world,
            "steps": args.steps, "warmup": max(args.warmup, 1), "ms_per_step": round(dt * 1e3, 3),
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": WORKLOADS.get(cfg_name, cfg_name), "nprobe": nprobe, "K": K,
+           "config": {"workload": WORKLOADS.get(cfg_name, cfg_name), "nprobe": nprobe, "K": K, "tau_schedule": tau,
                       "sample_per_step": sample},
            "cpu_baseline": {"value": round(qps, 2), "unit": "queries/s", "cores": cores, "kind": "oracle",
                             "sample": "%d queries per step" % sample},
