@@ -243,7 +243,8 @@ static int load_impl(mrq_index *ix, const char *build_file, const float *base, i
         for (int j = 0; j < D; j++) PT[(size_t)j * D + i] = b.P[(size_t)i * D + j];
     for (int j = 0; j < d; j++)
         for (int i = 0; i < d; i++) RT[(size_t)i * d + j] = b.R[(size_t)j * d + i];
-    std::vector<float> C32T((size_t)d * k), C32((size_t)k * d), cn32(k);
+    // ||c||^2 padded with +inf to a whole number of 256-column probe tiles
+    std::vector<float> C32T((size_t)d * k), C32((size_t)k * d), cn32((k + 255) / 256 * 256, INFINITY);
     double cmax = 0.0;
     for (int c = 0; c < k; c++) {
         double s = 0.0;
@@ -460,8 +461,8 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
             SCR("probe_kv", float, (size_t)nq * P * 16, kvbuf);
             const double kappa = mrq_probe_tc_kappa(ix);
             TRY(mrq_probe_tc_run_fused(ix, qd32, nq, np, qnorm, kappa, cbuf, capp, ccnt, kvbuf, st));
-            TRY(launch_probe_finish_w(nq, k, d, np, qp, D, ix->C, qnorm, ix->cmax, kappa, cbuf, P, capp, ccnt, kvbuf,
-                                      cand, probe, probe_qn2, ncand, st));
+            TRY(launch_probe_finish_w(nq, k, d, np, qp, D, ix->C, qnorm, ix->cmax, kappa, cbuf, P, capp,
+                                      mrq_probe_tc_grid(ix, nq), ccnt, kvbuf, cand, probe, probe_qn2, ncand, st));
         } else {
             SCR("approx", float, nq * k, approx);
             double kappa;

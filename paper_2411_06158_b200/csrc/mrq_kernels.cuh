@@ -65,7 +65,7 @@ bool supported_W(int W);
 void launch_scan_dbg(int W, const LaunchScan &a, double *dis, double *lb1, cudaStream_t st);
 int launch_probe_finish_w(int64_t nq, int k, int d, int np, const double *qp, int D, const double *C,
                           const double *qnorm, double cmax, double kappa, const uint2 *cbuf, int P, int capp,
-                          const uint32_t *ccnt, const float *kvbuf, uint32_t *cand, uint32_t *probe,
+                          int G, const uint32_t *ccnt, const float *kvbuf, uint32_t *cand, uint32_t *probe,
                           double *probe_qn2, uint32_t *ncand, cudaStream_t st);
 int launch_probe_select_w(const float *approx, int64_t nq, int k, int d, int np, const double *qp, int D,
                           const double *C, const double *qnorm, double cmax, double kappa, uint32_t *cand,

@@ -32,8 +32,6 @@
 
 #include "mrq_probe_tc.cuh"
 
-#define TC_BM 128
-#define TC_BN 256
 #define TC_BK 32                       // fp32 elements per 128-byte swizzle row
 #define TC_STAGES 4
 #define TC_A_BYTES (TC_BM * TC_BK * 4) // 16 KB
@@ -101,7 +99,7 @@ __host__ __device__ constexpr uint32_t tf32_idesc(int M, int N)
 }
 
 // Fused selection (FUSED = true, np <= TC_NPMAX).  A row's columns are split
-// into P = 2 gridDim.y parts (CTA column range x epilogue half); the thread
+// into parts (CTA column range x epilogue half, at most P = 2 maxparts); the thread
 // owning (row, part) keeps the 16 smallest screen values of its part sorted
 // in registers and appends every (a_c, c) with
 // a_c <= RU(its current np-th smallest + 2 delta_q) to the part's candidate
@@ -110,10 +108,11 @@ __host__ __device__ constexpr uint32_t tf32_idesc(int M, int N)
 // is appended by its part; the parts' 16 smallest go to kvbuf so that
 // k_probe_finish_w can form a_(np) and rescore the margin set.
 #define TC_NPMAX 16
+
 template <bool FUSED>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_probe_tc(const __grid_constant__ CUtensorMap mapA,
                                                             const __grid_constant__ CUtensorMap mapB, int nq, int k,
-                                                            int d, int tiles_per_cta, const float *__restrict__ cn32,
+                                                            int d, int G, int maxparts, const float *__restrict__ cn32,
                                                             float *__restrict__ approx, int np,
                                                             const double *__restrict__ qnorm, double cmax,
                                                             double kappa, uint2 *__restrict__ cbuf, int capp,
@@ -129,10 +128,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_probe_tc(const __grid_constan
     float *scratch = (float *)(tmem_slot + 4);   // FUSED: 256 x 33 floats (per-thread chunk staging)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int m0 = blockIdx.x * TC_BM;
     const int ntiles = (k + TC_BN - 1) / TC_BN;
-    const int t_begin = blockIdx.y * tiles_per_cta;
-    const int t_end = min(ntiles, t_begin + tiles_per_cta);
+    const int64_t U = (int64_t)((nq + TC_BM - 1) / TC_BM) * ntiles;
+    const int64_t ub = tc_u0(blockIdx.x, U, G), ue = tc_u0((int64_t)blockIdx.x + 1, U, G);
     const int kb_n = (d + TC_BK - 1) / TC_BK;
 
     if (warp == 0 && lane == 0) {
@@ -161,12 +159,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_probe_tc(const __grid_constan
         if (lane == 0) {   // ---------------- TMA producer
             int s = 0;
             uint32_t ph = 0;
-            for (int t = t_begin; t < t_end; t++) {
+            for (int64_t u = ub; u < ue; u++) {
+                const int mb = (int)(u / ntiles), t = (int)(u % ntiles);
                 for (int kb = 0; kb < kb_n; kb++) {
                     mbar_wait(empty + s, ph ^ 1u);
                     unsigned char *sa = ring + s * TC_STAGE_BYTES;
                     mbar_expect_tx(full + s, TC_STAGE_BYTES);
-                    tma_load_2d(sa, &mapA, full + s, kb * TC_BK, m0);
+                    tma_load_2d(sa, &mapA, full + s, kb * TC_BK, mb * TC_BM);
                     tma_load_2d(sa + TC_A_BYTES, &mapB, full + s, kb * TC_BK, t * TC_BN);
                     if (++s == TC_STAGES) {
                         s = 0;
@@ -181,7 +180,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_probe_tc(const __grid_constan
             int s = 0;
             uint32_t ph = 0;
             int it = 0;
-            for (int t = t_begin; t < t_end; t++, it++) {
+            for (int64_t u = ub; u < ue; u++, it++) {
                 const int b = it & 1;
                 mbar_wait(tempty + b, (((uint32_t)it >> 1) & 1u) ^ 1u);
                 asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
@@ -219,27 +218,52 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_probe_tc(const __grid_constan
     } else {   // ---------------------------- epilogue warps 2..5
         const int quad = warp & 3;            // TMEM lanes 32 quad .. 32 quad + 31
         const int half = (warp - 2) >> 2;     // column chunks half, half + 2, ... of each tile
-        const int row = m0 + quad * 32 + lane;
-        const int P = 2 * (int)gridDim.y, part = 2 * (int)blockIdx.y + half;
+        const int P = 2 * maxparts;
         const float FINF = __int_as_float(0x7f800000);
         float kv[TC_NPMAX];                   // FUSED: the np smallest screen values, ascending
         float tf = FINF;                      // FUSED: append threshold RU(kv[np-1] + margin)
         uint32_t cnt = 0;
         double margin = 0.0;
         uint2 *rb = nullptr;
-        if (FUSED) {
-            // kv holds 16 - np placeholders (-inf) followed by the np smallest
-            // values, so the running np-th smallest is always kv[TC_NPMAX - 1]
+        int row = 0, part = 0, cur_mb = -1;
+        // FUSED: the (row, part) state goes to kvbuf / ccnt when the query block changes
+        auto flush = [&]() {
+            if (FUSED && cur_mb >= 0 && row < nq) {
+                ccnt[(int64_t)row * P + part] = cnt;
+                float4 *kvo = (float4 *)(kvbuf + ((int64_t)row * P + part) * TC_NPMAX);
 #pragma unroll
-            for (int j = 0; j < TC_NPMAX; j++) kv[j] = j < TC_NPMAX - np ? -FINF : FINF;
-            if (row < nq) {
-                const double g = qnorm[row] + cmax;
-                margin = 2.0 * (kappa * (g * g));
-                rb = cbuf + ((int64_t)row * P + part) * capp;
+                for (int i = 0; i < TC_NPMAX; i += 4) {   // placeholders are not row values: +inf
+                    float4 o = make_float4(kv[i], kv[i + 1], kv[i + 2], kv[i + 3]);
+                    if (o.x == -FINF) o.x = FINF;
+                    if (o.y == -FINF) o.y = FINF;
+                    if (o.z == -FINF) o.z = FINF;
+                    if (o.w == -FINF) o.w = FINF;
+                    kvo[i / 4] = o;
+                }
             }
-        }
+        };
         int it = 0;
-        for (int t = t_begin; t < t_end; t++, it++) {
+        for (int64_t u = ub; u < ue; u++, it++) {
+            const int mb = (int)(u / ntiles), t = (int)(u % ntiles);
+            if (mb != cur_mb) {
+                flush();
+                cur_mb = mb;
+                row = mb * TC_BM + quad * 32 + lane;
+                part = 2 * (int)(blockIdx.x - tc_owner((int64_t)mb * ntiles, U, G)) + half;
+                cnt = 0;
+                tf = FINF;
+                if (FUSED) {
+                    // kv holds 16 - np placeholders (-inf) followed by the np smallest
+                    // values, so the running np-th smallest is always kv[TC_NPMAX - 1]
+#pragma unroll
+                    for (int j = 0; j < TC_NPMAX; j++) kv[j] = j < TC_NPMAX - np ? -FINF : FINF;
+                    if (row < nq) {
+                        const double g = qnorm[row] + cmax;
+                        margin = 2.0 * (kappa * (g * g));
+                        rb = cbuf + ((int64_t)row * P + part) * capp;
+                    }
+                }
+            }
             const int b = it & 1;
             mbar_wait(tfull + b, ((uint32_t)it >> 1) & 1u);
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
@@ -260,20 +284,24 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_probe_tc(const __grid_constan
                 asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
                 if (FUSED) {
                     // screen values of the chunk; mask of those <= the append threshold
+                    // (2 acc is exact, so the fma rounds exactly like cn - 2 acc;
+                    // cn32 is padded with +inf past k, so padded columns never pass)
                     float av[32];
-                    uint32_t mask = 0;
+                    float mn = FINF;
 #pragma unroll
                     for (int j = 0; j < 32; j += 4) {
                         const float4 cn = __ldg((const float4 *)(cn32 + n0 + c + j));
-                        av[j] = cn.x - 2.0f * __uint_as_float(v[j]);
-                        av[j + 1] = cn.y - 2.0f * __uint_as_float(v[j + 1]);
-                        av[j + 2] = cn.z - 2.0f * __uint_as_float(v[j + 2]);
-                        av[j + 3] = cn.w - 2.0f * __uint_as_float(v[j + 3]);
+                        av[j] = __fmaf_rn(-2.0f, __uint_as_float(v[j]), cn.x);
+                        av[j + 1] = __fmaf_rn(-2.0f, __uint_as_float(v[j + 1]), cn.y);
+                        av[j + 2] = __fmaf_rn(-2.0f, __uint_as_float(v[j + 2]), cn.z);
+                        av[j + 3] = __fmaf_rn(-2.0f, __uint_as_float(v[j + 3]), cn.w);
+                        mn = fminf(fminf(mn, fminf(av[j], av[j + 1])), fminf(av[j + 2], av[j + 3]));
                     }
+                    uint32_t mask = 0;
+                    if (mn <= tf && row < nq) {
 #pragma unroll
-                    for (int j = 0; j < 32; j++)
-                        mask |= (n0 + c + j < k && av[j] <= tf) ? (1u << j) : 0u;
-                    if (row >= nq) mask = 0;
+                        for (int j = 0; j < 32; j++) mask |= av[j] <= tf ? (1u << j) : 0u;
+                    }
                     if (mask) {   // rare after warm-up: stage the chunk, walk the passing values
                         float *sc = scratch + ((warp - 2) * 32 + lane) * 33;
 #pragma unroll
@@ -322,19 +350,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_probe_tc(const __grid_constan
             __syncwarp();
             if (lane == 0) mbar_arrive(tempty + b);
         }
-        if (FUSED && row < nq) {
-            ccnt[(int64_t)row * P + part] = cnt;
-            float4 *kvo = (float4 *)(kvbuf + ((int64_t)row * P + part) * TC_NPMAX);
-#pragma unroll
-            for (int i = 0; i < TC_NPMAX; i += 4) {   // placeholders are not row values: +inf
-                float4 o = make_float4(kv[i], kv[i + 1], kv[i + 2], kv[i + 3]);
-                if (o.x == -FINF) o.x = FINF;
-                if (o.y == -FINF) o.y = FINF;
-                if (o.z == -FINF) o.z = FINF;
-                if (o.w == -FINF) o.w = FINF;
-                kvo[i / 4] = o;
-            }
-        }
+        flush();
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
@@ -408,22 +424,24 @@ double mrq_probe_tc_kappa(const mrq_index *ix)
     return std::ldexp(1.0, -9) + (double)ix->d * std::ldexp(1.0, -22) + std::ldexp(1.0, -20);
 }
 
+// G <= 7 x (query blocks): a block's tiles then span at most 8 CTAs, i.e. at
+// most 16 parts per row (the finisher's limit)
+static int tc_grid(const mrq_index *ix, int64_t nq)
+{
+    const int64_t mblocks = (nq + TC_BM - 1) / TC_BM;
+    const int64_t U = mblocks * (int64_t)((ix->k + TC_BN - 1) / TC_BN);
+    return (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(ix->sm_count, U), 7 * mblocks));
+}
+
 int mrq_probe_tc_run(mrq_index *ix, const float *qd32, int64_t nq, float *approx, cudaStream_t st)
 {
     ProbeTC *tc = (ProbeTC *)ix->probe_tc;
     CUtensorMap mapA;
     int rc = make_map(tc, &mapA, qd32, (int)nq, ix->d, TC_BM);
     if (rc != MRQ_OK) return rc;
-    const int mblocks = (int)((nq + TC_BM - 1) / TC_BM);
-    const int ntiles = (ix->k + TC_BN - 1) / TC_BN;
-    // split the centroid tiles so the grid covers the SMs about once
-    int gy = (ix->sm_count + mblocks - 1) / mblocks;
-    gy = std::max(1, std::min(gy, ntiles));
-    const int per = (ntiles + gy - 1) / gy;
-    gy = (ntiles + per - 1) / per;
-    k_probe_tc<false><<<dim3(mblocks, gy), TC_THREADS, TC_SMEM, st>>>(mapA, tc->mapB, (int)nq, ix->k, ix->d, per,
-                                                                       ix->cn32, approx, 0, nullptr, 0.0, 0.0,
-                                                                       nullptr, 0, nullptr, nullptr);
+    const int G = tc_grid(ix, nq);
+    k_probe_tc<false><<<G, TC_THREADS, TC_SMEM, st>>>(mapA, tc->mapB, (int)nq, ix->k, ix->d, G, 1, ix->cn32, approx,
+                                                       0, nullptr, 0.0, 0.0, nullptr, 0, nullptr, nullptr);
     MRQ_CUDA_TRY(cudaGetLastError());
     return MRQ_OK;
 }
@@ -433,15 +451,15 @@ bool mrq_probe_tc_fusable(const mrq_index *ix, int np)
     return mrq_probe_tc_enabled(ix) && np <= TC_NPMAX && !ix->force_probe_unfused;
 }
 
+// parts per query row = 2 x (most CTAs any query block's tiles span)
 int mrq_probe_tc_parts(const mrq_index *ix, int64_t nq)
 {
-    const int mblocks = (int)((nq + TC_BM - 1) / TC_BM);
-    const int ntiles = (ix->k + TC_BN - 1) / TC_BN;
-    int gy = (ix->sm_count + mblocks - 1) / mblocks;
-    gy = std::max(1, std::min(std::min(gy, ntiles), 8));   // P = 2 gy <= 16 parts
-    const int per = (ntiles + gy - 1) / gy;
-    gy = (ntiles + per - 1) / per;
-    return 2 * gy;
+    const int64_t mblocks = (nq + TC_BM - 1) / TC_BM, ntiles = (ix->k + TC_BN - 1) / TC_BN;
+    const int64_t U = mblocks * ntiles, G = tc_grid(ix, nq);
+    int64_t mx = 1;
+    for (int64_t mb = 0; mb < mblocks; mb++)
+        mx = std::max(mx, tc_owner((mb + 1) * ntiles - 1, U, G) - tc_owner(mb * ntiles, U, G) + 1);
+    return (int)(2 * mx);
 }
 
 int mrq_probe_tc_run_fused(mrq_index *ix, const float *qd32, int64_t nq, int np, const double *qnorm, double kappa,
@@ -451,13 +469,12 @@ int mrq_probe_tc_run_fused(mrq_index *ix, const float *qd32, int64_t nq, int np,
     CUtensorMap mapA;
     int rc = make_map(tc, &mapA, qd32, (int)nq, ix->d, TC_BM);
     if (rc != MRQ_OK) return rc;
-    const int mblocks = (int)((nq + TC_BM - 1) / TC_BM);
-    const int ntiles = (ix->k + TC_BN - 1) / TC_BN;
-    const int gy = mrq_probe_tc_parts(ix, nq) / 2;
-    const int per = (ntiles + gy - 1) / gy;
-    k_probe_tc<true><<<dim3(mblocks, gy), TC_THREADS, TC_SMEM, st>>>(mapA, tc->mapB, (int)nq, ix->k, ix->d, per,
-                                                                      ix->cn32, nullptr, np, qnorm, ix->cmax, kappa,
-                                                                      cbuf, capp, ccnt, kvbuf);
+    const int G = tc_grid(ix, nq);
+    const int maxparts = mrq_probe_tc_parts(ix, nq) / 2;
+    k_probe_tc<true><<<G, TC_THREADS, TC_SMEM, st>>>(mapA, tc->mapB, (int)nq, ix->k, ix->d, G, maxparts, ix->cn32,
+                                                      nullptr, np, qnorm, ix->cmax, kappa, cbuf, capp, ccnt, kvbuf);
     MRQ_CUDA_TRY(cudaGetLastError());
     return MRQ_OK;
 }
+
+int mrq_probe_tc_grid(const mrq_index *ix, int64_t nq) { return tc_grid(ix, nq); }

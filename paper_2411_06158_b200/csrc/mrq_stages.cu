@@ -8,6 +8,7 @@
 
 #include "mrq_internal.cuh"
 #include "mrq_kernels.cuh"
+#include "mrq_probe_tc.cuh"
 
 // ----------------------------------------------------------------------- a4
 // Seeds S0 and tau0 (decision T; replaces "tau <- threshold of the
@@ -789,7 +790,7 @@ __device__ __forceinline__ double sqdist_rows8(const double *__restrict__ cr, co
 __global__ void __launch_bounds__(128) k_probe_finish_w(int64_t nq, int k, int d, int np, const double *__restrict__ qp,
                                                         int D, const double *__restrict__ C,
                                                         const double *__restrict__ qnorm, double cmax, double kappa,
-                                                        const uint2 *__restrict__ cbuf, int P, int capp,
+                                                        const uint2 *__restrict__ cbuf, int P, int capp, int G,
                                                         const uint32_t *__restrict__ ccnt,
                                                         const float *__restrict__ kvbuf, uint32_t *__restrict__ cand,
                                                         uint32_t *__restrict__ probe, double *__restrict__ probe_qn2,
@@ -801,16 +802,18 @@ __global__ void __launch_bounds__(128) k_probe_finish_w(int64_t nq, int k, int d
     if (q >= nq) return;
     SelItem *lst = (SelItem *)wsm + (size_t)warp * (np + MRQ_SELQ);
     SelItem *queue = lst + np;
-    // a_(np): the P * 16 part minima, up to 8 per lane (P <= 16)
-    const int nv = P * 16;
+    // a_(np): the used parts' 16 smallest, up to 8 per lane (<= 16 parts);
+    // buffers are laid out with P parts per row, of which Pq are used
+    const int Pq = tc_parts_of(q / TC_BM, nq, k, G);
+    const int nv = Pq * 16;
     uint32_t key[8];
     bool all = false;
 #pragma unroll
     for (int j = 0; j < 8; j++) {
         const int i = j * 32 + lane;
-        key[j] = i < nv ? f2key(kvbuf[q * nv + i]) : 0xFFFFFFFFu;
+        key[j] = i < nv ? f2key(kvbuf[q * P * 16 + i]) : 0xFFFFFFFFu;
     }
-    for (int pp = lane; pp < P; pp += 32) all |= ccnt[q * P + pp] > (uint32_t)capp;
+    for (int pp = lane; pp < Pq; pp += 32) all |= ccnt[q * P + pp] > (uint32_t)capp;
     all = __any_sync(0xffffffffu, all);
     uint32_t res = 0;
     for (int bit = 31; bit >= 0; bit--) {
@@ -830,7 +833,7 @@ __global__ void __launch_bounds__(128) k_probe_finish_w(int64_t nq, int k, int d
     } else {
         // the parts' buffers as one flat index space (lane p holds part p's
         // count and exclusive prefix), 4 batches of loads in flight
-        const uint32_t myc = lane < P ? ccnt[q * P + lane] : 0u;
+        const uint32_t myc = lane < Pq ? ccnt[q * P + lane] : 0u;
         uint32_t pre = myc;
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, pre, o);
@@ -846,7 +849,7 @@ __global__ void __launch_bounds__(128) k_probe_finish_w(int64_t nq, int k, int d
                 const uint32_t e = e0 + 32 * u + lane;
                 int part = 0;
                 uint32_t pbase = 0;
-                for (int pp = 1; pp < P; pp++) {   // last part whose prefix <= e
+                for (int pp = 1; pp < Pq; pp++) {   // last part whose prefix <= e
                     const uint32_t b = __shfl_sync(0xffffffffu, pre, pp);
                     if (b <= e) {
                         part = pp;
@@ -892,7 +895,7 @@ __global__ void __launch_bounds__(128) k_probe_finish_w(int64_t nq, int k, int d
 
 int launch_probe_finish_w(int64_t nq, int k, int d, int np, const double *qp, int D, const double *C,
                           const double *qnorm, double cmax, double kappa, const uint2 *cbuf, int P, int capp,
-                          const uint32_t *ccnt, const float *kvbuf, uint32_t *cand, uint32_t *probe,
+                          int G, const uint32_t *ccnt, const float *kvbuf, uint32_t *cand, uint32_t *probe,
                           double *probe_qn2, uint32_t *ncand, cudaStream_t st)
 {
     if (P > 16) {
@@ -904,7 +907,7 @@ int launch_probe_finish_w(int64_t nq, int k, int d, int np, const double *qp, in
     int rc = set_attr((const void *)k_probe_finish_w, smem);
     if (rc) return rc;
     k_probe_finish_w<<<(unsigned)((nq + wpb - 1) / wpb), wpb * 32, smem, st>>>(
-        nq, k, d, np, qp, D, C, qnorm, cmax, kappa, cbuf, P, capp, ccnt, kvbuf, cand, probe, probe_qn2, ncand);
+        nq, k, d, np, qp, D, C, qnorm, cmax, kappa, cbuf, P, capp, G, ccnt, kvbuf, cand, probe, probe_qn2, ncand);
     return MRQ_OK;
 }
 
