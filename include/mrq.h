@@ -175,6 +175,9 @@ int mrq_debug_fetch(mrq_index *idx, const char *name, void *dst, size_t dst_byte
  * multi-rank path (exchange buffers, device-copy all-gather, k_xmerge).
  * "cuda_core_probe" = 1 screens the probe on CUDA cores (fp32) instead of
  * the tcgen05 tf32 GEMM (the exact fp64 selection is the same).
+ * "probe_unfused" = 1 writes the screen to HBM and selects in a separate
+ * kernel.  "graphs" = 0 disables the CUDA-graph replay of repeated searches
+ * (also: environment MRQ_NO_GRAPHS).
  * Errors: MRQ_EINVAL (unknown name).
  */
 int mrq_debug_set(mrq_index *idx, const char *name, int64_t value);

@@ -1,6 +1,7 @@
 // mrq_api.cu -- the C ABI of libmrq (include/mrq.h): build-file parsing, HBM
 // layout and GPU encoding at load, and the batched search pipeline.
 #include <stdarg.h>
+#include <stdlib.h>
 #include <stdio.h>
 #include <string.h>
 
@@ -13,6 +14,13 @@
 #include "mrq_kernels.cuh"
 #include "mrq_probe_tc.cuh"
 #include "mrq_comm.cuh"
+
+// key of the cached CUDA graph of a search (search_dispatch)
+struct GraphKey {
+    const void *q, *ids, *dist, *stream;
+    int64_t nq;
+    mrq_search_params p;
+};
 
 // ------------------------------------------------------------------ errors
 static thread_local char g_err[1024] = "";
@@ -343,6 +351,11 @@ extern "C" int mrq_index_load(const char *build_file, const float *base, int64_t
     }
     *out = nullptr;
     mrq_index *ix = new mrq_index();
+    ix->g_key = new GraphKey();
+    ix->g_pending = new GraphKey();
+    memset(ix->g_key, 0, sizeof(GraphKey));
+    memset(ix->g_pending, 0, sizeof(GraphKey));
+    if (getenv("MRQ_NO_GRAPHS")) ix->graphs = 0;
     int rc = load_impl(ix, build_file, base, n, D, d, dist);
     if (rc != MRQ_OK) {
         mrq_free(ix);
@@ -361,6 +374,9 @@ extern "C" void mrq_free(mrq_index *ix)
     for (auto &kv : ix->scratch)
         if (kv.second.p) cudaFree(kv.second.p);
     mrq_probe_tc_free(ix);
+    if (ix->gexec) cudaGraphExecDestroy((cudaGraphExec_t)ix->gexec);
+    delete (GraphKey *)ix->g_key;
+    delete (GraphKey *)ix->g_pending;
     mrq_comm_free(ix);
     for (auto &e : ix->ev)
         if (e) cudaEventDestroy(e);
@@ -526,10 +542,8 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
 
     // ---- a4: seeds S0 and tau0 (decision T); EXACT mode scans everything
     if (mode == 2) {
-        std::vector<double> inf(nq, INFINITY);
-        MRQ_CUDA_TRY(cudaMemcpyAsync(tau0, inf.data(), nq * 8, cudaMemcpyHostToDevice, st));
+        launch_fill_f64(tau0, nq, INFINITY, st);
         MRQ_CUDA_TRY(cudaMemsetAsync(s0_cnt, 0, nq * 4, st));
-        MRQ_CUDA_TRY(cudaStreamSynchronize(st));
     } else {
         if (sharded) {   // local part of S0 -> all-gather -> global S0, tau0
             StageArgs sx = sa;
@@ -655,6 +669,60 @@ static int check_params(const mrq_index *ix, int64_t nq, const mrq_search_params
     return MRQ_OK;
 }
 
+// CUDA-graph replay of repeated searches: a search with the same shapes,
+// parameters, buffers and stream as the previous one is captured once (on its
+// second occurrence, when every scratch buffer has its final size) and then
+// replayed with a single cudaGraphLaunch.  Not used with stats, debug dumps,
+// the host all-gather, or when the candidate scratch needs the host-read total.
+
+static bool graph_key_eq(const GraphKey &a, const GraphKey &b) { return memcmp(&a, &b, sizeof a) == 0; }
+
+static int search_dispatch(mrq_index *ix, const float *d_q, int64_t nq, const mrq_search_params *p, int64_t *d_ids,
+                           float *d_dist, mrq_stats *stats, cudaStream_t st)
+{
+    const int np = std::min(p->nprobe, ix->k);
+    const uint64_t bound = (uint64_t)nq * ix->h_topsum[np];
+    const bool eligible = !stats && !ix->dbg_dump_dis && !ix->host_ag && ix->graphs && st != nullptr &&
+                          bound * 48 <= ((uint64_t)8 << 30);
+    if (!eligible) return search_impl(ix, d_q, nq, p, d_ids, d_dist, stats, st);
+    GraphKey key;
+    memset(&key, 0, sizeof key);
+    key.q = d_q;
+    key.ids = d_ids;
+    key.dist = d_dist;
+    key.stream = st;
+    key.nq = nq;
+    key.p = *p;
+    GraphKey *cur = (GraphKey *)ix->g_key, *pend = (GraphKey *)ix->g_pending;
+    if (ix->gexec && graph_key_eq(*cur, key)) {
+        MRQ_CUDA_TRY(cudaGraphLaunch((cudaGraphExec_t)ix->gexec, st));
+        return MRQ_OK;
+    }
+    if (!graph_key_eq(*pend, key)) {   // first occurrence: run, remember
+        *pend = key;
+        return search_impl(ix, d_q, nq, p, d_ids, d_dist, stats, st);
+    }
+    // second occurrence: capture, instantiate, launch
+    if (ix->gexec) cudaGraphExecDestroy((cudaGraphExec_t)ix->gexec);
+    ix->gexec = nullptr;
+    cudaGraph_t g = nullptr;
+    MRQ_CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+    const int rc = search_impl(ix, d_q, nq, p, d_ids, d_dist, nullptr, st);
+    const cudaError_t ce = cudaStreamEndCapture(st, &g);
+    cudaGraphExec_t ex = nullptr;
+    if (rc != MRQ_OK || ce != cudaSuccess || !g || cudaGraphInstantiate(&ex, g, 0) != cudaSuccess) {
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();
+        ix->graphs = 0;   // capture not possible here: plain launches from now on
+        return search_impl(ix, d_q, nq, p, d_ids, d_dist, stats, st);
+    }
+    cudaGraphDestroy(g);
+    ix->gexec = ex;
+    *cur = key;
+    MRQ_CUDA_TRY(cudaGraphLaunch(ex, st));
+    return MRQ_OK;
+}
+
 extern "C" int mrq_search_batch_device(mrq_index *ix, const float *d_queries, int64_t nq, const mrq_search_params *p,
                                        int64_t *d_out_ids, float *d_out_dist, mrq_stats *stats, void *stream)
 {
@@ -669,7 +737,7 @@ extern "C" int mrq_search_batch_device(mrq_index *ix, const float *d_queries, in
     }
     MRQ_CUDA_TRY(cudaSetDevice(ix->device));
     cudaStream_t st = stream ? (cudaStream_t)stream : ix->stream;
-    return search_impl(ix, d_queries, nq, p, d_out_ids, d_out_dist, stats, st);
+    return search_dispatch(ix, d_queries, nq, p, d_out_ids, d_out_dist, stats, st);
 }
 
 extern "C" int mrq_search_batch(mrq_index *ix, const float *queries, int64_t nq, const mrq_search_params *p,
@@ -692,7 +760,7 @@ extern "C" int mrq_search_batch(mrq_index *ix, const float *queries, int64_t nq,
     SCR("out_ids", int64_t, nq * p->K, dids);
     SCR("out_dist", float, nq * p->K, ddist);
     MRQ_CUDA_TRY(cudaMemcpyAsync(dq, queries, (size_t)nq * ix->D * 4, cudaMemcpyHostToDevice, ix->stream));
-    TRY(search_impl(ix, dq, nq, p, dids, ddist, stats, ix->stream));
+    TRY(search_dispatch(ix, dq, nq, p, dids, ddist, stats, ix->stream));
     MRQ_CUDA_TRY(cudaMemcpyAsync(out_ids, dids, (size_t)nq * p->K * 8, cudaMemcpyDeviceToHost, ix->stream));
     MRQ_CUDA_TRY(cudaMemcpyAsync(out_dist, ddist, (size_t)nq * p->K * 4, cudaMemcpyDeviceToHost, ix->stream));
     MRQ_CUDA_TRY(cudaStreamSynchronize(ix->stream));
@@ -790,6 +858,10 @@ extern "C" int mrq_debug_set(mrq_index *ix, const char *name, int64_t value)
     }
     if (std::string(name) == "cuda_core_probe") {  // probe screen on CUDA cores instead of tcgen05
         ix->force_cuda_core_probe = (int)value;
+        return MRQ_OK;
+    }
+    if (std::string(name) == "graphs") {           // CUDA-graph replay of repeated searches (default 1)
+        ix->graphs = (int)value;
         return MRQ_OK;
     }
     if (std::string(name) == "probe_unfused") {    // screen to HBM + separate selection kernel

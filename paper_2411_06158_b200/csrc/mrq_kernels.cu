@@ -534,6 +534,17 @@ __global__ void __launch_bounds__(256, (W <= 3 ? 4 : 1)) k_scan(
     if (threadIdx.x == 0) f1_cnt[q] = sh_cnt;
 }
 
+__global__ void k_fill_f64(double *p, int64_t n, double v)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+void launch_fill_f64(double *p, int64_t n, double v, cudaStream_t st)
+{
+    k_fill_f64<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(p, n, v);
+}
+
 // ================================================================ launchers
 template <int W>
 static void launch_scan_w(const LaunchScan &a, cudaStream_t st)

@@ -15,6 +15,7 @@ __global__ void k_qtail(const double *qp, int64_t nq, int D, int d, int W, const
                         double rscale, double m, double *qr2o, double *eps_r, double *r0, float *qd32,
                         double *qnorm);
 __global__ void k_probe_approx(const float *qd32, int64_t nq, int d, int k, const float *C32T, float *approx);
+void launch_fill_f64(double *p, int64_t n, double v, cudaStream_t st);
 void launch_quant(const uint32_t *probe, const double *probe_qn2, int64_t nq, int np, int d, int W,
                   const double *r0, const double *Rc, const double *qr2, double eps0, uint32_t *planes,
                   double *qconst, cudaStream_t st);

@@ -258,3 +258,21 @@ def test_probe_tensor_core_screen_bound(case):
         gf = gx.search(Q, K=10, nprobe=npb)
         assert np.array_equal(pu, gx.fetch("probe", "u32")), npb
         assert np.array_equal(gu[0], gf[0]) and np.array_equal(gu[1], gf[1])
+
+
+def test_graph_replay_identical(case):
+    """Repeated searches replay a captured CUDA graph (search_dispatch); every
+    replay, and a parameter change (re-capture), gives the graph-free result."""
+    m, gx, Q = case["m"], case["gx"], case["Q"]
+    npb = case["nprobe"][-1]
+    m.mrq_debug_set(gx.h, "graphs", 0)
+    ref = {}
+    for tau in ("TIGHT", "LOOSE"):
+        ref[tau] = m.mrq_search_batch(gx.h, Q, m.SearchParams.make(K=10, nprobe=npb, tau_schedule=tau),
+                                      with_stats=False)[:2]
+    m.mrq_debug_set(gx.h, "graphs", 1)
+    for tau in ("TIGHT", "LOOSE", "TIGHT"):
+        for _ in range(3):   # plain run, capture, replay
+            ids, dist, _ = m.mrq_search_batch(gx.h, Q, m.SearchParams.make(K=10, nprobe=npb, tau_schedule=tau),
+                                              with_stats=False)
+            assert np.array_equal(ids, ref[tau][0]) and np.array_equal(dist, ref[tau][1])
