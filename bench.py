@@ -201,6 +201,8 @@ def main():
     ap.add_argument("--nprobe", type=int, default=0, help="0 = smallest grid nprobe with recall@10 >= 0.95")
     ap.add_argument("--K", type=int, default=10)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--tails-host", action="store_true",
+                    help="tails in pinned host memory (MRQ_LOAD_TAILS_HOST, SURVEY NEXT-4)")
     ap.add_argument("--tau", default="auto", choices=["auto", "TIGHT", "LOOSE"],
                     help="decision-T schedule; auto = the faster one at the operating point")
     ap.add_argument("--seed-lists", type=int, default=2, help="decision T: seed pool spans >= this many lists")
@@ -254,7 +256,7 @@ def main():
         uid = obj[0]
     t0 = time.time()
     h = mrq.mrq_index_load(bfile, X, d, rank=rank, world=world, device=local, nccl_unique_id=uid,
-                           host_allgather=hx)
+                           host_allgather=hx, tails_host=args.tails_host)
     load_s = time.time() - t0
     info = mrq.mrq_index_info(h)
     log("index loaded in %.2fs: %s (sha match %s)" % (load_s, info, sha_ok))
@@ -419,6 +421,7 @@ def main():
                    "N": int(X.shape[0]), "Q": nq, "D": int(X.shape[1]), "d": d, "k": hdr["k"], "K": K,
                    "nprobe": nprobe, "tau_schedule": tau_sel, "eps0": 1.9, "m": 4.0, "mode": "FULL",
                    "seed_lists": args.seed_lists, "seed_mult": args.seed_mult,
+                   "tails": "host (pinned, mapped)" if args.tails_host else "HBM",
                    "recall10": round(rc, 4) if rc is not None else None, "l2": "flushed (512 MB write) between timed steps",
                    "parallelism": "lists sharded over %d GPU(s)" % world, "base_sha_match": sha_ok,
                    "scanned_per_step": scanned, "exact_per_query": round(float(np.mean([s.exact for s in sts])) / nq, 2),

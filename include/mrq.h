@@ -105,6 +105,18 @@ int mrq_index_load(const char *build_file, const float *base, int64_t n, int32_t
                    const mrq_dist_cfg *dist, mrq_index **out);
 
 /*
+ * mrq_index_load with flags.  MRQ_LOAD_TAILS_HOST: the fp32 tail rows
+ * x_p[d:D] (read only by the exact re-rank of the few surviving candidates,
+ * Alg.2 L14 P:316) stay in pinned, device-mapped HOST memory instead of HBM --
+ * the memory-limited ("disk-based") setting of P:296 / SURVEY NEXT-4; codes,
+ * factors and heads stay in HBM.  Results are identical; tails are read over
+ * the host link.  Errors as mrq_index_load; MRQ_EINVAL for unknown flags.
+ */
+#define MRQ_LOAD_TAILS_HOST 1u
+int mrq_index_load_ex(const char *build_file, const float *base, int64_t n, int32_t D, int32_t d,
+                      const mrq_dist_cfg *dist, uint32_t flags, mrq_index **out);
+
+/*
  * Batched search with HOST buffers: queries row-major nq x D float32
  * (borrowed); out_ids (nq x K int64) and out_dist (nq x K float32) are
  * caller-owned.  Row i of the outputs belongs to query i; within a row the

@@ -288,7 +288,17 @@ static int load_impl(mrq_index *ix, const char *build_file, const float *base, i
     TRY(dalloc(ix, (void **)&ix->f3, (size_t)npad * 4));
     TRY(dalloc(ix, (void **)&ix->xr2, (size_t)npad * 4));
     TRY(dalloc(ix, (void **)&ix->heads, (size_t)npad * d * 4));
-    TRY(dalloc(ix, (void **)&ix->tails, (size_t)npad * std::max(D - d, 1) * 4));
+    if (ix->tails_host) {   // NEXT-4: tails in pinned host memory, read through the mapped device pointer
+        const size_t tb = (size_t)npad * std::max(D - d, 1) * 4;
+        if (cudaHostAlloc(&ix->tails_hbuf, tb, cudaHostAllocMapped) != cudaSuccess) {
+            ix->tails_hbuf = nullptr;
+            mrq_set_error("cudaHostAlloc(%zu) for host tails failed", tb);
+            return MRQ_ENOMEM;
+        }
+        MRQ_CUDA_TRY(cudaHostGetDevicePointer((void **)&ix->tails, ix->tails_hbuf, 0));
+    } else {
+        TRY(dalloc(ix, (void **)&ix->tails, (size_t)npad * std::max(D - d, 1) * 4));
+    }
     MRQ_CUDA_TRY(cudaMemsetAsync(ix->codes, 0, (size_t)W * npad * 4, ix->stream));
     MRQ_CUDA_TRY(cudaMemsetAsync(ix->f1, 0, (size_t)npad * 4, ix->stream));
     MRQ_CUDA_TRY(cudaMemsetAsync(ix->f2, 0, (size_t)npad * 4, ix->stream));
@@ -345,12 +355,23 @@ static int load_impl(mrq_index *ix, const char *build_file, const float *base, i
 extern "C" int mrq_index_load(const char *build_file, const float *base, int64_t n, int32_t D, int32_t d,
                               const mrq_dist_cfg *dist, mrq_index **out)
 {
+    return mrq_index_load_ex(build_file, base, n, D, d, dist, 0u, out);
+}
+
+extern "C" int mrq_index_load_ex(const char *build_file, const float *base, int64_t n, int32_t D, int32_t d,
+                                 const mrq_dist_cfg *dist, uint32_t flags, mrq_index **out)
+{
     if (!out) {
         mrq_set_error("NULL out");
         return MRQ_EINVAL;
     }
     *out = nullptr;
+    if (flags & ~MRQ_LOAD_TAILS_HOST) {
+        mrq_set_error("InvalidConfig: unknown load flags 0x%x", flags);
+        return MRQ_EINVAL;
+    }
     mrq_index *ix = new mrq_index();
+    ix->tails_host = (flags & MRQ_LOAD_TAILS_HOST) != 0;
     ix->g_key = new GraphKey();
     ix->g_pending = new GraphKey();
     memset(ix->g_key, 0, sizeof(GraphKey));
@@ -371,6 +392,7 @@ extern "C" void mrq_free(mrq_index *ix)
     if (ix->device >= 0) cudaSetDevice(ix->device);
     if (ix->stream) cudaStreamSynchronize(ix->stream);
     for (void *p : ix->owned) cudaFree(p);
+    if (ix->tails_hbuf) cudaFreeHost(ix->tails_hbuf);
     for (auto &kv : ix->scratch)
         if (kv.second.p) cudaFree(kv.second.p);
     mrq_probe_tc_free(ix);
@@ -528,6 +550,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
     memset(&sa, 0, sizeof sa);
     sa.nq = nq; sa.np = np; sa.K = K; sa.Kp = Kp; sa.D = D; sa.d = d; sa.mode = mode; sa.tight = tight;
     sa.aligned = (D % 4 == 0) && (d % 4 == 0);
+    sa.aligned_tails = sa.aligned && !ix->tails_host;   // host tails: direct loads over the link, no cp.async
     sa.npad = ix->npad; sa.isd = isd; sa.probe = probe; sa.list_off = ix->list_off; sa.list_size = ix->list_size;
     sa.ids = ix->ids; sa.codes = ix->codes; sa.planes = planes; sa.f1 = ix->f1; sa.f2 = ix->f2; sa.f3 = ix->f3;
     sa.heads = ix->heads; sa.tails = ix->tails; sa.xr2 = ix->xr2; sa.qconst = qconst; sa.qp = qp; sa.qr2 = qr2;

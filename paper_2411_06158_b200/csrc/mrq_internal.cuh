@@ -58,6 +58,8 @@ struct mrq_index {
     int force_cuda_core_probe = 0;             // mrq_debug_set("cuda_core_probe"): CUDA-core screen instead
     int force_probe_unfused = 0;               // mrq_debug_set("probe_unfused"): screen to HBM + k_probe_select_w
     int graphs = 1;                            // CUDA-graph replay of repeated searches (mrq_debug_set "graphs")
+    int tails_host = 0;                        // MRQ_LOAD_TAILS_HOST: tails in mapped pinned host memory
+    void *tails_hbuf = nullptr;                // its host allocation
     void *gexec = nullptr;                     // cudaGraphExec_t of the cached search
     void *g_key = nullptr, *g_pending = nullptr;   // GraphKey of the cached / last uncached search
     int sm_count = 148;

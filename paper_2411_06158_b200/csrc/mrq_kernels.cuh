@@ -23,7 +23,7 @@ __global__ void k_cand_count(const uint32_t *probe, int64_t nq, int np, const ui
 __global__ void k_exclusive_scan(const uint64_t *in, int64_t n, uint64_t *out);
 struct StageArgs {
     int64_t nq;
-    int np, K, Kp, D, d, mode, tight, aligned, seed_lists;
+    int np, K, Kp, D, d, mode, tight, aligned, seed_lists, aligned_tails;
     int64_t npad;
     double isd;
     const uint32_t *probe, *list_off, *list_size, *ids, *codes, *planes;

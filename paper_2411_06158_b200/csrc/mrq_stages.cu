@@ -25,7 +25,7 @@ __global__ void __launch_bounds__(256) k_seed_w(
     const uint32_t *__restrict__ planes, const double *__restrict__ qconst, const double *__restrict__ qp,
     const double *__restrict__ eps_r_arr, double isd, uint32_t *__restrict__ s0_cnt, uint32_t *__restrict__ s0_pos,
     double *__restrict__ s0_exact, double *__restrict__ tau0, const uint32_t *__restrict__ list_size_g,
-    uint32_t *__restrict__ s0_id, XItem *__restrict__ xout, int seed_lists)
+    uint32_t *__restrict__ s0_id, XItem *__restrict__ xout, int seed_lists, int aligned_t)
 {
     extern __shared__ unsigned char wsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(256) k_seed_w(
               });
     __syncwarp();
     if (D > d)
-        warp_rows(aligned, tails, D - d, 0, D - d, qrow + d, ns0, tile, [&](int e) { return s0_pos[q * Kp + e]; },
+        warp_rows(aligned_t, tails, D - d, 0, D - d, qrow + d, ns0, tile, [&](int e) { return s0_pos[q * Kp + e]; },
                   [&](int e, uint32_t) { return s0_exact[q * Kp + e]; }, [&](int e, bool v, double acc) {
                       if (v) s0_exact[q * Kp + e] = acc;
                   });
@@ -558,7 +558,7 @@ int launch_seed_w(int W, const StageArgs &a, cudaStream_t st)
                                                    a.list_size, a.ids, a.codes, a.f1, a.f2, a.f3, a.heads, a.tails, \
                                                    a.planes, a.qconst, a.qp, a.eps_r, a.isd, a.s0_cnt, a.s0_pos,    \
                                                    a.s0_exact, a.tau0, a.list_size_g, a.s0_id, a.xout,              \
-                                                   a.seed_lists);                                                   \
+                                                   a.seed_lists, a.aligned_tails);                                  \
     } while (0)
     switch (W) {
     case 1: MRQ_SEED(1); break;
@@ -590,7 +590,7 @@ int launch_stage2_w(const StageArgs &a, cudaStream_t st, cudaEvent_t after_gathe
     int rc = set_attr((const void *)k_stage2_w, smem);
     if (rc) return rc;
     k_stage2_w<<<(unsigned)((a.nq + wpb - 1) / wpb), wpb * 32, smem, st>>>(
-        a.nq, a.aligned, a.mode, a.tight, a.K, a.Kp, a.D, a.d, a.tails, a.qp, a.eps_r, a.tau0, a.f1_off, a.f1_cnt,
+        a.nq, a.aligned_tails, a.mode, a.tight, a.K, a.Kp, a.D, a.d, a.tails, a.qp, a.eps_r, a.tau0, a.f1_off, a.f1_cnt,
         a.f1_pos, a.f1_head, a.f1_diso, a.f1_id, a.s0_cnt, a.s0_id, a.s0_exact, a.s1_cnt, a.s1_pos, a.s1_id,
         a.s1_exact, a.tau1, a.f2_cnt, a.f2_pos, a.f2_head, a.xout);
     return MRQ_OK;
@@ -631,8 +631,8 @@ int launch_topk_w(const StageArgs &a, cudaStream_t st)
     if (rc) return rc;
     k_topk_w<<<(unsigned)((a.nq + wpb - 1) / wpb), wpb * 32, smem, st>>>(
         a.nq, a.K, a.Kp, a.ids, a.s0_cnt, a.s0_pos, a.s0_id, a.s0_exact, a.s1_cnt, a.s1_pos, a.s1_id, a.s1_exact,
-        a.f1_off, a.f2_cnt, a.f2_pos, a.f2_exact, a.out_ids, a.out_dist, a.exact_cnt, a.xout, a.aligned, a.D, a.d,
-        a.tails, a.qp, a.f2_head);
+        a.f1_off, a.f2_cnt, a.f2_pos, a.f2_exact, a.out_ids, a.out_dist, a.exact_cnt, a.xout, a.aligned_tails, a.D,
+        a.d, a.tails, a.qp, a.f2_head);
     return MRQ_OK;
 }
 

@@ -69,6 +69,9 @@ def lib():
             getattr(L, f).restype = C.c_int
         L.mrq_index_load.argtypes = [C.c_char_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p,
                                      C.POINTER(C.c_void_p)]
+        L.mrq_index_load_ex.restype = C.c_int
+        L.mrq_index_load_ex.argtypes = [C.c_char_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p,
+                                        C.c_uint32, C.POINTER(C.c_void_p)]
         L.mrq_search_batch.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(SearchParams), C.c_void_p,
                                        C.c_void_p, C.c_void_p]
         L.mrq_search_batch_device.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(SearchParams),
@@ -121,8 +124,11 @@ def host_allgather_callback(fn):
     return ALLGATHER_FN(cb)
 
 
+MRQ_LOAD_TAILS_HOST = 1
+
+
 def mrq_index_load(build_file: str, base: np.ndarray, d: int, rank=0, world=1, device=-1, nccl_unique_id=None,
-                   host_allgather=None):
+                   host_allgather=None, tails_host=False):
     """host_allgather: optional python callable send_bytes -> all ranks' bytes
     (rank-major), used in place of NCCL when nccl_unique_id is None."""
     base = np.ascontiguousarray(base, dtype=np.float32)
@@ -133,7 +139,8 @@ def mrq_index_load(build_file: str, base: np.ndarray, d: int, rank=0, world=1, d
         uid = C.create_string_buffer(bytes(nccl_unique_id), 128)
     cb = host_allgather_callback(host_allgather) if host_allgather is not None else ALLGATHER_FN()
     cfg = DistCfg(rank, world, device, C.cast(uid, C.c_void_p) if uid is not None else None, cb, None)
-    _check(lib().mrq_index_load(build_file.encode(), _ptr(base), n, D, d, C.byref(cfg), C.byref(h)))
+    flags = MRQ_LOAD_TAILS_HOST if tails_host else 0
+    _check(lib().mrq_index_load_ex(build_file.encode(), _ptr(base), n, D, d, C.byref(cfg), flags, C.byref(h)))
     if host_allgather is not None:
         _CALLBACKS[h.value] = cb
     return h
@@ -206,6 +213,7 @@ class Index:
     """Convenience owner of an mrq_index handle."""
 
     def __init__(self, build_file, base, d, **kw):
+        self.build_file = build_file
         self.h = mrq_index_load(build_file, base, d, **kw)
         self.info = mrq_index_info(self.h)
 

@@ -276,3 +276,18 @@ def test_graph_replay_identical(case):
             ids, dist, _ = m.mrq_search_batch(gx.h, Q, m.SearchParams.make(K=10, nprobe=npb, tau_schedule=tau),
                                               with_stats=False)
             assert np.array_equal(ids, ref[tau][0]) and np.array_equal(dist, ref[tau][1])
+
+
+def test_host_resident_tails_identical(case):
+    """MRQ_LOAD_TAILS_HOST (the memory-limited setting of P:296):
+    tails in mapped pinned host memory give the HBM-resident results bit for bit."""
+    m, gx, Q = case["m"], case["gx"], case["Q"]
+    gh = m.Index(gx.build_file, case["X"], case["d"], tails_host=True)
+    try:
+        for tau in ("TIGHT", "LOOSE"):
+            a = gx.search(Q, K=10, nprobe=case["nprobe"][-1], tau_schedule=tau)
+            b = gh.search(Q, K=10, nprobe=case["nprobe"][-1], tau_schedule=tau)
+            assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+            assert a[2].exact == b[2].exact and a[2].stage2_pass == b[2].stage2_pass
+    finally:
+        gh.close()
