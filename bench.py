@@ -38,6 +38,14 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
+def bf16_peak():
+    try:
+        with open(MEASURED) as f:
+            return float(json.load(f)["bf16_tflops"])
+    except Exception:
+        return 1590.0
+
+
 def peaks():
     try:
         with open(MEASURED) as f:
@@ -363,16 +371,31 @@ def main():
         "k_scan": {"unit": "scanned code", "bytes_per_unit": bcode, "units_per_launch": scanned, "ms": ms_scan},
         "k_head_b": {"unit": "F1 survivor", "bytes_per_unit": bhead, "units_per_launch": int(f1), "ms": ms_head},
     }
+    f2 = float(np.mean([s.stage2_pass for s in sts]))
+    D_ = int(X.shape[1])
+    kern["k_topk_w"] = {"unit": "F2 survivor (exact re-rank gather; the launch also selects the top-K)",
+                        "bytes_per_unit": 4 * (D_ - d) + 20, "units_per_launch": int(f2),
+                        "ms": float(np.mean([s.ms_topk for s in sts]))}
     for nm, kk in kern.items():
         kk["achieved_gbs"] = round(kk["bytes_per_unit"] * kk["units_per_launch"] / (kk["ms"] * 1e-3) / 1e9, 1)
         kk["frac"] = round(kk["achieved_gbs"] / hbm, 4)
         kk["ms"] = round(kk["ms"], 4)
         kk["traffic"] = traffic.get(nm)
     dom = max(kern, key=lambda n: kern[n]["ms"])
+    # the probe screen GEMM on the tensor cores (kind::tf32): its flops against
+    # the tf32 peak = measured bf16 burst x the nominal tf32/bf16 ratio (1.1/2.25)
+    ms_gemm = float(np.mean([s.ms_probe_gemm for s in sts]))
+    gemm_tf = 2.0 * nq * hdr["k"] * d / (ms_gemm * 1e-3) / 1e12
+    tf32_peak = bf16_peak() * (1.1 / 2.25)
+    probe_tc = {"bound": "tensor", "kernel": "k_probe_tc (+ fused top-np selection epilogue)",
+                "flops_per_launch": 2.0 * nq * hdr["k"] * d, "ms": round(ms_gemm, 4),
+                "achieved_tflops": round(gemm_tf, 1), "peak_tflops_tf32": round(tf32_peak, 1),
+                "frac": round(gemm_tf / tf32_peak, 4),
+                "note": "selection-bound epilogue; the MMAs themselves are a few us"}
     achieved = kern[dom]["achieved_gbs"]
     stage_ms = {k: round(float(np.mean([getattr(s, k) for s in sts])), 4)
-                for k in ("ms_qprep", "ms_probe", "ms_quant", "ms_seed", "ms_scan", "ms_stage2", "ms_head",
-                          "ms_rerank", "ms_topk", "ms_comm")}
+                for k in ("ms_qprep", "ms_probe", "ms_probe_gemm", "ms_quant", "ms_seed", "ms_scan", "ms_stage2",
+                          "ms_head", "ms_rerank", "ms_topk", "ms_comm")}
 
     # e2e through the host-buffer call (pinned host queries; H2D + D2H inside the timed region)
     hq = torch.from_numpy(Q).pin_memory().numpy()
@@ -430,7 +453,7 @@ def main():
                      "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": kern[dom]["traffic"],
                      "bytes_per_unit": kern[dom]["bytes_per_unit"], "unit_kind": kern[dom]["unit"],
                      "kernels": kern, "codes_per_s_per_gpu": round(scanned / (ms_scan * 1e-3), 1),
-                     "scan_frac_of_hbm": kern["k_scan"]["frac"]},
+                     "scan_frac_of_hbm": kern["k_scan"]["frac"], "probe_gemm": probe_tc},
         "e2e": {"value": round(nq / e2e_s, 1), "unit": "queries/s", "h2d_bytes_per_step": int(nq * X.shape[1] * 4),
                 "d2h_bytes_per_step": int(nq * K * 12)},
         "gpu_launches": launches_per_step * args.steps,

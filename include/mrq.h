@@ -89,6 +89,7 @@ typedef struct {
     uint64_t seeds;        /* |S0| + |S1|                                        */
     double ms_total, ms_qprep, ms_probe, ms_quant, ms_seed, ms_scan, ms_stage2, ms_rerank, ms_topk, ms_comm;
     double ms_head;        /* the stage-2 head gather alone (part of ms_stage2)  */
+    double ms_probe_gemm;  /* the probe screen GEMM alone (part of ms_probe)     */
 } mrq_stats;
 
 /*
@@ -152,6 +153,31 @@ int mrq_nccl_unique_id(void *out, size_t bytes);
  * [0, world).  Errors: MRQ_EINVAL (NULL, k < 1, world < 1).
  */
 int mrq_shard_plan(const uint32_t *sizes, int32_t k, int32_t world, uint32_t *owner);
+
+/*
+ * GPU index build (Algorithm 1 L1-L6, plus the
+ * quantizer rotation P_r): PCA of a strided sample of <= pca_sample
+ * rows, heads x_d = P[0:d](x - mu), IVF* k-means on a strided sample of
+ * <= km_sample_per_k * k heads (<= km_iters Lloyd iterations), final
+ * assignment of all n, Haar rotation from `seed`; written to out_path as an
+ * MRQBLD01 build file (format below) that mrq_index_load reads.
+ * base: HOST n x D float32 (borrowed); base_sha256_hex: the 64-character hex
+ * SHA-256 of the base bytes to record in the header (NULL: zeros).  Same
+ * algorithm as the oracle's build, not the same bits (strided samples, other
+ * solvers): the contract is recall-equivalence.  times_ms (nullable, 4
+ * doubles): PCA, k-means, final assignment, total.
+ * Errors: MRQ_EINVAL, MRQ_EDEGENERATE (zero variance), MRQ_ENOMEM, MRQ_ECUDA,
+ * MRQ_EIO (cannot write).
+ */
+typedef struct {
+    int32_t k;               /* IVF clusters                          */
+    int32_t pca_sample;      /* PCA sample rows (e.g. 100000)         */
+    int32_t km_sample_per_k; /* k-means sample = this x k rows (64)   */
+    int32_t km_iters;        /* Lloyd iterations (25)                 */
+    uint64_t seed;           /* P_r seed (7)                          */
+} mrq_build_params;
+int mrq_build_gpu(const float *base, int64_t n, int32_t D, int32_t d, const mrq_build_params *bp,
+                  const char *base_sha256_hex, int32_t device, const char *out_path, double *times_ms);
 
 /* Free the index (NULL-safe): device memory, streams, NCCL communicator. */
 void mrq_free(mrq_index *idx);

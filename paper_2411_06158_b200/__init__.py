@@ -8,5 +8,5 @@ any call raises if libmrq.so is missing or no GPU is present.
 from .mrq import (  # noqa: F401
     MRQ_MODES, MRQError, SearchParams, Stats, lib, mrq_debug_fetch, mrq_debug_set, mrq_free, mrq_index_info, mrq_index_load,
     mrq_last_error, mrq_search_batch, mrq_search_batch_device, Index, mrq_nccl_unique_id, nccl_unique_id,
-    mrq_shard_plan,
+    mrq_shard_plan, mrq_build_gpu, BuildParams,
 )

@@ -499,6 +499,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
             SCR("probe_kv", float, (size_t)nq * P * 16, kvbuf);
             const double kappa = mrq_probe_tc_kappa(ix);
             TRY(mrq_probe_tc_run_fused(ix, qd32, nq, np, qnorm, kappa, cbuf, capp, ccnt, kvbuf, st));
+            if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[11], st));
             TRY(launch_probe_finish_w(nq, k, d, np, qp, D, ix->C, qnorm, ix->cmax, kappa, cbuf, P, capp,
                                       mrq_probe_tc_grid(ix, nq), ccnt, kvbuf, cand, probe, probe_qn2, ncand, st));
         } else {
@@ -512,6 +513,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
                 k_probe_approx<<<grid, 256, 8 * d * sizeof(float), st>>>(qd32, nq, d, k, ix->C32T, approx);
                 kappa = std::ldexp(1.0, -24) * (2.0 * d + 8.0);
             }
+            if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[11], st));
             TRY(launch_probe_select_w(approx, nq, k, d, np, qp, D, ix->C, qnorm, ix->cmax, kappa, cand, probe,
                                       probe_qn2, ncand, st));
         }
@@ -656,6 +658,9 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
         float mh = 0.f;
         MRQ_CUDA_TRY(cudaEventElapsedTime(&mh, ix->ev[5], ix->ev[10]));
         stats->ms_head = mh;
+        float mg = 0.f;
+        MRQ_CUDA_TRY(cudaEventElapsedTime(&mg, ix->ev[1], ix->ev[11]));
+        stats->ms_probe_gemm = mg;
         std::vector<uint32_t> h(nq);
         auto sum32 = [&](const uint32_t *dv) -> uint64_t {
             if (cudaMemcpy(h.data(), dv, nq * 4, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;

@@ -47,7 +47,8 @@ class SearchParams(C.Structure):
 class Stats(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in ("scanned", "stage1_pass", "stage2_pass", "exact", "seeds")] + \
                [(n, C.c_double) for n in ("ms_total", "ms_qprep", "ms_probe", "ms_quant", "ms_seed", "ms_scan",
-                                          "ms_stage2", "ms_rerank", "ms_topk", "ms_comm", "ms_head")]
+                                          "ms_stage2", "ms_rerank", "ms_topk", "ms_comm", "ms_head",
+                                          "ms_probe_gemm")]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
@@ -144,6 +145,29 @@ def mrq_index_load(build_file: str, base: np.ndarray, d: int, rank=0, world=1, d
     if host_allgather is not None:
         _CALLBACKS[h.value] = cb
     return h
+
+
+class BuildParams(C.Structure):
+    _fields_ = [("k", C.c_int32), ("pca_sample", C.c_int32), ("km_sample_per_k", C.c_int32),
+                ("km_iters", C.c_int32), ("seed", C.c_uint64)]
+
+
+def mrq_build_gpu(base: np.ndarray, d: int, k: int, out_path: str, pca_sample=100_000, km_sample_per_k=64,
+                  km_iters=25, seed=7, device=-1):
+    """GPU index build -> MRQBLD01 file; returns the phase
+    times in ms (PCA, k-means, final assignment, total)."""
+    import hashlib
+    base = np.ascontiguousarray(base, dtype=np.float32)
+    n, D = base.shape
+    sha = hashlib.sha256(base.tobytes()).hexdigest().encode()
+    bp = BuildParams(k, pca_sample, km_sample_per_k, km_iters, seed)
+    t = (C.c_double * 4)()
+    L = lib()
+    L.mrq_build_gpu.restype = C.c_int
+    L.mrq_build_gpu.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.POINTER(BuildParams), C.c_char_p,
+                                C.c_int32, C.c_char_p, C.c_void_p]
+    _check(L.mrq_build_gpu(_ptr(base), n, D, d, C.byref(bp), sha, device, out_path.encode(), t))
+    return {"pca_ms": t[0], "kmeans_ms": t[1], "assign_ms": t[2], "total_ms": t[3]}
 
 
 def mrq_nccl_unique_id() -> bytes:
