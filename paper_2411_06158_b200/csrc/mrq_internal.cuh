@@ -577,21 +577,46 @@ __device__ __forceinline__ int csa_weighted_popc(const uint32_t (&x)[NB][W])
 //   ip = ((A pop + Bc S) - C0) / sqrt(d)        = <x_hat, r_bar>
 //   dis' = (f1 + g1) - 2 (f2 ip)
 //   LB1 = (dis' - eb f3) - eps_r
+// Hand-written networks for W = 1 and 2 (the compiler's unrolling of the
+// generic one leaves register moves): W = 2 is a half adder at weight 1 and
+// full adders at weights 2, 4, 8 -> 5 POPCs for S.
+__device__ __forceinline__ int csa_S_w2(uint32_t c0, uint32_t c1, const uint32_t *pl)
+{
+    const uint32_t a0 = c0 & pl[0], b0 = c1 & pl[1];
+    const uint32_t a1 = c0 & pl[2], b1 = c1 & pl[3];
+    const uint32_t a2 = c0 & pl[4], b2 = c1 & pl[5];
+    const uint32_t a3 = c0 & pl[6], b3 = c1 & pl[7];
+    const uint32_t s0 = a0 ^ b0, k1 = a0 & b0;
+    const uint32_t s1 = lop_xor3(k1, a1, b1), k2 = lop_maj(k1, a1, b1);
+    const uint32_t s2 = lop_xor3(k2, a2, b2), k3 = lop_maj(k2, a2, b2);
+    const uint32_t s3 = lop_xor3(k3, a3, b3), k4 = lop_maj(k3, a3, b3);
+    return __popc(s0) + (__popc(s1) << 1) + (__popc(s2) << 2) + (__popc(s3) << 3) + (__popc(k4) << 4);
+}
+
 template <int W>
 __device__ __forceinline__ double mrq_lb1(const uint32_t *code, const uint32_t *pl, const double *qc, double isd,
                                           double eps_r, float f1, float f2, float f3, double *dis_out)
 {
-    uint32_t cw[1][W];
+    int pop, S;
+    if (W == 1) {
+        pop = __popc(code[0]);
+        S = __popc(code[0] & pl[0]) + (__popc(code[0] & pl[1]) << 1) + (__popc(code[0] & pl[2]) << 2) +
+            (__popc(code[0] & pl[3]) << 3);
+    } else if (W == 2) {
+        pop = __popc(code[0]) + __popc(code[W - 1]);
+        S = csa_S_w2(code[0], code[W - 1], pl);
+    } else {
+        uint32_t cw[1][W];
 #pragma unroll
-    for (int w = 0; w < W; w++) cw[0][w] = code[w];
-    const int pop = W <= 2 ? (W == 1 ? __popc(code[0]) : __popc(code[0]) + __popc(code[W - 1]))
-                           : csa_weighted_popc<1, W>(cw);
-    uint32_t x[MRQ_BQ][W];
+        for (int w = 0; w < W; w++) cw[0][w] = code[w];
+        pop = csa_weighted_popc<1, W>(cw);
+        uint32_t x[MRQ_BQ][W];
 #pragma unroll
-    for (int b = 0; b < MRQ_BQ; b++)
+        for (int b = 0; b < MRQ_BQ; b++)
 #pragma unroll
-        for (int w = 0; w < W; w++) x[b][w] = code[w] & pl[b * W + w];
-    const int S = csa_weighted_popc<MRQ_BQ, W>(x);
+            for (int w = 0; w < W; w++) x[b][w] = code[w] & pl[b * W + w];
+        S = csa_weighted_popc<MRQ_BQ, W>(x);
+    }
     const double t1 = qc[0] * (double)pop;
     const double t2 = qc[1] * (double)S;
     const double t4 = (t1 + t2) - qc[2];

@@ -186,11 +186,15 @@ def mrq_shard_plan(sizes, world: int) -> np.ndarray:
     return owner
 
 
-def mrq_search_batch(h, queries: np.ndarray, params: SearchParams, with_stats=True):
+def mrq_search_batch(h, queries: np.ndarray, params: SearchParams, with_stats=True, out_ids=None, out_dist=None):
+    """Host buffers in and out; out_ids/out_dist (nq x K int64 / float32,
+    e.g. pinned) are filled in place when given."""
     q = np.ascontiguousarray(queries, dtype=np.float32)
     nq = q.shape[0]
-    ids = np.empty((nq, params.K), np.int64)
-    dist = np.empty((nq, params.K), np.float32)
+    ids = out_ids if out_ids is not None else np.empty((nq, params.K), np.int64)
+    dist = out_dist if out_dist is not None else np.empty((nq, params.K), np.float32)
+    assert ids.shape == (nq, params.K) and ids.dtype == np.int64 and ids.flags.c_contiguous
+    assert dist.shape == (nq, params.K) and dist.dtype == np.float32 and dist.flags.c_contiguous
     st = Stats()
     _check(lib().mrq_search_batch(h, _ptr(q), nq, C.byref(params), _ptr(ids), _ptr(dist),
                                   C.byref(st) if with_stats else None))
