@@ -407,6 +407,10 @@ struct WarpTopBitonic {
 };
 
 #define MRQ_SELQ 64   // items of a WarpSel compaction queue
+// per-warp selection region for a list of L: list, queue, merge temp
+// lists longer than this use the merge selection (shorter: smem insertion)
+#define MRQ_MERGE_MIN 64
+#define MRQ_SELREG(L) ((L) + MRQ_SELQ + ((L) > MRQ_MERGE_MIN ? (L) + 32 : 0))
 
 // The L-th smallest (L <= 32) of the 32 lane values v (bitonic sort across
 // lanes).  Used as a selection pre-threshold: if every lane's v is the
@@ -431,25 +435,129 @@ __device__ __forceinline__ double warp_kth_smallest(double v, int L)
 // Selection of the L smallest distinct (key, id): registers for L <= 32,
 // the shared-memory list otherwise.  After finish() the sorted items are in
 // buf[0 .. L) either way.
-struct WarpSel {
+// Merge selection for 32 < L: the sorted list a[0..L) lives in shared
+// memory; a batch of up to 32 queued items is sorted across the lanes
+// (bitonic), every list item's and batch item's position in the merged order
+// is found by binary search (list items first on ties, so a repeated item
+// lands next to its first copy), the merge is written to t[0..L+32) and
+// compacted back into a[] dropping repeats -- a few hundred instructions per
+// 32 items instead of an O(L) insertion per item.
+struct WarpTopMerge {
+    __device__ __forceinline__ static bool le(const SelItem &x, const SelItem &y) { return !sel_less(y, x); }
+    __device__ __forceinline__ static void init(SelItem *a, int L)
+    {
+        const int lane = threadIdx.x & 31;
+        for (int i = lane; i < L; i += 32) a[i] = sel_inf();
+        __syncwarp();
+    }
+    __device__ __forceinline__ static void merge(SelItem *a, SelItem *t, int L, SelItem x, bool valid)
+    {
+        const int lane = threadIdx.x & 31;
+        if (!valid) x = sel_inf();
+        // sort the batch ascending across lanes
+#pragma unroll
+        for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                const bool up = (lane & k) == 0;
+                const bool lower = (lane & j) == 0;
+                WarpTopBitonic::cx(x.key, x.id, x.pay, j, lower == up);
+            }
+        }
+        __syncwarp();
+        // list items: pos = i + #{batch items < a_i} (warp-uniform trip count:
+        // every lane takes part in every shuffle)
+        for (int i0 = 0; i0 < L; i0 += 32) {
+            const int i = i0 + lane;
+            const bool in = i < L;
+            const SelItem e = in ? a[i] : sel_inf();
+            int lo = 0;   // number of batch items strictly less than e (batch sorted)
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const int probe = lo + step - 1;
+                // warp-divergent source lanes: every lane participates in each shuffle
+                const double pk = __shfl_sync(0xffffffffu, x.key, probe);
+                const uint32_t pi = __shfl_sync(0xffffffffu, x.id, probe);
+                SelItem pv;
+                pv.key = pk;
+                pv.id = pi;
+                if (sel_less(pv, e)) lo += step;
+            }
+            {
+                const double pk = __shfl_sync(0xffffffffu, x.key, lo < 32 ? lo : 31);
+                const uint32_t pi = __shfl_sync(0xffffffffu, x.id, lo < 32 ? lo : 31);
+                SelItem pv;
+                pv.key = pk;
+                pv.id = pi;
+                if (lo < 32 && sel_less(pv, e)) lo++;
+            }
+            if (in) t[i + lo] = e;
+        }
+        // batch items: pos = lane + #{list items <= x}
+        int lo = 0, hi = L;   // first index with a[idx] > x
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (le(a[mid], x))
+                lo = mid + 1;
+            else
+                hi = mid;
+        }
+        t[lane + lo] = x;
+        __syncwarp();
+        // compact t[0..L+32) into a[0..L), dropping repeats of the previous item
+        int out = 0;
+        for (int i0 = 0; i0 < L + 32 && out < L; i0 += 32) {
+            const int i = i0 + lane;
+            SelItem v = sel_inf();
+            bool keep = false;
+            if (i < L + 32) {
+                v = t[i];
+                keep = v.id != 0xFFFFFFFFu;
+                if (keep && i > 0) {
+                    const SelItem p = t[i - 1];
+                    keep = !(p.key == v.key && p.id == v.id);
+                }
+            }
+            const unsigned bal = __ballot_sync(0xffffffffu, keep);
+            const int o = out + __popc(bal & ((1u << lane) - 1u));
+            __syncwarp();
+            if (keep && o < L) a[o] = v;
+            out += __popc(bal);
+        }
+        __syncwarp();
+        for (int i = (out < L ? out : L) + lane; i < L; i += 32) a[i] = sel_inf();
+        __syncwarp();
+    }
+};
+
+// MG: the merge selection (mode 3) is compiled in; kernels instantiate it
+// only for lists longer than MRQ_MERGE_MIN, so the short-list instances keep
+// their register budget.
+template <bool MG = false>
+struct WarpSelT {
     WarpTop sm;
     WarpTopReg rg;
     WarpTopBitonic bt;
-    SelItem *qbuf;   // mode 2: compaction queue of MRQ_SELQ items
+    SelItem *qbuf;   // modes 2, 3: compaction queue of MRQ_SELQ items
     int qn;
-    int mode;        // 0 shared-memory list, 1 register insertion (dedup), 2 register bitonic (distinct items)
+    int mode;        // 0 shared-memory list, 1 register insertion (dedup), 2 register bitonic (distinct items),
+                     // 3 shared-memory merge (L > 32, dedup)
 
     // distinct: the caller guarantees no (key, id) is offered twice; then
     // qbuf (MRQ_SELQ items of shared memory) queues the items that pass the
     // current threshold and full batches of 32 go through one bitonic merge.
+    // L > MRQ_MERGE_MIN with a queue: merge selection, its temp (L + 32
+    // items) right after the queue (the MRQ_SELREG layout).
     __device__ __forceinline__ void init(SelItem *buf, int L, bool distinct = false, SelItem *queue = nullptr)
     {
-        mode = L > 32 ? 0 : (distinct && queue ? 2 : 1);
+        mode = L > 32 ? (MG && queue && L > MRQ_MERGE_MIN ? 3 : 0) : (distinct && queue ? 2 : 1);
         sm.a = buf;
         sm.L = L;
         qbuf = queue;
         qn = 0;
-        if (mode == 2)
+        if (mode == 3)
+            WarpTopMerge::init(buf, L);
+        else if (mode == 2)
             bt.init(L);
         else if (mode == 1)
             rg.init(L);
@@ -463,14 +571,25 @@ struct WarpSel {
         SelItem x = sel_inf();
         if (lane < n) x = qbuf[lane];
         __syncwarp();
-        bt.offer(x, lane < n);
+        if (mode == 3)
+            WarpTopMerge::merge(sm.a, qbuf + MRQ_SELQ, sm.L, x, lane < n);
+        else
+            bt.offer(x, lane < n);
     }
     __device__ __forceinline__ void offer(const SelItem &it, bool valid)
     {
-        if (mode == 2) {
+        if (mode == 2 || mode == 3) {
             const int lane = threadIdx.x & 31;
-            const double tk = __shfl_sync(0xffffffffu, bt.key, bt.L - 1);
-            const uint32_t ti = __shfl_sync(0xffffffffu, bt.id, bt.L - 1);
+            double tk;
+            uint32_t ti;
+            if (mode == 2) {
+                tk = __shfl_sync(0xffffffffu, bt.key, bt.L - 1);
+                ti = __shfl_sync(0xffffffffu, bt.id, bt.L - 1);
+            } else {
+                const SelItem th = sm.a[sm.L - 1];
+                tk = th.key;
+                ti = th.id;
+            }
             const bool pass = valid && WarpTopBitonic::lt(it.key, it.id, tk, ti);
             const unsigned m = __ballot_sync(0xffffffffu, pass);
             if (!m) return;
@@ -494,11 +613,11 @@ struct WarpSel {
     }
     __device__ __forceinline__ void finish()
     {
-        if (mode == 2 && qn > 0) {
+        if ((mode == 2 || mode == 3) && qn > 0) {
             flush(qn);
             qn = 0;
         }
-        if (mode != 0) {
+        if (mode == 1 || mode == 2) {
             const int lane = threadIdx.x & 31;
             __syncwarp();
             if (lane < sm.L) {
@@ -511,7 +630,8 @@ struct WarpSel {
         }
         __syncwarp();
     }
-};
+};using WarpSel = WarpSelT<false>;
+
 
 // ================================================================ a4 / a5
 // Weighted population counts with carry-save adders.  words[l] holds the

@@ -16,7 +16,7 @@
 // hold >= K' candidates and number >= seed_lists form the pool; S0 = the K' smallest (dis', id) of the
 // pool; exact distances ||x_p - q_p||^2 (Alg.2 L14 P:316) of S0; tau0 = K-th
 // smallest exact over S0 (+inf if |S0| < K).
-template <int W>
+template <int W, bool MG>
 __global__ void __launch_bounds__(256) k_seed_w(
     int64_t nq, int aligned, const uint32_t *__restrict__ probe, int np, int K, int Kp, int D, int d, int64_t npad,
     const uint32_t *__restrict__ list_off, const uint32_t *__restrict__ list_size, const uint32_t *__restrict__ ids,
@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(256) k_seed_w(
     const int64_t q = (int64_t)blockIdx.x * wpb + warp;
     if (q >= nq) return;
     float *tile = (float *)wsm + warp * MRQ_RG_FLOATS;
-    SelItem *lst = (SelItem *)((float *)wsm + wpb * MRQ_RG_FLOATS) + (size_t)warp * (Kp + MRQ_SELQ);
+    SelItem *lst = (SelItem *)((float *)wsm + wpb * MRQ_RG_FLOATS) + (size_t)warp * MRQ_SELREG(Kp);
     SelItem *queue = lst + Kp;
     const double eps_r = eps_r_arr[q];
     const double *qrow = qp + q * D;
@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(256) k_seed_w(
             nloc += (int)sz;
         }
     };
-    WarpSel top;
+    WarpSelT<MG> top;
     top.init(lst, Kp);
     // one pass: items below the running K'-th smallest are queued and merged
     // 32 at a time (bitonic) for K' <= 32; the shared-memory list otherwise
@@ -200,6 +200,7 @@ __global__ void __launch_bounds__(256) k_head_b(
 // tau1 = K-th smallest distinct exact over S0 u S1; LOOSE: tau1 = tau0.
 // F2 as in f2_compact.  Sharded TIGHT (xout != NULL): the local S1 goes to
 // the exchange and k_xmerge / k_f2_w finish tau1 and F2.
+template <bool MG>
 __global__ void __launch_bounds__(256) k_stage2_w(
     int64_t nq, int aligned, int mode, int tight, int K, int Kp, int D, int d, const float *__restrict__ tails,
     const double *__restrict__ qp, const double *__restrict__ eps_r_arr, const double *__restrict__ tau0_arr,
@@ -215,7 +216,7 @@ __global__ void __launch_bounds__(256) k_stage2_w(
     const int64_t q = (int64_t)blockIdx.x * wpb + warp;
     if (q >= nq) return;
     float *tile = (float *)wsm + warp * MRQ_RG_FLOATS;
-    SelItem *lst = (SelItem *)((float *)wsm + wpb * MRQ_RG_FLOATS) + (size_t)warp * (Kp + MRQ_SELQ);
+    SelItem *lst = (SelItem *)((float *)wsm + wpb * MRQ_RG_FLOATS) + (size_t)warp * MRQ_SELREG(Kp);
     SelItem *queue = lst + Kp;
     const bool sel1 = mode == 0 && tight;
     const uint64_t base = f1_off[q];
@@ -224,7 +225,7 @@ __global__ void __launch_bounds__(256) k_stage2_w(
     const double *qrow = qp + q * D;
     double tau1 = tau0_arr[q];
     if (sel1) {
-        WarpSel top;
+        WarpSelT<MG> top;
         top.init(lst, Kp);
         // each(it, valid) over F1: (dis_o', id, entry), 128 entries per round
         auto scan_f1 = [&](auto each) {
@@ -259,6 +260,7 @@ __global__ void __launch_bounds__(256) k_stage2_w(
             top.init(lst, Kp, true, queue);
             scan_f1([&](const SelItem &it, bool v) { top.offer(it, v && it.key <= U); });
         } else {
+            top.init(lst, Kp, true, queue);
             scan_f1([&](const SelItem &it, bool v) { top.offer(it, v); });
         }
         top.finish();
@@ -290,7 +292,7 @@ __global__ void __launch_bounds__(256) k_stage2_w(
             return;
         }
         // tau1 = K-th smallest distinct exact over S0 u S1 (duplicates dropped by the selection)
-        top.init(lst, K);
+        top.init(lst, K, false, queue);
         const int ns0 = (int)s0_cnt[q];
         for (int g = 0; g < ns0 + ns1; g += 32) {
             const int e = g + lane;
@@ -339,6 +341,7 @@ __global__ void __launch_bounds__(256) k_f2_w(int64_t nq, int mode, const double
 // distances rounded to fp32, padding id -1 / +inf.  Sharded (xout != NULL):
 // the local top-K (exact fp64, id) goes to the exchange and k_xmerge writes
 // the outputs.
+template <bool MG>
 __global__ void __launch_bounds__(256) k_topk_w(
     int64_t nq, int K, int Kp, const uint32_t *__restrict__ ids, const uint32_t *__restrict__ s0_cnt,
     const uint32_t *__restrict__ s0_pos, const uint32_t *__restrict__ s0_id, const double *__restrict__ s0_exact,
@@ -353,7 +356,8 @@ __global__ void __launch_bounds__(256) k_topk_w(
     const int64_t q = (int64_t)blockIdx.x * wpb + warp;
     if (q >= nq) return;
     float *tile = (float *)wsm + warp * MRQ_RG_FLOATS;
-    SelItem *lst = (SelItem *)((float *)wsm + wpb * MRQ_RG_FLOATS) + (size_t)warp * K;
+    SelItem *lst = (SelItem *)((float *)wsm + wpb * MRQ_RG_FLOATS) + (size_t)warp * MRQ_SELREG(K);
+    SelItem *queue = lst + K;
     const int ns0 = (int)s0_cnt[q], ns1 = (int)s1_cnt[q], n2 = (int)f2_cnt[q];
     const uint64_t base = f1_off[q];
     // a7 exact re-rank of F2 (Alg.2 L14 P:316): exact = HEAD continued over
@@ -366,8 +370,8 @@ __global__ void __launch_bounds__(256) k_topk_w(
     else
         for (int e = lane; e < n2; e += 32) f2_exact[base + e] = f2_head[base + e];
     __syncwarp();
-    WarpSel top;
-    top.init(lst, K);
+    WarpSelT<MG> top;
+    top.init(lst, K, false, queue);
     const int n = ns0 + ns1 + n2;
     for (int g = 0; g < n; g += 32) {
         const int e = g + lane;
@@ -443,6 +447,7 @@ __global__ void __launch_bounds__(256) k_topk_w(
 //                    distinct exact over S0 u S1
 //   kind 2 (final):  top-K (key = exact) -> out_ids / out_dist
 // Slots of items that came from another rank become PAD.
+template <bool MG>
 __global__ void __launch_bounds__(128) k_xmerge(int kind, int64_t nq, int world, int rank, int L, int K, int Kp,
                                                 const XItem *__restrict__ recv, uint32_t *__restrict__ s_cnt,
                                                 uint32_t *__restrict__ s_pos, uint32_t *__restrict__ s_id,
@@ -455,9 +460,9 @@ __global__ void __launch_bounds__(128) k_xmerge(int kind, int64_t nq, int world,
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
     const int64_t q = (int64_t)blockIdx.x * wpb + warp;
     if (q >= nq) return;
-    SelItem *lst = (SelItem *)wsm + (size_t)warp * (L + MRQ_SELQ);
+    SelItem *lst = (SelItem *)wsm + (size_t)warp * MRQ_SELREG(L);
     SelItem *queue = lst + L;
-    WarpSel top;
+    WarpSelT<MG> top;
     top.init(lst, L, true, queue);
     for (int r = 0; r < world; r++) {
         const XItem *src = recv + ((int64_t)r * nq + q) * L;
@@ -503,7 +508,7 @@ __global__ void __launch_bounds__(128) k_xmerge(int kind, int64_t nq, int world,
     }
     __syncwarp();
     // tau = K-th smallest distinct exact over S0 (kind 0) or S0 u S1 (kind 1)
-    top.init(lst, K);
+    top.init(lst, K, false, queue);
     const int n0 = kind == 1 ? (int)s0_cnt[q] : 0;
     for (int g = 0; g < n0 + n; g += 32) {
         const int e = g + lane;
@@ -546,15 +551,17 @@ static int set_attr(const void *fn, size_t smem)
 
 int launch_seed_w(int W, const StageArgs &a, cudaStream_t st)
 {
-    const size_t per = MRQ_RG_FLOATS * 4 + (size_t)(a.Kp + MRQ_SELQ) * sizeof(SelItem);
+    const size_t per = MRQ_RG_FLOATS * 4 + (size_t)MRQ_SELREG(a.Kp) * sizeof(SelItem);
     const int wpb = warps_for(per);
     const size_t smem = per * wpb;
     const unsigned grid = (unsigned)((a.nq + wpb - 1) / wpb);
+    const bool mg = a.Kp > MRQ_MERGE_MIN;
 #define MRQ_SEED(WW)                                                                                                \
     do {                                                                                                            \
-        int rc = set_attr((const void *)k_seed_w<WW>, smem);                                                        \
+        auto fn = mg ? k_seed_w<WW, true> : k_seed_w<WW, false>;                                                    \
+        int rc = set_attr((const void *)fn, smem);                                                                  \
         if (rc) return rc;                                                                                          \
-        k_seed_w<WW><<<grid, wpb * 32, smem, st>>>(a.nq, a.aligned, a.probe, a.np, a.K, a.Kp, a.D, a.d, a.npad, a.list_off,   \
+        fn<<<grid, wpb * 32, smem, st>>>(a.nq, a.aligned, a.probe, a.np, a.K, a.Kp, a.D, a.d, a.npad, a.list_off,   \
                                                    a.list_size, a.ids, a.codes, a.f1, a.f2, a.f3, a.heads, a.tails, \
                                                    a.planes, a.qconst, a.qp, a.eps_r, a.isd, a.s0_cnt, a.s0_pos,    \
                                                    a.s0_exact, a.tau0, a.list_size_g, a.s0_id, a.xout,              \
@@ -584,12 +591,13 @@ int launch_stage2_w(const StageArgs &a, cudaStream_t st, cudaEvent_t after_gathe
                                                           a.f1_off, a.f1_cnt, a.f1_pos, a.f1_head, a.f1_diso, a.f1_id);
     }
     if (after_gather) MRQ_CUDA_TRY(cudaEventRecord(after_gather, st));
-    const size_t per = MRQ_RG_FLOATS * 4 + (size_t)(std::max(a.Kp, a.K) + MRQ_SELQ) * sizeof(SelItem);
+    const size_t per = MRQ_RG_FLOATS * 4 + (size_t)MRQ_SELREG(std::max(a.Kp, a.K)) * sizeof(SelItem);
     const int wpb = warps_for(per);
     const size_t smem = per * wpb;
-    int rc = set_attr((const void *)k_stage2_w, smem);
+    auto fn = std::max(a.Kp, a.K) > MRQ_MERGE_MIN ? k_stage2_w<true> : k_stage2_w<false>;
+    int rc = set_attr((const void *)fn, smem);
     if (rc) return rc;
-    k_stage2_w<<<(unsigned)((a.nq + wpb - 1) / wpb), wpb * 32, smem, st>>>(
+    fn<<<(unsigned)((a.nq + wpb - 1) / wpb), wpb * 32, smem, st>>>(
         a.nq, a.aligned_tails, a.mode, a.tight, a.K, a.Kp, a.D, a.d, a.tails, a.qp, a.eps_r, a.tau0, a.f1_off, a.f1_cnt,
         a.f1_pos, a.f1_head, a.f1_diso, a.f1_id, a.s0_cnt, a.s0_id, a.s0_exact, a.s1_cnt, a.s1_pos, a.s1_id,
         a.s1_exact, a.tau1, a.f2_cnt, a.f2_pos, a.f2_head, a.xout);
@@ -606,17 +614,18 @@ int launch_f2_w(const StageArgs &a, cudaStream_t st)
 int launch_xmerge(int kind, const StageArgs &a, int world, int rank, const XItem *recv, cudaStream_t st)
 {
     const int L = kind == 2 ? a.K : a.Kp;
-    const size_t per = (size_t)(std::max(L, a.K) + MRQ_SELQ) * sizeof(SelItem);
+    const size_t per = (size_t)MRQ_SELREG(std::max(L, a.K)) * sizeof(SelItem);
     const int wpb = warps_for(per);
     const size_t smem = per * wpb;
-    int rc = set_attr((const void *)k_xmerge, smem);
+    auto fn = std::max(L, a.K) > MRQ_MERGE_MIN ? k_xmerge<true> : k_xmerge<false>;
+    int rc = set_attr((const void *)fn, smem);
     if (rc) return rc;
     uint32_t *cnt = kind == 0 ? a.s0_cnt : a.s1_cnt;
     uint32_t *pos = kind == 0 ? a.s0_pos : a.s1_pos;
     uint32_t *sid = kind == 0 ? a.s0_id : a.s1_id;
     double *ex = kind == 0 ? a.s0_exact : a.s1_exact;
     double *tau = kind == 0 ? a.tau0 : a.tau1;
-    k_xmerge<<<(unsigned)((a.nq + wpb - 1) / wpb), wpb * 32, smem, st>>>(kind, a.nq, world, rank, L, a.K, a.Kp, recv,
+    fn<<<(unsigned)((a.nq + wpb - 1) / wpb), wpb * 32, smem, st>>>(kind, a.nq, world, rank, L, a.K, a.Kp, recv,
                                                                         cnt, pos, sid, ex, tau, a.s0_cnt, a.s0_id,
                                                                         a.s0_exact, a.out_ids, a.out_dist);
     return MRQ_OK;
@@ -624,12 +633,13 @@ int launch_xmerge(int kind, const StageArgs &a, int world, int rank, const XItem
 
 int launch_topk_w(const StageArgs &a, cudaStream_t st)
 {
-    const size_t per = MRQ_RG_FLOATS * 4 + (size_t)a.K * sizeof(SelItem);
+    const size_t per = MRQ_RG_FLOATS * 4 + (size_t)MRQ_SELREG(a.K) * sizeof(SelItem);
     const int wpb = warps_for(per);
     const size_t smem = per * wpb;
-    int rc = set_attr((const void *)k_topk_w, smem);
+    auto fn = a.K > MRQ_MERGE_MIN ? k_topk_w<true> : k_topk_w<false>;
+    int rc = set_attr((const void *)fn, smem);
     if (rc) return rc;
-    k_topk_w<<<(unsigned)((a.nq + wpb - 1) / wpb), wpb * 32, smem, st>>>(
+    fn<<<(unsigned)((a.nq + wpb - 1) / wpb), wpb * 32, smem, st>>>(
         a.nq, a.K, a.Kp, a.ids, a.s0_cnt, a.s0_pos, a.s0_id, a.s0_exact, a.s1_cnt, a.s1_pos, a.s1_id, a.s1_exact,
         a.f1_off, a.f2_cnt, a.f2_pos, a.f2_exact, a.out_ids, a.out_dist, a.exact_cnt, a.xout, a.aligned_tails, a.D,
         a.d, a.tails, a.qp, a.f2_head);
@@ -661,7 +671,7 @@ __global__ void __launch_bounds__(128) k_probe_select_w(
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
     const int64_t q = (int64_t)blockIdx.x * wpb + warp;
     if (q >= nq) return;
-    SelItem *lst = (SelItem *)wsm + (size_t)warp * (np + MRQ_SELQ);
+    SelItem *lst = (SelItem *)wsm + (size_t)warp * MRQ_SELREG(np);
     SelItem *queue = lst + np;
     const float *row = approx + q * k;
     const float FINF = __int_as_float(0x7f800000);
@@ -800,7 +810,7 @@ __global__ void __launch_bounds__(128) k_probe_finish_w(int64_t nq, int k, int d
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
     const int64_t q = (int64_t)blockIdx.x * wpb + warp;
     if (q >= nq) return;
-    SelItem *lst = (SelItem *)wsm + (size_t)warp * (np + MRQ_SELQ);
+    SelItem *lst = (SelItem *)wsm + (size_t)warp * MRQ_SELREG(np);
     SelItem *queue = lst + np;
     // a_(np): the used parts' 16 smallest, up to 8 per lane (<= 16 parts);
     // buffers are laid out with P parts per row, of which Pq are used
@@ -903,7 +913,7 @@ int launch_probe_finish_w(int64_t nq, int k, int d, int np, const double *qp, in
         return MRQ_EINVAL;
     }
     const int wpb = 4;
-    const size_t smem = (size_t)wpb * (np + MRQ_SELQ) * sizeof(SelItem);
+    const size_t smem = (size_t)wpb * MRQ_SELREG(np) * sizeof(SelItem);
     int rc = set_attr((const void *)k_probe_finish_w, smem);
     if (rc) return rc;
     k_probe_finish_w<<<(unsigned)((nq + wpb - 1) / wpb), wpb * 32, smem, st>>>(
@@ -916,7 +926,7 @@ int launch_probe_select_w(const float *approx, int64_t nq, int k, int d, int np,
                           uint32_t *probe, double *probe_qn2, uint32_t *ncand, cudaStream_t st)
 {
     const int wpb = 4;
-    const size_t smem = (size_t)wpb * (np + MRQ_SELQ) * sizeof(SelItem);
+    const size_t smem = (size_t)wpb * MRQ_SELREG(np) * sizeof(SelItem);
     const int m = (np + 31) / 32;
     const unsigned grid = (unsigned)((nq + wpb - 1) / wpb);
 #define MRQ_PSEL(MM)                                                                                          \

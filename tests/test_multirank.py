@@ -145,14 +145,14 @@ def test_forced_exchange_equals_fast_path(tau):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world,K", [(2, 10), (3, 10), (2, 100)])
 @pytest.mark.parametrize("tau,mode", [("TIGHT", "FULL"), ("LOOSE", "FULL"), ("TIGHT", "STAGE1_ONLY"),
                                       ("TIGHT", "EXACT")])
-def test_virtual_ranks_equal_single_gpu(world, tau, mode):
+def test_virtual_ranks_equal_single_gpu(world, K, tau, mode):
     m = _lib()
     X, Q, bfile = _tiny()
     ref = m.Index(bfile, X, 16)
-    ir, dr, sr = ref.search(Q, K=10, nprobe=4, tau_schedule=tau, mode=mode)
+    ir, dr, sr = ref.search(Q, K=K, nprobe=4, tau_schedule=tau, mode=mode)
     t0r, t1r = ref.fetch("tau0", "f64").copy(), ref.fetch("tau1", "f64").copy()
     ref.close()
     ex = _ThreadExchange(world)
@@ -160,7 +160,7 @@ def test_virtual_ranks_equal_single_gpu(world, tau, mode):
     res = [None] * world
 
     def run(r):
-        res[r] = idx[r].search(Q, K=10, nprobe=4, tau_schedule=tau, mode=mode)
+        res[r] = idx[r].search(Q, K=K, nprobe=4, tau_schedule=tau, mode=mode)
 
     th = [threading.Thread(target=run, args=(r,)) for r in range(world)]
     for t in th:
