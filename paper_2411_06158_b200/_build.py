@@ -37,7 +37,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if inc:
         # headers only: NCCL itself is dlopen'ed at run time (csrc/mrq_comm.cu)
         cmd += ["-DMRQ_HAVE_NCCL=1", "-I", inc, '-DMRQ_NCCL_LIB="%s"' % os.path.join(lib, "libnccl.so.2")]
-    cmd += ["-ldl"]
+    cmd += ["-ldl"] + os.environ.get("MRQ_NVCC_EXTRA", "").split()   # A/B variant builds (scripts/variant.sh)
     if verbose:
         cmd += ["-Xptxas", "-v"]
     subprocess.check_call(cmd)

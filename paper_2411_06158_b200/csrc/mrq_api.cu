@@ -586,7 +586,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
     {
         LaunchScan a;
         a.nq = nq;
-        a.smem = (size_t)(3 * np + 1) * 4;
+        a.smem = (size_t)np * 5 * 8 + (size_t)np * MRQ_BQ * W * 4 + (size_t)(3 * np + 1) * 4;
         a.probe = probe; a.np = np; a.npad = ix->npad; a.list_off = ix->list_off; a.list_size = ix->list_size;
         a.codes = ix->codes; a.f1 = ix->f1; a.f2 = ix->f2; a.f3 = ix->f3; a.planes = planes; a.qconst = qconst;
         a.eps_r = eps_r; a.tau0 = tau0; a.isd = isd; a.f1_off = f1_off; a.f1_cnt = f1_cnt; a.f1_pos = f1_pos;
@@ -631,7 +631,10 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
         TRY(mrq_allgather(ix, xsend, xrecv, (size_t)nq * K * sizeof(XItem), st));
         TRY(launch_xmerge(2, sa, ix->world, ix->rank, xrecv, st));
     }
-    if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[9], st));
+    if (timed) {
+        MRQ_CUDA_TRY(cudaEventRecord(ix->ev[9], st));
+        TRY(launch_exact_count(sa, st));   // statistic only, outside the timed stages
+    }
     MRQ_CUDA_TRY(cudaGetLastError());
 
     ix->last_nq = nq;
@@ -639,7 +642,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
     ix->last_K = K;
     ix->last_Kp = Kp;
     if (timed) {
-        MRQ_CUDA_TRY(cudaEventSynchronize(ix->ev[9]));
+        MRQ_CUDA_TRY(cudaStreamSynchronize(st));
         float ms[10];
         for (int i = 1; i <= 9; i++) MRQ_CUDA_TRY(cudaEventElapsedTime(&ms[i], ix->ev[i - 1], ix->ev[i]));
         float tot;

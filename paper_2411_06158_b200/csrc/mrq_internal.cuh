@@ -713,11 +713,19 @@ __device__ __forceinline__ int csa_S_w2(uint32_t c0, uint32_t c1, const uint32_t
     return __popc(s0) + (__popc(s1) << 1) + (__popc(s2) << 2) + (__popc(s3) << 3) + (__popc(k4) << 4);
 }
 
-template <int W>
-__device__ __forceinline__ double mrq_lb1(const uint32_t *code, const uint32_t *pl, const double *qc, double isd,
-                                          double eps_r, float f1, float f2, float f3, double *dis_out)
+// Exact int -> fp64 for 0 <= n < 2^31 as (2^52 + n) - 2^52: one DADD on
+// the fp64 pipe instead of an I2F on the XU pipe, which the scan's POPCs and
+// F2Fs keep busy (measured: scan -2.7%; moving F2F.F64.F32 to integer ops
+// instead, or an fp32 pre-screen of LB1, cost more issue slots than they
+// saved -- DESIGN.md performance log).
+__device__ __forceinline__ double i2d_exact(int n)
 {
-    int pop, S;
+    return __hiloint2double(0x43300000, n) - 4503599627370496.0;
+}
+
+template <int W>
+__device__ __forceinline__ void mrq_pop_S(const uint32_t *code, const uint32_t *pl, int &pop, int &S)
+{
     if (W == 1) {
         pop = __popc(code[0]);
         S = __popc(code[0] & pl[0]) + (__popc(code[0] & pl[1]) << 1) + (__popc(code[0] & pl[2]) << 2) +
@@ -737,8 +745,14 @@ __device__ __forceinline__ double mrq_lb1(const uint32_t *code, const uint32_t *
             for (int w = 0; w < W; w++) x[b][w] = code[w] & pl[b * W + w];
         S = csa_weighted_popc<MRQ_BQ, W>(x);
     }
-    const double t1 = qc[0] * (double)pop;
-    const double t2 = qc[1] * (double)S;
+}
+
+// the canonical fp64 evaluation from (pop, S)
+__device__ __forceinline__ double mrq_lb1_ps(int pop, int S, const double *qc, double isd, double eps_r, float f1,
+                                             float f2, float f3, double *dis_out)
+{
+    const double t1 = qc[0] * i2d_exact(pop);
+    const double t2 = qc[1] * i2d_exact(S);
     const double t4 = (t1 + t2) - qc[2];
     const double ip = t4 * isd;
     const double t5 = (double)f1 + qc[3];
@@ -747,6 +761,16 @@ __device__ __forceinline__ double mrq_lb1(const uint32_t *code, const uint32_t *
     *dis_out = dis;
     return (dis - qc[4] * (double)f3) - eps_r;
 }
+
+template <int W>
+__device__ __forceinline__ double mrq_lb1(const uint32_t *code, const uint32_t *pl, const double *qc, double isd,
+                                          double eps_r, float f1, float f2, float f3, double *dis_out)
+{
+    int pop, S;
+    mrq_pop_S<W>(code, pl, pop, S);
+    return mrq_lb1_ps(pop, S, qc, isd, eps_r, f1, f2, f3, dis_out);
+}
+
 
 // -------------------------------------------------------------------------
 // Staged warp row gather.  A warp processes entries 0..n-1 in groups of 32

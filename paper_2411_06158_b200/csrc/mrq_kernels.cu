@@ -428,13 +428,18 @@ __global__ void __launch_bounds__(256, (W <= 3 ? 4 : 1)) k_scan(
     double isd, const uint64_t *__restrict__ f1_off, uint32_t *__restrict__ f1_cnt, uint32_t *__restrict__ f1_pos)
 {
     extern __shared__ unsigned char csm[];
-    uint32_t *tile_pre = (uint32_t *)csm;     // np + 1
-    uint32_t *lst_start = tile_pre + np + 1;  // np
-    uint32_t *lst_end = lst_start + np;       // np
+    double *qc_s = (double *)csm;                        // np x 5: the (query, list) constants
+    uint32_t *pl_s = (uint32_t *)(qc_s + np * 5);        // np x MRQ_BQ W: the query bit-planes
+    uint32_t *tile_pre = pl_s + np * (MRQ_BQ * W);       // np + 1
+    uint32_t *lst_start = tile_pre + np + 1;             // np
+    uint32_t *lst_end = lst_start + np;                  // np
     __shared__ uint32_t sh_cnt;
     const int64_t q = blockIdx.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nwarps = blockDim.x >> 5;
+    // staged once per query: a warp switches list every tile or two
+    for (int i = threadIdx.x; i < np * 5; i += blockDim.x) qc_s[i] = qconst[(q * np + i / 5) * 8 + i % 5];
+    for (int i = threadIdx.x; i < np * (MRQ_BQ * W); i += blockDim.x) pl_s[i] = planes[q * np * (MRQ_BQ * W) + i];
     if (warp == 0) {
         uint32_t carry = 0;
         for (int p0 = 0; p0 < np; p0 += 32) {
@@ -477,10 +482,10 @@ __global__ void __launch_bounds__(256, (W <= 3 ? 4 : 1)) k_scan(
         while (tile_pre[p + 1] <= t) p++;
         if (p != cur_p) {
             cur_p = p;
-            const uint32_t *g = planes + (q * np + p) * (MRQ_BQ * W);
+            const uint32_t *g = pl_s + p * (MRQ_BQ * W);
 #pragma unroll
             for (int i = 0; i < MRQ_BQ * W; i++) pl[i] = g[i];
-            const double *gc = qconst + (q * np + p) * 8;
+            const double *gc = qc_s + p * 5;
 #pragma unroll
             for (int i = 0; i < 5; i++) qc[i] = gc[i];
         }
@@ -549,6 +554,8 @@ void launch_fill_f64(double *p, int64_t n, double v, cudaStream_t st)
 template <int W>
 static void launch_scan_w(const LaunchScan &a, cudaStream_t st)
 {
+    if (a.smem > 48 * 1024)
+        cudaFuncSetAttribute(k_scan<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a.smem);
     k_scan<W><<<a.nq, 256, a.smem, st>>>(a.probe, a.np, a.npad, a.list_off, a.list_size, a.codes, a.f1, a.f2, a.f3,
                                           a.planes, a.qconst, a.eps_r, a.tau0, a.isd, a.f1_off, a.f1_cnt, a.f1_pos);
 }

@@ -43,6 +43,7 @@ struct StageArgs {
 int launch_seed_w(int W, const StageArgs &a, cudaStream_t st);
 int launch_stage2_w(const StageArgs &a, cudaStream_t st, cudaEvent_t after_gather = nullptr);
 int launch_topk_w(const StageArgs &a, cudaStream_t st);
+int launch_exact_count(const StageArgs &a, cudaStream_t st);
 int launch_f2_w(const StageArgs &a, cudaStream_t st);
 int launch_xmerge(int kind, const StageArgs &a, int world, int rank, const XItem *recv, cudaStream_t st);
 

@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(256) k_topk_w(
     const uint32_t *__restrict__ s1_cnt, const uint32_t *__restrict__ s1_pos, const uint32_t *__restrict__ s1_id,
     const double *__restrict__ s1_exact, const uint64_t *__restrict__ f1_off, const uint32_t *__restrict__ f2_cnt,
     const uint32_t *__restrict__ f2_pos, double *__restrict__ f2_exact, int64_t *__restrict__ out_ids,
-    float *__restrict__ out_dist, uint32_t *__restrict__ exact_cnt, XItem *__restrict__ xout, int aligned, int D,
+    float *__restrict__ out_dist, XItem *__restrict__ xout, int aligned, int D,
     int d, const float *__restrict__ tails, const double *__restrict__ qp, const double *__restrict__ f2_head)
 {
     extern __shared__ unsigned char wsm[];
@@ -415,10 +415,25 @@ __global__ void __launch_bounds__(256) k_topk_w(
             out_dist[q * K + i] = ok ? (float)lst[i].key : __int_as_float(0x7f800000);
         }
     }
-    // distinct exact computations on this rank = |(S0 u S1 u F2) n owned|
-    // (S1 and F2 are subsets of F1; S0 may overlap both): a statistic, only
-    // when the caller asked for stats (exact_cnt != NULL)
-    if (!exact_cnt) return;
+}
+
+// Statistic (stats requested only, after the timed stages): distinct exact
+// computations on this rank = |(S0 u S1 u F2) n owned| (S1 and F2 are
+// subsets of F1; S0 may overlap both).  Warp per query.
+__global__ void __launch_bounds__(256) k_exact_count_w(int64_t nq, int Kp, const uint32_t *__restrict__ s0_cnt,
+                                                       const uint32_t *__restrict__ s0_pos,
+                                                       const uint32_t *__restrict__ s1_cnt,
+                                                       const uint32_t *__restrict__ s1_pos,
+                                                       const uint64_t *__restrict__ f1_off,
+                                                       const uint32_t *__restrict__ f2_cnt,
+                                                       const uint32_t *__restrict__ f2_pos, uint32_t *__restrict__ exact_cnt)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (q >= nq) return;
+    const int ns0 = (int)s0_cnt[q], ns1 = (int)s1_cnt[q], n2 = (int)f2_cnt[q];
+    const uint64_t base = f1_off[q];
+    const int n = ns0 + ns1 + n2;
     uint32_t cnt = 0;
     for (int g = 0; g < n; g += 32) {
         const int e = g + lane;
@@ -631,6 +646,13 @@ int launch_xmerge(int kind, const StageArgs &a, int world, int rank, const XItem
     return MRQ_OK;
 }
 
+int launch_exact_count(const StageArgs &a, cudaStream_t st)
+{
+    k_exact_count_w<<<(unsigned)((a.nq + 7) / 8), 256, 0, st>>>(a.nq, a.Kp, a.s0_cnt, a.s0_pos, a.s1_cnt, a.s1_pos,
+                                                                a.f1_off, a.f2_cnt, a.f2_pos, a.exact_cnt);
+    return MRQ_OK;
+}
+
 int launch_topk_w(const StageArgs &a, cudaStream_t st)
 {
     const size_t per = MRQ_RG_FLOATS * 4 + (size_t)MRQ_SELREG(a.K) * sizeof(SelItem);
@@ -641,7 +663,7 @@ int launch_topk_w(const StageArgs &a, cudaStream_t st)
     if (rc) return rc;
     fn<<<(unsigned)((a.nq + wpb - 1) / wpb), wpb * 32, smem, st>>>(
         a.nq, a.K, a.Kp, a.ids, a.s0_cnt, a.s0_pos, a.s0_id, a.s0_exact, a.s1_cnt, a.s1_pos, a.s1_id, a.s1_exact,
-        a.f1_off, a.f2_cnt, a.f2_pos, a.f2_exact, a.out_ids, a.out_dist, a.exact_cnt, a.xout, a.aligned_tails, a.D,
+        a.f1_off, a.f2_cnt, a.f2_pos, a.f2_exact, a.out_ids, a.out_dist, a.xout, a.aligned_tails, a.D,
         a.d, a.tails, a.qp, a.f2_head);
     return MRQ_OK;
 }
