@@ -418,9 +418,12 @@ __global__ void k_exclusive_scan(const uint64_t *__restrict__ in, int64_t n, uin
 // segment of f1_pos.  Warp 0 builds the tile prefix of the probed lists in
 // shared memory with a shuffle scan.
 #define MRQ_SCAN_TILE 128
+#ifndef MRQ_SCAN_THREADS
+#define MRQ_SCAN_THREADS 128   // 4 warps per query: a smaller end-of-query tail than 8 (measured)
+#endif
 #define MRQ_SCAN_H (MRQ_SCAN_TILE / 128)
 template <int W>
-__global__ void __launch_bounds__(256, (W <= 3 ? 4 : 1)) k_scan(
+__global__ void __launch_bounds__(MRQ_SCAN_THREADS, (W <= 3 ? 1024 / MRQ_SCAN_THREADS : 1)) k_scan(
     const uint32_t *__restrict__ probe, int np, int64_t npad, const uint32_t *__restrict__ list_off,
     const uint32_t *__restrict__ list_size, const uint32_t *__restrict__ codes, const float *__restrict__ f1,
     const float *__restrict__ f2, const float *__restrict__ f3, const uint32_t *__restrict__ planes,
@@ -556,7 +559,7 @@ static void launch_scan_w(const LaunchScan &a, cudaStream_t st)
 {
     if (a.smem > 48 * 1024)
         cudaFuncSetAttribute(k_scan<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a.smem);
-    k_scan<W><<<a.nq, 256, a.smem, st>>>(a.probe, a.np, a.npad, a.list_off, a.list_size, a.codes, a.f1, a.f2, a.f3,
+    k_scan<W><<<a.nq, MRQ_SCAN_THREADS, a.smem, st>>>(a.probe, a.np, a.npad, a.list_off, a.list_size, a.codes, a.f1, a.f2, a.f3,
                                           a.planes, a.qconst, a.eps_r, a.tau0, a.isd, a.f1_off, a.f1_cnt, a.f1_pos);
 }
 
