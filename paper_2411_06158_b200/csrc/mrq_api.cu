@@ -431,6 +431,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
     const double isd = 1.0 / std::sqrt((double)d);
     const bool timed = stats != nullptr;
     if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[0], st));
+    uint32_t *qorder = nullptr;
 
     double *qp, *qr2, *eps_r, *r0, *qnorm, *tau0, *tau1, *probe_qn2, *qconst, *s0_exact, *s1_exact;
     float *qd32, *approx;
@@ -474,13 +475,19 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
 
     // ---- a1: query projection (Alg.2 L1-L4)
     {
+        uint16_t *qkey = nullptr;
+        if (ix->qorder_on && nq > 1) {
+            SCR("qorder", uint32_t, nq, qorder);
+            SCR("qkey", uint16_t, nq, qkey);
+        }
         launch_rowmat_f32(d_q, nq, D, D, ix->mu, ix->PT, D, qp, D, st);             // q_p = P (q - mu)
         const size_t qsmem = (size_t)D * 8 * 9;                                    // lambda + 8 query rows
         if (qsmem > 48 * 1024)
             MRQ_CUDA_TRY(cudaFuncSetAttribute(k_qtail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsmem));
         k_qtail<<<(unsigned)((nq + 7) / 8), 256, qsmem, st>>>(qp, nq, D, d, W, ix->lam, ix->RT, p->resid_scale, p->m,
-                                                              qr2, eps_r, r0, qd32, qnorm);
+                                                              qr2, eps_r, r0, qd32, qnorm, qkey);
         launch_rowmat_f64(qp, nq, D, d, nullptr, ix->RT, d, r0, d, st);             // r0 = R q_d
+        if (qkey) launch_qorder(qkey, nq, qorder, st);
     }
     if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[1], st));
 
@@ -558,6 +565,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
     sa.heads = ix->heads; sa.tails = ix->tails; sa.xr2 = ix->xr2; sa.qconst = qconst; sa.qp = qp; sa.qr2 = qr2;
     sa.eps_r = eps_r; sa.s0_cnt = s0_cnt; sa.s0_pos = s0_pos; sa.s1_cnt = s1_cnt; sa.s1_pos = s1_pos;
     sa.f1_cnt = f1_cnt; sa.f1_pos = f1_pos; sa.f2_cnt = f2_cnt; sa.f2_pos = f2_pos; sa.exact_cnt = timed ? exact_cnt : nullptr;
+    sa.qorder = qorder;
     sa.s0_exact = s0_exact; sa.s1_exact = s1_exact; sa.tau0 = tau0; sa.tau1 = tau1; sa.f1_head = f1_head;
     sa.f1_diso = f1_diso; sa.f2_head = f2_head; sa.f2_exact = f2_exact; sa.f1_off = f1_off;
     sa.out_ids = d_ids; sa.out_dist = d_dist;
@@ -590,6 +598,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
         a.probe = probe; a.np = np; a.npad = ix->npad; a.list_off = ix->list_off; a.list_size = ix->list_size;
         a.codes = ix->codes; a.f1 = ix->f1; a.f2 = ix->f2; a.f3 = ix->f3; a.planes = planes; a.qconst = qconst;
         a.eps_r = eps_r; a.tau0 = tau0; a.isd = isd; a.f1_off = f1_off; a.f1_cnt = f1_cnt; a.f1_pos = f1_pos;
+        a.qorder = qorder;
         launch_scan(W, a, st);
         if (ix->dbg_dump_dis) {
             double *dd, *dl;
@@ -878,6 +887,15 @@ extern "C" int mrq_debug_set(mrq_index *ix, const char *name, int64_t value)
     if (!ix || !name) {
         mrq_set_error("NULL index or name");
         return MRQ_EINVAL;
+    }
+    // a switch changes what search_impl launches: drop the captured graph
+    if (ix->gexec) cudaGraphExecDestroy((cudaGraphExec_t)ix->gexec);
+    ix->gexec = nullptr;
+    memset(ix->g_key, 0, sizeof(GraphKey));
+    memset(ix->g_pending, 0, sizeof(GraphKey));
+    if (std::string(name) == "qorder") {           // list-locality query processing order (default 1)
+        ix->qorder_on = (int)value;
+        return MRQ_OK;
     }
     if (std::string(name) == "dump_dis") {
         ix->dbg_dump_dis = (int)value;

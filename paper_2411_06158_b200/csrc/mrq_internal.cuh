@@ -56,6 +56,10 @@ struct mrq_index {
     int force_exchange = 0;                    // mrq_debug_set("force_exchange"): world-1 runs the sharded path
     void *probe_tc = nullptr;                  // tcgen05 probe state (mrq_probe_tc.cu)
     int force_cuda_core_probe = 0;             // mrq_debug_set("cuda_core_probe"): CUDA-core screen instead
+#ifndef MRQ_QORDER_DEFAULT
+#define MRQ_QORDER_DEFAULT 1
+#endif
+    int qorder_on = MRQ_QORDER_DEFAULT;        // mrq_debug_set("qorder"): list-locality query order
     int force_probe_unfused = 0;               // mrq_debug_set("probe_unfused"): screen to HBM + k_probe_select_w
     int graphs = 1;                            // CUDA-graph replay of repeated searches (mrq_debug_set "graphs")
     int tails_host = 0;                        // MRQ_LOAD_TAILS_HOST: tails in mapped pinned host memory
@@ -405,6 +409,23 @@ struct WarpTopBitonic {
         for (int j = 16; j > 0; j >>= 1) cx(key, id, pay, j, (lane & j) == 0);
     }
 };
+
+// Query-order key (k_qtail -> k_qorder): Morton interleave of the three
+// leading principal coordinates, z_i = q_p[i] / sqrt(lambda_i) in 16 levels
+// over [-2, 2) -> 12 bits.
+#define MRQ_QO_KEYS 4096
+__device__ __forceinline__ uint32_t mrq_qorder_key(const double *row, const double *lam, int D)
+{
+    uint32_t key = 0;
+    const int nd = D < 3 ? D : 3;
+    for (int i = 0; i < nd; i++) {
+        const double z = lam[i] > 0.0 ? row[i] / sqrt(lam[i]) : 0.0;
+        int lv = (int)floor((z + 2.0) * 4.0);
+        lv = lv < 0 ? 0 : (lv > 15 ? 15 : lv);
+        for (int b = 0; b < 4; b++) key |= (uint32_t)((lv >> b) & 1) << (3 * b + i);
+    }
+    return key;
+}
 
 #define MRQ_SELQ 64   // items of a WarpSel compaction queue
 // per-warp selection region for a list of L: list, queue, merge temp

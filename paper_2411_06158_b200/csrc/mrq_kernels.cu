@@ -191,7 +191,8 @@ __global__ void __launch_bounds__(256) k_qtail(const double *__restrict__ qp, in
                                                const double *__restrict__ lam, const double *__restrict__ RT,
                                                double rscale, double m, double *__restrict__ qr2o,
                                                double *__restrict__ eps_r, double *__restrict__ r0,
-                                               float *__restrict__ qd32, double *__restrict__ qnorm)
+                                               float *__restrict__ qd32, double *__restrict__ qnorm,
+                                               uint16_t *__restrict__ qkey)
 {
     extern __shared__ double qsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
@@ -217,6 +218,8 @@ __global__ void __launch_bounds__(256) k_qtail(const double *__restrict__ qp, in
         double n2 = 0.0;
         for (int i = 0; i < d; i++) n2 = n2 + row[i] * row[i];
         qnorm[q] = sqrt(n2);
+    } else if (lane == 3 && qkey) {
+        qkey[q] = (uint16_t)mrq_qorder_key(row, lams, D);
     }
 }
 
@@ -359,6 +362,56 @@ void launch_quant(const uint32_t *probe, const double *probe_qn2, int64_t nq, in
         k_quant_g<16><<<grid, 256, 0, st>>>(probe, probe_qn2, npairs, np, d, W, G, r0, Rc, qr2, eps0, planes, qconst);
 }
 
+// Processing order of the queries (a permutation; every query's result is
+// independent of it): a counting sort on the 12-bit key k_qtail computes
+// (mrq_qorder_key).  Queries close in the leading PCs probe mostly the same
+// lists, so the list-major kernels that follow (scan, head gather, re-rank)
+// run neighbouring queries at the same time and share the lists' codes and
+// rows in L2.  One block; order within a key is arbitrary.
+__global__ void __launch_bounds__(1024) k_qorder(const uint16_t *__restrict__ qkey, int64_t nq,
+                                                 uint32_t *__restrict__ order)
+{
+    __shared__ uint32_t hist[MRQ_QO_KEYS];
+    __shared__ uint32_t wsum[32];
+    for (int i = threadIdx.x; i < MRQ_QO_KEYS; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    for (int64_t q = threadIdx.x; q < nq; q += blockDim.x) atomicAdd(&hist[qkey[q]], 1u);
+    __syncthreads();
+    // exclusive scan of hist (MRQ_QO_KEYS / blockDim.x consecutive keys per thread)
+    const int per = MRQ_QO_KEYS / blockDim.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t loc = 0;
+    for (int j = 0; j < per; j++) loc += hist[threadIdx.x * per + j];
+    uint32_t x = loc;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        wsum[lane] = w;
+    }
+    __syncthreads();
+    uint32_t run = (warp > 0 ? wsum[warp - 1] : 0) + x - loc;
+    for (int j = 0; j < per; j++) {
+        const uint32_t c = hist[threadIdx.x * per + j];
+        hist[threadIdx.x * per + j] = run;
+        run += c;
+    }
+    __syncthreads();
+    for (int64_t q = threadIdx.x; q < nq; q += blockDim.x) order[atomicAdd(&hist[qkey[q]], 1u)] = (uint32_t)q;
+}
+
+void launch_qorder(const uint16_t *qkey, int64_t nq, uint32_t *order, cudaStream_t st)
+{
+    k_qorder<<<1, 1024, 0, st>>>(qkey, nq, order);
+}
+
 // Candidate count per query (sum of its probed list sizes) ...
 __global__ void k_cand_count(const uint32_t *__restrict__ probe, int64_t nq, int np,
                              const uint32_t *__restrict__ list_size, uint64_t *__restrict__ cnt)
@@ -428,7 +481,8 @@ __global__ void __launch_bounds__(MRQ_SCAN_THREADS, (W <= 3 ? 1024 / MRQ_SCAN_TH
     const uint32_t *__restrict__ list_size, const uint32_t *__restrict__ codes, const float *__restrict__ f1,
     const float *__restrict__ f2, const float *__restrict__ f3, const uint32_t *__restrict__ planes,
     const double *__restrict__ qconst, const double *__restrict__ eps_r_arr, const double *__restrict__ tau0_arr,
-    double isd, const uint64_t *__restrict__ f1_off, uint32_t *__restrict__ f1_cnt, uint32_t *__restrict__ f1_pos)
+    double isd, const uint64_t *__restrict__ f1_off, uint32_t *__restrict__ f1_cnt, uint32_t *__restrict__ f1_pos,
+    const uint32_t *__restrict__ qorder)
 {
     extern __shared__ unsigned char csm[];
     double *qc_s = (double *)csm;                        // np x 5: the (query, list) constants
@@ -437,7 +491,7 @@ __global__ void __launch_bounds__(MRQ_SCAN_THREADS, (W <= 3 ? 1024 / MRQ_SCAN_TH
     uint32_t *lst_start = tile_pre + np + 1;             // np
     uint32_t *lst_end = lst_start + np;                  // np
     __shared__ uint32_t sh_cnt;
-    const int64_t q = blockIdx.x;
+    const int64_t q = qorder ? (int64_t)qorder[blockIdx.x] : (int64_t)blockIdx.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nwarps = blockDim.x >> 5;
     // staged once per query: a warp switches list every tile or two
@@ -560,7 +614,8 @@ static void launch_scan_w(const LaunchScan &a, cudaStream_t st)
     if (a.smem > 48 * 1024)
         cudaFuncSetAttribute(k_scan<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a.smem);
     k_scan<W><<<a.nq, MRQ_SCAN_THREADS, a.smem, st>>>(a.probe, a.np, a.npad, a.list_off, a.list_size, a.codes, a.f1, a.f2, a.f3,
-                                          a.planes, a.qconst, a.eps_r, a.tau0, a.isd, a.f1_off, a.f1_cnt, a.f1_pos);
+                                          a.planes, a.qconst, a.eps_r, a.tau0, a.isd, a.f1_off, a.f1_cnt, a.f1_pos,
+                                          a.qorder);
 }
 
 void launch_scan(int W, const LaunchScan &a, cudaStream_t st)

@@ -13,9 +13,10 @@ __global__ void k_encode_finish(const double *xp, int64_t n0, int64_t cnt, int D
 __global__ void k_rc(const double *C, const double *RT, int k, int d, int W, double *Rc);
 __global__ void k_qtail(const double *qp, int64_t nq, int D, int d, int W, const double *lam, const double *RT,
                         double rscale, double m, double *qr2o, double *eps_r, double *r0, float *qd32,
-                        double *qnorm);
+                        double *qnorm, uint16_t *qkey);
 __global__ void k_probe_approx(const float *qd32, int64_t nq, int d, int k, const float *C32T, float *approx);
 void launch_fill_f64(double *p, int64_t n, double v, cudaStream_t st);
+void launch_qorder(const uint16_t *qkey, int64_t nq, uint32_t *order, cudaStream_t st);
 void launch_quant(const uint32_t *probe, const double *probe_qn2, int64_t nq, int np, int d, int W,
                   const double *r0, const double *Rc, const double *qr2, double eps0, uint32_t *planes,
                   double *qconst, cudaStream_t st);
@@ -38,6 +39,7 @@ struct StageArgs {
     const uint64_t *f1_off;
     int64_t *out_ids;
     float *out_dist;
+    const uint32_t *qorder;   // processing order of the queries (NULL: 0..nq-1)
 };
 
 int launch_seed_w(int W, const StageArgs &a, cudaStream_t st);
@@ -60,6 +62,7 @@ struct LaunchScan {
     double isd;
     const uint64_t *f1_off;
     uint32_t *f1_cnt, *f1_pos;
+    const uint32_t *qorder;   // processing order of the queries (NULL: 0..nq-1)
 };
 
 void launch_scan(int W, const LaunchScan &a, cudaStream_t st);

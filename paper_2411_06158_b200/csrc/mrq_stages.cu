@@ -25,12 +25,14 @@ __global__ void __launch_bounds__(256) k_seed_w(
     const uint32_t *__restrict__ planes, const double *__restrict__ qconst, const double *__restrict__ qp,
     const double *__restrict__ eps_r_arr, double isd, uint32_t *__restrict__ s0_cnt, uint32_t *__restrict__ s0_pos,
     double *__restrict__ s0_exact, double *__restrict__ tau0, const uint32_t *__restrict__ list_size_g,
-    uint32_t *__restrict__ s0_id, XItem *__restrict__ xout, int seed_lists, int aligned_t)
+    uint32_t *__restrict__ s0_id, XItem *__restrict__ xout, int seed_lists, int aligned_t,
+    const uint32_t *__restrict__ qorder)
 {
     extern __shared__ unsigned char wsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
-    const int64_t q = (int64_t)blockIdx.x * wpb + warp;
-    if (q >= nq) return;
+    const int64_t qi = (int64_t)blockIdx.x * wpb + warp;
+    if (qi >= nq) return;
+    const int64_t q = qorder ? (int64_t)qorder[qi] : qi;
     float *tile = (float *)wsm + warp * MRQ_RG_FLOATS;
     SelItem *lst = (SelItem *)((float *)wsm + wpb * MRQ_RG_FLOATS) + (size_t)warp * MRQ_SELREG(Kp);
     SelItem *queue = lst + Kp;
@@ -168,11 +170,12 @@ __global__ void __launch_bounds__(256) k_head_b(
     int aligned, int D, int d, const uint32_t *__restrict__ ids, const float *__restrict__ heads,
     const float *__restrict__ xr2, const double *__restrict__ qp, const double *__restrict__ qr2_arr,
     const uint64_t *__restrict__ f1_off, const uint32_t *__restrict__ f1_cnt, const uint32_t *__restrict__ f1_pos,
-    double *__restrict__ f1_head, double *__restrict__ f1_diso, uint32_t *__restrict__ f1_id)
+    double *__restrict__ f1_head, double *__restrict__ f1_diso, uint32_t *__restrict__ f1_id,
+    const uint32_t *__restrict__ qorder)
 {
     extern __shared__ unsigned char wsm[];
     const int warp = threadIdx.x >> 5, wpb = blockDim.x >> 5;
-    const int64_t q = blockIdx.x;
+    const int64_t q = qorder ? (int64_t)qorder[blockIdx.x] : (int64_t)blockIdx.x;
     float *tile = (float *)wsm + warp * MRQ_RG_FLOATS;
     const uint64_t base = f1_off[q];
     const int n1 = (int)f1_cnt[q];
@@ -209,12 +212,14 @@ __global__ void __launch_bounds__(256) k_stage2_w(
     const uint32_t *__restrict__ s0_cnt, const uint32_t *__restrict__ s0_id, const double *__restrict__ s0_exact,
     uint32_t *__restrict__ s1_cnt, uint32_t *__restrict__ s1_pos, uint32_t *__restrict__ s1_id,
     double *__restrict__ s1_exact, double *__restrict__ tau1_arr, uint32_t *__restrict__ f2_cnt,
-    uint32_t *__restrict__ f2_pos, double *__restrict__ f2_head, XItem *__restrict__ xout)
+    uint32_t *__restrict__ f2_pos, double *__restrict__ f2_head, XItem *__restrict__ xout,
+    const uint32_t *__restrict__ qorder)
 {
     extern __shared__ unsigned char wsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
-    const int64_t q = (int64_t)blockIdx.x * wpb + warp;
-    if (q >= nq) return;
+    const int64_t qi = (int64_t)blockIdx.x * wpb + warp;
+    if (qi >= nq) return;
+    const int64_t q = qorder ? (int64_t)qorder[qi] : qi;
     float *tile = (float *)wsm + warp * MRQ_RG_FLOATS;
     SelItem *lst = (SelItem *)((float *)wsm + wpb * MRQ_RG_FLOATS) + (size_t)warp * MRQ_SELREG(Kp);
     SelItem *queue = lst + Kp;
@@ -349,12 +354,14 @@ __global__ void __launch_bounds__(256) k_topk_w(
     const double *__restrict__ s1_exact, const uint64_t *__restrict__ f1_off, const uint32_t *__restrict__ f2_cnt,
     const uint32_t *__restrict__ f2_pos, double *__restrict__ f2_exact, int64_t *__restrict__ out_ids,
     float *__restrict__ out_dist, XItem *__restrict__ xout, int aligned, int D,
-    int d, const float *__restrict__ tails, const double *__restrict__ qp, const double *__restrict__ f2_head)
+    int d, const float *__restrict__ tails, const double *__restrict__ qp, const double *__restrict__ f2_head,
+    const uint32_t *__restrict__ qorder)
 {
     extern __shared__ unsigned char wsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
-    const int64_t q = (int64_t)blockIdx.x * wpb + warp;
-    if (q >= nq) return;
+    const int64_t qi = (int64_t)blockIdx.x * wpb + warp;
+    if (qi >= nq) return;
+    const int64_t q = qorder ? (int64_t)qorder[qi] : qi;
     float *tile = (float *)wsm + warp * MRQ_RG_FLOATS;
     SelItem *lst = (SelItem *)((float *)wsm + wpb * MRQ_RG_FLOATS) + (size_t)warp * MRQ_SELREG(K);
     SelItem *queue = lst + K;
@@ -580,7 +587,7 @@ int launch_seed_w(int W, const StageArgs &a, cudaStream_t st)
                                                    a.list_size, a.ids, a.codes, a.f1, a.f2, a.f3, a.heads, a.tails, \
                                                    a.planes, a.qconst, a.qp, a.eps_r, a.isd, a.s0_cnt, a.s0_pos,    \
                                                    a.s0_exact, a.tau0, a.list_size_g, a.s0_id, a.xout,              \
-                                                   a.seed_lists, a.aligned_tails);                                  \
+                                                   a.seed_lists, a.aligned_tails, a.qorder);                        \
     } while (0)
     switch (W) {
     case 1: MRQ_SEED(1); break;
@@ -603,7 +610,8 @@ int launch_stage2_w(const StageArgs &a, cudaStream_t st, cudaEvent_t after_gathe
         int rc = set_attr((const void *)k_head_b, smem);
         if (rc) return rc;
         k_head_b<<<(unsigned)a.nq, wpb * 32, smem, st>>>(a.aligned, a.D, a.d, a.ids, a.heads, a.xr2, a.qp, a.qr2,
-                                                          a.f1_off, a.f1_cnt, a.f1_pos, a.f1_head, a.f1_diso, a.f1_id);
+                                                          a.f1_off, a.f1_cnt, a.f1_pos, a.f1_head, a.f1_diso, a.f1_id,
+                                                          a.qorder);
     }
     if (after_gather) MRQ_CUDA_TRY(cudaEventRecord(after_gather, st));
     const size_t per = MRQ_RG_FLOATS * 4 + (size_t)MRQ_SELREG(std::max(a.Kp, a.K)) * sizeof(SelItem);
@@ -615,7 +623,7 @@ int launch_stage2_w(const StageArgs &a, cudaStream_t st, cudaEvent_t after_gathe
     fn<<<(unsigned)((a.nq + wpb - 1) / wpb), wpb * 32, smem, st>>>(
         a.nq, a.aligned_tails, a.mode, a.tight, a.K, a.Kp, a.D, a.d, a.tails, a.qp, a.eps_r, a.tau0, a.f1_off, a.f1_cnt,
         a.f1_pos, a.f1_head, a.f1_diso, a.f1_id, a.s0_cnt, a.s0_id, a.s0_exact, a.s1_cnt, a.s1_pos, a.s1_id,
-        a.s1_exact, a.tau1, a.f2_cnt, a.f2_pos, a.f2_head, a.xout);
+        a.s1_exact, a.tau1, a.f2_cnt, a.f2_pos, a.f2_head, a.xout, a.qorder);
     return MRQ_OK;
 }
 
@@ -664,7 +672,7 @@ int launch_topk_w(const StageArgs &a, cudaStream_t st)
     fn<<<(unsigned)((a.nq + wpb - 1) / wpb), wpb * 32, smem, st>>>(
         a.nq, a.K, a.Kp, a.ids, a.s0_cnt, a.s0_pos, a.s0_id, a.s0_exact, a.s1_cnt, a.s1_pos, a.s1_id, a.s1_exact,
         a.f1_off, a.f2_cnt, a.f2_pos, a.f2_exact, a.out_ids, a.out_dist, a.xout, a.aligned_tails, a.D,
-        a.d, a.tails, a.qp, a.f2_head);
+        a.d, a.tails, a.qp, a.f2_head, a.qorder);
     return MRQ_OK;
 }
 

@@ -291,3 +291,26 @@ def test_host_resident_tails_identical(case):
             assert a[2].exact == b[2].exact and a[2].stage2_pass == b[2].stage2_pass
     finally:
         gh.close()
+
+
+def test_query_order_invariance(case):
+    """The list-locality processing order (k_qorder, a permutation of the
+    queries) changes no result: ids, distances, tau0/tau1 and every survivor
+    count equal the identity order's, for both schedules and K = 1 / 10 / 100."""
+    m, gx, Q = case["m"], case["gx"], case["Q"]
+    npb = case["nprobe"][-1]
+    try:
+        for tau in ("TIGHT", "LOOSE"):
+            for K in (1, 10, 100):
+                res = []
+                for on in (0, 1):
+                    m.mrq_debug_set(gx.h, "qorder", on)
+                    ids, dist, st = gx.search(Q, K=K, nprobe=npb, tau_schedule=tau)
+                    res.append((ids, dist, st, gx.fetch("tau0", "f64").copy(), gx.fetch("tau1", "f64").copy()))
+                a, b = res
+                assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+                assert np.array_equal(a[3], b[3]) and np.array_equal(a[4], b[4])
+                for f in ("scanned", "stage1_pass", "stage2_pass", "exact", "seeds"):
+                    assert getattr(a[2], f) == getattr(b[2], f), f
+    finally:
+        m.mrq_debug_set(gx.h, "qorder", 1)
