@@ -827,15 +827,23 @@ __device__ __forceinline__ void warp_gather_rows(const float *__restrict__ base,
     const int mygroups = ngroups > g0 ? (ngroups - g0 + gs - 1) / gs : 0;
     const int njobs = mygroups * nchunk;
     if (njobs == 0) return;
-    uint32_t slot_cur = 0;
+    // slots are loaded one group ahead (slot_nxt), so the index load's
+    // latency is hidden behind the current group's copies
+    auto load_slot = [&](int g) -> uint32_t {
+        const int e = g * 32 + lane;
+        return e < n ? slot_of(e) : 0u;
+    };
+    uint32_t slot_cur = 0, slot_nxt = load_slot(g0);
     // job (g, c): 32 rows x MRQ_RG_CH floats; lane copies 16-B unit (lane & 7)
     // of rows (lane >> 3) + 4 i, i = 0..7 (one 128-B row segment per 8 lanes).
     auto issue = [&](int job, int g, int c) {
-        const int e = g * 32 + lane;
         const int c0 = c * MRQ_RG_CH;
         const int nu = min(MRQ_RG_CH, len - c0) >> 2;
         const int st = job & 1;
-        if (c == 0 && e < n) slot_cur = slot_of(e);
+        if (c == 0) {
+            slot_cur = slot_nxt;
+            slot_nxt = load_slot(g + gs);
+        }
         const int cnt = min(32, n - g * 32);
         const int u = lane & 7;
         float *dst0 = sbuf + st * MRQ_RG_STAGE + 4 * u;
