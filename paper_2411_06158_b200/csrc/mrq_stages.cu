@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(256) k_f2_w(int64_t nq, int mode, const double
 
 // ----------------------------------------------------------------------- a8
 // Exact re-rank of F2 (a7) and per-query top-K (Alg.2 L15-L16),
-// one warp per query: F2's tails are gathered first (f2_exact), then the K
+// block per query: F2's tails are gathered first (f2_exact), then the K
 // smallest (exact, id) over
 // the distinct union S0 u S1 u F2 restricted to this rank's slots (a
 // candidate in several sets has the same exact value in each, so WarpTop
@@ -346,8 +346,10 @@ __global__ void __launch_bounds__(256) k_f2_w(int64_t nq, int mode, const double
 // distances rounded to fp32, padding id -1 / +inf.  Sharded (xout != NULL):
 // the local top-K (exact fp64, id) goes to the exchange and k_xmerge writes
 // the outputs.
+// Block of 1 or 2 warps per query: the warps split the F2 re-rank rows,
+// warp 0 selects.  2 for LOOSE (F2 ~ 2x larger), 1 for TIGHT (measured).
 template <bool MG>
-__global__ void __launch_bounds__(256) k_topk_w(
+__global__ void __launch_bounds__(64) k_topk_w(
     int64_t nq, int K, int Kp, const uint32_t *__restrict__ ids, const uint32_t *__restrict__ s0_cnt,
     const uint32_t *__restrict__ s0_pos, const uint32_t *__restrict__ s0_id, const double *__restrict__ s0_exact,
     const uint32_t *__restrict__ s1_cnt, const uint32_t *__restrict__ s1_pos, const uint32_t *__restrict__ s1_id,
@@ -359,24 +361,24 @@ __global__ void __launch_bounds__(256) k_topk_w(
 {
     extern __shared__ unsigned char wsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
-    const int64_t qi = (int64_t)blockIdx.x * wpb + warp;
-    if (qi >= nq) return;
-    const int64_t q = qorder ? (int64_t)qorder[qi] : qi;
+    const int64_t q = qorder ? (int64_t)qorder[blockIdx.x] : (int64_t)blockIdx.x;
     float *tile = (float *)wsm + warp * MRQ_RG_FLOATS;
-    SelItem *lst = (SelItem *)((float *)wsm + wpb * MRQ_RG_FLOATS) + (size_t)warp * MRQ_SELREG(K);
+    SelItem *lst = (SelItem *)((float *)wsm + wpb * MRQ_RG_FLOATS);
     SelItem *queue = lst + K;
     const int ns0 = (int)s0_cnt[q], ns1 = (int)s1_cnt[q], n2 = (int)f2_cnt[q];
     const uint64_t base = f1_off[q];
     // a7 exact re-rank of F2 (Alg.2 L14 P:316): exact = HEAD continued over
     // the tail = ||x_p - q_p||^2 left to right over i = 0..D-1 (R-8)
+    // (the block's warps split the F2 rows; warp 0 then selects)
     if (D > d)
         warp_rows(aligned, tails, D - d, 0, D - d, qp + q * D + d, n2, tile, [&](int e) { return f2_pos[base + e]; },
                   [&](int e, uint32_t) { return f2_head[base + e]; }, [&](int e, bool v, double acc) {
                       if (v) f2_exact[base + e] = acc;
-                  });
+                  }, warp, wpb);
     else
-        for (int e = lane; e < n2; e += 32) f2_exact[base + e] = f2_head[base + e];
-    __syncwarp();
+        for (int e = threadIdx.x; e < n2; e += blockDim.x) f2_exact[base + e] = f2_head[base + e];
+    __syncthreads();
+    if (warp != 0) return;
     WarpSelT<MG> top;
     top.init(lst, K, false, queue);
     const int n = ns0 + ns1 + n2;
@@ -663,13 +665,12 @@ int launch_exact_count(const StageArgs &a, cudaStream_t st)
 
 int launch_topk_w(const StageArgs &a, cudaStream_t st)
 {
-    const size_t per = MRQ_RG_FLOATS * 4 + (size_t)MRQ_SELREG(a.K) * sizeof(SelItem);
-    const int wpb = warps_for(per);
-    const size_t smem = per * wpb;
+    const int wpb = a.tight ? 1 : 2;
+    const size_t smem = (size_t)wpb * MRQ_RG_FLOATS * 4 + (size_t)MRQ_SELREG(a.K) * sizeof(SelItem);
     auto fn = a.K > MRQ_MERGE_MIN ? k_topk_w<true> : k_topk_w<false>;
     int rc = set_attr((const void *)fn, smem);
     if (rc) return rc;
-    fn<<<(unsigned)((a.nq + wpb - 1) / wpb), wpb * 32, smem, st>>>(
+    fn<<<(unsigned)a.nq, wpb * 32, smem, st>>>(
         a.nq, a.K, a.Kp, a.ids, a.s0_cnt, a.s0_pos, a.s0_id, a.s0_exact, a.s1_cnt, a.s1_pos, a.s1_id, a.s1_exact,
         a.f1_off, a.f2_cnt, a.f2_pos, a.f2_exact, a.out_ids, a.out_dist, a.xout, a.aligned_tails, a.D,
         a.d, a.tails, a.qp, a.f2_head, a.qorder);
