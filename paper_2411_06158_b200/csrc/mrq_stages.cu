@@ -554,9 +554,12 @@ __global__ void __launch_bounds__(128) k_xmerge(int kind, int64_t nq, int world,
 }
 
 // ---------------------------------------------------------------- launchers
+#ifndef MRQ_WPB_MAX
+#define MRQ_WPB_MAX 1   // one warp (query) per block measured best of 1/2/4/8 for seed / stage 2 / merge
+#endif
 static int warps_for(size_t per_warp)
 {
-    int w = 4;
+    int w = MRQ_WPB_MAX;
     while (w > 1 && per_warp * w > 100 * 1024) w >>= 1;
     return w;
 }
