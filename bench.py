@@ -438,7 +438,7 @@ def main():
             cpu = {"value": None, "unit": "queries/s", "cores": os.cpu_count(), "kind": "oracle",
                    "sample": "failed: %s" % e}
 
-    launches_per_step = 12 + (4 if world > 1 else 0)   # DESIGN.md §8; + 3 k_xmerge + k_f2_w when sharded
+    launches_per_step = 14 + (4 if world > 1 else 0)   # DESIGN.md §8; + 3 k_xmerge + k_f2_w when sharded
     out = {
         "metric": METRIC,
         "value": round(nq / (ms * 1e-3), 1),

@@ -429,37 +429,37 @@ __global__ void k_cand_count(const uint32_t *__restrict__ probe, int64_t nq, int
 // ... and its exclusive prefix sum (one block; out[nq] = total).
 __global__ void k_exclusive_scan(const uint64_t *__restrict__ in, int64_t n, uint64_t *__restrict__ out)
 {
-    __shared__ uint64_t warp_sums[32];
-    __shared__ uint64_t carry;
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int64_t base = 0; base < n; base += blockDim.x) {
-        const int64_t i = base + threadIdx.x;
-        uint64_t v = i < n ? in[i] : 0;
-        uint64_t x = v;
-        for (int o = 1; o < 32; o <<= 1) {
-            uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        if (lane == 31) warp_sums[warp] = x;
-        __syncthreads();
-        if (warp == 0) {
-            uint64_t s = lane < (int)(blockDim.x >> 5) ? warp_sums[lane] : 0;
-            for (int o = 1; o < 32; o <<= 1) {
-                uint64_t y = __shfl_up_sync(0xffffffffu, s, o);
-                if (lane >= o) s += y;
-            }
-            warp_sums[lane] = s;
-        }
-        __syncthreads();
-        const uint64_t before = carry + (warp > 0 ? warp_sums[warp - 1] : 0) + (x - v);
-        if (i < n) out[i] = before;
-        __syncthreads();
-        if (threadIdx.x == blockDim.x - 1) carry = before + v;
-        __syncthreads();
+    // thread t owns the contiguous run [t per, (t + 1) per): its total, a
+    // block scan of the totals, then the run's prefixes -- two passes over in[]
+    __shared__ uint64_t wsum[32];
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int64_t per = (n + blockDim.x - 1) / blockDim.x;
+    const int64_t i0 = t * per, i1 = i0 + per < n ? i0 + per : n;
+    uint64_t loc = 0;
+#pragma unroll 8
+    for (int64_t i = i0; i < i1; i++) loc += in[i];
+    uint64_t x = loc;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
     }
-    if (threadIdx.x == 0) out[n] = carry;
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        uint64_t w = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        wsum[lane] = w;
+    }
+    __syncthreads();
+    uint64_t run = (warp > 0 ? wsum[warp - 1] : 0) + x - loc;
+    for (int64_t i = i0; i < i1; i++) {
+        out[i] = run;
+        run += in[i];
+    }
+    if (t == (int)blockDim.x - 1) out[n] = run;
 }
 
 // The code scan (hot loop of Alg.2 L7-L12): block per query, every
