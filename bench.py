@@ -390,7 +390,7 @@ def main():
         kk["achieved_gbs"] = round(kk["bytes_per_unit"] * kk["units_per_launch"] / (kk["ms"] * 1e-3) / 1e9, 1)
         kk["frac"] = round(kk["achieved_gbs"] / hbm, 4)
         kk["ms"] = round(kk["ms"], 4)
-        kk["traffic"] = traffic.get(nm)
+        kk["traffic"] = traffic.get(nm, next((v for k, v in traffic.items() if k.startswith(nm + "<")), None))
     dom = max(kern, key=lambda n: kern[n]["ms"])
     # the probe screen GEMM on the tensor cores (kind::tf32): its flops against
     # the tf32 peak = measured bf16 burst x the nominal tf32/bf16 ratio (1.1/2.25)
