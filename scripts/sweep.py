@@ -26,6 +26,10 @@ def main():
     ap.add_argument("--nprobe", default="16,24,32,48,64,96,128,192,256")
     ap.add_argument("--K", default="10")
     ap.add_argument("--modes", default="FULL/TIGHT,FULL/LOOSE,STAGE1_ONLY/TIGHT")
+    # SURVEY NEXT-2 parameter sweeps: every combination is a point
+    ap.add_argument("--eps0", default="1.9")
+    ap.add_argument("--m", default="4")
+    ap.add_argument("--rscale", default="2")
     args = ap.parse_args()
     import torch
     import bench
@@ -47,15 +51,21 @@ def main():
     for K in [int(x) for x in args.K.split(",")]:
         gtf = os.path.join(ROOT, "data", args.config, "gt_k%d.npy" % K)
         gt10 = np.load(os.path.join(ROOT, "data", args.config, "gt_k10.npy"))
-        gtK = np.load(gtf) if os.path.exists(gtf) else None
+        gt100 = os.path.join(ROOT, "data", args.config, "gt_k100.npy")
+        gtK = np.load(gtf) if os.path.exists(gtf) else (np.load(gt100)[:, :K] if os.path.exists(gt100) and K < 100
+                                                       else None)   # exact KNN lists are sorted: a prefix
         d_ids = torch.empty((nq, K), dtype=torch.int64, device=dev)
         d_dist = torch.empty((nq, K), dtype=torch.float32, device=dev)
         for mt in args.modes.split(","):
             mode, tau = mt.split("/")
-            for npb in [int(x) for x in args.nprobe.split(",")]:
+            grid = [(npb, e0, mm, rs) for npb in [int(x) for x in args.nprobe.split(",")]
+                    for e0 in [float(x) for x in args.eps0.split(",")] for mm in [float(x) for x in args.m.split(",")]
+                    for rs in [float(x) for x in args.rscale.split(",")]]
+            for npb, e0, mm, rs in grid:
                 if npb > cfg.k:
                     continue
-                p = mrq.SearchParams.make(K=K, nprobe=npb, mode=mode, tau_schedule=tau, seed_lists=2)
+                p = mrq.SearchParams.make(K=K, nprobe=npb, mode=mode, tau_schedule=tau, seed_lists=2, eps0=e0, m=mm,
+                                          resid_scale=rs)
                 st = mrq.Stats()
                 mrq.mrq_search_batch_device(h, dq, p, d_ids, d_dist, st, stream.cuda_stream)
                 ids = d_ids.cpu().numpy()
@@ -71,7 +81,8 @@ def main():
                     ev.append((a, b))
                 torch.cuda.synchronize()
                 ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
-                pt = {"K": K, "mode": mode, "tau_schedule": tau, "nprobe": npb, "ms": round(ms, 4),
+                pt = {"K": K, "mode": mode, "tau_schedule": tau, "nprobe": npb, "eps0": e0, "m": mm,
+                      "resid_scale": rs, "ms": round(ms, 4),
                       "qps": round(nq / (ms * 1e-3), 1), "recall10": round(bench.recall_at_k(ids, gt10, 10), 4),
                       "f1_per_q": round(st.stage1_pass / nq, 1), "f2_per_q": round(st.stage2_pass / nq, 1),
                       "exact_per_q": round(st.exact / nq, 1), "scanned_per_q": round(st.scanned / nq, 1)}
