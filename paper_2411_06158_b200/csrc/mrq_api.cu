@@ -198,6 +198,8 @@ static int load_impl(mrq_index *ix, const char *build_file, const float *base, i
     MRQ_CUDA_TRY(cudaDeviceGetAttribute(&ix->sm_count, cudaDevAttrMultiProcessorCount, ix->device));
     MRQ_CUDA_TRY(cudaStreamCreateWithFlags(&ix->stream, cudaStreamNonBlocking));
     for (auto &e : ix->ev) MRQ_CUDA_TRY(cudaEventCreate(&e));
+    MRQ_CUDA_TRY(cudaStreamCreateWithFlags(&ix->side, cudaStreamNonBlocking));
+    for (auto &e : ix->ev_fork) MRQ_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
 
     std::vector<uint32_t> cnt(k, 0);
     for (int64_t i = 0; i < n; i++) cnt[b.assign[i]]++;
@@ -403,6 +405,9 @@ extern "C" void mrq_free(mrq_index *ix)
     for (auto &e : ix->ev)
         if (e) cudaEventDestroy(e);
     if (ix->stream) cudaStreamDestroy(ix->stream);
+    for (auto e : ix->ev_fork)
+        if (e) cudaEventDestroy(e);
+    if (ix->side) cudaStreamDestroy(ix->side);
     delete ix;
 }
 
@@ -486,8 +491,12 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
             MRQ_CUDA_TRY(cudaFuncSetAttribute(k_qtail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsmem));
         k_qtail<<<(unsigned)((nq + 7) / 8), 256, qsmem, st>>>(qp, nq, D, d, W, ix->lam, ix->RT, p->resid_scale, p->m,
                                                               qr2, eps_r, r0, qd32, qnorm, qkey);
+        if (qkey) {   // the order's single-block sort runs beside r0 and the probe
+            MRQ_CUDA_TRY(cudaEventRecord(ix->ev_fork[0], st));
+            MRQ_CUDA_TRY(cudaStreamWaitEvent(ix->side, ix->ev_fork[0], 0));
+            launch_qorder(qkey, nq, qorder, ix->side);
+        }
         launch_rowmat_f64(qp, nq, D, d, nullptr, ix->RT, d, r0, d, st);             // r0 = R q_d
-        if (qkey) launch_qorder(qkey, nq, qorder, st);
     }
     if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[1], st));
 
@@ -529,9 +538,14 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
 
     // ---- a3: per-(query, list) quantization into bit-planes
     {
+        // F1 segment offsets on the side stream, beside the quantizer; join
+        MRQ_CUDA_TRY(cudaEventRecord(ix->ev_fork[1], st));
+        MRQ_CUDA_TRY(cudaStreamWaitEvent(ix->side, ix->ev_fork[1], 0));
+        k_cand_count<<<(unsigned)((nq + 255) / 256), 256, 0, ix->side>>>(probe, nq, np, ix->list_size, cand_cnt);
+        k_exclusive_scan<<<1, 1024, 0, ix->side>>>(cand_cnt, nq, f1_off);
+        MRQ_CUDA_TRY(cudaEventRecord(ix->ev_fork[2], ix->side));
         launch_quant(probe, probe_qn2, nq, np, d, W, r0, ix->Rc, qr2, p->eps0, planes, qconst, st);
-        k_cand_count<<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(probe, nq, np, ix->list_size, cand_cnt);
-        k_exclusive_scan<<<1, 1024, 0, st>>>(cand_cnt, nq, f1_off);
+        MRQ_CUDA_TRY(cudaStreamWaitEvent(st, ix->ev_fork[2], 0));
     }
     // candidate-indexed scratch: sized by the host bound nq x (sum of the np
     // largest lists) when that fits the budget, so the search never waits on
