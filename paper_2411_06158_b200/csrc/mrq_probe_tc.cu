@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_probe_tc(const __grid_constan
         float kv[TC_NPMAX];                   // FUSED: the np smallest screen values, ascending
         float tf = FINF;                      // FUSED: append threshold RU(kv[np-1] + margin)
         uint32_t cnt = 0;
-        double margin = 0.0;
+        float margin = 0.f;                   // RU(2 delta_q): th + margin rounded up >= th + 2 delta_q
         uint2 *rb = nullptr;
         int row = 0, part = 0, cur_mb = -1;
         // FUSED: the (row, part) state goes to kvbuf / ccnt when the query block changes
@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_probe_tc(const __grid_constan
                     for (int j = 0; j < TC_NPMAX; j++) kv[j] = j < TC_NPMAX - np ? -FINF : FINF;
                     if (row < nq) {
                         const double g = qnorm[row] + cmax;
-                        margin = 2.0 * (kappa * (g * g));
+                        margin = __double2float_ru(2.0 * (kappa * (g * g)));
                         rb = cbuf + ((int64_t)row * P + part) * capp;
                     }
                 }
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_probe_tc(const __grid_constan
                                     kv[i] = lo;
                                 }
                                 const float th = kv[TC_NPMAX - 1];
-                                tf = th == FINF ? FINF : __double2float_ru((double)th + margin);
+                                tf = __fadd_ru(th, margin);   // +inf stays +inf
                             }
                         }
                     }
