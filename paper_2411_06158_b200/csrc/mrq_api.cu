@@ -439,7 +439,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
     uint32_t *qorder = nullptr;
 
     double *qp, *qr2, *eps_r, *r0, *qnorm, *tau0, *tau1, *probe_qn2, *qconst, *s0_exact, *s1_exact;
-    float *qd32, *approx;
+    float *qd32, *approx, *qa3 = nullptr;
     uint32_t *probe, *planes, *s0_cnt, *s0_pos, *s1_cnt, *s1_pos, *f1_cnt, *f2_cnt, *exact_cnt, *fallback;
     uint64_t *cand_cnt, *f1_off;
     SCR("qp", double, nq * D, qp);
@@ -448,6 +448,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
     SCR("r0", double, nq * d, r0);
     SCR("qnorm", double, nq, qnorm);
     SCR("qd32", float, nq * d, qd32);
+    if (mrq_probe_tc_enabled(ix)) SCR("qa3", float, nq * 3 * d, qa3);   // 3xTF32 A operand
     SCR("tau0", double, nq, tau0);
     SCR("tau1", double, nq, tau1);
     SCR("probe", uint32_t, nq * np, probe);
@@ -490,7 +491,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
         if (qsmem > 48 * 1024)
             MRQ_CUDA_TRY(cudaFuncSetAttribute(k_qtail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsmem));
         k_qtail<<<(unsigned)((nq + 7) / 8), 256, qsmem, st>>>(qp, nq, D, d, W, ix->lam, ix->RT, p->resid_scale, p->m,
-                                                              qr2, eps_r, r0, qd32, qnorm, qkey);
+                                                              qr2, eps_r, r0, qd32, qnorm, qkey, qa3);
         if (qkey) {   // the order's single-block sort runs beside r0 and the probe
             MRQ_CUDA_TRY(cudaEventRecord(ix->ev_fork[0], st));
             MRQ_CUDA_TRY(cudaStreamWaitEvent(ix->side, ix->ev_fork[0], 0));
@@ -514,7 +515,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
             SCR("probe_ccnt", uint32_t, (size_t)nq * P, ccnt);
             SCR("probe_kv", float, (size_t)nq * P * 16, kvbuf);
             const double kappa = mrq_probe_tc_kappa(ix);
-            TRY(mrq_probe_tc_run_fused(ix, qd32, nq, np, qnorm, kappa, cbuf, capp, ccnt, kvbuf, st));
+            TRY(mrq_probe_tc_run_fused(ix, qa3, nq, np, qnorm, kappa, cbuf, capp, ccnt, kvbuf, st));
             if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[11], st));
             TRY(launch_probe_finish_w(nq, k, d, np, qp, D, ix->C, qnorm, ix->cmax, kappa, cbuf, P, capp,
                                       mrq_probe_tc_grid(ix, nq), ccnt, kvbuf, cand, probe, probe_qn2, ncand, st));
@@ -522,7 +523,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
             SCR("approx", float, nq * k, approx);
             double kappa;
             if (mrq_probe_tc_enabled(ix)) {
-                TRY(mrq_probe_tc_run(ix, qd32, nq, approx, st));
+                TRY(mrq_probe_tc_run(ix, qa3, nq, approx, st));
                 kappa = mrq_probe_tc_kappa(ix);
             } else {
                 dim3 grid((k + 255) / 256, (unsigned)((nq + 7) / 8));

@@ -429,6 +429,17 @@ __device__ __forceinline__ uint32_t mrq_qorder_key(const double *row, const doub
     return key;
 }
 
+// x = hi + lo + r with hi = RN_tf32(x), lo = RN_tf32(x - hi), |r| <= 2^-22 |x|
+// (the probe's 3xTF32 operands; x - hi is exact in fp32)
+__device__ __forceinline__ void tf32_split(float x, float &hi, float &lo)
+{
+    uint32_t h, l;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+    hi = __uint_as_float(h);
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(x - hi));
+    lo = __uint_as_float(l);
+}
+
 #define MRQ_SELQ 64   // items of a WarpSel compaction queue
 // per-warp selection region for a list of L: list, queue, merge temp
 // lists longer than this use the merge selection (shorter: smem insertion)

@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(256) k_qtail(const double *__restrict__ qp, in
                                                double rscale, double m, double *__restrict__ qr2o,
                                                double *__restrict__ eps_r, double *__restrict__ r0,
                                                float *__restrict__ qd32, double *__restrict__ qnorm,
-                                               uint16_t *__restrict__ qkey)
+                                               uint16_t *__restrict__ qkey, float *__restrict__ qa3)
 {
     extern __shared__ double qsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
@@ -204,7 +204,17 @@ __global__ void __launch_bounds__(256) k_qtail(const double *__restrict__ qp, in
     double *row = qsm + D + (size_t)warp * D;
     const double *g = qp + q * D;
     for (int i = lane; i < D; i += 32) row[i] = g[i];
-    for (int j = lane; j < d; j += 32) qd32[q * d + j] = (float)g[j];
+    for (int j = lane; j < d; j += 32) {
+        const float x = (float)g[j];
+        qd32[q * d + j] = x;
+        if (qa3) {   // the tensor-core probe's A3 row [q_hi | q_hi | q_lo]
+            float hi, lo;
+            tf32_split(x, hi, lo);
+            qa3[q * 3 * d + j] = hi;
+            qa3[q * 3 * d + d + j] = hi;
+            qa3[q * 3 * d + 2 * d + j] = lo;
+        }
+    }
     __syncwarp();
     if (lane == 0) {
         double a = 0.0;

@@ -13,7 +13,7 @@ __global__ void k_encode_finish(const double *xp, int64_t n0, int64_t cnt, int D
 __global__ void k_rc(const double *C, const double *RT, int k, int d, int W, double *Rc);
 __global__ void k_qtail(const double *qp, int64_t nq, int D, int d, int W, const double *lam, const double *RT,
                         double rscale, double m, double *qr2o, double *eps_r, double *r0, float *qd32,
-                        double *qnorm, uint16_t *qkey);
+                        double *qnorm, uint16_t *qkey, float *qa3);
 __global__ void k_probe_approx(const float *qd32, int64_t nq, int d, int k, const float *C32T, float *approx);
 void launch_fill_f64(double *p, int64_t n, double v, cudaStream_t st);
 void launch_qorder(const uint16_t *qkey, int64_t nq, uint32_t *order, cudaStream_t st);

@@ -4,7 +4,11 @@
 //
 //   approx[q][c] = ||c||^2 - 2 <q_d, c>        (fp32; the q-only term ||q_d||^2 is dropped)
 //
-// A = q_d (fp32 [nq][d], K-major), B = centroids (fp32 [k][d], K-major);
+// A = q_d, B = centroids, each split into tf32 parts (x = hi + lo + r, hi =
+// RN_tf32(x), lo = RN_tf32(x - hi), |r| <= 2^-22 |x|) and laid out as
+// A3 = [q_hi | q_hi | q_lo], B3 = [c_hi | c_lo | c_hi] (fp32 [rows][3d],
+// K-major), so one K = 3d GEMM gives q_hi c_hi + q_hi c_lo + q_lo c_hi
+// ("3xTF32": close to fp32 products instead of tf32 ones);
 // kind::tf32 MMAs (M = 128 queries, N = 256 centroids, K = 8) accumulate in
 // TMEM.  Warp roles (one CTA = one 128-query block x a range of 256-centroid
 // tiles):
@@ -16,12 +20,13 @@
 // Two TMEM accumulators (2 x 256 columns) let the epilogue of tile j overlap
 // the MMAs of tile j+1.  Out-of-range rows/columns/k are zero-filled by TMA.
 //
-// Exactness (DESIGN.md §4 "probe exactness"): tf32 keeps 10 mantissa bits of
-// each fp32 input (relative error <= 2^-10 whether truncated or rounded), the
-// fp32 accumulation of d products adds <= d 2^-23 sum|q_i c_i|, and ||c||^2,
-// q_d, c are fp32 roundings of fp64 values; with sum|q_i c_i| <= ||q|| ||c||
-// and 2 ||q|| ||c|| <= (||q|| + ||c||)^2 / 2 ... the screen is within
-//   delta_q = kappa (||q_d|| + max ||c||)^2,  kappa = 2^-9 + d 2^-22 + 2^-20
+// Exactness (DESIGN.md §4 "probe exactness"): the three tf32 products (exact
+// in fp32) differ from q32 c32 by <= 3.01 2^-22 |q32 c32| (the dropped
+// q_lo c_lo and the lo residuals), the fp32 accumulation of 3d products adds
+// <= 3d 2^-23 (1 + 2^-10) sum|q_i c_i|, and ||c||^2, q_d, c are fp32
+// roundings of fp64 values; with sum|q_i c_i| <= ||q|| ||c|| <= (||q|| +
+// ||c||)^2 / 4 the screen is within
+//   delta_q = kappa (||q_d|| + max ||c||)^2,  kappa = 2^-20 + 3d 2^-23
 // of the exact key ||c||^2 - 2 <q_d, c> (a generous bound: each term is at
 // least 2x the derivation).  k_probe_select_w then rescores every centroid
 // within 2 delta_q of the np-th smallest screen value in canonical fp64.
@@ -42,7 +47,8 @@
 
 struct ProbeTC {
     bool enabled = false;
-    CUtensorMap mapB;                  // centroids
+    CUtensorMap mapB;                  // centroids, split: B3 [k][3d]
+    float *B3 = nullptr;
     PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
 };
 
@@ -375,6 +381,20 @@ static int make_map(ProbeTC *tc, CUtensorMap *map, const float *ptr, int rows, i
     return MRQ_OK;
 }
 
+// B3 row c = [c_hi | c_lo | c_hi] (see the header comment)
+__global__ void k_split3_b(const float *__restrict__ C32, int k, int d, float *__restrict__ B3)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (int64_t)k * d) return;
+    const int64_t c = i / d;
+    const int j = (int)(i % d);
+    float hi, lo;
+    tf32_split(C32[i], hi, lo);
+    B3[c * 3 * d + j] = hi;
+    B3[c * 3 * d + d + j] = lo;
+    B3[c * 3 * d + 2 * d + j] = hi;
+}
+
 int mrq_probe_tc_init(mrq_index *ix)
 {
     ix->probe_tc = nullptr;
@@ -390,8 +410,17 @@ int mrq_probe_tc_init(mrq_index *ix)
         return MRQ_ECUDA;
     }
     tc->encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
-    int rc = make_map(tc, &tc->mapB, ix->C32, ix->k, ix->d, TC_BN);
+    const int d3 = 3 * ix->d;
+    if (cudaMalloc(&tc->B3, (size_t)ix->k * d3 * 4) != cudaSuccess) {
+        delete tc;
+        mrq_set_error("cudaMalloc B3");
+        return MRQ_ENOMEM;
+    }
+    k_split3_b<<<(unsigned)(((int64_t)ix->k * ix->d + 255) / 256), 256, 0, ix->stream>>>(ix->C32, ix->k, ix->d, tc->B3);
+    MRQ_CUDA_TRY(cudaStreamSynchronize(ix->stream));
+    int rc = make_map(tc, &tc->mapB, tc->B3, ix->k, d3, TC_BN);
     if (rc != MRQ_OK) {
+        cudaFree(tc->B3);
         delete tc;
         return rc;
     }
@@ -410,7 +439,9 @@ int mrq_probe_tc_init(mrq_index *ix)
 
 void mrq_probe_tc_free(mrq_index *ix)
 {
-    delete (ProbeTC *)ix->probe_tc;
+    ProbeTC *tc = (ProbeTC *)ix->probe_tc;
+    if (tc && tc->B3) cudaFree(tc->B3);
+    delete tc;
     ix->probe_tc = nullptr;
 }
 
@@ -421,7 +452,7 @@ bool mrq_probe_tc_enabled(const mrq_index *ix)
 
 double mrq_probe_tc_kappa(const mrq_index *ix)
 {
-    return std::ldexp(1.0, -9) + (double)ix->d * std::ldexp(1.0, -22) + std::ldexp(1.0, -20);
+    return std::ldexp(1.0, -20) + 3.0 * (double)ix->d * std::ldexp(1.0, -23);
 }
 
 // G <= 7 x (query blocks): a block's tiles then span at most 8 CTAs, i.e. at
@@ -437,10 +468,10 @@ int mrq_probe_tc_run(mrq_index *ix, const float *qd32, int64_t nq, float *approx
 {
     ProbeTC *tc = (ProbeTC *)ix->probe_tc;
     CUtensorMap mapA;
-    int rc = make_map(tc, &mapA, qd32, (int)nq, ix->d, TC_BM);
+    int rc = make_map(tc, &mapA, qd32, (int)nq, 3 * ix->d, TC_BM);
     if (rc != MRQ_OK) return rc;
     const int G = tc_grid(ix, nq);
-    k_probe_tc<false><<<G, TC_THREADS, TC_SMEM, st>>>(mapA, tc->mapB, (int)nq, ix->k, ix->d, G, 1, ix->cn32, approx,
+    k_probe_tc<false><<<G, TC_THREADS, TC_SMEM, st>>>(mapA, tc->mapB, (int)nq, ix->k, 3 * ix->d, G, 1, ix->cn32, approx,
                                                        0, nullptr, 0.0, 0.0, nullptr, 0, nullptr, nullptr);
     MRQ_CUDA_TRY(cudaGetLastError());
     return MRQ_OK;
@@ -467,11 +498,11 @@ int mrq_probe_tc_run_fused(mrq_index *ix, const float *qd32, int64_t nq, int np,
 {
     ProbeTC *tc = (ProbeTC *)ix->probe_tc;
     CUtensorMap mapA;
-    int rc = make_map(tc, &mapA, qd32, (int)nq, ix->d, TC_BM);
+    int rc = make_map(tc, &mapA, qd32, (int)nq, 3 * ix->d, TC_BM);
     if (rc != MRQ_OK) return rc;
     const int G = tc_grid(ix, nq);
     const int maxparts = mrq_probe_tc_parts(ix, nq) / 2;
-    k_probe_tc<true><<<G, TC_THREADS, TC_SMEM, st>>>(mapA, tc->mapB, (int)nq, ix->k, ix->d, G, maxparts, ix->cn32,
+    k_probe_tc<true><<<G, TC_THREADS, TC_SMEM, st>>>(mapA, tc->mapB, (int)nq, ix->k, 3 * ix->d, G, maxparts, ix->cn32,
                                                       nullptr, np, qnorm, ix->cmax, kappa, cbuf, capp, ccnt, kvbuf);
     MRQ_CUDA_TRY(cudaGetLastError());
     return MRQ_OK;
