@@ -492,12 +492,13 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
             MRQ_CUDA_TRY(cudaFuncSetAttribute(k_qtail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsmem));
         k_qtail<<<(unsigned)((nq + 7) / 8), 256, qsmem, st>>>(qp, nq, D, d, W, ix->lam, ix->RT, p->resid_scale, p->m,
                                                               qr2, eps_r, r0, qd32, qnorm, qkey, qa3);
-        if (qkey) {   // the order's single-block sort runs beside r0 and the probe
-            MRQ_CUDA_TRY(cudaEventRecord(ix->ev_fork[0], st));
-            MRQ_CUDA_TRY(cudaStreamWaitEvent(ix->side, ix->ev_fork[0], 0));
-            launch_qorder(qkey, nq, qorder, ix->side);
-        }
-        launch_rowmat_f64(qp, nq, D, d, nullptr, ix->RT, d, r0, d, st);             // r0 = R q_d
+        // side stream, beside the probe: the order's single-block sort and
+        // r0 = R q_d (only the quantizer needs it)
+        MRQ_CUDA_TRY(cudaEventRecord(ix->ev_fork[0], st));
+        MRQ_CUDA_TRY(cudaStreamWaitEvent(ix->side, ix->ev_fork[0], 0));
+        if (qkey) launch_qorder(qkey, nq, qorder, ix->side);
+        launch_rowmat_f64(qp, nq, D, d, nullptr, ix->RT, d, r0, d, ix->side);
+        MRQ_CUDA_TRY(cudaEventRecord(ix->ev_fork[3], ix->side));
     }
     if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[1], st));
 
@@ -545,6 +546,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
         k_cand_count<<<(unsigned)((nq + 255) / 256), 256, 0, ix->side>>>(probe, nq, np, ix->list_size, cand_cnt);
         k_exclusive_scan<<<1, 1024, 0, ix->side>>>(cand_cnt, nq, f1_off);
         MRQ_CUDA_TRY(cudaEventRecord(ix->ev_fork[2], ix->side));
+        MRQ_CUDA_TRY(cudaStreamWaitEvent(st, ix->ev_fork[3], 0));   // r0
         launch_quant(probe, probe_qn2, nq, np, d, W, r0, ix->Rc, qr2, p->eps0, planes, qconst, st);
         MRQ_CUDA_TRY(cudaStreamWaitEvent(st, ix->ev_fork[2], 0));
     }

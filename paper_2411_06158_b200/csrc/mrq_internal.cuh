@@ -46,7 +46,7 @@ struct mrq_index {
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[12] = {};
     cudaStream_t side = nullptr;      // fork/join stream for the single-block kernels (query order, F1 offsets)
-    cudaEvent_t ev_fork[3] = {};
+    cudaEvent_t ev_fork[4] = {};
     int64_t N = 0, npad = 0;
     int D = 0, d = 0, k = 0, W = 0;
     int rank = 0, world = 1;
