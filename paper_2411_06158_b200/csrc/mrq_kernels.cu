@@ -15,40 +15,47 @@
 // x_p = P (x - mu) (Alg.1 L3 P:283 for base vectors, Alg.2 L1 P:303 for
 // queries; MT = P^T) and for r0 = R q_d (Alg.2 L4 P:306; MT = R^T, mu = 0).
 // Register-tiled across rows and outputs only, which leaves each output's
-// reduction order untouched: a 64-row x 64-output tile per 256-thread block,
+// reduction order untouched: a 32-row x 64-output tile per 128-thread block,
 // 4 x 4 outputs per thread, j in shared-memory chunks of 16 (8 shared loads
 // feed 16 products); the next chunk's global loads are issued before the
 // current chunk is consumed.  Padded j (beyond Din) contribute exact zeros,
 // which never change a sum that starts at +0.
-#define PJ_T 64
+#define PJ_TR 32   // rows per block tile (32 x 64 tiles, 128 threads: ~4 resident blocks per SM, no tail wave)
+#define PJ_TC 64   // outputs per block tile
 #define PJ_K 16
+#define PJ_NT ((PJ_TR / 4) * (PJ_TC / 4))
 template <typename TIn>
-__global__ void __launch_bounds__(256) k_rowmat(const TIn *__restrict__ X, int64_t nrows, int ldx, int Din,
-                                                const double *__restrict__ mu, const double *__restrict__ MT,
-                                                int Dout, double *__restrict__ out, int ldo)
+__global__ void __launch_bounds__(PJ_NT) k_rowmat(const TIn *__restrict__ X, int64_t nrows, int ldx, int Din,
+                                                  const double *__restrict__ mu, const double *__restrict__ MT,
+                                                  int Dout, double *__restrict__ out, int ldo)
 {
-    __shared__ double us[PJ_K][PJ_T + 1];
-    __shared__ double ps[PJ_K][PJ_T + 1];
+    __shared__ double us[PJ_K][PJ_TR + 1];
+    __shared__ double ps[PJ_K][PJ_TC + 1];
+    constexpr int NU = PJ_TR * PJ_K / PJ_NT, NP = PJ_K * PJ_TC / PJ_NT;
     const int tid = threadIdx.x;
-    const int tx = tid & 15, ty = tid >> 4;
-    const int i0 = blockIdx.x * PJ_T;
-    const int64_t r0 = (int64_t)blockIdx.y * PJ_T;
+    const int tx = tid % (PJ_TC / 4), ty = tid / (PJ_TC / 4);
+    const int i0 = blockIdx.x * PJ_TC;
+    const int64_t r0 = (int64_t)blockIdx.y * PJ_TR;
     double acc[4][4];
 #pragma unroll
     for (int r = 0; r < 4; r++)
 #pragma unroll
         for (int c = 0; c < 4; c++) acc[r][c] = 0.0;
-    double ur[4], pr[4];
+    double ur[NU], pr[NP];
     auto fetch = [&](int j0) {
 #pragma unroll
-        for (int k = 0; k < 4; k++) {
-            const int t = tid + 256 * k;
+        for (int k = 0; k < NU; k++) {
+            const int t = tid + PJ_NT * k;
             const int rr = t / PJ_K, jj = t % PJ_K;
             const int64_t r = r0 + rr;
             const int j = j0 + jj;
             ur[k] = 0.0;
             if (r < nrows && j < Din) ur[k] = mu ? ((double)X[r * ldx + j] - mu[j]) : (double)X[r * ldx + j];
-            const int ii = t % PJ_T, jq = t / PJ_T;
+        }
+#pragma unroll
+        for (int k = 0; k < NP; k++) {
+            const int t = tid + PJ_NT * k;
+            const int ii = t % PJ_TC, jq = t / PJ_TC;
             const int i = i0 + ii, jp = j0 + jq;
             pr[k] = (jp < Din && i < Dout) ? MT[(int64_t)jp * Dout + i] : 0.0;
         }
@@ -56,10 +63,14 @@ __global__ void __launch_bounds__(256) k_rowmat(const TIn *__restrict__ X, int64
     fetch(0);
     for (int j0 = 0; j0 < Din; j0 += PJ_K) {
 #pragma unroll
-        for (int k = 0; k < 4; k++) {
-            const int t = tid + 256 * k;
+        for (int k = 0; k < NU; k++) {
+            const int t = tid + PJ_NT * k;
             us[t % PJ_K][t / PJ_K] = ur[k];
-            ps[t / PJ_T][t % PJ_T] = pr[k];
+        }
+#pragma unroll
+        for (int k = 0; k < NP; k++) {
+            const int t = tid + PJ_NT * k;
+            ps[t / PJ_TC][t % PJ_TC] = pr[k];
         }
         __syncthreads();
         if (j0 + PJ_K < Din) fetch(j0 + PJ_K);
@@ -67,9 +78,9 @@ __global__ void __launch_bounds__(256) k_rowmat(const TIn *__restrict__ X, int64
         for (int jj = 0; jj < PJ_K; jj++) {
             double a[4], b[4];
 #pragma unroll
-            for (int r = 0; r < 4; r++) a[r] = us[jj][ty + 16 * r];
+            for (int r = 0; r < 4; r++) a[r] = us[jj][ty + (PJ_TR / 4) * r];
 #pragma unroll
-            for (int c = 0; c < 4; c++) b[c] = ps[jj][tx + 16 * c];
+            for (int c = 0; c < 4; c++) b[c] = ps[jj][tx + (PJ_TC / 4) * c];
 #pragma unroll
             for (int r = 0; r < 4; r++)
 #pragma unroll
@@ -79,11 +90,11 @@ __global__ void __launch_bounds__(256) k_rowmat(const TIn *__restrict__ X, int64
     }
 #pragma unroll
     for (int r = 0; r < 4; r++) {
-        const int64_t row = r0 + ty + 16 * r;
+        const int64_t row = r0 + ty + (PJ_TR / 4) * r;
         if (row >= nrows) continue;
 #pragma unroll
         for (int c = 0; c < 4; c++) {
-            const int i = i0 + tx + 16 * c;
+            const int i = i0 + tx + (PJ_TC / 4) * c;
             if (i < Dout) out[row * ldo + i] = acc[r][c];
         }
     }
@@ -92,15 +103,23 @@ __global__ void __launch_bounds__(256) k_rowmat(const TIn *__restrict__ X, int64
 void launch_rowmat_f32(const float *X, int64_t nrows, int ldx, int Din, const double *mu, const double *MT, int Dout,
                        double *out, int ldo, cudaStream_t st)
 {
-    dim3 grid((Dout + PJ_T - 1) / PJ_T, (unsigned)((nrows + PJ_T - 1) / PJ_T));
-    k_rowmat<float><<<grid, 256, 0, st>>>(X, nrows, ldx, Din, mu, MT, Dout, out, ldo);
+    const int64_t CH = (int64_t)65535 * PJ_TR;   // grid.y limit
+    for (int64_t r = 0; r < nrows; r += CH) {
+        const int64_t n = nrows - r < CH ? nrows - r : CH;
+        dim3 grid((Dout + PJ_TC - 1) / PJ_TC, (unsigned)((n + PJ_TR - 1) / PJ_TR));
+        k_rowmat<float><<<grid, PJ_NT, 0, st>>>(X + r * ldx, n, ldx, Din, mu, MT, Dout, out + r * ldo, ldo);
+    }
 }
 
 void launch_rowmat_f64(const double *X, int64_t nrows, int ldx, int Din, const double *mu, const double *MT,
                        int Dout, double *out, int ldo, cudaStream_t st)
 {
-    dim3 grid((Dout + PJ_T - 1) / PJ_T, (unsigned)((nrows + PJ_T - 1) / PJ_T));
-    k_rowmat<double><<<grid, 256, 0, st>>>(X, nrows, ldx, Din, mu, MT, Dout, out, ldo);
+    const int64_t CH = (int64_t)65535 * PJ_TR;   // grid.y limit
+    for (int64_t r = 0; r < nrows; r += CH) {
+        const int64_t n = nrows - r < CH ? nrows - r : CH;
+        dim3 grid((Dout + PJ_TC - 1) / PJ_TC, (unsigned)((n + PJ_TR - 1) / PJ_TR));
+        k_rowmat<double><<<grid, PJ_NT, 0, st>>>(X + r * ldx, n, ldx, Din, mu, MT, Dout, out + r * ldo, ldo);
+    }
 }
 
 // ======================================================================= a0
