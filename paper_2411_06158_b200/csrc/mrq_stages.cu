@@ -166,7 +166,7 @@ __device__ __forceinline__ void f2_compact(int64_t q, int mode, int n1, uint64_t
 // for every F1 entry HEAD = ||x_d - q_d||^2 (left to right over i < d),
 // dis_o' = (HEAD + ||x_r||^2) + ||q_r||^2, and the global id, written to the
 // entry's F1 slot (f1_head, f1_diso, f1_id).
-__global__ void __launch_bounds__(256) k_head_b(
+__global__ void __launch_bounds__(128) k_head_b(
     int aligned, int D, int d, const uint32_t *__restrict__ ids, const float *__restrict__ heads,
     const float *__restrict__ xr2, const double *__restrict__ qp, const double *__restrict__ qr2_arr,
     const uint64_t *__restrict__ f1_off, const uint32_t *__restrict__ f1_cnt, const uint32_t *__restrict__ f1_pos,
@@ -177,12 +177,15 @@ __global__ void __launch_bounds__(256) k_head_b(
     const int warp = threadIdx.x >> 5, wpb = blockDim.x >> 5;
     const int64_t q = qorder ? (int64_t)qorder[blockIdx.x] : (int64_t)blockIdx.x;
     float *tile = (float *)wsm + warp * MRQ_RG_FLOATS;
+    double *qs = (double *)((float *)wsm + wpb * MRQ_RG_FLOATS);   // q_d staged once per block
+    for (int i = threadIdx.x; i < d; i += blockDim.x) qs[i] = qp[q * D + i];
+    __syncthreads();
     const uint64_t base = f1_off[q];
     const int n1 = (int)f1_cnt[q];
     const double qr2 = qr2_arr[q];
     float xr2v = 0.f;   // ||x_r||^2 and id of the lane's row, loaded while the row is in flight
     uint32_t idv = 0;
-    warp_rows(aligned, heads, d, 0, d, qp + q * D, n1, tile, [&](int e) { return f1_pos[base + e]; },
+    warp_rows(aligned, heads, d, 0, d, qs, n1, tile, [&](int e) { return f1_pos[base + e]; },
               [&](int, uint32_t slot) {
                   xr2v = xr2[slot];
                   idv = ids[slot];
@@ -611,7 +614,7 @@ int launch_stage2_w(const StageArgs &a, cudaStream_t st, cudaEvent_t after_gathe
 {
     {   // gather half: block per query, its 4 warps split the F1 rows (4 measured best of 2/4/8)
         const int wpb = 4;
-        const size_t smem = (size_t)wpb * MRQ_RG_FLOATS * 4;
+        const size_t smem = (size_t)wpb * MRQ_RG_FLOATS * 4 + (size_t)a.d * 8;
         int rc = set_attr((const void *)k_head_b, smem);
         if (rc) return rc;
         k_head_b<<<(unsigned)a.nq, wpb * 32, smem, st>>>(a.aligned, a.D, a.d, a.ids, a.heads, a.xr2, a.qp, a.qr2,
