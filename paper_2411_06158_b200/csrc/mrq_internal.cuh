@@ -825,6 +825,7 @@ __device__ __forceinline__ double mrq_lb1(const uint32_t *code, const uint32_t *
 #define MRQ_RG_STRIDE (MRQ_RG_CH + 4)
 #define MRQ_RG_STAGE (32 * MRQ_RG_STRIDE)
 #define MRQ_RG_FLOATS (2 * MRQ_RG_STAGE)       // >= 32 * 33 (the unaligned fallback's tile)
+#define MRQ_QS(D) (((D) + 1) & ~1)              // doubles of a staged query row (16-B multiple)
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 

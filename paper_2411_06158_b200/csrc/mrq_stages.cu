@@ -33,11 +33,16 @@ __global__ void __launch_bounds__(256) k_seed_w(
     const int64_t qi = (int64_t)blockIdx.x * wpb + warp;
     if (qi >= nq) return;
     const int64_t q = qorder ? (int64_t)qorder[qi] : qi;
-    float *tile = (float *)wsm + warp * MRQ_RG_FLOATS;
-    SelItem *lst = (SelItem *)((float *)wsm + wpb * MRQ_RG_FLOATS) + (size_t)warp * MRQ_SELREG(Kp);
+    // shared memory: [query rows (MRQ_QS(D) doubles per warp)][gather tiles][selection lists]
+    double *qs = (double *)wsm + (size_t)warp * MRQ_QS(D);
+    float *tile = (float *)((double *)wsm + (size_t)wpb * MRQ_QS(D)) + warp * MRQ_RG_FLOATS;
+    SelItem *lst = (SelItem *)((float *)((double *)wsm + (size_t)wpb * MRQ_QS(D)) + wpb * MRQ_RG_FLOATS) +
+                   (size_t)warp * MRQ_SELREG(Kp);
     SelItem *queue = lst + Kp;
+    for (int i = lane; i < D; i += 32) qs[i] = qp[q * D + i];   // the query row, read by every gathered row
+    __syncwarp();
     const double eps_r = eps_r_arr[q];
-    const double *qrow = qp + q * D;
+    const double *qrow = qs;
     // the pool is defined on GLOBAL list sizes (decision T); a rank scans only
     // the lists it owns (list_size = 0 for the others).  each(it, valid) sees
     // every pool item (dis', id, slot) of this rank, 32 at a time.
@@ -223,14 +228,19 @@ __global__ void __launch_bounds__(256) k_stage2_w(
     const int64_t qi = (int64_t)blockIdx.x * wpb + warp;
     if (qi >= nq) return;
     const int64_t q = qorder ? (int64_t)qorder[qi] : qi;
-    float *tile = (float *)wsm + warp * MRQ_RG_FLOATS;
-    SelItem *lst = (SelItem *)((float *)wsm + wpb * MRQ_RG_FLOATS) + (size_t)warp * MRQ_SELREG(Kp);
+    // shared memory: [query rows (MRQ_QS(D) doubles per warp)][gather tiles][selection lists]
+    double *qs = (double *)wsm + (size_t)warp * MRQ_QS(D);
+    float *tile = (float *)((double *)wsm + (size_t)wpb * MRQ_QS(D)) + warp * MRQ_RG_FLOATS;
+    SelItem *lst = (SelItem *)((float *)((double *)wsm + (size_t)wpb * MRQ_QS(D)) + wpb * MRQ_RG_FLOATS) +
+                   (size_t)warp * MRQ_SELREG(Kp);
     SelItem *queue = lst + Kp;
+    for (int i = lane; i < D; i += 32) qs[i] = qp[q * D + i];   // the query row, read by every gathered row
+    __syncwarp();
     const bool sel1 = mode == 0 && tight;
     const uint64_t base = f1_off[q];
     const int n1 = (int)f1_cnt[q];
     const double eps_r = eps_r_arr[q];
-    const double *qrow = qp + q * D;
+    const double *qrow = qs;
     double tau1 = tau0_arr[q];
     if (sel1) {
         WarpSelT<MG> top;
@@ -365,16 +375,20 @@ __global__ void __launch_bounds__(64) k_topk_w(
     extern __shared__ unsigned char wsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
     const int64_t q = qorder ? (int64_t)qorder[blockIdx.x] : (int64_t)blockIdx.x;
-    float *tile = (float *)wsm + warp * MRQ_RG_FLOATS;
-    SelItem *lst = (SelItem *)((float *)wsm + wpb * MRQ_RG_FLOATS);
+    // shared memory: [query tail][gather tiles][selection list]
+    double *qs = (double *)wsm;
+    float *tile = (float *)(qs + MRQ_QS(D)) + warp * MRQ_RG_FLOATS;
+    SelItem *lst = (SelItem *)((float *)(qs + MRQ_QS(D)) + wpb * MRQ_RG_FLOATS);
     SelItem *queue = lst + K;
+    for (int i = d + threadIdx.x; i < D; i += blockDim.x) qs[i] = qp[q * D + i];
+    __syncthreads();
     const int ns0 = (int)s0_cnt[q], ns1 = (int)s1_cnt[q], n2 = (int)f2_cnt[q];
     const uint64_t base = f1_off[q];
     // a7 exact re-rank of F2 (Alg.2 L14 P:316): exact = HEAD continued over
     // the tail = ||x_p - q_p||^2 left to right over i = 0..D-1 (R-8)
     // (the block's warps split the F2 rows; warp 0 then selects)
     if (D > d)
-        warp_rows(aligned, tails, D - d, 0, D - d, qp + q * D + d, n2, tile, [&](int e) { return f2_pos[base + e]; },
+        warp_rows(aligned, tails, D - d, 0, D - d, qs + d, n2, tile, [&](int e) { return f2_pos[base + e]; },
                   [&](int e, uint32_t) { return f2_head[base + e]; }, [&](int e, bool v, double acc) {
                       if (v) f2_exact[base + e] = acc;
                   }, warp, wpb);
@@ -581,7 +595,7 @@ static int set_attr(const void *fn, size_t smem)
 
 int launch_seed_w(int W, const StageArgs &a, cudaStream_t st)
 {
-    const size_t per = MRQ_RG_FLOATS * 4 + (size_t)MRQ_SELREG(a.Kp) * sizeof(SelItem);
+    const size_t per = (size_t)MRQ_QS(a.D) * 8 + MRQ_RG_FLOATS * 4 + (size_t)MRQ_SELREG(a.Kp) * sizeof(SelItem);
     const int wpb = warps_for(per);
     const size_t smem = per * wpb;
     const unsigned grid = (unsigned)((a.nq + wpb - 1) / wpb);
@@ -622,7 +636,8 @@ int launch_stage2_w(const StageArgs &a, cudaStream_t st, cudaEvent_t after_gathe
                                                           a.qorder);
     }
     if (after_gather) MRQ_CUDA_TRY(cudaEventRecord(after_gather, st));
-    const size_t per = MRQ_RG_FLOATS * 4 + (size_t)MRQ_SELREG(std::max(a.Kp, a.K)) * sizeof(SelItem);
+    const size_t per = (size_t)MRQ_QS(a.D) * 8 + MRQ_RG_FLOATS * 4 +
+                       (size_t)MRQ_SELREG(std::max(a.Kp, a.K)) * sizeof(SelItem);
     const int wpb = warps_for(per);
     const size_t smem = per * wpb;
     auto fn = std::max(a.Kp, a.K) > MRQ_MERGE_MIN ? k_stage2_w<true> : k_stage2_w<false>;
@@ -672,7 +687,8 @@ int launch_exact_count(const StageArgs &a, cudaStream_t st)
 int launch_topk_w(const StageArgs &a, cudaStream_t st)
 {
     const int wpb = a.tight ? 1 : 2;
-    const size_t smem = (size_t)wpb * MRQ_RG_FLOATS * 4 + (size_t)MRQ_SELREG(a.K) * sizeof(SelItem);
+    const size_t smem =
+        (size_t)MRQ_QS(a.D) * 8 + (size_t)wpb * MRQ_RG_FLOATS * 4 + (size_t)MRQ_SELREG(a.K) * sizeof(SelItem);
     auto fn = a.K > MRQ_MERGE_MIN ? k_topk_w<true> : k_topk_w<false>;
     int rc = set_attr((const void *)fn, smem);
     if (rc) return rc;
