@@ -359,8 +359,8 @@ __global__ void __launch_bounds__(256) k_f2_w(int64_t nq, int mode, const double
 // distances rounded to fp32, padding id -1 / +inf.  Sharded (xout != NULL):
 // the local top-K (exact fp64, id) goes to the exchange and k_xmerge writes
 // the outputs.
-// Block of 1 or 2 warps per query: the warps split the F2 re-rank rows,
-// warp 0 selects.  2 for LOOSE (F2 ~ 2x larger), 1 for TIGHT (measured).
+// Block per query (MRQ_TOPK_WPB warps split the F2 re-rank rows, warp 0
+// selects; 1 measured best once the query row is staged in shared memory).
 template <bool MG>
 __global__ void __launch_bounds__(64) k_topk_w(
     int64_t nq, int K, int Kp, const uint32_t *__restrict__ ids, const uint32_t *__restrict__ s0_cnt,
@@ -686,7 +686,10 @@ int launch_exact_count(const StageArgs &a, cudaStream_t st)
 
 int launch_topk_w(const StageArgs &a, cudaStream_t st)
 {
-    const int wpb = a.tight ? 1 : 2;
+#ifndef MRQ_TOPK_WPB
+#define MRQ_TOPK_WPB 1   // with the query row in shared memory one warp beats 2 (LOOSE 0.177 -> 0.149 ms)
+#endif
+    const int wpb = MRQ_TOPK_WPB;
     const size_t smem =
         (size_t)MRQ_QS(a.D) * 8 + (size_t)wpb * MRQ_RG_FLOATS * 4 + (size_t)MRQ_SELREG(a.K) * sizeof(SelItem);
     auto fn = a.K > MRQ_MERGE_MIN ? k_topk_w<true> : k_topk_w<false>;
