@@ -627,7 +627,10 @@ int launch_seed_w(int W, const StageArgs &a, cudaStream_t st)
 int launch_stage2_w(const StageArgs &a, cudaStream_t st, cudaEvent_t after_gather)
 {
     {   // gather half: block per query, its 4 warps split the F1 rows (4 measured best of 2/4/8)
-        const int wpb = 4;
+#ifndef MRQ_HEAD_WPB
+#define MRQ_HEAD_WPB 4   // measured best of 2/4/8 (launch bounds 128)
+#endif
+        const int wpb = MRQ_HEAD_WPB;
         const size_t smem = (size_t)wpb * MRQ_RG_FLOATS * 4 + (size_t)a.d * 8;
         int rc = set_attr((const void *)k_head_b, smem);
         if (rc) return rc;
