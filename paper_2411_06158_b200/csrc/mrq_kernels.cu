@@ -331,6 +331,11 @@ __global__ void __launch_bounds__(256) k_quant_g(const uint32_t *__restrict__ pr
         hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o, G));
     }
     const double delta = (hi - lo) / 15.0;
+    // level = floor((r - lo) / delta + 0.5), canonical (IEEE division).  Fast
+    // path: y = (r - lo) * (1/delta) + 0.5 is within 1e-14 of the canonical
+    // fl(fl((r - lo) / delta) + 0.5) (both quotients <= 15); unless y is
+    // within 1e-12 of an integer the two floors agree, else divide.
+    const double inv = delta > 0.0 ? 1.0 / delta : 0.0;
     int sumL = 0;
     uint32_t bits[MRQ_BQ] = {0u, 0u, 0u, 0u};
 #pragma unroll
@@ -338,7 +343,9 @@ __global__ void __launch_bounds__(256) k_quant_g(const uint32_t *__restrict__ pr
         const int j = s * E + t;
         int v = 0;
         if (ok && j < d && delta > 0.0) {
-            const double f = floor((rv[t] - lo) / delta + 0.5);
+            const double y = (rv[t] - lo) * inv + 0.5;
+            double f = floor(y);
+            if (y - f < 1e-12 || f + 1.0 - y < 1e-12) f = floor((rv[t] - lo) / delta + 0.5);
             v = f < 0.0 ? 0 : (f > 15.0 ? 15 : (int)f);
         }
         sumL += v;
