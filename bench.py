@@ -55,85 +55,70 @@ def peaks():
         return 6650.0, "fallback"
 
 
-_SAMPLER = r"""
-import sys, time, select
-import pynvml as n
-n.nvmlInit()
-h = n.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
-names = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
-         ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
-         ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
-         ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
-         ("hw_power_brake_slowdown", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
-mx = n.nvmlDeviceGetMaxClockInfo(h, n.NVML_CLOCK_SM)
-print("ready", flush=True)
-sys.stdin.readline()          # "go": the timed region starts
-while True:
-    r, _, _ = select.select([sys.stdin], [], [], 0.001)
-    if r and not sys.stdin.readline():
-        break
-    sm = n.nvmlDeviceGetClockInfo(h, n.NVML_CLOCK_SM)
-    rs = n.nvmlDeviceGetCurrentClocksEventReasons(h)
-    act = ",".join(nm for nm, at in names if rs & getattr(n, at, 0)) or "-"
-    print("%.6f %d %d %s" % (time.time(), sm, mx, act), flush=True)
-"""
-
-
 class Clocks:
     """SM clock and clock-event (throttle) reasons sampled DURING the timed
-    region (B200_PROFILING.md clocks line) by a separate sampler process (NVML
-    every ~1 ms, so the GIL of this process cannot starve it); only samples
-    whose timestamps fall inside the region count.  Start it before the
-    warm-up (start()), then bracket the timed region with `with clk:`."""
+    region (B200_PROFILING.md clocks line): the timed steps are enqueued
+    asynchronously, then this process polls NVML (in-process, tens of us per
+    sample) until the last step's end event completes, so every sample is
+    taken while the GPU runs the timed work.  start() before the warm-up, then
+    bracket the timed region with `with clk:` and call poll_until(event)."""
+
+    NAMES = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+             ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+             ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+             ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+             ("hw_power_brake_slowdown", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
 
     def __init__(self, gpu=0):
         self.gpu = gpu
-        self.proc = None
+        self.h = None
+        self.nvml = None
         self.err = None
-        self.t0 = self.t1 = None
-        self.lines = []
+        self.mx = None
+        self.samples = []
+        self.active = False
 
     def start(self):
         try:
-            self.proc = subprocess.Popen([sys.executable, "-c", _SAMPLER, str(self.gpu)], stdin=subprocess.PIPE,
-                                         stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)
-            ready = self.proc.stdout.readline()
-            if not ready.startswith("ready"):
-                self.err = (ready + self.proc.stderr.read())[:200]
-                self.proc = None
+            import pynvml as n
+            n.nvmlInit()
+            self.nvml = n
+            self.h = n.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.mx = n.nvmlDeviceGetMaxClockInfo(self.h, n.NVML_CLOCK_SM)
         except Exception as e:  # pragma: no cover
-            self.err = str(e)
-            self.proc = None
+            self.err = str(e)[:200]
+            self.h = None
         return self
 
+    def sample(self):
+        if self.h is None or not self.active:
+            return
+        n = self.nvml
+        sm = n.nvmlDeviceGetClockInfo(self.h, n.NVML_CLOCK_SM)
+        rs = n.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        self.samples.append((sm, [nm for nm, at in self.NAMES if rs & getattr(n, at, 0)]))
+
+    def poll_until(self, event):
+        """Sample while the GPU still runs the timed work (event not done)."""
+        while not event.query():
+            self.sample()
+        if not self.samples:   # the work ended before the first sample: one right at the end
+            self.sample()
+
     def __enter__(self):
-        if self.proc:
-            self.proc.stdin.write("go\n")
-            self.proc.stdin.flush()
-            time.sleep(0.002)
-        self.t0 = time.time()
+        self.active = True
         return self
 
     def __exit__(self, *a):
-        self.t1 = time.time()
-        if self.proc:
-            time.sleep(0.003)
-            self.proc.stdin.close()
-            self.lines = self.proc.stdout.read().splitlines()
-            self.proc.wait(10)
+        self.active = False
 
     def summary(self):
-        samples = []
-        for ln in self.lines:
-            p = ln.split()
-            if len(p) == 4 and self.t0 <= float(p[0]) <= self.t1 + 0.002:
-                samples.append((float(p[1]), float(p[2]), [] if p[3] == "-" else p[3].split(",")))
-        if not samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "error": self.err,
-                    "source": "nvml sampler process"}
-        return {"sm_mhz": float(np.median([x[0] for x in samples])), "sm_max_mhz": max(x[1] for x in samples),
-                "reasons": sorted({r for x in samples for r in x[2]}), "samples": len(samples),
-                "source": "nvml sampler process, ~1 ms"}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.mx, "reasons": ["unsampled"], "error": self.err,
+                    "source": "nvml, in-process polling during the timed region"}
+        return {"sm_mhz": float(np.median([x[0] for x in self.samples])), "sm_max_mhz": self.mx,
+                "reasons": sorted({r for x in self.samples for r in x[1]}), "samples": len(self.samples),
+                "source": "nvml, in-process polling while the timed steps run"}
 
 
 def dist_env():
@@ -348,6 +333,8 @@ def main():
             ev[i][0].record(stream)
             run(nprobe, tau_sel, stats=False)          # asynchronous: no host round trip inside the step
             ev[i][1].record(stream)
+            clk.sample()
+        clk.poll_until(ev[-1][1])                      # clocks sampled while the queued steps run
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
