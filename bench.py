@@ -378,6 +378,9 @@ def main():
         kk["frac"] = round(kk["achieved_gbs"] / hbm, 4)
         kk["ms"] = round(kk["ms"], 4)
         kk["traffic"] = traffic.get(nm, next((v for k, v in traffic.items() if k.startswith(nm + "<")), None))
+        if kk["traffic"]:   # the DRAM side: ncu bytes per launch over the same launch time
+            kk["dram_gbs"] = round(kk["traffic"] / (kk["ms"] * 1e-3) / 1e9, 1)
+            kk["dram_frac"] = round(kk["dram_gbs"] / hbm, 4)
     dom = max(kern, key=lambda n: kern[n]["ms"])
     # the probe screen GEMM on the tensor cores (kind::tf32): its flops against
     # the tf32 peak = measured bf16 burst x the nominal tf32/bf16 ratio (1.1/2.25)
@@ -454,7 +457,9 @@ def main():
                      "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": kern[dom]["traffic"],
                      "bytes_per_unit": kern[dom]["bytes_per_unit"], "unit_kind": kern[dom]["unit"],
                      "kernels": kern, "codes_per_s_per_gpu": round(scanned / (ms_scan * 1e-3), 1),
-                     "scan_frac_of_hbm": kern["k_scan"]["frac"], "probe_gemm": probe_tc},
+                     "scan_frac_of_hbm": kern["k_scan"]["frac"], "probe_gemm": probe_tc,
+                     "note": "achieved = algorithmic bytes / launch time; above 1.0 when L2 serves re-reads "
+                             "(list-locality query order): dram_gbs / dram_frac give the DRAM side"},
         "e2e": {"value": round(nq / e2e_s, 1), "unit": "queries/s", "h2d_bytes_per_step": int(nq * X.shape[1] * 4),
                 "d2h_bytes_per_step": int(nq * K * 12)},
         "gpu_launches": launches_per_step * args.steps,
