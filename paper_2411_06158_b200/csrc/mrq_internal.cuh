@@ -821,7 +821,9 @@ __device__ __forceinline__ double mrq_lb1(const uint32_t *code, const uint32_t *
 // warp-uniform, so the compiler serializes the 32 lanes' copies.)
 // Per-warp shared memory: MRQ_RG_FLOATS floats.
 // Requirements: row stride, off and len multiples of 4 floats (16-B copies).
+#ifndef MRQ_RG_CH
 #define MRQ_RG_CH 32
+#endif
 #define MRQ_RG_STRIDE (MRQ_RG_CH + 4)
 #define MRQ_RG_STAGE (32 * MRQ_RG_STRIDE)
 #define MRQ_RG_FLOATS (2 * MRQ_RG_STAGE)       // >= 32 * 33 (the unaligned fallback's tile)
@@ -866,11 +868,14 @@ __device__ __forceinline__ void warp_gather_rows(const float *__restrict__ base,
         for (int i = 0; i < 8; i++) {
             const int r = (lane >> 3) + 4 * i;
             const uint32_t s = __shfl_sync(0xffffffffu, slot_cur, r);
-            if (r < cnt && u < nu) {
-                const unsigned d = smem_u32(dst0 + r * MRQ_RG_STRIDE);
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src0 + (int64_t)s * stride)
-                             : "memory");
-            }
+#pragma unroll
+            for (int uu = 0; uu < MRQ_RG_CH / 32; uu++)   // 128-B segments of the row chunk
+                if (r < cnt && u + 8 * uu < nu) {
+                    const unsigned d = smem_u32(dst0 + 32 * uu + r * MRQ_RG_STRIDE);
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d),
+                                 "l"(src0 + 32 * uu + (int64_t)s * stride)
+                                 : "memory");
+                }
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
