@@ -428,7 +428,10 @@ def main():
             cpu = {"value": None, "unit": "queries/s", "cores": os.cpu_count(), "kind": "oracle",
                    "sample": "failed: %s" % e}
 
-    launches_per_step = 14 + (4 if world > 1 else 0)   # DESIGN.md §8; + 3 k_xmerge + k_f2_w when sharded
+    # 13 kernels per search, + k_stage2_w for TIGHT; sharded: + k_xmerge (S0, final),
+    # + k_xmerge (S1) + k_f2_w for TIGHT
+    tight_sel = tau_sel == "TIGHT"
+    launches_per_step = 13 + (1 if tight_sel else 0) + ((4 if tight_sel else 2) if world > 1 else 0)
     out = {
         "metric": METRIC,
         "value": round(nq / (ms * 1e-3), 1),

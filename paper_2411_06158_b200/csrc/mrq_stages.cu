@@ -176,34 +176,65 @@ __global__ void __launch_bounds__(128) k_head_b(
     const float *__restrict__ xr2, const double *__restrict__ qp, const double *__restrict__ qr2_arr,
     const uint64_t *__restrict__ f1_off, const uint32_t *__restrict__ f1_cnt, const uint32_t *__restrict__ f1_pos,
     double *__restrict__ f1_head, double *__restrict__ f1_diso, uint32_t *__restrict__ f1_id,
-    const uint32_t *__restrict__ qorder)
+    const uint32_t *__restrict__ qorder, int fuse_f2, int mode, const double *__restrict__ eps_r_arr,
+    const double *__restrict__ tau0_arr, uint32_t *__restrict__ f2_cnt, uint32_t *__restrict__ f2_pos,
+    double *__restrict__ f2_head, uint32_t *__restrict__ s1_cnt, double *__restrict__ tau1_arr)
 {
     extern __shared__ unsigned char wsm[];
-    const int warp = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+    __shared__ uint32_t f2n;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
     const int64_t q = qorder ? (int64_t)qorder[blockIdx.x] : (int64_t)blockIdx.x;
     float *tile = (float *)wsm + warp * MRQ_RG_FLOATS;
     double *qs = (double *)((float *)wsm + wpb * MRQ_RG_FLOATS);   // q_d staged once per block
     for (int i = threadIdx.x; i < d; i += blockDim.x) qs[i] = qp[q * D + i];
+    if (threadIdx.x == 0) f2n = 0;
     __syncthreads();
     const uint64_t base = f1_off[q];
     const int n1 = (int)f1_cnt[q];
     const double qr2 = qr2_arr[q];
-    float xr2v = 0.f;   // ||x_r||^2 and id of the lane's row, loaded while the row is in flight
-    uint32_t idv = 0;
+    // fused F2 (every schedule but FULL/TIGHT: tau1 = tau0, no S1): the test
+    // of f2_compact on the dis_o' just formed, appended unordered (F2 is a set)
+    const double eps_r = fuse_f2 ? eps_r_arr[q] : 0.0, tau1 = fuse_f2 ? tau0_arr[q] : 0.0;
+    float xr2v = 0.f;   // ||x_r||^2, id and slot of the lane's row, loaded while the row is in flight
+    uint32_t idv = 0, slotv = 0;
     warp_rows(aligned, heads, d, 0, d, qs, n1, tile, [&](int e) { return f1_pos[base + e]; },
               [&](int, uint32_t slot) {
                   xr2v = xr2[slot];
                   idv = ids[slot];
+                  slotv = slot;
                   return 0.0;
               },
               [&](int e, bool v, double head) {
+                  double diso = 0.0;
                   if (v) {
+                      diso = (head + (double)xr2v) + qr2;
                       f1_head[base + e] = head;
-                      f1_diso[base + e] = (head + (double)xr2v) + qr2;
+                      f1_diso[base + e] = diso;
                       f1_id[base + e] = idv;
+                  }
+                  if (fuse_f2) {
+                      const bool pass = v && ((mode != 0) || (diso - eps_r < tau1));
+                      const unsigned bal = __ballot_sync(0xffffffffu, pass);
+                      if (bal) {
+                          uint32_t o = 0;
+                          if (lane == 0) o = atomicAdd(&f2n, (uint32_t)__popc(bal));
+                          o = __shfl_sync(0xffffffffu, o, 0) + __popc(bal & ((1u << lane) - 1u));
+                          if (pass) {
+                              f2_pos[base + o] = slotv;
+                              f2_head[base + o] = head;
+                          }
+                      }
                   }
               },
               warp, wpb);
+    if (fuse_f2) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            f2_cnt[q] = f2n;
+            s1_cnt[q] = 0;
+            tau1_arr[q] = tau1;
+        }
+    }
 }
 
 // Stage 2, decision half, warp per query.  TIGHT: S1 = the K' smallest
@@ -626,6 +657,9 @@ int launch_seed_w(int W, const StageArgs &a, cudaStream_t st)
 
 int launch_stage2_w(const StageArgs &a, cudaStream_t st, cudaEvent_t after_gather)
 {
+    // without an S1 selection (every schedule but FULL/TIGHT) stage 2 is the
+    // F2 test alone, done inside the head gather
+    const int fuse = !(a.mode == 0 && a.tight);
     {   // gather half: block per query, its 4 warps split the F1 rows (4 measured best of 2/4/8)
 #ifndef MRQ_HEAD_WPB
 #define MRQ_HEAD_WPB 4   // measured best of 2/4/8 (launch bounds 128)
@@ -636,9 +670,11 @@ int launch_stage2_w(const StageArgs &a, cudaStream_t st, cudaEvent_t after_gathe
         if (rc) return rc;
         k_head_b<<<(unsigned)a.nq, wpb * 32, smem, st>>>(a.aligned, a.D, a.d, a.ids, a.heads, a.xr2, a.qp, a.qr2,
                                                           a.f1_off, a.f1_cnt, a.f1_pos, a.f1_head, a.f1_diso, a.f1_id,
-                                                          a.qorder);
+                                                          a.qorder, fuse, a.mode, a.eps_r, a.tau0, a.f2_cnt, a.f2_pos,
+                                                          a.f2_head, a.s1_cnt, a.tau1);
     }
     if (after_gather) MRQ_CUDA_TRY(cudaEventRecord(after_gather, st));
+    if (fuse) return MRQ_OK;   // F2 written by the gather kernel
     const size_t per = (size_t)MRQ_QS(a.D) * 8 + MRQ_RG_FLOATS * 4 +
                        (size_t)MRQ_SELREG(std::max(a.Kp, a.K)) * sizeof(SelItem);
     const int wpb = warps_for(per);
