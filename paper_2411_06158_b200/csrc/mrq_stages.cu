@@ -892,7 +892,10 @@ __device__ __forceinline__ double sqdist_rows8(const double *__restrict__ cr, co
 // mrq_probe_tc.cu) is rescored in fp64 left to right over i and the np
 // smallest (qn2, c) are kept.  If a buffer overflowed, all k centroids are
 // rescored.
-__global__ void __launch_bounds__(128) k_probe_finish_w(int64_t nq, int k, int d, int np, const double *__restrict__ qp,
+#ifndef MRQ_PF_MINB
+#define MRQ_PF_MINB 10   // <= 48 registers: more resident warps (measured)
+#endif
+__global__ void __launch_bounds__(128, MRQ_PF_MINB) k_probe_finish_w(int64_t nq, int k, int d, int np, const double *__restrict__ qp,
                                                         int D, const double *__restrict__ C,
                                                         const double *__restrict__ qnorm, double cmax, double kappa,
                                                         const uint2 *__restrict__ cbuf, int P, int capp, int G,
