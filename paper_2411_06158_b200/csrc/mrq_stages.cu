@@ -16,8 +16,16 @@
 // hold >= K' candidates and number >= seed_lists form the pool; S0 = the K' smallest (dis', id) of the
 // pool; exact distances ||x_p - q_p||^2 (Alg.2 L14 P:316) of S0; tau0 = K-th
 // smallest exact over S0 (+inf if |S0| < K).
+#ifndef MRQ_SEED_MINB
+#define MRQ_SEED_MINB 32  // one-warp blocks, 32 resident per SM: <= 64 registers (seed 0.134 -> 0.126 ms); 0: plain bounds
+#endif
+#if MRQ_SEED_MINB > 0   // (short codes only: W > 2 would spill at 64 registers)
+#define MRQ_SEED_LB __launch_bounds__(W <= 2 ? 32 : 256, W <= 2 ? MRQ_SEED_MINB : 0)
+#else
+#define MRQ_SEED_LB __launch_bounds__(256)
+#endif
 template <int W, bool MG>
-__global__ void __launch_bounds__(256) k_seed_w(
+__global__ void MRQ_SEED_LB k_seed_w(
     int64_t nq, int aligned, const uint32_t *__restrict__ probe, int np, int K, int Kp, int D, int d, int64_t npad,
     const uint32_t *__restrict__ list_off, const uint32_t *__restrict__ list_size, const uint32_t *__restrict__ ids,
     const uint32_t *__restrict__ codes, const float *__restrict__ f1, const float *__restrict__ f2,
