@@ -336,6 +336,36 @@ def test_distance_level_unbiased_and_eq5(tiny):
     assert viol / tot <= (1.0 - erf(1.9 / sqrt(2.0))) + 0.01
 
 
+@pytest.mark.parametrize("eps0", [0.5, 1.0, 1.9])
+def test_eq5_bound_width_two_sided(eps0):
+    """Eq.5 pinned from BOTH sides at the distance level (d = D, the
+    unquantized query, est_kind 1, mode NOCORR): the standardized estimator
+    error is close to Gaussian (RaBitQ's concentration), so the share
+    of candidates with |dis' - dis| > eps_b = eb*f3 must track the Gaussian
+    tail 2(1 - Phi(eps0)) -- not exceed it (a bound too narrow) and not fall
+    far below it (a bound too wide: 2x wider at eps0 = 0.5 gives ~0.30 against
+    the tail's 0.62).  Tolerances: -15% relative -0.01 / +0.01 absolute."""
+    from math import erf, sqrt
+    import synth
+    cfg = synth.config_by_name("tiny")
+    X, Q = synth.generate(cfg, N=4000, Q=20, D=32)
+    bf = B.build(X, 32, 8)
+    ix = oracle.Index(bf, X)
+    full = np.concatenate([ix.head, ix.tail], 1).astype(np.float64)
+    _, _, _, dp = ix.search(Q, K=10, nprobe=8, mode="NOCORR", est_kind=1, dump=True, eps0=eps0)
+    viol, tot = 0, 0
+    for qi in range(Q.shape[0]):
+        n = dp["scan_cnt"][qi]
+        ids = dp["scan_ids"][qi, :n]
+        exact = ((full[ids] - dp["qp"][qi]) ** 2).sum(1)
+        epsb = dp["scan_dis"][qi, :n] - dp["scan_lb1"][qi, :n]     # eps_r = 0 at d = D
+        viol += int(np.sum(np.abs(dp["scan_dis"][qi, :n] - exact) > epsb))
+        tot += n
+    tail = 1.0 - erf(eps0 / sqrt(2.0))
+    rate = viol / tot
+    assert tail * 0.85 - 0.01 <= rate <= tail + 0.01, (rate, tail)
+
+
 # ------------------------------------------------------------ L4: search
 
 def test_exact_mode_equals_bruteforce(tiny):
@@ -375,7 +405,17 @@ def _check_tau_schedule(ix, Q, K, nprobe, tau):
         s0 = np.sort(dp["s0_exact"][qi, :dp["s0_cnt"][qi]])
         t0 = s0[K - 1] if len(s0) >= K else np.inf
         assert dp["tau0"][qi] == t0
-        assert dp["s0_cnt"][qi] == min(Kp, n) or dp["s0_cnt"][qi] <= Kp
+        # the seed pool (decision T): the probed lists in probe
+        # order until they hold >= K' candidates; S0 = the K' smallest
+        # (dis', id) of the pool -- scan order is probe order, so the pool is
+        # the first `pool` scanned candidates
+        sizes = np.array([ix.list_off[c + 1] - ix.list_off[c] for c in dp["probe"][qi]])
+        cum = np.cumsum(sizes)
+        pool = int(cum[min(int(np.searchsorted(cum, Kp)), len(cum) - 1)])
+        assert dp["s0_cnt"][qi] == min(Kp, pool)
+        pd = dp["scan_dis"][qi, :pool]
+        order = np.lexsort((sid[:pool], pd))[:min(Kp, pool)]
+        assert sorted(sid[:pool][order].tolist()) == sorted(dp["s0_ids"][qi, :dp["s0_cnt"][qi]].tolist())
         # P-11 pruning safety: every c not in F1 has LB1 >= tau0, every c in F1 has LB1 < tau0
         inf1 = np.array([i in f1 for i in sid.tolist()])
         assert np.all(lb1[~inf1] >= t0) and np.all(lb1[inf1] < t0)
@@ -413,6 +453,67 @@ def test_full_matches_exact_except_bound_failures(tiny):
         # the literal sequential Alg.2 also tracks EXACT
         i_s, _, _ = ix.search(Q, K=10, nprobe=npb, mode="SEQ")
         assert oracle.recall_at_k(i_s, gi, 10) >= oracle.recall_at_k(ie, gi, 10) - 0.02
+
+
+@pytest.mark.parametrize("tau", ["TIGHT", "LOOSE"])
+@pytest.mark.parametrize("K", [1, 10])
+def test_decision_t_tau_is_safe(tiny, tau, K):
+    """Decision T's safety property (P:311 read as
+    "tau = the K-th smallest exact distance of >= K real candidates"): tau0
+    and tau1 are never below the K-th smallest EXACT distance over every
+    probed candidate (the IVF*-restricted top-K, mode EXACT at the same
+    nprobe), so no candidate the bounds classify correctly is pruned.  fp32
+    rounding is monotone, so fp32(tau) >= the EXACT mode's fp32 K-th value."""
+    cfg, X, Q, bf, ix = tiny
+    for npb in (1, 4):
+        _, de, _ = ix.search(Q, K=K, nprobe=npb, mode="EXACT")
+        _, _, _, dp = ix.search(Q, K=K, nprobe=npb, mode="FULL", tau_schedule=tau, dump=True)
+        kth = de[:, K - 1]
+        assert np.all(dp["tau0"].astype(np.float32) >= kth)
+        assert np.all(dp["tau1"].astype(np.float32) >= kth)
+        assert np.all(dp["tau1"] <= dp["tau0"])
+
+
+def test_probe_order_self_query():
+    """Probe (Alg.2 L7: "the top N^probe centroid to q_d"): a base vector
+    used as a query at nprobe = 1 (of k > 1 lists) must find itself first in
+    EXACT mode -- its list is its nearest centroid by construction (Alg.1 L6,
+    P:286), so a probe that took any other list (farthest-first, centroid-id
+    order, ...) would miss it.  At nprobe = p the probed lists must be the p
+    nearest centroids in ascending distance (checked against an independent
+    numpy fp64 distance table with a tie margin)."""
+    import synth
+    cfg = synth.config_by_name("tiny")
+    X, _ = synth.generate(cfg, N=3000, Q=1, D=32)
+    bf = B.build(X, 16, 12)
+    ix = oracle.Index(bf, X)
+    sel = np.arange(0, 3000, 37)
+    ids, dist, _ = ix.search(X[sel], K=3, nprobe=1, mode="EXACT")
+    assert np.array_equal(ids[:, 0], sel)
+    _, _, _, dp = ix.search(X[sel], K=3, nprobe=5, mode="EXACT", dump=True)
+    qd = dp["qp"][:, :16]
+    dd = ((qd[:, None, :] - bf.C[None, :, :]) ** 2).sum(2)
+    for r in range(sel.shape[0]):
+        got = dp["probe"][r]
+        assert np.all(np.diff(dp["probe_qn2"][r]) >= 0)
+        assert np.allclose(dp["probe_qn2"][r], dd[r, got], rtol=1e-12, atol=0)
+        rest = np.setdiff1d(np.arange(bf.k), got)
+        assert dd[r, rest].min() >= dd[r, got].max() * (1 - 1e-12)
+
+
+def test_groundtruth_equals_bruteforce():
+    """oracle.groundtruth (the BLAS-screened exact KNN that writes every
+    committed gt_k*.npy, recall P:99-103) equals the plain-loop brute force
+    oracle.bruteforce on Tiny and on a 50k slice of the SIFT-shaped corpus."""
+    import synth
+    for name, N, Qn, K in (("tiny", None, None, 10), ("sift", 50_000, 120, 10), ("sift", 20_000, 40, 100)):
+        cfg = synth.config_by_name(name)
+        X, Q = synth.generate(cfg, N=N, Q=Qn)
+        bi, bd = oracle.bruteforce(X, Q, K)
+        for block in (4096, 37):          # one base block, and many (block x 64 rows each)
+            gi, gd = oracle.groundtruth(X, Q, K, block=block)
+            assert np.array_equal(gi, bi), (name, block)
+            assert np.array_equal(gd, bd), (name, block)
 
 
 def test_recall_monotone_and_frugal(tiny):
