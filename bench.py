@@ -359,11 +359,11 @@ def main():
     ms_head = float(np.mean([s.ms_head for s in sts]))
     hbm, peak_kind = peaks()
     traffic = ncu_traffic(cfg_name, nprobe)
-    # algorithmic bytes per unit: scan = one scanned code (W code
-    # words + f1/f2/f3); head gather = one F1 survivor (fp32 head row, ||x_r||^2,
-    # id, its F1 slot read, f1_head/f1_diso/f1_id written)
+    # algorithmic bytes per unit: scan = one
+    # scanned code (W code words + f1/f2/f3); head gather = one F1 survivor
+    # (fp32 head row, ||x_r||^2, id)
     bcode = 4 * ((d + 31) // 32) + 12
-    bhead = 4 * d + 32
+    bhead = 4 * d + 8        # fp32 head row + ||x_r||^2 + id (264 B at d = 64)
     kern = {
         "k_scan": {"unit": "scanned code", "bytes_per_unit": bcode, "units_per_launch": scanned, "ms": ms_scan},
         "k_head_b": {"unit": "F1 survivor", "bytes_per_unit": bhead, "units_per_launch": int(f1), "ms": ms_head},

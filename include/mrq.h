@@ -32,8 +32,9 @@ typedef struct mrq_index mrq_index;  /* opaque; owns all device memory of one ra
 
 typedef enum {
     MRQ_OK = 0,
-    MRQ_EINVAL = -1,      /* InvalidConfig: bad K, nprobe, eps0, m, mode, sizes, NULL    */
-    MRQ_EDIM = -2,        /* DimensionMismatch: D, d or n differ from the build file     */
+    MRQ_EINVAL = -1,      /* InvalidConfig: bad K, nprobe, eps0, m, mode, sizes, NULL;
+                             n != the build file's N                      */
+    MRQ_EDIM = -2,        /* DimensionMismatch: D or d differ from the build file        */
     MRQ_EFORMAT = -3,     /* FormatError: truncated/corrupt build file (message: offset) */
     MRQ_EVERSION = -4,    /* VersionMismatch: bad magic or version                       */
     MRQ_EDEGENERATE = -5, /* DegenerateData                                              */
@@ -65,13 +66,19 @@ typedef struct {
 /* Search parameters (Alg.2 inputs N^probe, eps0, m). */
 typedef struct {
     int32_t K;            /* results per query, 1 <= K <= 1024                               */
-    int32_t nprobe;       /* probed lists, 1 <= nprobe <= min(k, 1024)                       */
+    int32_t nprobe;       /* probed lists, 1 <= nprobe <= min(k, 1024); the scan keeps every
+                             probed list's bit-planes in shared memory, so nprobe * (52 +
+                             16 ceil(d/32)) + 4 bytes must fit the device (d = 512: nprobe
+                             <= ~750), else MRQ_EINVAL                                       */
     double eps0;          /* Eq.5 confidence parameter, > 0; default 1.9              */
     double m;             /* Chebyshev multiplier (Eq.7), > 0; default 4.0             */
     int32_t mode;         /* 0 FULL (IVF-MRQ+: stage 1 + stage 2), 1 STAGE1_ONLY (IVF-MRQ),
-                             2 EXACT (exact distance of every probed candidate)              */
+                             2 EXACT (exact distance of every probed candidate),
+                             3 NOCORR (no correction, no re-rank: the K smallest (dis', id)
+                               of every probed candidate; the distance returned is dis',
+                               Eq.4 P:245-250 -- SPEC S:425)                                  */
     int32_t tau_schedule; /* 0 TIGHT, 1 LOOSE (DESIGN.md decision T)                          */
-    int32_t seed_mult;    /* K' = seed_mult * K seeds (>= 1; default 2)                        */
+    int32_t seed_mult;    /* K' = seed_mult * K seeds (>= 1, seed_mult * K <= 4096; default 2)  */
     double resid_scale;   /* eps_r = (resid_scale * m) * sigma; 2 = distance domain (default) */
     int32_t seed_lists;   /* decision T seed pool: the first probed lists until they hold >= K'
                              candidates AND at least seed_lists lists (>= 1; 0 means 1)      */
@@ -99,8 +106,14 @@ typedef struct {
  * Encodes every vector on the GPU (Alg.1 L3-L8): PCA rotation, head/tail
  * split, centring on the own centroid, sign code under P_r, stored factors.
  * On success *out owns the device memory until mrq_free.
- * Errors: MRQ_EIO, MRQ_EVERSION, MRQ_EFORMAT, MRQ_EDIM, MRQ_EINVAL (d < 2,
- * d > D, NULL), MRQ_ECUDA, MRQ_ENOMEM, MRQ_ENCCL.
+ * Errors (checked in this order, before any device work):
+ *   MRQ_EINVAL  NULL argument, d < 2 or d > D, unknown flags;
+ *   MRQ_EIO     the file cannot be opened or read;
+ *   MRQ_EVERSION  bad magic or version;
+ *   MRQ_EFORMAT header values out of range (message names the offset);
+ *   MRQ_EDIM    D or d differ from the file's;  MRQ_EINVAL  n != the file's N;
+ *   MRQ_EFORMAT truncated payload, bad end marker, assignment >= k;
+ * then MRQ_ECUDA (no device, launch failure), MRQ_ENOMEM, MRQ_ENCCL.
  */
 int mrq_index_load(const char *build_file, const float *base, int64_t n, int32_t D, int32_t d,
                    const mrq_dist_cfg *dist, mrq_index **out);
@@ -215,8 +228,13 @@ int mrq_debug_fetch(mrq_index *idx, const char *name, void *dst, size_t dst_byte
  * the tcgen05 tf32 GEMM (the exact fp64 selection is the same).
  * "probe_unfused" = 1 writes the screen to HBM and selects in a separate
  * kernel.  "graphs" = 0 disables the CUDA-graph replay of repeated searches
- * (also: environment MRQ_NO_GRAPHS).
- * Errors: MRQ_EINVAL (unknown name).
+ * (also: environment MRQ_NO_GRAPHS).  "probe_capp" = n (1..4096, default
+ * 256) sizes the fused probe's per-part candidate buffer (a small value
+ * forces its overflow path: every centroid rescored).  "cand_budget_mb" = n
+ * (default 8192): candidate scratch above this is sized by the exact total
+ * read back from the device (one sync) instead of the host bound.
+ * "qorder" = 0 disables the list-locality query order.
+ * Errors: MRQ_EINVAL (unknown name, value out of range).
  */
 int mrq_debug_set(mrq_index *idx, const char *name, int64_t value);
 

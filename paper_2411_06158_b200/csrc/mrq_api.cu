@@ -16,10 +16,14 @@
 #include "mrq_comm.cuh"
 
 // key of the cached CUDA graph of a search (search_dispatch)
+// (gen: the index's scratch generation -- a search that reallocated a
+// scratch buffer invalidates every graph captured before, whose kernels hold
+// the freed pointers)
 struct GraphKey {
     const void *q, *ids, *dist, *stream;
     int64_t nq;
     mrq_search_params p;
+    uint64_t gen;
 };
 
 // ------------------------------------------------------------------ errors
@@ -76,6 +80,7 @@ int mrq_scratch(mrq_index *ix, const char *name, size_t bytes, void **out)
             return MRQ_ENOMEM;
         }
         a.bytes = want;
+        ix->scratch_gen++;
     }
     *out = a.p;
     return MRQ_OK;
@@ -91,7 +96,14 @@ struct BuildFile {
     std::vector<uint32_t> assign;
 };
 
-static int read_build_file(const char *path, BuildFile &b)
+// Parses an MRQBLD01 file (format: include/mrq.h) and checks it against the
+// caller's D, d, n before any size-dependent allocation: header fields are
+// bounded first, the payload size is then computed in 64 bits (no wrap) and
+// compared with the file size.  Errors: MRQ_EIO (open/read), MRQ_EVERSION
+// (magic, version), MRQ_EDIM (D or d differ), MRQ_EINVAL (n differs from N),
+// MRQ_EFORMAT (bad header values, truncation, end marker, assignment >= k;
+// the message carries the byte offset).
+static int read_build_file(const char *path, BuildFile &b, int32_t D_call, int32_t d_call, int64_t n_call)
 {
     FILE *f = fopen(path, "rb");
     if (!f) {
@@ -99,41 +111,82 @@ static int read_build_file(const char *path, BuildFile &b)
         return MRQ_EIO;
     }
     std::vector<unsigned char> buf;
-    unsigned char tmp[1 << 16];
-    size_t r;
-    while ((r = fread(tmp, 1, sizeof tmp, f)) > 0) buf.insert(buf.end(), tmp, tmp + r);
+    if (fseek(f, 0, SEEK_END) != 0) {
+        fclose(f);
+        mrq_set_error("cannot read build file '%s'", path);
+        return MRQ_EIO;
+    }
+    const long fsz = ftell(f);
+    rewind(f);
+    if (fsz < 0) {
+        fclose(f);
+        mrq_set_error("cannot read build file '%s'", path);
+        return MRQ_EIO;
+    }
+    buf.resize((size_t)fsz);
+    const size_t got = fsz > 0 ? fread(buf.data(), 1, (size_t)fsz, f) : 0;
     fclose(f);
-    if (buf.size() < 104 || memcmp(buf.data(), "MRQBLD01", 8) != 0) {
+    if (got != (size_t)fsz) {
+        mrq_set_error("short read of build file '%s' (%zu of %ld bytes)", path, got, fsz);
+        return MRQ_EIO;
+    }
+    if (buf.size() < 8 || memcmp(buf.data(), "MRQBLD01", 8) != 0) {
         mrq_set_error("build file '%s': bad magic (VersionMismatch)", path);
         return MRQ_EVERSION;
+    }
+    if (buf.size() < 104) {
+        mrq_set_error("build file '%s': truncated header at offset %zu (FormatError)", path, buf.size());
+        return MRQ_EFORMAT;
     }
     uint32_t ver;
     memcpy(&ver, buf.data() + 8, 4);
     if (ver != 1) {
-        mrq_set_error("build file '%s': version %u != 1", path, ver);
+        mrq_set_error("build file '%s': version %u != 1 (VersionMismatch)", path, ver);
         return MRQ_EVERSION;
     }
     memcpy(&b.D, buf.data() + 12, 4);
     memcpy(&b.d, buf.data() + 16, 4);
     memcpy(&b.k, buf.data() + 20, 4);
     memcpy(&b.N, buf.data() + 24, 8);
+    if (b.D < 1 || b.D > 65536 || b.d < 1 || b.d > b.D || b.k < 1 || b.k > (1u << 24) || b.N > (1ull << 32)) {
+        mrq_set_error("build file '%s': bad header D=%u d=%u k=%u N=%llu at offset 12 (FormatError)", path, b.D, b.d,
+                      b.k, (unsigned long long)b.N);
+        return MRQ_EFORMAT;
+    }
+    if ((int64_t)b.D != D_call || (int64_t)b.d != d_call) {
+        mrq_set_error("DimensionMismatch: file D=%u d=%u, call D=%d d=%d", b.D, b.d, D_call, d_call);
+        return MRQ_EDIM;
+    }
+    if ((int64_t)b.N != n_call) {
+        mrq_set_error("InvalidConfig: build file N=%llu, call n=%lld", (unsigned long long)b.N, (long long)n_call);
+        return MRQ_EINVAL;
+    }
+    const uint64_t D = b.D, d = b.d, k = b.k;
+    const uint64_t ndbl = D + D * D + D + d * d + k * d;      // all bounded above: no wrap in 64 bits
+    const uint64_t need = 104 + 8 * ndbl + 4 * b.N + 8;
+    if ((uint64_t)buf.size() < need) {
+        // report the offset of the first incomplete section
+        uint64_t off = 104;
+        const uint64_t sec[6] = {8 * D, 8 * D * D, 8 * D, 8 * d * d, 8 * k * d, 4 * b.N};
+        for (uint64_t s : sec) {
+            if (off + s > buf.size()) break;
+            off += s;
+        }
+        mrq_set_error("build file '%s': truncated at offset %llu (FormatError; %zu of %llu bytes)", path,
+                      (unsigned long long)off, buf.size(), (unsigned long long)need);
+        return MRQ_EFORMAT;
+    }
     size_t off = 104;
-    auto take = [&](std::vector<double> &v, size_t n) -> bool {
-        if (off + n * 8 > buf.size()) return false;
+    auto take = [&](std::vector<double> &v, size_t n) {
         v.resize(n);
         memcpy(v.data(), buf.data() + off, n * 8);
         off += n * 8;
-        return true;
     };
-    const size_t D = b.D, d = b.d, k = b.k;
-    if (!take(b.mu, D) || !take(b.P, D * D) || !take(b.lam, D) || !take(b.R, d * d) || !take(b.C, k * d)) {
-        mrq_set_error("build file '%s': truncated at offset %zu (FormatError)", path, off);
-        return MRQ_EFORMAT;
-    }
-    if (off + b.N * 4 + 8 > buf.size()) {
-        mrq_set_error("build file '%s': truncated at offset %zu (FormatError)", path, off);
-        return MRQ_EFORMAT;
-    }
+    take(b.mu, D);
+    take(b.P, D * D);
+    take(b.lam, D);
+    take(b.R, d * d);
+    take(b.C, k * d);
     b.assign.resize(b.N);
     memcpy(b.assign.data(), buf.data() + off, b.N * 4);
     off += b.N * 4;
@@ -143,8 +196,8 @@ static int read_build_file(const char *path, BuildFile &b)
     }
     for (uint64_t n = 0; n < b.N; n++)
         if (b.assign[n] >= b.k) {
-            mrq_set_error("build file '%s': assignment %u >= k at vector %llu (FormatError)", path, b.assign[n],
-                          (unsigned long long)n);
+            mrq_set_error("build file '%s': assignment %u >= k at vector %llu, offset %llu (FormatError)", path,
+                          b.assign[n], (unsigned long long)n, (unsigned long long)(off - b.N * 4 + n * 4));
             return MRQ_EFORMAT;
         }
     return MRQ_OK;
@@ -163,15 +216,7 @@ static int load_impl(mrq_index *ix, const char *build_file, const float *base, i
         return MRQ_EINVAL;
     }
     BuildFile b;
-    TRY(read_build_file(build_file, b));
-    if ((int32_t)b.D != D || (int32_t)b.d != d) {
-        mrq_set_error("DimensionMismatch: file D=%u d=%u, call D=%d d=%d", b.D, b.d, D, d);
-        return MRQ_EDIM;
-    }
-    if ((int64_t)b.N != n) {
-        mrq_set_error("DimensionMismatch: file N=%llu, call n=%lld", (unsigned long long)b.N, (long long)n);
-        return MRQ_EDIM;
-    }
+    TRY(read_build_file(build_file, b, D, d, n));
     ix->N = n;
     ix->D = D;
     ix->d = d;
@@ -196,6 +241,7 @@ static int load_impl(mrq_index *ix, const char *build_file, const float *base, i
     if (ix->device < 0) MRQ_CUDA_TRY(cudaGetDevice(&ix->device));
     MRQ_CUDA_TRY(cudaSetDevice(ix->device));
     MRQ_CUDA_TRY(cudaDeviceGetAttribute(&ix->sm_count, cudaDevAttrMultiProcessorCount, ix->device));
+    MRQ_CUDA_TRY(cudaDeviceGetAttribute(&ix->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ix->device));
     MRQ_CUDA_TRY(cudaStreamCreateWithFlags(&ix->stream, cudaStreamNonBlocking));
     for (auto &e : ix->ev) MRQ_CUDA_TRY(cudaEventCreate(&e));
     MRQ_CUDA_TRY(cudaStreamCreateWithFlags(&ix->side, cudaStreamNonBlocking));
@@ -379,7 +425,7 @@ extern "C" int mrq_index_load_ex(const char *build_file, const float *base, int6
     memset(ix->g_key, 0, sizeof(GraphKey));
     memset(ix->g_pending, 0, sizeof(GraphKey));
     if (getenv("MRQ_NO_GRAPHS")) ix->graphs = 0;
-    int rc = load_impl(ix, build_file, base, n, D, d, dist);
+    int rc = mrq_guard([&] { return load_impl(ix, build_file, base, n, D, d, dist); });
     if (rc != MRQ_OK) {
         mrq_free(ix);
         return rc;
@@ -508,7 +554,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
         SCR("probe_cand", uint32_t, nq * k, cand);
         SCR("probe_ncand", uint32_t, nq, ncand);
         if (mrq_probe_tc_fusable(ix, np)) {   // tcgen05 screen with the running top-np in its epilogue
-            const int P = mrq_probe_tc_parts(ix, nq), capp = 256;
+            const int P = mrq_probe_tc_parts(ix, nq), capp = ix->probe_capp;
             uint2 *cbuf;
             uint32_t *ccnt;
             float *kvbuf;
@@ -555,7 +601,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
     // the device; else by the exact total (one D2H + stream sync)
     uint64_t total = (uint64_t)nq * ix->h_topsum[std::min(np, k)];
     const uint64_t per_entry = 4 + 8 + 8 + 4 + 4 + 8 + 8;   // f1_pos/head/diso/id, f2_pos/head/exact
-    if (total * per_entry > ((uint64_t)8 << 30) || ix->dbg_dump_dis) {
+    if (total * per_entry > ix->cand_budget || ix->dbg_dump_dis) {
         MRQ_CUDA_TRY(cudaMemcpyAsync(&total, f1_off + nq, 8, cudaMemcpyDeviceToHost, st));
         MRQ_CUDA_TRY(cudaStreamSynchronize(st));
     }
@@ -589,69 +635,85 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
     sa.f1_id = f1_id;
     sa.seed_lists = p->seed_lists > 0 ? p->seed_lists : 1;
     sa.list_size_g = ix->list_size_g; sa.s0_id = s0_id; sa.s1_id = s1_id; sa.xout = nullptr;
+    sa.store_f1 = ix->dbg_dump_dis;
 
-    // ---- a4: seeds S0 and tau0 (decision T); EXACT mode scans everything
-    if (mode == 2) {
+    if (mode == 3) {
+        // ---- NOCORR: top-K by dis' over every probed candidate, no bounds, no re-rank
+        for (uint32_t *z : {s0_cnt, s1_cnt, f1_cnt, f2_cnt})
+            MRQ_CUDA_TRY(cudaMemsetAsync(z, 0, (size_t)nq * 4, st));
+        if (timed) MRQ_CUDA_TRY(cudaMemsetAsync(exact_cnt, 0, (size_t)nq * 4, st));
         launch_fill_f64(tau0, nq, INFINITY, st);
-        MRQ_CUDA_TRY(cudaMemsetAsync(s0_cnt, 0, nq * 4, st));
+        launch_fill_f64(tau1, nq, INFINITY, st);
+        if (timed)
+            for (int e : {4, 5, 10, 6, 7}) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[e], st));
+        StageArgs sx = sa;
+        if (sharded) sx.xout = xsend;
+        TRY(launch_nocorr_w(W, sx, st));
+        if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[8], st));
     } else {
-        if (sharded) {   // local part of S0 -> all-gather -> global S0, tau0
+        // ---- a4: seeds S0 and tau0 (decision T); EXACT mode scans everything
+        if (mode == 2) {
+            launch_fill_f64(tau0, nq, INFINITY, st);
+            MRQ_CUDA_TRY(cudaMemsetAsync(s0_cnt, 0, nq * 4, st));
+        } else {
+            if (sharded) {   // local part of S0 -> all-gather -> global S0, tau0
+                StageArgs sx = sa;
+                sx.xout = xsend;
+                TRY(launch_seed_w(W, sx, st));
+                TRY(mrq_allgather(ix, xsend, xrecv, (size_t)nq * Kp * sizeof(XItem), st));
+                TRY(launch_xmerge(0, sa, ix->world, ix->rank, xrecv, st));
+            } else {
+                TRY(launch_seed_w(W, sa, st));
+            }
+        }
+        if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[4], st));
+
+        // ---- a5: the code scan -> F1
+        {
+            LaunchScan a;
+            a.nq = nq;
+            a.smem = mrq_scan_smem(np, W);
+            a.probe = probe; a.np = np; a.npad = ix->npad; a.list_off = ix->list_off; a.list_size = ix->list_size;
+            a.codes = ix->codes; a.f1 = ix->f1; a.f2 = ix->f2; a.f3 = ix->f3; a.planes = planes; a.qconst = qconst;
+            a.eps_r = eps_r; a.tau0 = tau0; a.isd = isd; a.f1_off = f1_off; a.f1_cnt = f1_cnt; a.f1_pos = f1_pos;
+            a.qorder = qorder;
+            TRY(launch_scan(W, a, st));
+            if (ix->dbg_dump_dis) {
+                double *dd, *dl;
+                SCR("dbg_dis", double, total, dd);
+                SCR("dbg_lb1", double, total, dl);
+                launch_scan_dbg(W, a, dd, dl, st);
+            }
+        }
+        if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[5], st));
+
+        // ---- a6: stage 2 -> F2 (and S1, tau1)
+        if (sharded && mode == 0 && tight) {   // local S1 -> all-gather -> global S1, tau1 -> F2
             StageArgs sx = sa;
             sx.xout = xsend;
-            TRY(launch_seed_w(W, sx, st));
+            TRY(launch_stage2_w(sx, st, timed ? ix->ev[10] : nullptr));
             TRY(mrq_allgather(ix, xsend, xrecv, (size_t)nq * Kp * sizeof(XItem), st));
-            TRY(launch_xmerge(0, sa, ix->world, ix->rank, xrecv, st));
+            TRY(launch_xmerge(1, sa, ix->world, ix->rank, xrecv, st));
+            TRY(launch_f2_w(sa, st));
         } else {
-            TRY(launch_seed_w(W, sa, st));
+            TRY(launch_stage2_w(sa, st, timed ? ix->ev[10] : nullptr));
         }
-    }
-    if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[4], st));
+        if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[6], st));
 
-    // ---- a5: the code scan -> F1
-    {
-        LaunchScan a;
-        a.nq = nq;
-        a.smem = (size_t)np * 5 * 8 + (size_t)np * MRQ_BQ * W * 4 + (size_t)(3 * np + 1) * 4;
-        a.probe = probe; a.np = np; a.npad = ix->npad; a.list_off = ix->list_off; a.list_size = ix->list_size;
-        a.codes = ix->codes; a.f1 = ix->f1; a.f2 = ix->f2; a.f3 = ix->f3; a.planes = planes; a.qconst = qconst;
-        a.eps_r = eps_r; a.tau0 = tau0; a.isd = isd; a.f1_off = f1_off; a.f1_cnt = f1_cnt; a.f1_pos = f1_pos;
-        a.qorder = qorder;
-        launch_scan(W, a, st);
-        if (ix->dbg_dump_dis) {
-            double *dd, *dl;
-            SCR("dbg_dis", double, total, dd);
-            SCR("dbg_lb1", double, total, dl);
-            launch_scan_dbg(W, a, dd, dl, st);
+        // ---- a7: exact re-rank of F2
+        // (a7, the exact re-rank of F2, runs inside the top-K kernel)
+        if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[7], st));
+
+        // ---- a8: per-query top-K
+        if (sharded) {
+            StageArgs sx = sa;
+            sx.xout = xsend;
+            TRY(launch_topk_w(sx, st));
+        } else {
+            TRY(launch_topk_w(sa, st));
         }
+        if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[8], st));
     }
-    if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[5], st));
-
-    // ---- a6: stage 2 -> F2 (and S1, tau1)
-    if (sharded && mode == 0 && tight) {   // local S1 -> all-gather -> global S1, tau1 -> F2
-        StageArgs sx = sa;
-        sx.xout = xsend;
-        TRY(launch_stage2_w(sx, st, timed ? ix->ev[10] : nullptr));
-        TRY(mrq_allgather(ix, xsend, xrecv, (size_t)nq * Kp * sizeof(XItem), st));
-        TRY(launch_xmerge(1, sa, ix->world, ix->rank, xrecv, st));
-        TRY(launch_f2_w(sa, st));
-    } else {
-        TRY(launch_stage2_w(sa, st, timed ? ix->ev[10] : nullptr));
-    }
-    if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[6], st));
-
-    // ---- a7: exact re-rank of F2
-    // (a7, the exact re-rank of F2, runs inside the top-K kernel)
-    if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[7], st));
-
-    // ---- a8: per-query top-K
-    if (sharded) {
-        StageArgs sx = sa;
-        sx.xout = xsend;
-        TRY(launch_topk_w(sx, st));
-    } else {
-        TRY(launch_topk_w(sa, st));
-    }
-    if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[8], st));
     // ---- a9: multi-GPU merge (all-gather of the per-rank top-K)
     if (sharded) {
         TRY(mrq_allgather(ix, xsend, xrecv, (size_t)nq * K * sizeof(XItem), st));
@@ -715,12 +777,20 @@ static int check_params(const mrq_index *ix, int64_t nq, const mrq_search_params
         return MRQ_EINVAL;
     }
     if (nq < 0 || p->K < 1 || p->K > MRQ_MAX_K || p->nprobe < 1 || p->nprobe > MRQ_MAX_NPROBE ||
-        p->nprobe > ix->k || !(p->eps0 > 0) || !(p->m > 0) || p->mode < 0 || p->mode > 2 ||
-        p->tau_schedule < 0 || p->tau_schedule > 1 || p->seed_mult < 1 || !(p->resid_scale > 0) ||
-        p->seed_lists < 0) {
-        mrq_set_error("InvalidConfig: K=%d nprobe=%d (k=%d) eps0=%g m=%g mode=%d tau=%d seed_mult=%d rscale=%g",
+        p->nprobe > ix->k || !(p->eps0 > 0) || !(p->m > 0) || p->mode < 0 || p->mode > 3 ||
+        p->tau_schedule < 0 || p->tau_schedule > 1 || p->seed_mult < 1 ||
+        (int64_t)p->seed_mult * p->K > MRQ_MAX_SEEDS || !(p->resid_scale > 0) || p->seed_lists < 0) {
+        mrq_set_error("InvalidConfig: K=%d nprobe=%d (k=%d) eps0=%g m=%g mode=%d tau=%d seed_mult=%d rscale=%g "
+                      "(seed_mult*K <= %d)",
                       p->K, p->nprobe, ix->k, p->eps0, p->m, p->mode, p->tau_schedule, p->seed_mult,
-                      p->resid_scale);
+                      p->resid_scale, MRQ_MAX_SEEDS);
+        return MRQ_EINVAL;
+    }
+    // the scan stages every probed list's constants and bit-planes in shared memory
+    const size_t scan_smem = mrq_scan_smem(std::min(p->nprobe, ix->k), ix->W);
+    if (scan_smem > (size_t)ix->smem_optin) {
+        mrq_set_error("InvalidConfig: nprobe=%d with d=%d needs %zu B of scan shared memory (device max %d)",
+                      p->nprobe, ix->d, scan_smem, ix->smem_optin);
         return MRQ_EINVAL;
     }
     return MRQ_OK;
@@ -740,7 +810,7 @@ static int search_dispatch(mrq_index *ix, const float *d_q, int64_t nq, const mr
     const int np = std::min(p->nprobe, ix->k);
     const uint64_t bound = (uint64_t)nq * ix->h_topsum[np];
     const bool eligible = !stats && !ix->dbg_dump_dis && !ix->host_ag && ix->graphs && st != nullptr &&
-                          bound * 48 <= ((uint64_t)8 << 30);
+                          bound * 48 <= ix->cand_budget;
     if (!eligible) return search_impl(ix, d_q, nq, p, d_ids, d_dist, stats, st);
     GraphKey key;
     memset(&key, 0, sizeof key);
@@ -750,6 +820,7 @@ static int search_dispatch(mrq_index *ix, const float *d_q, int64_t nq, const mr
     key.stream = st;
     key.nq = nq;
     key.p = *p;
+    key.gen = ix->scratch_gen;
     GraphKey *cur = (GraphKey *)ix->g_key, *pend = (GraphKey *)ix->g_pending;
     if (ix->gexec && graph_key_eq(*cur, key)) {
         MRQ_CUDA_TRY(cudaGraphLaunch((cudaGraphExec_t)ix->gexec, st));
@@ -794,8 +865,11 @@ extern "C" int mrq_search_batch_device(mrq_index *ix, const float *d_queries, in
     }
     MRQ_CUDA_TRY(cudaSetDevice(ix->device));
     cudaStream_t st = stream ? (cudaStream_t)stream : ix->stream;
-    return search_dispatch(ix, d_queries, nq, p, d_out_ids, d_out_dist, stats, st);
+    return mrq_guard([&] { return search_dispatch(ix, d_queries, nq, p, d_out_ids, d_out_dist, stats, st); });
 }
+
+static int search_host(mrq_index *ix, const float *queries, int64_t nq, const mrq_search_params *p, int64_t *out_ids,
+                       float *out_dist, mrq_stats *stats);
 
 extern "C" int mrq_search_batch(mrq_index *ix, const float *queries, int64_t nq, const mrq_search_params *p,
                                 int64_t *out_ids, float *out_dist, mrq_stats *stats)
@@ -809,6 +883,12 @@ extern "C" int mrq_search_batch(mrq_index *ix, const float *queries, int64_t nq,
         mrq_set_error("NULL buffer");
         return MRQ_EINVAL;
     }
+    return mrq_guard([&] { return search_host(ix, queries, nq, p, out_ids, out_dist, stats); });
+}
+
+static int search_host(mrq_index *ix, const float *queries, int64_t nq, const mrq_search_params *p, int64_t *out_ids,
+                       float *out_dist, mrq_stats *stats)
+{
     MRQ_CUDA_TRY(cudaSetDevice(ix->device));
     float *dq;
     int64_t *dids;
@@ -825,7 +905,13 @@ extern "C" int mrq_search_batch(mrq_index *ix, const float *queries, int64_t nq,
 }
 
 // ------------------------------------------------------------- debug fetch
+static int debug_fetch(mrq_index *ix, const char *name, void *dst, size_t dst_bytes, size_t *bytes_needed);
 extern "C" int mrq_debug_fetch(mrq_index *ix, const char *name, void *dst, size_t dst_bytes, size_t *bytes_needed)
+{
+    return mrq_guard([&] { return debug_fetch(ix, name, dst, dst_bytes, bytes_needed); });
+}
+
+static int debug_fetch(mrq_index *ix, const char *name, void *dst, size_t dst_bytes, size_t *bytes_needed)
 {
     if (!ix || !name) {
         mrq_set_error("NULL index or name");
@@ -928,6 +1014,18 @@ extern "C" int mrq_debug_set(mrq_index *ix, const char *name, int64_t value)
     }
     if (std::string(name) == "graphs") {           // CUDA-graph replay of repeated searches (default 1)
         ix->graphs = (int)value;
+        return MRQ_OK;
+    }
+    if (std::string(name) == "probe_capp") {       // per-part candidate buffer of the fused probe (default 256)
+        if (value < 1 || value > 4096) {
+            mrq_set_error("probe_capp must be in [1, 4096]");
+            return MRQ_EINVAL;
+        }
+        ix->probe_capp = (int)value;
+        return MRQ_OK;
+    }
+    if (std::string(name) == "cand_budget_mb") {   // candidate scratch sized by the host bound below this (8192)
+        ix->cand_budget = (uint64_t)std::max<int64_t>(value, 0) << 20;
         return MRQ_OK;
     }
     if (std::string(name) == "probe_unfused") {    // screen to HBM + separate selection kernel

@@ -240,7 +240,9 @@ __global__ void k_sum_f32(const float *__restrict__ x, int64_t n, double *__rest
 
 // --------------------------------------------------- host linear algebra
 // Symmetric eigen-decomposition (Householder tridiagonalisation + implicit
-// QL with Wilkinson shifts; the classic tred2/tql2 pair).  a: n x n row-major
+// QL with Wilkinson shifts): a transcription of the classic public-domain
+// EISPACK tred2/tql2 pair as given in JAMA's EigenvalueDecomposition (the
+// variable names follow it).  Off the hot path (NEXT-1 host PCA, D x D).  a: n x n row-major
 // (destroyed); on return w[i] are the eigenvalues and column i of V (row-major
 // n x n) the eigenvector of w[i].
 void sym_eig(int n, std::vector<double> &a, std::vector<double> &w, std::vector<double> &V)
@@ -444,8 +446,17 @@ struct Dev {
 
 }  // namespace
 
+static int build_gpu_impl(const float *base, int64_t n, int32_t D, int32_t d, const mrq_build_params *bp,
+                          const char *base_sha256_hex, int32_t device, const char *out_path, double *times_ms);
+
 extern "C" int mrq_build_gpu(const float *base, int64_t n, int32_t D, int32_t d, const mrq_build_params *bp,
                              const char *base_sha256_hex, int32_t device, const char *out_path, double *times_ms)
+{
+    return mrq_guard([&] { return build_gpu_impl(base, n, D, d, bp, base_sha256_hex, device, out_path, times_ms); });
+}
+
+static int build_gpu_impl(const float *base, int64_t n, int32_t D, int32_t d, const mrq_build_params *bp,
+                          const char *base_sha256_hex, int32_t device, const char *out_path, double *times_ms)
 {
     if (!base || !bp || !out_path || n < 2 || D < 1 || d < 2 || d > D || bp->k < 1 || bp->k > n ||
         bp->pca_sample < 2 || bp->km_sample_per_k < 1 || bp->km_iters < 1) {

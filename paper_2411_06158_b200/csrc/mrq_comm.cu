@@ -43,10 +43,12 @@ extern "C" int mrq_shard_plan(const uint32_t *sizes, int32_t k, int32_t world, u
         mrq_set_error("InvalidConfig: mrq_shard_plan needs sizes, owner, k >= 1, world >= 1");
         return MRQ_EINVAL;
     }
-    std::vector<uint32_t> s(sizes, sizes + k), o;
-    mrq_shard_lists(s, world, o);
-    memcpy(owner, o.data(), (size_t)k * 4);
-    return MRQ_OK;
+    return mrq_guard([&] {
+        std::vector<uint32_t> s(sizes, sizes + k), o;
+        mrq_shard_lists(s, world, o);
+        memcpy(owner, o.data(), (size_t)k * 4);
+        return (int)MRQ_OK;
+    });
 }
 
 #if MRQ_HAVE_NCCL

@@ -10,7 +10,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <exception>
 #include <map>
+#include <new>
 #include <string>
 #include <vector>
 
@@ -19,6 +21,7 @@
 #define MRQ_BQ 4                 // query bit-planes (levels 0..15), R-7
 #define MRQ_MAX_K 1024
 #define MRQ_MAX_NPROBE 1024
+#define MRQ_MAX_SEEDS 4096          // seed_mult * K: the seed kernels' per-warp selection region
 #define MRQ_SLOT_ALIGN 4         // list starts aligned to 4 slots (16 B) for 128-bit loads
 #define MRQ_PAD_ID 0xFFFFFFFFu
 
@@ -34,6 +37,25 @@ void mrq_set_error(const char *fmt, ...);
             return MRQ_ECUDA;                                                       \
         }                                                                           \
     } while (0)
+
+// Entry-point guard: C++ exceptions (std::bad_alloc from a vector resize, ...)
+// never cross the extern "C" boundary; they become MRQ_ENOMEM / MRQ_EINVAL.
+template <class F>
+int mrq_guard(F &&f)
+{
+    try {
+        return f();
+    } catch (const std::bad_alloc &) {
+        mrq_set_error("host allocation failed (std::bad_alloc)");
+        return MRQ_ENOMEM;
+    } catch (const std::exception &e) {
+        mrq_set_error("internal error: %s", e.what());
+        return MRQ_EINVAL;
+    } catch (...) {
+        mrq_set_error("internal error (unknown exception)");
+        return MRQ_EINVAL;
+    }
+}
 
 // ------------------------------------------------------------ index object
 struct DevArr {
@@ -69,6 +91,10 @@ struct mrq_index {
     void *gexec = nullptr;                     // cudaGraphExec_t of the cached search
     void *g_key = nullptr, *g_pending = nullptr;   // GraphKey of the cached / last uncached search
     int sm_count = 148;
+    int probe_capp = 256;                      // mrq_debug_set("probe_capp"): fused-probe candidate buffer per part
+    uint64_t cand_budget = (uint64_t)8 << 30;  // mrq_debug_set("cand_budget_mb"): host-bound scratch budget
+    int smem_optin = 227 * 1024;               // max dynamic shared memory per block (opt-in)
+    uint64_t scratch_gen = 0;                  // bumped whenever a scratch buffer is reallocated (graph key)
 
     // host mirrors
     std::vector<uint32_t> h_list_off, h_list_size;

@@ -645,25 +645,27 @@ void launch_fill_f64(double *p, int64_t n, double v, cudaStream_t st)
 
 // ================================================================ launchers
 template <int W>
-static void launch_scan_w(const LaunchScan &a, cudaStream_t st)
+static int launch_scan_w(const LaunchScan &a, cudaStream_t st)
 {
     if (a.smem > 48 * 1024)
-        cudaFuncSetAttribute(k_scan<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a.smem);
+        MRQ_CUDA_TRY(cudaFuncSetAttribute(k_scan<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a.smem));
     k_scan<W><<<a.nq, MRQ_SCAN_THREADS, a.smem, st>>>(a.probe, a.np, a.npad, a.list_off, a.list_size, a.codes, a.f1, a.f2, a.f3,
                                           a.planes, a.qconst, a.eps_r, a.tau0, a.isd, a.f1_off, a.f1_cnt, a.f1_pos,
                                           a.qorder);
+    MRQ_CUDA_TRY(cudaGetLastError());
+    return MRQ_OK;
 }
 
-void launch_scan(int W, const LaunchScan &a, cudaStream_t st)
+int launch_scan(int W, const LaunchScan &a, cudaStream_t st)
 {
     switch (W) {
-    case 1: launch_scan_w<1>(a, st); break;
-    case 2: launch_scan_w<2>(a, st); break;
-    case 3: launch_scan_w<3>(a, st); break;
-    case 4: launch_scan_w<4>(a, st); break;
-    case 8: launch_scan_w<8>(a, st); break;
-    case 16: launch_scan_w<16>(a, st); break;
-    default: break;
+    case 1: return launch_scan_w<1>(a, st);
+    case 2: return launch_scan_w<2>(a, st);
+    case 3: return launch_scan_w<3>(a, st);
+    case 4: return launch_scan_w<4>(a, st);
+    case 8: return launch_scan_w<8>(a, st);
+    case 16: return launch_scan_w<16>(a, st);
+    default: mrq_set_error("unsupported W=%d", W); return MRQ_EINVAL;
     }
 }
 

@@ -25,6 +25,7 @@ __global__ void k_exclusive_scan(const uint64_t *in, int64_t n, uint64_t *out);
 struct StageArgs {
     int64_t nq;
     int np, K, Kp, D, d, mode, tight, aligned, seed_lists, aligned_tails;
+    int store_f1;             // k_head_b also writes f1_head/f1_diso/f1_id when F2 is fused (debug dumps)
     int64_t npad;
     double isd;
     const uint32_t *probe, *list_off, *list_size, *ids, *codes, *planes;
@@ -45,6 +46,7 @@ struct StageArgs {
 int launch_seed_w(int W, const StageArgs &a, cudaStream_t st);
 int launch_stage2_w(const StageArgs &a, cudaStream_t st, cudaEvent_t after_gather = nullptr);
 int launch_topk_w(const StageArgs &a, cudaStream_t st);
+int launch_nocorr_w(int W, const StageArgs &a, cudaStream_t st);
 int launch_exact_count(const StageArgs &a, cudaStream_t st);
 int launch_f2_w(const StageArgs &a, cudaStream_t st);
 int launch_xmerge(int kind, const StageArgs &a, int world, int rank, const XItem *recv, cudaStream_t st);
@@ -65,7 +67,12 @@ struct LaunchScan {
     const uint32_t *qorder;   // processing order of the queries (NULL: 0..nq-1)
 };
 
-void launch_scan(int W, const LaunchScan &a, cudaStream_t st);
+// dynamic shared memory of k_scan: per probed list 5 constants, 4 W plane words, tile prefix / start / end
+inline size_t mrq_scan_smem(int np, int W)
+{
+    return (size_t)np * 5 * 8 + (size_t)np * MRQ_BQ * W * 4 + (size_t)(3 * np + 1) * 4;
+}
+int launch_scan(int W, const LaunchScan &a, cudaStream_t st);
 bool supported_W(int W);
 void launch_scan_dbg(int W, const LaunchScan &a, double *dis, double *lb1, cudaStream_t st);
 int launch_probe_finish_w(int64_t nq, int k, int d, int np, const double *qp, int D, const double *C,

@@ -140,6 +140,71 @@ __global__ void MRQ_SEED_LB k_seed_w(
     }
 }
 
+// ------------------------------------------------------------- NOCORR mode
+// mode 3: no error-bound correction and no re-rank
+// -- the K smallest (dis', id) over every probed candidate, dis' the Eq.4
+// estimate (reading R-1) reported as the distance.  Warp per query
+// (one-warp blocks); the same epilogue (mrq_lb1) as the scan.  Sharded
+// (xout != NULL): the local top-K goes to the exchange (key = exact = dis').
+template <int W, bool MG>
+__global__ void __launch_bounds__(32) k_nocorr_w(
+    int64_t nq, const uint32_t *__restrict__ probe, int np, int K, int64_t npad,
+    const uint32_t *__restrict__ list_off, const uint32_t *__restrict__ list_size, const uint32_t *__restrict__ ids,
+    const uint32_t *__restrict__ codes, const float *__restrict__ f1, const float *__restrict__ f2,
+    const float *__restrict__ f3, const uint32_t *__restrict__ planes, const double *__restrict__ qconst,
+    const double *__restrict__ eps_r_arr, double isd, int64_t *__restrict__ out_ids, float *__restrict__ out_dist,
+    XItem *__restrict__ xout)
+{
+    extern __shared__ unsigned char wsm[];
+    const int lane = threadIdx.x & 31;
+    const int64_t q = blockIdx.x;
+    if (q >= nq) return;
+    SelItem *lst = (SelItem *)wsm;
+    SelItem *queue = lst + K;
+    const double eps_r = eps_r_arr[q];
+    WarpSelT<MG> top;
+    top.init(lst, K, true, queue);
+    for (int p = 0; p < np; p++) {
+        const uint32_t c = probe[q * np + p];
+        if (c == 0xFFFFFFFFu) continue;
+        const uint32_t off = list_off[c], sz = list_size[c];
+        const uint32_t *pl = planes + (q * np + p) * (MRQ_BQ * W);
+        const double *qc = qconst + (q * np + p) * 8;
+        for (uint32_t e0 = 0; e0 < sz; e0 += 32) {
+            const uint32_t e = e0 + lane;
+            const bool v = e < sz;
+            SelItem it = sel_inf();
+            if (v) {
+                const uint32_t slot = off + e;
+                uint32_t code[W];
+#pragma unroll
+                for (int w = 0; w < W; w++) code[w] = codes[(int64_t)w * npad + slot];
+                double dis;
+                mrq_lb1<W>(code, pl, qc, isd, eps_r, f1[slot], f2[slot], f3[slot], &dis);
+                it.key = dis;
+                it.id = ids[slot];
+                it.pay = slot;
+            }
+            top.offer(it, v);
+        }
+    }
+    top.finish();
+    for (int i = lane; i < K; i += 32) {
+        const bool ok = lst[i].id != MRQ_PAD_ID;
+        if (xout) {
+            XItem x;
+            x.key = lst[i].key;
+            x.exact = lst[i].key;
+            x.id = ok ? lst[i].id : MRQ_PAD_ID;
+            x.slot = ok ? lst[i].pay : MRQ_PAD_ID;
+            xout[q * K + i] = x;
+        } else {
+            out_ids[q * K + i] = ok ? (int64_t)lst[i].id : (int64_t)-1;
+            out_dist[q * K + i] = ok ? (float)lst[i].key : __int_as_float(0x7f800000);
+        }
+    }
+}
+
 // ----------------------------------------------------------------------- a6
 // F2 = {e in F1 : dis_o' - eps_r < tau1} (FULL), all of F1 otherwise:
 // ordered warp compaction (no atomics) of the query's F1 segment.
@@ -186,7 +251,7 @@ __global__ void __launch_bounds__(128) k_head_b(
     double *__restrict__ f1_head, double *__restrict__ f1_diso, uint32_t *__restrict__ f1_id,
     const uint32_t *__restrict__ qorder, int fuse_f2, int mode, const double *__restrict__ eps_r_arr,
     const double *__restrict__ tau0_arr, uint32_t *__restrict__ f2_cnt, uint32_t *__restrict__ f2_pos,
-    double *__restrict__ f2_head, uint32_t *__restrict__ s1_cnt, double *__restrict__ tau1_arr)
+    double *__restrict__ f2_head, uint32_t *__restrict__ s1_cnt, double *__restrict__ tau1_arr, int store_f1)
 {
     extern __shared__ unsigned char wsm[];
     __shared__ uint32_t f2n;
@@ -216,9 +281,11 @@ __global__ void __launch_bounds__(128) k_head_b(
                   double diso = 0.0;
                   if (v) {
                       diso = (head + (double)xr2v) + qr2;
-                      f1_head[base + e] = head;
-                      f1_diso[base + e] = diso;
-                      f1_id[base + e] = idv;
+                      if (store_f1) {   // read only by the S1 selection / F2 compaction of k_stage2_w
+                          f1_head[base + e] = head;
+                          f1_diso[base + e] = diso;
+                          f1_id[base + e] = idv;
+                      }
                   }
                   if (fuse_f2) {
                       const bool pass = v && ((mode != 0) || (diso - eps_r < tau1));
@@ -663,6 +730,32 @@ int launch_seed_w(int W, const StageArgs &a, cudaStream_t st)
     return MRQ_OK;
 }
 
+int launch_nocorr_w(int W, const StageArgs &a, cudaStream_t st)
+{
+    const size_t smem = (size_t)MRQ_SELREG(a.K) * sizeof(SelItem);
+    const bool mg = a.K > MRQ_MERGE_MIN;
+#define MRQ_NOC(WW)                                                                                              \
+    do {                                                                                                         \
+        auto fn = mg ? k_nocorr_w<WW, true> : k_nocorr_w<WW, false>;                                             \
+        int rc = set_attr((const void *)fn, smem);                                                               \
+        if (rc) return rc;                                                                                       \
+        fn<<<(unsigned)a.nq, 32, smem, st>>>(a.nq, a.probe, a.np, a.K, a.npad, a.list_off, a.list_size, a.ids,  \
+                                             a.codes, a.f1, a.f2, a.f3, a.planes, a.qconst, a.eps_r, a.isd,     \
+                                             a.out_ids, a.out_dist, a.xout);                                    \
+    } while (0)
+    switch (W) {
+    case 1: MRQ_NOC(1); break;
+    case 2: MRQ_NOC(2); break;
+    case 3: MRQ_NOC(3); break;
+    case 4: MRQ_NOC(4); break;
+    case 8: MRQ_NOC(8); break;
+    case 16: MRQ_NOC(16); break;
+    default: mrq_set_error("unsupported W"); return MRQ_EINVAL;
+    }
+#undef MRQ_NOC
+    return MRQ_OK;
+}
+
 int launch_stage2_w(const StageArgs &a, cudaStream_t st, cudaEvent_t after_gather)
 {
     // without an S1 selection (every schedule but FULL/TIGHT) stage 2 is the
@@ -679,7 +772,7 @@ int launch_stage2_w(const StageArgs &a, cudaStream_t st, cudaEvent_t after_gathe
         k_head_b<<<(unsigned)a.nq, wpb * 32, smem, st>>>(a.aligned, a.D, a.d, a.ids, a.heads, a.xr2, a.qp, a.qr2,
                                                           a.f1_off, a.f1_cnt, a.f1_pos, a.f1_head, a.f1_diso, a.f1_id,
                                                           a.qorder, fuse, a.mode, a.eps_r, a.tau0, a.f2_cnt, a.f2_pos,
-                                                          a.f2_head, a.s1_cnt, a.tau1);
+                                                          a.f2_head, a.s1_cnt, a.tau1, !fuse || a.store_f1);
     }
     if (after_gather) MRQ_CUDA_TRY(cudaEventRecord(after_gather, st));
     if (fuse) return MRQ_OK;   // F2 written by the gather kernel

@@ -13,7 +13,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libmrq.so")
 
-MRQ_MODES = {"FULL": 0, "STAGE1_ONLY": 1, "EXACT": 2}
+MRQ_MODES = {"FULL": 0, "STAGE1_ONLY": 1, "EXACT": 2, "NOCORR": 3}
 ERRORS = {-1: "EINVAL", -2: "EDIM", -3: "EFORMAT", -4: "EVERSION", -5: "EDEGENERATE", -6: "ECUDA",
           -7: "ENOMEM", -8: "ENCCL", -9: "EIO"}
 
@@ -186,24 +186,49 @@ def mrq_shard_plan(sizes, world: int) -> np.ndarray:
     return owner
 
 
+MRQ_EDIM = -2
+MRQ_EINVAL = -1
+
+
+def _index_D(h):
+    return mrq_index_info(h)["D"]
+
+
 def mrq_search_batch(h, queries: np.ndarray, params: SearchParams, with_stats=True, out_ids=None, out_dist=None):
     """Host buffers in and out; out_ids/out_dist (nq x K int64 / float32,
     e.g. pinned) are filled in place when given."""
     q = np.ascontiguousarray(queries, dtype=np.float32)
+    if q.ndim != 2 or q.shape[1] != _index_D(h):
+        raise MRQError(MRQ_EDIM, "queries must be (nq, D=%d), got %s" % (_index_D(h), q.shape))
     nq = q.shape[0]
     ids = out_ids if out_ids is not None else np.empty((nq, params.K), np.int64)
     dist = out_dist if out_dist is not None else np.empty((nq, params.K), np.float32)
-    assert ids.shape == (nq, params.K) and ids.dtype == np.int64 and ids.flags.c_contiguous
-    assert dist.shape == (nq, params.K) and dist.dtype == np.float32 and dist.flags.c_contiguous
+    if not (ids.shape == (nq, params.K) and ids.dtype == np.int64 and ids.flags.c_contiguous):
+        raise MRQError(MRQ_EINVAL, "out_ids must be C-contiguous int64 (%d, %d)" % (nq, params.K))
+    if not (dist.shape == (nq, params.K) and dist.dtype == np.float32 and dist.flags.c_contiguous):
+        raise MRQError(MRQ_EINVAL, "out_dist must be C-contiguous float32 (%d, %d)" % (nq, params.K))
     st = Stats()
     _check(lib().mrq_search_batch(h, _ptr(q), nq, C.byref(params), _ptr(ids), _ptr(dist),
                                   C.byref(st) if with_stats else None))
     return ids, dist, st
 
 
+def _check_dev(t, name, dtype, shape):
+    import torch
+    if not isinstance(t, torch.Tensor) or t.device.type != "cuda":
+        raise MRQError(MRQ_EINVAL, "%s must be a CUDA tensor" % name)
+    if t.dtype != dtype or not t.is_contiguous() or tuple(t.shape) != tuple(shape):
+        raise MRQError(MRQ_EDIM if name == "d_queries" else MRQ_EINVAL,
+                       "%s must be contiguous %s %s, got %s %s" % (name, dtype, tuple(shape), t.dtype, tuple(t.shape)))
+
+
 def mrq_search_batch_device(h, d_queries, params: SearchParams, d_ids, d_dist, stats: Stats | None = None,
                             stream=None):
-    nq = d_queries.shape[0]
+    import torch
+    nq = d_queries.shape[0] if d_queries.ndim == 2 else -1
+    _check_dev(d_queries, "d_queries", torch.float32, (max(nq, 0), _index_D(h)))
+    _check_dev(d_ids, "d_ids", torch.int64, (nq, params.K))
+    _check_dev(d_dist, "d_dist", torch.float32, (nq, params.K))
     s = C.c_void_p(stream) if stream else None
     _check(lib().mrq_search_batch_device(h, _ptr(d_queries), nq, C.byref(params), _ptr(d_ids), _ptr(d_dist),
                                          C.byref(stats) if stats is not None else None, s))

@@ -34,6 +34,11 @@ CASES = {
     "gist_small": ("gist", 8_000, 24, 960, 128, 32, (4,), None),
     "gist_d256": ("gist", 6_000, 16, 960, 256, 24, (3, 24), None),        # W = 8 code words
     "emb_d512": ("emb", 5_000, 12, 1536, 512, 16, (2, 16), None),         # W = 16, D = 1536
+    # k = 2048, Q = 300: the tcgen05 probe's 8 column tiles per 128-query block
+    # are split over several CTAs ("parts"), 3 query blocks, a ragged last one
+    "sift_k2048": ("sift", 100_000, 300, 128, 64, 2048, (16, 40), None),
+    # d = D: no residual (tails of width 0, eps_r = 0), one ragged code word
+    "tiny_dD": ("tiny", 4_000, 40, 24, 24, 8, (2, 8), None),
 }
 
 
@@ -280,14 +285,17 @@ def test_graph_replay_identical(case):
 
 def test_host_resident_tails_identical(case):
     """MRQ_LOAD_TAILS_HOST (the memory-limited setting of P:296):
-    tails in mapped pinned host memory give the HBM-resident results bit for bit."""
-    m, gx, Q = case["m"], case["gx"], case["Q"]
+    tails in mapped pinned host memory give the oracle's results bit for bit
+    (and the HBM-resident run's counters)."""
+    m, gx, ox, Q = case["m"], case["gx"], case["ox"], case["Q"]
     gh = m.Index(gx.build_file, case["X"], case["d"], tails_host=True)
     try:
         for tau in ("TIGHT", "LOOSE"):
             a = gx.search(Q, K=10, nprobe=case["nprobe"][-1], tau_schedule=tau)
             b = gh.search(Q, K=10, nprobe=case["nprobe"][-1], tau_schedule=tau)
-            assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+            o = ox.search(Q, K=10, nprobe=case["nprobe"][-1], tau_schedule=tau)
+            assert np.array_equal(b[0], o[0]) and np.array_equal(b[1].view(np.uint32), o[1].view(np.uint32))
+            assert b[2].exact == o[2]["exact"] and b[2].stage2_pass == o[2]["f2"]
             assert a[2].exact == b[2].exact and a[2].stage2_pass == b[2].stage2_pass
     finally:
         gh.close()
@@ -314,3 +322,99 @@ def test_query_order_invariance(case):
                     assert getattr(a[2], f) == getattr(b[2], f), f
     finally:
         m.mrq_debug_set(gx.h, "qorder", 1)
+
+
+def test_nocorr_parity(case):
+    """mode NOCORR: the K smallest (dis', id) over every
+    probed candidate, distance = fp32(dis'); ids and distances bit-exact."""
+    gx, ox, Q = case["gx"], case["ox"], case["Q"]
+    for npb in case["nprobe"]:
+        for K in (1, 10, 100):
+            gi, gd, gst = gx.search(Q, K=K, nprobe=npb, mode="NOCORR")
+            oi, od, ost = ox.search(Q, K=K, nprobe=npb, mode="NOCORR")
+            assert np.array_equal(gi, oi), (npb, K)
+            assert np.array_equal(gd.view(np.uint32), od.view(np.uint32)), (npb, K)
+            assert gst.scanned == ost["scanned"] and gst.stage1_pass == 0 and gst.exact == 0
+
+
+def test_graph_replay_survives_scratch_growth(case):
+    """A, A (captured), a larger B (scratch reallocated), A
+    again must not replay a graph holding freed scratch pointers; every call
+    equals the graph-free result."""
+    m, gx, Q = case["m"], case["gx"], case["Q"]
+    npb = case["nprobe"][0]
+    k = case["ox"].k
+    QA = Q[: max(1, Q.shape[0] // 3)]
+    QB = np.concatenate([Q, Q, Q], 0)
+    pa = m.SearchParams.make(K=10, nprobe=npb)
+    pb = m.SearchParams.make(K=100, nprobe=min(k, max(npb * 2, npb + 1)))
+    m.mrq_debug_set(gx.h, "graphs", 0)
+    ra = m.mrq_search_batch(gx.h, QA, pa, with_stats=False)[:2]
+    rb = m.mrq_search_batch(gx.h, QB, pb, with_stats=False)[:2]
+    m.mrq_debug_set(gx.h, "graphs", 1)
+    for qq, pp, ref in ((QA, pa, ra), (QA, pa, ra), (QA, pa, ra), (QB, pb, rb), (QA, pa, ra), (QA, pa, ra),
+                        (QB, pb, rb), (QB, pb, rb), (QA, pa, ra)):
+        ids, dist, _ = m.mrq_search_batch(gx.h, qq, pp, with_stats=False)
+        assert np.array_equal(ids, ref[0]) and np.array_equal(dist, ref[1])
+
+
+def test_close_twice_and_reload(case):
+    """Index.close is idempotent, mrq_free(NULL) is a no-op, and a reloaded
+    index gives the same results."""
+    m, Q = case["m"], case["Q"]
+    a = m.Index(case["gx"].build_file, case["X"], case["d"])
+    ia, da, _ = a.search(Q, K=10, nprobe=case["nprobe"][0])
+    a.close()
+    a.close()
+    m.mrq_free(None)
+    b = m.Index(case["gx"].build_file, case["X"], case["d"])
+    ib, db, _ = b.search(Q, K=10, nprobe=case["nprobe"][0])
+    b.close()
+    assert np.array_equal(ia, ib) and np.array_equal(da, db)
+
+
+def test_binding_shape_errors(case):
+    import torch
+    m, gx, Q = case["m"], case["gx"], case["Q"]
+    with pytest.raises(m.MRQError) as e:
+        gx.search(Q[:, :-1], K=10, nprobe=2)
+    assert e.value.code == -2
+    dq = torch.from_numpy(Q).cuda()
+    ids = torch.empty((Q.shape[0], 10), dtype=torch.int64, device="cuda")
+    dist = torch.empty((Q.shape[0], 10), dtype=torch.float32, device="cuda")
+    p = m.SearchParams.make(K=10, nprobe=2)
+    with pytest.raises(m.MRQError):
+        m.mrq_search_batch_device(gx.h, dq.double(), p, ids, dist)
+    with pytest.raises(m.MRQError):
+        m.mrq_search_batch_device(gx.h, dq, p, ids[:-1], dist)
+    with pytest.raises(m.MRQError):
+        m.mrq_search_batch_device(gx.h, dq, m.SearchParams.make(K=10, nprobe=2, seed_mult=1000), ids, dist)
+    m.mrq_search_batch_device(gx.h, dq, p, ids, dist)
+    torch.cuda.synchronize()
+
+
+def test_probe_overflow_and_sync_fallbacks(case):
+    """Rarely-taken paths give the default results bit for bit: the fused
+    probe's candidate-buffer overflow (probe_capp = 1: every centroid is
+    rescored) and the candidate scratch sized by the exact device total
+    (cand_budget_mb = 0: one D2H + stream sync instead of the host bound)."""
+    m, gx, ox, Q = case["m"], case["gx"], case["ox"], case["Q"]
+    npb = min(case["nprobe"][0], 16)
+    ref = gx.search(Q, K=10, nprobe=npb)
+    ref_probe = gx.fetch("probe", "u32").copy()
+    oi, od, _ = ox.search(Q, K=10, nprobe=npb)
+    assert np.array_equal(ref[0], oi)
+    try:
+        m.mrq_debug_set(gx.h, "probe_capp", 1)
+        a = gx.search(Q, K=10, nprobe=npb)
+        assert np.array_equal(gx.fetch("probe", "u32"), ref_probe)
+        assert np.array_equal(a[0], ref[0]) and np.array_equal(a[1], ref[1])
+        m.mrq_debug_set(gx.h, "probe_capp", 256)
+        m.mrq_debug_set(gx.h, "cand_budget_mb", 0)
+        for tau in ("TIGHT", "LOOSE"):
+            b = gx.search(Q, K=10, nprobe=npb, tau_schedule=tau)
+            o = ox.search(Q, K=10, nprobe=npb, tau_schedule=tau)
+            assert np.array_equal(b[0], o[0]) and np.array_equal(b[1].view(np.uint32), o[1].view(np.uint32))
+    finally:
+        m.mrq_debug_set(gx.h, "probe_capp", 256)
+        m.mrq_debug_set(gx.h, "cand_budget_mb", 8192)

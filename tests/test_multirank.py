@@ -120,6 +120,18 @@ class _ThreadExchange:
         return f
 
 
+_ORC = {}
+
+
+def _oracle_tiny(X):
+    """The oracle index of the committed Tiny build file (test infrastructure)."""
+    if "ix" not in _ORC:
+        import oracle
+        from oracle import build as B
+        _ORC["ix"] = oracle.Index(B.read(os.path.join(ROOT, "data", "tiny", "build_d16.mrqb")), X)
+    return _ORC["ix"]
+
+
 def _tiny():
     import synth
     cfg = synth.config_by_name("tiny")
@@ -147,7 +159,7 @@ def test_forced_exchange_equals_fast_path(tau):
 @pytest.mark.gpu
 @pytest.mark.parametrize("world,K", [(2, 10), (3, 10), (2, 100)])
 @pytest.mark.parametrize("tau,mode", [("TIGHT", "FULL"), ("LOOSE", "FULL"), ("TIGHT", "STAGE1_ONLY"),
-                                      ("TIGHT", "EXACT")])
+                                      ("TIGHT", "EXACT"), ("TIGHT", "NOCORR")])
 def test_virtual_ranks_equal_single_gpu(world, K, tau, mode):
     m = _lib()
     X, Q, bfile = _tiny()
@@ -167,16 +179,22 @@ def test_virtual_ranks_equal_single_gpu(world, K, tau, mode):
         t.start()
     for t in th:
         t.join(120)
+    oi, od, ost = _oracle_tiny(X).search(Q, K=K, nprobe=4, tau_schedule=tau, mode=mode)
     for r in range(world):
         ids, dd, st = res[r]
         assert np.array_equal(ids, ir), r                  # every rank holds the merged result
         assert np.array_equal(dd, dr), r
+        # ... which is the oracle's result queue (Alg.2 L15-L16)
+        assert np.array_equal(ids, oi), r
+        assert np.array_equal(dd.view(np.uint32), od.view(np.uint32)), r
         assert np.array_equal(idx[r].fetch("tau0", "f64"), t0r)
         assert np.array_equal(idx[r].fetch("tau1", "f64"), t1r)
     tot = lambda f: sum(getattr(res[r][2], f) for r in range(world))  # noqa: E731
-    assert tot("scanned") == sr.scanned
+    assert tot("scanned") == sr.scanned == ost["scanned"]
     assert tot("stage1_pass") == sr.stage1_pass                           # F1 as a set: sizes add up
     assert tot("stage2_pass") == sr.stage2_pass
+    if mode != "NOCORR":
+        assert tot("stage1_pass") == ost["f1"] and tot("stage2_pass") == ost["f2"]
     for x in idx:
         x.close()
 
@@ -197,6 +215,8 @@ def test_nccl_one_rank_exchange_equals_fast_path():
     m.mrq_debug_set(a.h, "force_exchange", 1)
     for tau in ("TIGHT", "LOOSE"):
         ia, da, _ = a.search(Q, K=10, nprobe=4, tau_schedule=tau)
+        oi, od, _ = _oracle_tiny(X).search(Q, K=10, nprobe=4, tau_schedule=tau)
+        assert np.array_equal(ia, oi) and np.array_equal(da.view(np.uint32), od.view(np.uint32)), tau
         if tau == "TIGHT":
             assert np.array_equal(ia, ir) and np.array_equal(da, dr)
     a.close()
