@@ -202,7 +202,21 @@ def main():
     ap.add_argument("--seed-lists", type=int, default=2, help="decision T: seed pool spans >= this many lists")
     ap.add_argument("--seed-mult", type=int, default=2, help="decision T: K' = seed_mult * K")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # launched without torchrun: start one process per GPU ourselves
+        # (the same launch the driver uses; rendezvous on 127.0.0.1)
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        log("spawning %d ranks: %s" % (args.gpus, " ".join(cmd)))
+        return subprocess.call(cmd)
     rank, world, local = dist_env()
+    if world != args.gpus:
+        log("note: WORLD_SIZE=%d, --gpus %d: the launch decides (n_gpus = WORLD_SIZE)" % (world, args.gpus))
     cfg_name = args.config
     dsel = args.d or {"tiny": 16, "sift": 64, "gist": 128, "deep": 64, "emb": 512}.get(cfg_name, 64)
     bfile = os.path.join(ROOT, "data", cfg_name, "build_d%d.mrqb" % dsel)
