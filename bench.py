@@ -371,6 +371,8 @@ def main():
     f1 = float(np.mean([s.stage1_pass for s in sts]))
     ms_scan = float(np.mean([s.ms_scan for s in sts]))
     ms_head = float(np.mean([s.ms_head for s in sts]))
+    ms_sketch = float(np.mean([s.ms_sketch for s in sts]))
+    sk_pass = float(np.mean([s.sketch_pass for s in sts]))
     hbm, peak_kind = peaks()
     traffic = ncu_traffic(cfg_name, nprobe)
     # algorithmic bytes per unit: scan = one
@@ -382,6 +384,17 @@ def main():
         "k_scan": {"unit": "scanned code", "bytes_per_unit": bcode, "units_per_launch": scanned, "ms": ms_scan},
         "k_head_b": {"unit": "F1 survivor", "bytes_per_unit": bhead, "units_per_launch": int(f1), "ms": ms_head},
     }
+    if ms_sketch > 0.002:
+        # the head gather split in two launches (DESIGN.md §5 head sketch): the
+        # sketch pre-pass reads (dq + 18) B per F1 entry, the fp32 gather 4d + 8
+        # B per sketch survivor; k_head_b's entry above is the pair together
+        dqb = (d + 15) // 16 * 16
+        kern["k_head_b"]["note"] = ("sketch pre-pass + fp32 gather of the %.0f%% survivors; algorithmic bytes "
+                                    "%.0f B per F1 entry" % (100.0 * sk_pass / max(f1, 1),
+                                                             dqb + 18 + bhead * sk_pass / max(f1, 1)))
+        kern["k_head_b"]["bytes_per_unit_design"] = round(dqb + 18 + bhead * sk_pass / max(f1, 1), 1)
+        kern["k_head_sketch"] = {"unit": "F1 entry (sketch row + slot/probe/scale/E/xr2)", "bytes_per_unit": dqb + 18,
+                                 "units_per_launch": int(f1), "ms": ms_sketch}
     f2 = float(np.mean([s.stage2_pass for s in sts]))
     D_ = int(X.shape[1])
     kern["k_topk_w"] = {"unit": "F2 survivor (exact re-rank gather; the launch also selects the top-K)",
@@ -395,7 +408,7 @@ def main():
         if kk["traffic"]:   # the DRAM side: ncu bytes per launch over the same launch time
             kk["dram_gbs"] = round(kk["traffic"] / (kk["ms"] * 1e-3) / 1e9, 1)
             kk["dram_frac"] = round(kk["dram_gbs"] / hbm, 4)
-    dom = max(kern, key=lambda n: kern[n]["ms"])
+    dom = max((n for n in kern if n != "k_head_sketch"), key=lambda n: kern[n]["ms"])
     # the probe screen GEMM on the tensor cores (kind::tf32): its flops against
     # the tf32 peak = measured bf16 burst x the nominal tf32/bf16 ratio (1.1/2.25)
     ms_gemm = float(np.mean([s.ms_probe_gemm for s in sts]))
@@ -409,7 +422,7 @@ def main():
     achieved = kern[dom]["achieved_gbs"]
     stage_ms = {k: round(float(np.mean([getattr(s, k) for s in sts])), 4)
                 for k in ("ms_qprep", "ms_probe", "ms_probe_gemm", "ms_quant", "ms_seed", "ms_scan", "ms_stage2",
-                          "ms_head", "ms_rerank", "ms_topk", "ms_comm")}
+                          "ms_head", "ms_sketch", "ms_rerank", "ms_topk", "ms_comm")}
 
     # e2e through the host-buffer call (pinned host queries; H2D + D2H inside the timed region)
     hq = torch.from_numpy(Q).pin_memory().numpy()
@@ -467,6 +480,7 @@ def main():
                    "recall10": round(rc, 4) if rc is not None else None, "l2": "flushed (512 MB write) between timed steps",
                    "parallelism": "lists sharded over %d GPU(s)" % world, "base_sha_match": sha_ok,
                    "scanned_per_step": scanned, "exact_per_query": round(float(np.mean([s.exact for s in sts])) / nq, 2),
+                   "f1_per_query": round(f1 / nq, 1), "sketch_pass_per_query": round(sk_pass / nq, 1),
                    "stage_ms": stage_ms, "sweep": sweep, "index_load_s": round(load_s, 2),
                    "index_build": "oracle build file (committed)" if build_info is None else
                    {"by": "mrq_build_gpu", **{k_: round(v_, 1) for k_, v_ in build_info.items()}}},

@@ -97,6 +97,9 @@ typedef struct {
     double ms_total, ms_qprep, ms_probe, ms_quant, ms_seed, ms_scan, ms_stage2, ms_rerank, ms_topk, ms_comm;
     double ms_head;        /* the stage-2 head gather alone (part of ms_stage2)  */
     double ms_probe_gemm;  /* the probe screen GEMM alone (part of ms_probe)     */
+    double ms_sketch;      /* the head-sketch pre-pass alone (part of ms_head; 0 if not run) */
+    uint64_t sketch_pass;  /* F1 entries the head sketch could not prune (= stage1_pass
+                              when the pre-pass does not run): the fp32 head rows read   */
 } mrq_stats;
 
 /*

@@ -336,6 +336,11 @@ static int load_impl(mrq_index *ix, const char *build_file, const float *base, i
     TRY(dalloc(ix, (void **)&ix->f3, (size_t)npad * 4));
     TRY(dalloc(ix, (void **)&ix->xr2, (size_t)npad * 4));
     TRY(dalloc(ix, (void **)&ix->heads, (size_t)npad * d * 4));
+    ix->dq = (d + 15) / 16 * 16;
+    TRY(dalloc(ix, (void **)&ix->hq, (size_t)npad * ix->dq));
+    TRY(dalloc(ix, (void **)&ix->hs, (size_t)npad * sizeof(float4)));
+    MRQ_CUDA_TRY(cudaMemsetAsync(ix->hq, 0, (size_t)npad * ix->dq, ix->stream));
+    MRQ_CUDA_TRY(cudaMemsetAsync(ix->hs, 0, (size_t)npad * sizeof(float4), ix->stream));
     if (ix->tails_host) {   // NEXT-4: tails in pinned host memory, read through the mapped device pointer
         const size_t tb = (size_t)npad * std::max(D - d, 1) * 4;
         if (cudaHostAlloc(&ix->tails_hbuf, tb, cudaHostAllocMapped) != cudaSuccess) {
@@ -386,7 +391,7 @@ static int load_impl(mrq_index *ix, const char *build_file, const float *base, i
         launch_rowmat_f32(dX, m, D, D, ix->mu, ix->PT, D, dXp, D, ix->stream);
         k_encode_finish<<<(unsigned)((m + enc_warps - 1) / enc_warps), enc_warps * 32, enc_smem, ix->stream>>>(
             dXp, 0, m, D, d, W, dAssign, dSlot, ix->C, ix->RT, npad, ix->heads, ix->tails, ix->xr2, ix->codes, ix->f1,
-            ix->f2, ix->f3);
+            ix->f2, ix->f3, ix->hq, ix->hs, ix->dq);
         MRQ_CUDA_TRY(cudaGetLastError());
         MRQ_CUDA_TRY(cudaStreamSynchronize(ix->stream));   // hx is reused
     }
@@ -425,6 +430,7 @@ extern "C" int mrq_index_load_ex(const char *build_file, const float *base, int6
     memset(ix->g_key, 0, sizeof(GraphKey));
     memset(ix->g_pending, 0, sizeof(GraphKey));
     if (getenv("MRQ_NO_GRAPHS")) ix->graphs = 0;
+    if (getenv("MRQ_NO_SKETCH")) ix->sketch_on = 0;
     int rc = mrq_guard([&] { return load_impl(ix, build_file, base, n, D, d, dist); });
     if (rc != MRQ_OK) {
         mrq_free(ix);
@@ -484,23 +490,34 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
     if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[0], st));
     uint32_t *qorder = nullptr;
 
+    // Query-sharded front end (world > 1): rank r computes a1-a3
+    // (projection, probe, quantization) for the query rows [q0, q0 + nr) only;
+    // the per-query results are then all-gathered (in place, rank-major rows
+    // of S = ceil(nq / world)) so every rank holds every query's probe order,
+    // planes and constants -- bit-identical to computing them itself.
+    const bool sharded = ix->world > 1 || ix->force_exchange;
+    const bool fshard = ix->world > 1 && ix->front_shard;
+    const int64_t S = fshard ? (nq + ix->world - 1) / ix->world : nq;
+    const int64_t q0 = fshard ? (int64_t)ix->rank * S : 0;
+    const int64_t nr = fshard ? std::max<int64_t>(0, std::min<int64_t>(nq, q0 + S) - q0) : nq;
+    const int64_t nrow = fshard ? S * ix->world : nq;   // rows of the per-query front arrays
     double *qp, *qr2, *eps_r, *r0, *qnorm, *tau0, *tau1, *probe_qn2, *qconst, *s0_exact, *s1_exact;
     float *qd32, *approx, *qa3 = nullptr;
     uint32_t *probe, *planes, *s0_cnt, *s0_pos, *s1_cnt, *s1_pos, *f1_cnt, *f2_cnt, *exact_cnt, *fallback;
     uint64_t *cand_cnt, *f1_off;
-    SCR("qp", double, nq * D, qp);
-    SCR("qr2", double, nq, qr2);
-    SCR("eps_r", double, nq, eps_r);
-    SCR("r0", double, nq * d, r0);
-    SCR("qnorm", double, nq, qnorm);
-    SCR("qd32", float, nq * d, qd32);
-    if (mrq_probe_tc_enabled(ix)) SCR("qa3", float, nq * 3 * d, qa3);   // 3xTF32 A operand
+    SCR("qp", double, nrow * D, qp);
+    SCR("qr2", double, nrow, qr2);
+    SCR("eps_r", double, nrow, eps_r);
+    SCR("r0", double, nrow * d, r0);
+    SCR("qnorm", double, nrow, qnorm);
+    SCR("qd32", float, nrow * d, qd32);
+    if (mrq_probe_tc_enabled(ix)) SCR("qa3", float, nrow * 3 * d, qa3);   // 3xTF32 A operand
     SCR("tau0", double, nq, tau0);
     SCR("tau1", double, nq, tau1);
-    SCR("probe", uint32_t, nq * np, probe);
-    SCR("probe_qn2", double, nq * np, probe_qn2);
-    SCR("planes", uint32_t, nq * np * MRQ_BQ * W, planes);
-    SCR("qconst", double, nq * np * 8, qconst);
+    SCR("probe", uint32_t, nrow * np, probe);
+    SCR("probe_qn2", double, nrow * np, probe_qn2);
+    SCR("planes", uint32_t, nrow * np * MRQ_BQ * W, planes);
+    SCR("qconst", double, nrow * np * 8, qconst);
     SCR("cand_cnt", uint64_t, nq + 1, cand_cnt);
     SCR("f1_off", uint64_t, nq + 1, f1_off);
     SCR("s0_cnt", uint32_t, nq, s0_cnt);
@@ -512,7 +529,6 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
     uint32_t *s0_id, *s1_id;
     SCR("s0_id", uint32_t, nq * Kp, s0_id);
     SCR("s1_id", uint32_t, nq * Kp, s1_id);
-    const bool sharded = ix->world > 1 || ix->force_exchange;
     const int Lx = std::max(Kp, K);
     XItem *xsend = nullptr, *xrecv = nullptr;
     if (sharded) {
@@ -525,77 +541,130 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
     SCR("fallback", uint32_t, 1, fallback);
     MRQ_CUDA_TRY(cudaMemsetAsync(fallback, 0, 4, st));
 
-    // ---- a1: query projection (Alg.2 L1-L4)
-    {
-        uint16_t *qkey = nullptr;
-        if (ix->qorder_on && nq > 1) {
-            SCR("qorder", uint32_t, nq, qorder);
-            SCR("qkey", uint16_t, nq, qkey);
-        }
-        launch_rowmat_f32(d_q, nq, D, D, ix->mu, ix->PT, D, qp, D, st);             // q_p = P (q - mu)
-        const size_t qsmem = (size_t)D * 8 * 9;                                    // lambda + 8 query rows
+    // head sketch: the scan drops F1 entries whose lower bound
+    // of the canonical dis_o' already fails the F2 test (LOOSE: tau1 = tau0)
+    const bool want_sketch = ix->sketch_on && mode == 0 && !tight && !ix->dbg_dump_dis &&
+                             mrq_scan_smem_sk(np, W, ix->dq) <= (size_t)std::min(ix->smem_optin, 64 * 1024);
+    uint8_t *qsk_b = nullptr;
+    double *qsk_c = nullptr;
+    if (want_sketch) {
+        SCR("qsk_b", uint8_t, (size_t)nrow * np * ix->dq, qsk_b);
+        SCR("qsk_c", double, (size_t)nrow * np * 4, qsk_c);
+    }
+    uint16_t *qkey = nullptr;
+    if (ix->qorder_on && nq > 1) {
+        SCR("qorder", uint32_t, nq, qorder);
+        SCR("qkey", uint16_t, nrow, qkey);
+    }
+    // ---- a1: query projection (Alg.2 L1-L4), rows [q0, q0 + nr)
+    if (nr > 0) {
+        launch_rowmat_f32(d_q + q0 * D, nr, D, D, ix->mu, ix->PT, D, qp + q0 * D, D, st);   // q_p = P (q - mu)
+        const size_t qsmem = (size_t)D * 8 * 9;                                              // lambda + 8 query rows
         if (qsmem > 48 * 1024)
             MRQ_CUDA_TRY(cudaFuncSetAttribute(k_qtail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsmem));
-        k_qtail<<<(unsigned)((nq + 7) / 8), 256, qsmem, st>>>(qp, nq, D, d, W, ix->lam, ix->RT, p->resid_scale, p->m,
-                                                              qr2, eps_r, r0, qd32, qnorm, qkey, qa3);
-        // side stream, beside the probe: the order's single-block sort and
-        // r0 = R q_d (only the quantizer needs it)
+        k_qtail<<<(unsigned)((nr + 7) / 8), 256, qsmem, st>>>(
+            qp + q0 * D, nr, D, d, W, ix->lam, ix->RT, p->resid_scale, p->m, qr2 + q0, eps_r + q0, r0 + q0 * d,
+            qd32 + q0 * d, qnorm + q0, qkey ? qkey + q0 : nullptr, qa3 ? qa3 + q0 * 3 * d : nullptr);
+        // side stream, beside the probe: the order's single-block sort (all
+        // queries are local unless the front end is sharded) and r0 = R q_d
+        // (only the quantizer needs it)
         MRQ_CUDA_TRY(cudaEventRecord(ix->ev_fork[0], st));
         MRQ_CUDA_TRY(cudaStreamWaitEvent(ix->side, ix->ev_fork[0], 0));
-        if (qkey) launch_qorder(qkey, nq, qorder, ix->side);
-        launch_rowmat_f64(qp, nq, D, d, nullptr, ix->RT, d, r0, d, ix->side);
+        if (qkey && !fshard) launch_qorder(qkey, nq, qorder, ix->side);
+        launch_rowmat_f64(qp + q0 * D, nr, D, d, nullptr, ix->RT, d, r0 + q0 * d, d, ix->side);
         MRQ_CUDA_TRY(cudaEventRecord(ix->ev_fork[3], ix->side));
     }
     if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[1], st));
 
-    // ---- a2: probe (Alg.2 L7): screen + exact selection
-    {
+    // ---- a2: probe (Alg.2 L7): screen + exact selection, rows [q0, q0 + nr)
+    if (nr > 0) {
         uint32_t *cand, *ncand;
-        SCR("probe_cand", uint32_t, nq * k, cand);
-        SCR("probe_ncand", uint32_t, nq, ncand);
+        SCR("probe_cand", uint32_t, nr * k, cand);
+        SCR("probe_ncand", uint32_t, nr, ncand);
+        double *qp_r = qp + q0 * D, *qn_r = qnorm + q0, *pq_r = probe_qn2 + q0 * np;
+        uint32_t *pr_r = probe + q0 * np;
         if (mrq_probe_tc_fusable(ix, np)) {   // tcgen05 screen with the running top-np in its epilogue
-            const int P = mrq_probe_tc_parts(ix, nq), capp = ix->probe_capp;
+            const int P = mrq_probe_tc_parts(ix, nr), capp = ix->probe_capp;
             uint2 *cbuf;
             uint32_t *ccnt;
             float *kvbuf;
-            SCR("probe_cbuf", uint2, (size_t)nq * P * capp, cbuf);
-            SCR("probe_ccnt", uint32_t, (size_t)nq * P, ccnt);
-            SCR("probe_kv", float, (size_t)nq * P * 16, kvbuf);
+            SCR("probe_cbuf", uint2, (size_t)nr * P * capp, cbuf);
+            SCR("probe_ccnt", uint32_t, (size_t)nr * P, ccnt);
+            SCR("probe_kv", float, (size_t)nr * P * 16, kvbuf);
             const double kappa = mrq_probe_tc_kappa(ix);
-            TRY(mrq_probe_tc_run_fused(ix, qa3, nq, np, qnorm, kappa, cbuf, capp, ccnt, kvbuf, st));
+            TRY(mrq_probe_tc_run_fused(ix, qa3 + q0 * 3 * d, nr, np, qn_r, kappa, cbuf, capp, ccnt, kvbuf, st));
             if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[11], st));
-            TRY(launch_probe_finish_w(nq, k, d, np, qp, D, ix->C, qnorm, ix->cmax, kappa, cbuf, P, capp,
-                                      mrq_probe_tc_grid(ix, nq), ccnt, kvbuf, cand, probe, probe_qn2, ncand, st));
+            TRY(launch_probe_finish_w(nr, k, d, np, qp_r, D, ix->C, qn_r, ix->cmax, kappa, cbuf, P, capp,
+                                      mrq_probe_tc_grid(ix, nr), ccnt, kvbuf, cand, pr_r, pq_r, ncand, st));
         } else {
-            SCR("approx", float, nq * k, approx);
+            SCR("approx", float, nr * k, approx);
             double kappa;
             if (mrq_probe_tc_enabled(ix)) {
-                TRY(mrq_probe_tc_run(ix, qa3, nq, approx, st));
+                TRY(mrq_probe_tc_run(ix, qa3 + q0 * 3 * d, nr, approx, st));
                 kappa = mrq_probe_tc_kappa(ix);
             } else {
-                dim3 grid((k + 255) / 256, (unsigned)((nq + 7) / 8));
-                k_probe_approx<<<grid, 256, 8 * d * sizeof(float), st>>>(qd32, nq, d, k, ix->C32T, approx);
+                dim3 grid((k + 255) / 256, (unsigned)((nr + 7) / 8));
+                k_probe_approx<<<grid, 256, 8 * d * sizeof(float), st>>>(qd32 + q0 * d, nr, d, k, ix->C32T, approx);
                 kappa = std::ldexp(1.0, -24) * (2.0 * d + 8.0);
             }
             if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[11], st));
-            TRY(launch_probe_select_w(approx, nq, k, d, np, qp, D, ix->C, qnorm, ix->cmax, kappa, cand, probe,
-                                      probe_qn2, ncand, st));
+            TRY(launch_probe_select_w(approx, nr, k, d, np, qp_r, D, ix->C, qn_r, ix->cmax, kappa, cand, pr_r, pq_r,
+                                      ncand, st));
         }
+    } else if (timed) {
+        MRQ_CUDA_TRY(cudaEventRecord(ix->ev[11], st));
     }
     if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[2], st));
 
-    // ---- a3: per-(query, list) quantization into bit-planes
-    {
-        // F1 segment offsets on the side stream, beside the quantizer; join
+    // ---- a3: per-(query, list) quantization into bit-planes, rows [q0, q0 + nr)
+    auto fork_offsets = [&]() -> int {   // F1 segment offsets of all nq queries on the side stream
         MRQ_CUDA_TRY(cudaEventRecord(ix->ev_fork[1], st));
         MRQ_CUDA_TRY(cudaStreamWaitEvent(ix->side, ix->ev_fork[1], 0));
+        if (qkey && fshard) launch_qorder(qkey, nq, qorder, ix->side);
         k_cand_count<<<(unsigned)((nq + 255) / 256), 256, 0, ix->side>>>(probe, nq, np, ix->list_size, cand_cnt);
         k_exclusive_scan<<<1, 1024, 0, ix->side>>>(cand_cnt, nq, f1_off);
         MRQ_CUDA_TRY(cudaEventRecord(ix->ev_fork[2], ix->side));
+        return MRQ_OK;
+    };
+    if (!fshard) TRY(fork_offsets());   // beside the quantizer
+    if (nr > 0) {
         MRQ_CUDA_TRY(cudaStreamWaitEvent(st, ix->ev_fork[3], 0));   // r0
-        launch_quant(probe, probe_qn2, nq, np, d, W, r0, ix->Rc, qr2, p->eps0, planes, qconst, st);
-        MRQ_CUDA_TRY(cudaStreamWaitEvent(st, ix->ev_fork[2], 0));
+        launch_quant(probe + q0 * np, probe_qn2 + q0 * np, nr, np, d, W, r0 + q0 * d, ix->Rc, qr2 + q0, p->eps0,
+                     planes + q0 * np * MRQ_BQ * W, qconst + q0 * np * 8, qsk_b ? qsk_b + q0 * np * ix->dq : nullptr,
+                     qsk_c ? qsk_c + q0 * np * 4 : nullptr, ix->dq, qnorm + q0, ix->cmax, st);
     }
+    if (fshard) {
+        // every rank's rows to every rank: one grouped in-place all-gather
+        std::vector<char *> base;
+        std::vector<size_t> rowb;
+        auto sec = [&](void *ptr, size_t b) {
+            base.push_back((char *)ptr);
+            rowb.push_back(b);
+        };
+        sec(qp, (size_t)D * 8);
+        sec(qr2, 8);
+        sec(eps_r, 8);
+        sec(probe, (size_t)np * 4);
+        sec(probe_qn2, (size_t)np * 8);
+        sec(planes, (size_t)np * MRQ_BQ * W * 4);
+        sec(qconst, (size_t)np * 8 * 8);
+        if (qkey) sec(qkey, 2);
+        if (qsk_b) {
+            sec(qsk_b, (size_t)np * ix->dq);
+            sec(qsk_c, (size_t)np * 4 * 8);
+        }
+        std::vector<const void *> sends(base.size());
+        std::vector<void *> recvs(base.size());
+        std::vector<size_t> bytes(base.size());
+        for (size_t i = 0; i < base.size(); i++) {
+            bytes[i] = (size_t)S * rowb[i];
+            sends[i] = base[i] + (size_t)ix->rank * bytes[i];
+            recvs[i] = base[i];
+        }
+        TRY(mrq_allgather_group(ix, (int)base.size(), sends.data(), recvs.data(), bytes.data(), st));
+    }
+    if (fshard) TRY(fork_offsets());      // after the all-gather: every query's probe lists
+    MRQ_CUDA_TRY(cudaStreamWaitEvent(st, ix->ev_fork[2], 0));   // join
     // candidate-indexed scratch: sized by the host bound nq x (sum of the np
     // largest lists) when that fits the budget, so the search never waits on
     // the device; else by the exact total (one D2H + stream sync)
@@ -616,6 +685,10 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
     SCR("f2_exact", double, total, f2_exact);
     uint32_t *f1_id;
     SCR("f1_id", uint32_t, total, f1_id);
+    // head sketch pre-pass of the stage-2 gather (LOOSE): probe index per F1
+    // entry (written by the scan) and the compacted survivors
+    uint32_t *surv_cnt = nullptr;
+    if (want_sketch) SCR("surv_cnt", uint32_t, nq, surv_cnt);
     if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[3], st));
 
     StageArgs sa;
@@ -636,6 +709,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
     sa.seed_lists = p->seed_lists > 0 ? p->seed_lists : 1;
     sa.list_size_g = ix->list_size_g; sa.s0_id = s0_id; sa.s1_id = s1_id; sa.xout = nullptr;
     sa.store_f1 = ix->dbg_dump_dis;
+    sa.sketch = want_sketch; sa.surv_cnt = surv_cnt;
 
     if (mode == 3) {
         // ---- NOCORR: top-K by dis' over every probed candidate, no bounds, no re-rank
@@ -677,6 +751,9 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
             a.codes = ix->codes; a.f1 = ix->f1; a.f2 = ix->f2; a.f3 = ix->f3; a.planes = planes; a.qconst = qconst;
             a.eps_r = eps_r; a.tau0 = tau0; a.isd = isd; a.f1_off = f1_off; a.f1_cnt = f1_cnt; a.f1_pos = f1_pos;
             a.qorder = qorder;
+            a.hq = ix->hq; a.hs = ix->hs; a.qsk_b = qsk_b; a.qsk_c = qsk_c; a.qr2 = qr2;
+            a.dq = ix->dq; a.surv_cnt = surv_cnt;   // NULL: plain F1 (no fused sketch test)
+            if (surv_cnt) a.smem = mrq_scan_smem_sk(np, W, ix->dq);
             TRY(launch_scan(W, a, st));
             if (ix->dbg_dump_dis) {
                 double *dd, *dl;
@@ -749,6 +826,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
         float mh = 0.f;
         MRQ_CUDA_TRY(cudaEventElapsedTime(&mh, ix->ev[5], ix->ev[10]));
         stats->ms_head = mh;
+        stats->ms_sketch = 0.0;   // the sketch test runs inside the scan (ms_scan)
         float mg = 0.f;
         MRQ_CUDA_TRY(cudaEventElapsedTime(&mg, ix->ev[1], ix->ev[11]));
         stats->ms_probe_gemm = mg;
@@ -766,6 +844,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
         stats->stage2_pass = sum32(f2_cnt);
         stats->exact = sum32(exact_cnt);
         stats->seeds = sum32(s0_cnt) + sum32(s1_cnt);
+        stats->sketch_pass = surv_cnt ? sum32(surv_cnt) : stats->stage1_pass;
     }
     return MRQ_OK;
 }
@@ -933,6 +1012,7 @@ static int debug_fetch(mrq_index *ix, const char *name, void *dst, size_t dst_by
         {"f3", ix->f3, (size_t)npad * 4},                {"xr2", ix->xr2, (size_t)npad * 4},
         {"heads", ix->heads, (size_t)npad * d * 4},      {"tails", ix->tails, (size_t)npad * std::max(D - d, 0) * 4},
         {"Rc", ix->Rc, (size_t)k * d * 8},
+        {"hq", ix->hq, (size_t)npad * ix->dq},          {"hs", ix->hs, (size_t)npad * 16},
     };
     for (auto &e : fixed)
         if (nm == e.n) {
@@ -960,6 +1040,7 @@ static int debug_fetch(mrq_index *ix, const char *name, void *dst, size_t dst_by
             {"f2_head", (size_t)ix->last_total * 8}, {"f2_exact", (size_t)ix->last_total * 8},
             {"fallback", 4}, {"approx", (size_t)nq * k * 4}, {"probe_ncand", (size_t)nq * 4},
             {"dbg_dis", (size_t)ix->last_total * 8}, {"dbg_lb1", (size_t)ix->last_total * 8},
+            {"surv_cnt", (size_t)nq * 4},
         };
         for (auto &e : per)
             if (nm == e.n) {
@@ -1014,6 +1095,14 @@ extern "C" int mrq_debug_set(mrq_index *ix, const char *name, int64_t value)
     }
     if (std::string(name) == "graphs") {           // CUDA-graph replay of repeated searches (default 1)
         ix->graphs = (int)value;
+        return MRQ_OK;
+    }
+    if (std::string(name) == "front_shard") {      // world > 1: query-sharded a1-a3 + all-gather (default 1)
+        ix->front_shard = (int)value;
+        return MRQ_OK;
+    }
+    if (std::string(name) == "sketch") {           // head-sketch pre-pass of the stage-2 gather (default 1)
+        ix->sketch_on = (int)value;
         return MRQ_OK;
     }
     if (std::string(name) == "probe_capp") {       // per-part candidate buffer of the fused probe (default 256)

@@ -60,6 +60,9 @@ struct NcclApi {
     ncclResult_t (*commInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
     ncclResult_t (*allGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*commAbort)(ncclComm_t) = nullptr;
+    ncclResult_t (*groupStart)() = nullptr;
+    ncclResult_t (*groupEnd)() = nullptr;
     const char *(*getErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -81,7 +84,11 @@ NcclApi &nccl()
         api.allGather = (decltype(api.allGather))dlsym(h, "ncclAllGather");
         api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
         api.getErrorString = (decltype(api.getErrorString))dlsym(h, "ncclGetErrorString");
-        api.ok = api.getUniqueId && api.commInitRank && api.allGather && api.commDestroy && api.getErrorString;
+        api.commAbort = (decltype(api.commAbort))dlsym(h, "ncclCommAbort");
+        api.groupStart = (decltype(api.groupStart))dlsym(h, "ncclGroupStart");
+        api.groupEnd = (decltype(api.groupEnd))dlsym(h, "ncclGroupEnd");
+        api.ok = api.getUniqueId && api.commInitRank && api.allGather && api.commDestroy && api.getErrorString &&
+                 api.commAbort && api.groupStart && api.groupEnd;
         if (!api.ok) snprintf(api.err, sizeof api.err, "libnccl.so.2 lacks a required symbol");
     });
     return api;
@@ -168,13 +175,18 @@ int mrq_allgather(mrq_index *ix, const void *send, void *recv, size_t bytes, cud
         ncclResult_t r = a.allGather(send, recv, bytes, ncclUint8, (ncclComm_t)ix->nccl_comm, st);
         if (r != ncclSuccess) {
             mrq_set_error("ncclAllGather(%zu B): %s", bytes, a.getErrorString(r));
+            mrq_comm_fail(ix);
             return MRQ_ENCCL;
         }
         return MRQ_OK;
     }
 #endif
+    if (ix->comm_failed) {
+        mrq_set_error("the NCCL communicator of this index was aborted after a failure");
+        return MRQ_ENCCL;
+    }
     if (ix->world == 1) {
-        MRQ_CUDA_TRY(cudaMemcpyAsync(recv, send, bytes, cudaMemcpyDeviceToDevice, st));
+        if (send != recv) MRQ_CUDA_TRY(cudaMemcpyAsync(recv, send, bytes, cudaMemcpyDeviceToDevice, st));
         return MRQ_OK;
     }
     if (!ix->host_ag) {
@@ -199,4 +211,46 @@ int mrq_allgather(mrq_index *ix, const void *send, void *recv, size_t bytes, cud
     }
     MRQ_CUDA_TRY(cudaMemcpyAsync(recv, h + bytes, bytes * (size_t)ix->world, cudaMemcpyHostToDevice, st));
     return MRQ_OK;
+}
+
+// Several all-gathers at once (the sharded front end's per-query sections):
+// one NCCL group (a single fused launch), else one host exchange per section.
+int mrq_allgather_group(mrq_index *ix, int n, const void *const *send, void *const *recv, const size_t *bytes,
+                        cudaStream_t st)
+{
+#if MRQ_HAVE_NCCL
+    if (ix->nccl_comm) {
+        NcclApi &a = nccl();
+        ncclResult_t r = a.groupStart();
+        for (int i = 0; i < n && r == ncclSuccess; i++)
+            r = a.allGather(send[i], recv[i], bytes[i], ncclUint8, (ncclComm_t)ix->nccl_comm, st);
+        const ncclResult_t r2 = a.groupEnd();
+        if (r == ncclSuccess) r = r2;
+        if (r != ncclSuccess) {
+            mrq_set_error("ncclAllGather group (%d sections): %s", n, a.getErrorString(r));
+            mrq_comm_fail(ix);
+            return MRQ_ENCCL;
+        }
+        return MRQ_OK;
+    }
+#endif
+    for (int i = 0; i < n; i++) {
+        const int rc = mrq_allgather(ix, send[i], recv[i], bytes[i], st);
+        if (rc != MRQ_OK) return rc;
+    }
+    return MRQ_OK;
+}
+
+// A failed collective leaves the communicator unusable (and its peers
+// possibly blocked): abort it instead of a destroy that could hang, so every
+// later call on this index fails fast with MRQ_ENCCL.
+void mrq_comm_fail(mrq_index *ix)
+{
+#if MRQ_HAVE_NCCL
+    if (ix->nccl_comm) {
+        nccl().commAbort((ncclComm_t)ix->nccl_comm);
+        ix->nccl_comm = nullptr;
+        ix->comm_failed = 1;
+    }
+#endif
 }

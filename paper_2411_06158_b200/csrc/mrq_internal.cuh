@@ -66,7 +66,7 @@ struct DevArr {
 struct mrq_index {
     int device = 0;
     cudaStream_t stream = nullptr;
-    cudaEvent_t ev[12] = {};
+    cudaEvent_t ev[13] = {};
     cudaStream_t side = nullptr;      // fork/join stream for the single-block kernels (query order, F1 offsets)
     cudaEvent_t ev_fork[4] = {};
     int64_t N = 0, npad = 0;
@@ -78,6 +78,8 @@ struct mrq_index {
     void *xhost = nullptr;                     // pinned staging of the host exchange
     size_t xhost_bytes = 0;
     int force_exchange = 0;                    // mrq_debug_set("force_exchange"): world-1 runs the sharded path
+    int front_shard = 1;                       // mrq_debug_set("front_shard"): a1-a3 per query slice + all-gather
+    int comm_failed = 0;                       // the NCCL communicator was aborted (mrq_comm_fail)
     void *probe_tc = nullptr;                  // tcgen05 probe state (mrq_probe_tc.cu)
     int force_cuda_core_probe = 0;             // mrq_debug_set("cuda_core_probe"): CUDA-core screen instead
 #ifndef MRQ_QORDER_DEFAULT
@@ -91,6 +93,7 @@ struct mrq_index {
     void *gexec = nullptr;                     // cudaGraphExec_t of the cached search
     void *g_key = nullptr, *g_pending = nullptr;   // GraphKey of the cached / last uncached search
     int sm_count = 148;
+    int sketch_on = 1;                         // mrq_debug_set("sketch"): head-sketch pre-pass of the stage-2 gather
     int probe_capp = 256;                      // mrq_debug_set("probe_capp"): fused-probe candidate buffer per part
     uint64_t cand_budget = (uint64_t)8 << 30;  // mrq_debug_set("cand_budget_mb"): host-bound scratch budget
     int smem_optin = 227 * 1024;               // max dynamic shared memory per block (opt-in)
@@ -114,6 +117,9 @@ struct mrq_index {
     uint32_t *codes = nullptr;                                            // [W][npad]
     float *f1 = nullptr, *f2 = nullptr, *f3 = nullptr, *xr2 = nullptr;    // [npad]
     float *heads = nullptr, *tails = nullptr;                             // [npad][d], [npad][D-d]
+    uint8_t *hq = nullptr;                                                // [npad][dq] head sketch (biased int8)
+    float4 *hs = nullptr;                                                 // [npad] sketch (s, E, ||x_r||^2, -)
+    int dq = 0;                                                           // sketch row bytes: d rounded up to 16
 
     // per-search scratch (grow only)
     std::map<std::string, DevArr> scratch;

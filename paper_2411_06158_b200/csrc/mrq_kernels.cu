@@ -123,6 +123,52 @@ void launch_rowmat_f64(const double *X, int64_t nrows, int ldx, int Din, const d
 }
 
 // ======================================================================= a0
+// Head sketch (an acceleration structure of the stage-2 gather, DESIGN.md
+// §5 "head sketch"; not part of the paper's method).  HEAD = ||h - q_d||^2 of
+// the STORED fp32 head h is rotation invariant, so it is sketched in the
+// quantizer's rotated frame, where the query side R (q_d - c) already exists
+// (k_quant_g): y = R (h - c) (fp64, the encoder's matvec on the fp32 head),
+// quantized to signed int8 levels a_i (|a_i| <= 127; padding to dq bytes is
+// 0) with a per-vector scale s (fp32, rounded up from max|y| / 127) and a
+// rigorous bound E >= ||R (h - c) - s a||_2 (fp32, rounded up; it covers the
+// rounding of the fp64 matvec and of the quantization residual).  The scan
+// turns it into a lower bound of the canonical HEAD that prunes stage-2
+// candidates without reading the fp32 head row; every candidate it cannot
+// prune is decided by the canonical fp64 HEAD, so F2 is unchanged.  Warp per
+// vector; y (d doubles, shared memory) is the rotated residual.
+__device__ void mrq_head_sketch(const double *y, double ynorm_bound, float xr2, int d, int dq, uint8_t *out,
+                                float4 *se)
+{
+    const int lane = threadIdx.x & 31;
+    double mx = 0.0;
+    for (int i = lane; i < d; i += 32) mx = fmax(mx, fabs(y[i]));
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const float s = mx > 0.0 ? __double2float_ru(mx / 127.0) : 0.f;
+    double e2 = 0.0;
+    for (int i = lane; i < dq; i += 32) {
+        int a = 0;
+        if (i < d && s > 0.f) {
+            const double q = rint(y[i] / (double)s);
+            a = (int)fmin(127.0, fmax(-127.0, q));
+            const double e = y[i] - (double)s * (double)a;
+            e2 = e2 + e * e;
+        } else if (i < d) {
+            e2 = e2 + y[i] * y[i];
+        }
+        out[i] = (uint8_t)(int8_t)a;
+    }
+    for (int o = 16; o > 0; o >>= 1) e2 = e2 + __shfl_xor_sync(0xffffffffu, e2, o);
+    if (lane == 0) {
+        // margins: the fp64 residual e per element <= 2^-50 mx; the matvec
+        // y_j = sum_i R_ji (h_i - c_i) (d terms, |R_j| = 1) per element <=
+        // (d + 2) 2^-53 ||h - c|| <= (d + 2) 2^-52 ynorm_bound
+        const double E = __dsqrt_ru(e2) * (1.0 + 0x1p-40) + 0x1p-49 * mx * sqrt((double)d) +
+                         0x1p-50 * (double)(d + 2) * sqrt((double)d) * ynorm_bound;
+        *se = make_float4(s, __double2float_ru(E), xr2, 0.f);   // (s, E, ||x_r||^2, -)
+    }
+    __syncwarp();
+}
+
 // Alg.1 L4-L8, one warp per vector, results scattered to the
 // vector's list slot.  t = x_d - c_{a(x)}; y = R t (y_j = sum_i R[j][i] t_i);
 // bit_j = [y_j >= 0]; u = <x_bar, x_b> = sum|y_j| / (sqrt(d) ||t||), clamped
@@ -134,7 +180,7 @@ __global__ void k_encode_finish(const double *__restrict__ xp, int64_t n0, int64
                                 const double *__restrict__ C, const double *__restrict__ RT, int64_t npad,
                                 float *__restrict__ heads, float *__restrict__ tails, float *__restrict__ xr2o,
                                 uint32_t *__restrict__ codes, float *__restrict__ f1, float *__restrict__ f2,
-                                float *__restrict__ f3)
+                                float *__restrict__ f3, uint8_t *__restrict__ hq, float4 *__restrict__ hs, int dq)
 {
     extern __shared__ double esm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -163,6 +209,7 @@ __global__ void k_encode_finish(const double *__restrict__ xp, int64_t n0, int64
         if (lane == 0) codes[(int64_t)w * npad + slot] = bits;
     }
     __syncwarp();
+    float xr2f = 0.f;   // lane 0: fp32 ||x_r||^2 (the sketch record carries a copy)
     if (lane == 0) {
         double xr2 = 0.0;
         for (int i = d; i < D; i++) xr2 = xr2 + row[i] * row[i];
@@ -176,10 +223,29 @@ __global__ void k_encode_finish(const double *__restrict__ xp, int64_t n0, int64
             if (u > 1.0) u = 1.0;
         }
         const double nrm = sqrt(n2);
-        xr2o[slot] = (float)xr2;
+        xr2f = (float)xr2;
+        xr2o[slot] = xr2f;
         f1[slot] = (float)(n2 + xr2);
         f2[slot] = (float)(nrm / u);
         f3[slot] = (float)(nrm * (sqrt(1.0 - u * u) / (u * sqrt((double)(d - 1)))));
+    }
+    __syncwarp();   // lane 0's sums above read t and y; the sketch reuses them
+    if (hq) {
+        // y = R (h - c) for the fp32 head h (the sketch's rotated residual)
+        double hn2 = 0.0;
+        for (int i = lane; i < d; i += 32) {
+            t[i] = (double)(float)row[i] - C[(int64_t)c * d + i];
+            hn2 = hn2 + t[i] * t[i];
+        }
+        for (int o = 16; o > 0; o >>= 1) hn2 = hn2 + __shfl_xor_sync(0xffffffffu, hn2, o);
+        __syncwarp();
+        for (int j = lane; j < d; j += 32) {
+            double acc = 0.0;
+            for (int i = 0; i < d; i++) acc = acc + RT[(int64_t)i * d + j] * t[i];
+            y[j] = acc;
+        }
+        __syncwarp();
+        mrq_head_sketch(y, sqrt(hn2) * (1.0 + 0x1p-40), xr2f, d, dq, hq + slot * dq, hs + slot);
     }
 }
 
@@ -303,7 +369,9 @@ __global__ void __launch_bounds__(256) k_quant_g(const uint32_t *__restrict__ pr
                                                  int W, int G, const double *__restrict__ r0,
                                                  const double *__restrict__ Rc, const double *__restrict__ qr2,
                                                  double eps0, uint32_t *__restrict__ planes,
-                                                 double *__restrict__ qconst)
+                                                 double *__restrict__ qconst, uint8_t *__restrict__ qsk_b,
+                                                 double *__restrict__ qsk_c, int dq, const double *__restrict__ qnorm,
+                                                 double cmax)
 {
     const int lane = threadIdx.x & 31;
     const int P = 32 / G;
@@ -362,6 +430,49 @@ __global__ void __launch_bounds__(256) k_quant_g(const uint32_t *__restrict__ pr
         for (int o = 1; o < Lg; o <<= 1) x |= __shfl_xor_sync(0xffffffffu, x, o, G);
         if (pv && s % L == 0 && w < W) planes[gw * (MRQ_BQ * W) + b * W + w] = ok ? x : 0u;
     }
+    if (qsk_b) {
+        // the query side of the head sketch (mrq_head_sketch):
+        // r = R (q_d - c) = t b + f, b int8 (|b_j| <= 127), ||f|| <= F
+        // (rounded up; margins cover the fp64 rounding of f and of r0 - Rc)
+        const double mx = fmax(fabs(lo), fabs(hi));
+        const double tq = (ok && mx > 0.0) ? mx / 127.0 : 0.0;
+        double f2 = 0.0;
+        int B = 0;
+        uint32_t pk[E / 4];
+#pragma unroll
+        for (int w = 0; w < E / 4; w++) pk[w] = 0u;
+#pragma unroll
+        for (int t = 0; t < E; t++) {
+            const int j = s * E + t;
+            int b = 0;
+            if (ok && j < d) {
+                if (tq > 0.0) b = (int)fmin(127.0, fmax(-127.0, rint(rv[t] / tq)));
+                const double f = rv[t] - tq * (double)b;
+                f2 = f2 + f * f;
+            }
+            B += b * b;
+            pk[t / 4] |= (uint32_t)(uint8_t)(int8_t)b << (8 * (t % 4));
+        }
+        for (int o = G >> 1; o > 0; o >>= 1) {
+            f2 = f2 + __shfl_xor_sync(0xffffffffu, f2, o, G);
+            B += __shfl_xor_sync(0xffffffffu, B, o, G);
+        }
+        if (pv && s * E < dq) {
+            uint32_t *dst = (uint32_t *)(qsk_b + gw * dq + s * E);
+#pragma unroll
+            for (int w = 0; w < E / 4; w++) dst[w] = pk[w];
+        }
+        if (pv && s == 0) {
+            // r0 = R q_d and R c are d-term fp64 dots (|R_j| = 1): per element
+            // <= (d + 1) 2^-53 (||q_d|| + ||c||), plus 2^-53 |r_j| for r0 - Rc
+            const double sd = sqrt((double)d);
+            qsk_c[gw * 4 + 0] = tq;
+            qsk_c[gw * 4 + 1] = __dsqrt_ru(f2) * (1.0 + 0x1p-40) + 0x1p-49 * mx * sd +
+                                0x1p-50 * (double)(d + 2) * sd * (qnorm[q] + cmax);
+            qsk_c[gw * 4 + 2] = (double)B;
+            qsk_c[gw * 4 + 3] = 0.0;
+        }
+    }
     if (pv && s == 0) {
         double *qc = qconst + gw * 8;
         if (!ok) {
@@ -382,7 +493,8 @@ __global__ void __launch_bounds__(256) k_quant_g(const uint32_t *__restrict__ pr
 
 void launch_quant(const uint32_t *probe, const double *probe_qn2, int64_t nq, int np, int d, int W,
                   const double *r0, const double *Rc, const double *qr2, double eps0, uint32_t *planes,
-                  double *qconst, cudaStream_t st)
+                  double *qconst, uint8_t *qsk_b, double *qsk_c, int dq, const double *qnorm, double cmax,
+                  cudaStream_t st)
 {
     const int64_t npairs = nq * np;
     const int E = d <= 256 ? 8 : 16;
@@ -393,9 +505,11 @@ void launch_quant(const uint32_t *probe, const double *probe_qn2, int64_t nq, in
     const int64_t warps = (npairs + P - 1) / P;
     const unsigned grid = (unsigned)((warps + 7) / 8);
     if (E == 8)
-        k_quant_g<8><<<grid, 256, 0, st>>>(probe, probe_qn2, npairs, np, d, W, G, r0, Rc, qr2, eps0, planes, qconst);
+        k_quant_g<8><<<grid, 256, 0, st>>>(probe, probe_qn2, npairs, np, d, W, G, r0, Rc, qr2, eps0, planes, qconst,
+                                           qsk_b, qsk_c, dq, qnorm, cmax);
     else
-        k_quant_g<16><<<grid, 256, 0, st>>>(probe, probe_qn2, npairs, np, d, W, G, r0, Rc, qr2, eps0, planes, qconst);
+        k_quant_g<16><<<grid, 256, 0, st>>>(probe, probe_qn2, npairs, np, d, W, G, r0, Rc, qr2, eps0, planes, qconst,
+                                            qsk_b, qsk_c, dq, qnorm, cmax);
 }
 
 // Processing order of the queries (a permutation; every query's result is
@@ -498,6 +612,61 @@ __global__ void k_exclusive_scan(const uint64_t *__restrict__ in, int64_t n, uin
     if (t == (int)blockDim.x - 1) out[n] = run;
 }
 
+// Sketch arguments of the fused scan (SK = true; LOOSE FULL, tau1 = tau0):
+// every F1 candidate is immediately tested against the head-sketch lower
+// bound of its canonical dis_o' (mrq_sketch_decide); F1 is only counted
+// (f1_cnt), and the candidates the bound cannot prune are appended to f1_pos
+// (count surv_cnt) for the canonical fp32 head gather of k_head_b.
+struct ScanSketch {
+    const uint8_t *hq;      // [npad][dq] int8 sketch rows
+    const float4 *hs;       // [npad] (s, E, ||x_r||^2, -): one 16-byte gather
+    const uint8_t *qsk_b;   // [nq][np][dq] query-side int8 rows
+    const double *qsk_c;    // [nq][np][4] (t, F, <b,b>, 0)
+    const double *qr2;      // [nq]
+    int dq;
+    uint32_t *surv_cnt;     // [nq]
+};
+
+// Head-sketch test of one F1 candidate (DESIGN.md §5 "head sketch"): in the
+// quantizer's rotated frame R (h - q_d) = R (h - c) - R (q_d - c) with
+// R (h - c) = s a + e (||e|| <= E, mrq_head_sketch) and R (q_d - c) = t b + f
+// (||f|| <= F, k_quant_g), so by the triangle inequality
+//   ||h - q_d|| >= ||s a - t b|| - E - F,
+//   ||s a - t b||^2 = s^2 <a,a> - 2 s t <a,b> + t^2 <b,b>,
+// the inner products exact in int32 (dp4a over the packed bytes; |<a,b>| <=
+// d 127^2 < 2^31) and the fp64 combination's rounding bounded by 2^-50 times
+// the sum of the magnitudes.  The canonical fp64 HEAD (k_head_b) is >= (lower
+// bound)^2 (1 - 2^-40), and fl(fl(fl(HEAD + xr2) + qr2) - eps_r) is monotone
+// in HEAD under round-to-nearest, so a candidate whose bound already fails
+// the F2 test (dlo - eps_r >= tau1) is not in F2: the canonical test decides
+// it the same way.  keep = true: the candidate must be gathered.
+// <a,b> and <a,a> over one 16-byte chunk of packed int8:
+__device__ __forceinline__ void mrq_dp4a_chunk(const uint4 &u, const uint4 &b, int &ab, int &aa)
+{
+    ab = __dp4a((int)u.x, (int)b.x, ab);
+    ab = __dp4a((int)u.y, (int)b.y, ab);
+    ab = __dp4a((int)u.z, (int)b.z, ab);
+    ab = __dp4a((int)u.w, (int)b.w, ab);
+    aa = __dp4a((int)u.x, (int)u.x, aa);
+    aa = __dp4a((int)u.y, (int)u.y, aa);
+    aa = __dp4a((int)u.z, (int)u.z, aa);
+    aa = __dp4a((int)u.w, (int)u.w, aa);
+}
+__device__ __forceinline__ bool mrq_sketch_decide(int ab, int aa, float4 se, const double *bc, double qr2, double eps_r,
+                                                  double tau1)
+{
+    const float xv = se.z;   // ||x_r||^2
+    const double t = bc[0], F = bc[1], B = bc[2], sv = (double)se.x;
+    const double y1 = (sv * sv) * (double)aa, y2 = (2.0 * sv * t) * (double)ab, y3 = (t * t) * B;
+    const double y = (y1 - y2) + y3;
+    const double ylo = y - 0x1p-50 * ((y1 + fabs(y2)) + y3);
+    const double n = ylo > 0.0 ? sqrt(ylo) * (1.0 - 0x1p-50) : 0.0;
+    const double L = (n - (double)se.y - F) * (1.0 - 0x1p-50);
+    const double lb = L > 0.0 ? (L * L) * (1.0 - 0x1p-40) : 0.0;
+    const double dlo = (lb + (double)xv) + qr2;
+    return !(dlo - eps_r >= tau1);
+}
+
 // The code scan (hot loop of Alg.2 L7-L12): block per query, every
 // warp streams (list, MRQ_SCAN_TILE-slot) tiles of the query's probed lists.
 // Each lane owns slots base + 128 h .. base + 128 h + 3 of its tile and reads
@@ -505,34 +674,46 @@ __global__ void k_exclusive_scan(const uint64_t *__restrict__ in, int64_t n, uin
 // codes[w][slot], then f1/f2/f3) before evaluating any, evaluates LB1 in
 // registers and appends slots with LB1 < tau0 (stage 1, F1) to the query's
 // segment of f1_pos.  Warp 0 builds the tile prefix of the probed lists in
-// shared memory with a shuffle scan.
+// shared memory with a shuffle scan.  SK: F1 candidates go through a per-warp
+// shared-memory queue and are sketch-tested 32 at a time (lane per
+// candidate); only the survivors are appended (see ScanSketch).
 #define MRQ_SCAN_TILE 128
 #ifndef MRQ_SCAN_THREADS
 #define MRQ_SCAN_THREADS 128   // 4 warps per query: a smaller end-of-query tail than 8 (measured)
 #endif
 #define MRQ_SCAN_H (MRQ_SCAN_TILE / 128)
-template <int W>
+#define MRQ_SKQ 640            // per-warp sketch queue, drained after the tile loop
+template <int W, bool SK>
 __global__ void __launch_bounds__(MRQ_SCAN_THREADS, (W <= 3 ? 1024 / MRQ_SCAN_THREADS : 1)) k_scan(
     const uint32_t *__restrict__ probe, int np, int64_t npad, const uint32_t *__restrict__ list_off,
     const uint32_t *__restrict__ list_size, const uint32_t *__restrict__ codes, const float *__restrict__ f1,
     const float *__restrict__ f2, const float *__restrict__ f3, const uint32_t *__restrict__ planes,
     const double *__restrict__ qconst, const double *__restrict__ eps_r_arr, const double *__restrict__ tau0_arr,
     double isd, const uint64_t *__restrict__ f1_off, uint32_t *__restrict__ f1_cnt, uint32_t *__restrict__ f1_pos,
-    const uint32_t *__restrict__ qorder)
+    const uint32_t *__restrict__ qorder, ScanSketch sk)
 {
-    extern __shared__ unsigned char csm[];
+    extern __shared__ __align__(16) unsigned char csm[];
     double *qc_s = (double *)csm;                        // np x 5: the (query, list) constants
-    uint32_t *pl_s = (uint32_t *)(qc_s + np * 5);        // np x MRQ_BQ W: the query bit-planes
+    double *skc_s = qc_s + np * 5;                       // SK: np x 3 sketch constants (t, F, <b,b>)
+    uint32_t *pl_s = (uint32_t *)(skc_s + (SK ? np * 3 : 0));   // np x MRQ_BQ W: the query bit-planes
     uint32_t *tile_pre = pl_s + np * (MRQ_BQ * W);       // np + 1
     uint32_t *lst_start = tile_pre + np + 1;             // np
     uint32_t *lst_end = lst_start + np;                  // np
-    __shared__ uint32_t sh_cnt;
+    uint8_t *skb_s = (uint8_t *)(((uintptr_t)(lst_end + np) + 15) & ~(uintptr_t)15);   // SK: np x dq sketch rows
+    __shared__ uint32_t sh_cnt, sh_surv;
+    __shared__ uint32_t skq[SK ? (MRQ_SCAN_THREADS / 32) * MRQ_SKQ : 1];   // SK: per-warp queue, slots
+    __shared__ uint16_t skp[SK ? (MRQ_SCAN_THREADS / 32) * MRQ_SKQ : 1];
     const int64_t q = qorder ? (int64_t)qorder[blockIdx.x] : (int64_t)blockIdx.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nwarps = blockDim.x >> 5;
     // staged once per query: a warp switches list every tile or two
     for (int i = threadIdx.x; i < np * 5; i += blockDim.x) qc_s[i] = qconst[(q * np + i / 5) * 8 + i % 5];
     for (int i = threadIdx.x; i < np * (MRQ_BQ * W); i += blockDim.x) pl_s[i] = planes[q * np * (MRQ_BQ * W) + i];
+    if (SK) {
+        for (int i = threadIdx.x; i < np * 3; i += blockDim.x) skc_s[i] = sk.qsk_c[(q * np + i / 3) * 4 + i % 3];
+        const uint4 *src = (const uint4 *)(sk.qsk_b + q * np * sk.dq);
+        for (int i = threadIdx.x; i < np * sk.dq / 16; i += blockDim.x) ((uint4 *)skb_s)[i] = src[i];
+    }
     if (warp == 0) {
         uint32_t carry = 0;
         for (int p0 = 0; p0 < np; p0 += 32) {
@@ -561,6 +742,7 @@ __global__ void __launch_bounds__(MRQ_SCAN_THREADS, (W <= 3 ? 1024 / MRQ_SCAN_TH
         if (lane == 0) {
             tile_pre[np] = carry;
             sh_cnt = 0;
+            sh_surv = 0;
         }
     }
     __syncthreads();
@@ -571,6 +753,54 @@ __global__ void __launch_bounds__(MRQ_SCAN_THREADS, (W <= 3 ? 1024 / MRQ_SCAN_TH
     uint32_t pl[MRQ_BQ * W];
     double qc[5];
     int cur_p = -1;
+    // SK: the warp's queue of F1 candidates awaiting the sketch test
+    uint32_t *wq = skq + warp * MRQ_SKQ;
+    uint16_t *wp = skp + warp * MRQ_SKQ;
+    int qn = 0;
+    const double qr2 = SK ? sk.qr2[q] : 0.0;
+    // SK: sketch-test queue entries [i0, i0 + 64): two per lane, both rows in
+    // flight before any arithmetic; survivors appended to f1_pos
+    auto drain = [&](int i0) {
+        const int nw = sk.dq / 16;
+        uint32_t slot[2];
+        int pp[2];
+        bool in[2];
+        float4 se[2];
+        int ab[2] = {0, 0}, aa[2] = {0, 0};
+#pragma unroll
+        for (int u = 0; u < 2; u++) {
+            const int i = i0 + u * 32 + lane;
+            in[u] = i < qn;
+            slot[u] = in[u] ? wq[i] : 0u;
+            pp[u] = in[u] ? wp[i] : 0;
+            se[u] = in[u] ? sk.hs[slot[u]] : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        for (int w0 = 0; w0 < nw; w0 += 2) {   // 2 chunks x 2 entries of loads in flight
+            uint4 r[2][2];
+#pragma unroll
+            for (int u = 0; u < 2; u++)
+#pragma unroll
+                for (int c = 0; c < 2; c++)
+                    r[u][c] = (in[u] && w0 + c < nw) ? __ldg((const uint4 *)(sk.hq + (int64_t)slot[u] * sk.dq) + w0 + c)
+                                                     : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+            for (int u = 0; u < 2; u++)
+#pragma unroll
+                for (int c = 0; c < 2; c++)
+                    if (w0 + c < nw) mrq_dp4a_chunk(r[u][c], ((const uint4 *)(skb_s + pp[u] * sk.dq))[w0 + c], ab[u], aa[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < 2; u++) {
+            const bool keep = in[u] && mrq_sketch_decide(ab[u], aa[u], se[u], skc_s + pp[u] * 3, qr2, eps_r, tau0);
+            const unsigned bal = __ballot_sync(0xffffffffu, keep);
+            if (bal) {
+                uint32_t o = 0;
+                if (lane == 0) o = atomicAdd(&sh_surv, (uint32_t)__popc(bal));
+                o = __shfl_sync(0xffffffffu, o, 0) + __popc(bal & ((1u << lane) - 1u));
+                if (keep) out[o] = slot[u];
+            }
+        }
+    };
     for (uint32_t t = warp; t < ntiles; t += nwarps) {
         while (tile_pre[p + 1] <= t) p++;
         if (p != cur_p) {
@@ -617,19 +847,44 @@ __global__ void __launch_bounds__(MRQ_SCAN_THREADS, (W <= 3 ? 1024 / MRQ_SCAN_TH
             const int n0 = __popc(b0), n1 = __popc(b1), n2 = __popc(b2), n3 = __popc(b3);
             const int tot = n0 + n1 + n2 + n3;
             if (tot) {
-                uint32_t wb = 0;
-                if (lane == 0) wb = atomicAdd(&sh_cnt, (uint32_t)tot);
-                wb = __shfl_sync(0xffffffffu, wb, 0);
                 const unsigned lt = (1u << lane) - 1u;
-                if (fl[0]) out[wb + __popc(b0 & lt)] = b;
-                if (fl[1]) out[wb + n0 + __popc(b1 & lt)] = b + 1;
-                if (fl[2]) out[wb + n0 + n1 + __popc(b2 & lt)] = b + 2;
-                if (fl[3]) out[wb + n0 + n1 + n2 + __popc(b3 & lt)] = b + 3;
+                if (SK && qn + tot <= MRQ_SKQ) {
+                    // F1 is counted; its members queue for the sketch test after the tile loop
+                    if (lane == 0) atomicAdd(&sh_cnt, (uint32_t)tot);
+                    const uint32_t o0 = qn + __popc(b0 & lt), o1 = qn + n0 + __popc(b1 & lt);
+                    const uint32_t o2 = qn + n0 + n1 + __popc(b2 & lt), o3 = qn + n0 + n1 + n2 + __popc(b3 & lt);
+                    if (fl[0]) { wq[o0] = b; wp[o0] = (uint16_t)p; }
+                    if (fl[1]) { wq[o1] = b + 1; wp[o1] = (uint16_t)p; }
+                    if (fl[2]) { wq[o2] = b + 2; wp[o2] = (uint16_t)p; }
+                    if (fl[3]) { wq[o3] = b + 3; wp[o3] = (uint16_t)p; }
+                    qn += tot;
+                } else {
+                    // (SK with a full queue: these F1 members skip the sketch test and are
+                    // gathered -- the sketch only ever prunes, so F2 is unchanged)
+                    uint32_t *ctr = SK ? &sh_surv : &sh_cnt;
+                    if (SK && lane == 0) atomicAdd(&sh_cnt, (uint32_t)tot);
+                    uint32_t wb = 0;
+                    if (lane == 0) wb = atomicAdd(ctr, (uint32_t)tot);
+                    wb = __shfl_sync(0xffffffffu, wb, 0);
+                    const uint32_t o0 = wb + __popc(b0 & lt), o1 = wb + n0 + __popc(b1 & lt);
+                    const uint32_t o2 = wb + n0 + n1 + __popc(b2 & lt), o3 = wb + n0 + n1 + n2 + __popc(b3 & lt);
+                    if (fl[0]) out[o0] = b;
+                    if (fl[1]) out[o1] = b + 1;
+                    if (fl[2]) out[o2] = b + 2;
+                    if (fl[3]) out[o3] = b + 3;
+                }
             }
         }
     }
+    if (SK) {
+        __syncwarp();
+        for (int i0 = 0; i0 < qn; i0 += 64) drain(i0);
+    }
     __syncthreads();
-    if (threadIdx.x == 0) f1_cnt[q] = sh_cnt;
+    if (threadIdx.x == 0) {
+        f1_cnt[q] = sh_cnt;
+        if (SK) sk.surv_cnt[q] = sh_surv;
+    }
 }
 
 __global__ void k_fill_f64(double *p, int64_t n, double v)
@@ -644,16 +899,25 @@ void launch_fill_f64(double *p, int64_t n, double v, cudaStream_t st)
 }
 
 // ================================================================ launchers
+template <int W, bool SK>
+static int launch_scan_ws(const LaunchScan &a, cudaStream_t st)
+{
+    if (a.smem > 48 * 1024)
+        MRQ_CUDA_TRY(cudaFuncSetAttribute(k_scan<W, SK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a.smem));
+    ScanSketch sk;
+    sk.hq = a.hq; sk.hs = a.hs; sk.qsk_b = a.qsk_b; sk.qsk_c = a.qsk_c; sk.qr2 = a.qr2;
+    sk.dq = a.dq; sk.surv_cnt = a.surv_cnt;
+    k_scan<W, SK><<<a.nq, MRQ_SCAN_THREADS, a.smem, st>>>(a.probe, a.np, a.npad, a.list_off, a.list_size, a.codes,
+                                                           a.f1, a.f2, a.f3, a.planes, a.qconst, a.eps_r, a.tau0,
+                                                           a.isd, a.f1_off, a.f1_cnt, a.f1_pos, a.qorder, sk);
+    MRQ_CUDA_TRY(cudaGetLastError());
+    return MRQ_OK;
+}
+
 template <int W>
 static int launch_scan_w(const LaunchScan &a, cudaStream_t st)
 {
-    if (a.smem > 48 * 1024)
-        MRQ_CUDA_TRY(cudaFuncSetAttribute(k_scan<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a.smem));
-    k_scan<W><<<a.nq, MRQ_SCAN_THREADS, a.smem, st>>>(a.probe, a.np, a.npad, a.list_off, a.list_size, a.codes, a.f1, a.f2, a.f3,
-                                          a.planes, a.qconst, a.eps_r, a.tau0, a.isd, a.f1_off, a.f1_cnt, a.f1_pos,
-                                          a.qorder);
-    MRQ_CUDA_TRY(cudaGetLastError());
-    return MRQ_OK;
+    return a.surv_cnt ? launch_scan_ws<W, true>(a, st) : launch_scan_ws<W, false>(a, st);
 }
 
 int launch_scan(int W, const LaunchScan &a, cudaStream_t st)

@@ -9,7 +9,7 @@ void launch_rowmat_f64(const double *X, int64_t nrows, int ldx, int Din, const d
 __global__ void k_encode_finish(const double *xp, int64_t n0, int64_t cnt, int D, int d, int W,
                                 const uint32_t *assign, const uint32_t *slot_of, const double *C, const double *RT,
                                 int64_t npad, float *heads, float *tails, float *xr2o, uint32_t *codes, float *f1,
-                                float *f2, float *f3);
+                                float *f2, float *f3, uint8_t *hq, float4 *hs, int dq);
 __global__ void k_rc(const double *C, const double *RT, int k, int d, int W, double *Rc);
 __global__ void k_qtail(const double *qp, int64_t nq, int D, int d, int W, const double *lam, const double *RT,
                         double rscale, double m, double *qr2o, double *eps_r, double *r0, float *qd32,
@@ -19,13 +19,16 @@ void launch_fill_f64(double *p, int64_t n, double v, cudaStream_t st);
 void launch_qorder(const uint16_t *qkey, int64_t nq, uint32_t *order, cudaStream_t st);
 void launch_quant(const uint32_t *probe, const double *probe_qn2, int64_t nq, int np, int d, int W,
                   const double *r0, const double *Rc, const double *qr2, double eps0, uint32_t *planes,
-                  double *qconst, cudaStream_t st);
+                  double *qconst, uint8_t *qsk_b, double *qsk_c, int dq, const double *qnorm, double cmax,
+                  cudaStream_t st);
 __global__ void k_cand_count(const uint32_t *probe, int64_t nq, int np, const uint32_t *list_size, uint64_t *cnt);
 __global__ void k_exclusive_scan(const uint64_t *in, int64_t n, uint64_t *out);
 struct StageArgs {
     int64_t nq;
     int np, K, Kp, D, d, mode, tight, aligned, seed_lists, aligned_tails;
     int store_f1;             // k_head_b also writes f1_head/f1_diso/f1_id when F2 is fused (debug dumps)
+    int sketch;               // the scan dropped F1 entries with the head sketch (LOOSE): f1_pos holds
+    uint32_t *surv_cnt;       // surv_cnt[q] survivors per query
     int64_t npad;
     double isd;
     const uint32_t *probe, *list_off, *list_size, *ids, *codes, *planes;
@@ -43,6 +46,12 @@ struct StageArgs {
     const uint32_t *qorder;   // processing order of the queries (NULL: 0..nq-1)
 };
 
+// the fused head-sketch test of the scan (FULL with tau1 = tau0, i.e. LOOSE;
+// no debug dumps): k_head_b then gathers only the survivors
+inline bool mrq_sketch_used(const StageArgs &a)
+{
+    return a.sketch && a.mode == 0 && !a.tight && !a.store_f1 && a.surv_cnt;
+}
 int launch_seed_w(int W, const StageArgs &a, cudaStream_t st);
 int launch_stage2_w(const StageArgs &a, cudaStream_t st, cudaEvent_t after_gather = nullptr);
 int launch_topk_w(const StageArgs &a, cudaStream_t st);
@@ -65,6 +74,12 @@ struct LaunchScan {
     const uint64_t *f1_off;
     uint32_t *f1_cnt, *f1_pos;
     const uint32_t *qorder;   // processing order of the queries (NULL: 0..nq-1)
+    // fused head-sketch test (surv_cnt != NULL): see ScanSketch in mrq_kernels.cu
+    const uint8_t *hq, *qsk_b;
+    const float4 *hs;
+    const double *qsk_c, *qr2;
+    int dq;
+    uint32_t *surv_cnt;
 };
 
 // dynamic shared memory of k_scan: per probed list 5 constants, 4 W plane words, tile prefix / start / end
@@ -72,6 +87,8 @@ inline size_t mrq_scan_smem(int np, int W)
 {
     return (size_t)np * 5 * 8 + (size_t)np * MRQ_BQ * W * 4 + (size_t)(3 * np + 1) * 4;
 }
+// ... plus, with the fused head-sketch test, the per-list sketch constants and rows
+inline size_t mrq_scan_smem_sk(int np, int W, int dq) { return mrq_scan_smem(np, W) + (size_t)np * 24 + 16 + (size_t)np * dq; }
 int launch_scan(int W, const LaunchScan &a, cudaStream_t st);
 bool supported_W(int W);
 void launch_scan_dbg(int W, const LaunchScan &a, double *dis, double *lb1, cudaStream_t st);

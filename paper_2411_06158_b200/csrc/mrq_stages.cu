@@ -4,6 +4,8 @@
 // warp once; rows are gathered through per-warp shared-memory stages
 // (warp_gather_rows) and each lane sums its own row left to right (the
 // canonical order of DESIGN.md).
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "mrq_internal.cuh"
@@ -239,11 +241,9 @@ __device__ __forceinline__ void f2_compact(int64_t q, int mode, int n1, uint64_t
     if (lane == 0) f2_cnt[q] = at;
 }
 
-// Stage 2, gather half (Alg.2 L13 P:315; "Optimization" P:327, reading R-6):
-// block per query, its warps split the query's F1 entries in 32-row groups;
-// for every F1 entry HEAD = ||x_d - q_d||^2 (left to right over i < d),
-// dis_o' = (HEAD + ||x_r||^2) + ||q_r||^2, and the global id, written to the
-// entry's F1 slot (f1_head, f1_diso, f1_id).
+// With the head sketch (sketch != 0, LOOSE) the scan has already dropped the
+// F1 entries whose sketch bound fails the F2 test (k_scan<W, true>): f1_pos
+// then holds only the surv_cnt[q] survivors, which are gathered here.
 __global__ void __launch_bounds__(128) k_head_b(
     int aligned, int D, int d, const uint32_t *__restrict__ ids, const float *__restrict__ heads,
     const float *__restrict__ xr2, const double *__restrict__ qp, const double *__restrict__ qr2_arr,
@@ -251,7 +251,8 @@ __global__ void __launch_bounds__(128) k_head_b(
     double *__restrict__ f1_head, double *__restrict__ f1_diso, uint32_t *__restrict__ f1_id,
     const uint32_t *__restrict__ qorder, int fuse_f2, int mode, const double *__restrict__ eps_r_arr,
     const double *__restrict__ tau0_arr, uint32_t *__restrict__ f2_cnt, uint32_t *__restrict__ f2_pos,
-    double *__restrict__ f2_head, uint32_t *__restrict__ s1_cnt, double *__restrict__ tau1_arr, int store_f1)
+    double *__restrict__ f2_head, uint32_t *__restrict__ s1_cnt, double *__restrict__ tau1_arr, int store_f1,
+    int sketch, const uint32_t *__restrict__ surv_cnt)
 {
     extern __shared__ unsigned char wsm[];
     __shared__ uint32_t f2n;
@@ -268,12 +269,15 @@ __global__ void __launch_bounds__(128) k_head_b(
     // fused F2 (every schedule but FULL/TIGHT: tau1 = tau0, no S1): the test
     // of f2_compact on the dis_o' just formed, appended unordered (F2 is a set)
     const double eps_r = fuse_f2 ? eps_r_arr[q] : 0.0, tau1 = fuse_f2 ? tau0_arr[q] : 0.0;
+    const uint32_t *rows = f1_pos + base;   // the entries whose fp32 head rows are gathered
+    int n = n1;
+    if (sketch) n = (int)surv_cnt[q];   // the scan kept only the sketch survivors in f1_pos
     float xr2v = 0.f;   // ||x_r||^2, id and slot of the lane's row, loaded while the row is in flight
     uint32_t idv = 0, slotv = 0;
-    warp_rows(aligned, heads, d, 0, d, qs, n1, tile, [&](int e) { return f1_pos[base + e]; },
+    warp_rows(aligned, heads, d, 0, d, qs, n, tile, [&](int e) { return rows[e]; },
               [&](int, uint32_t slot) {
                   xr2v = xr2[slot];
-                  idv = ids[slot];
+                  if (store_f1) idv = ids[slot];
                   slotv = slot;
                   return 0.0;
               },
@@ -766,13 +770,15 @@ int launch_stage2_w(const StageArgs &a, cudaStream_t st, cudaEvent_t after_gathe
 #define MRQ_HEAD_WPB 4   // measured best of 2/4/8 (launch bounds 128)
 #endif
         const int wpb = MRQ_HEAD_WPB;
+        const bool sk = mrq_sketch_used(a);
         const size_t smem = (size_t)wpb * MRQ_RG_FLOATS * 4 + (size_t)a.d * 8;
         int rc = set_attr((const void *)k_head_b, smem);
         if (rc) return rc;
         k_head_b<<<(unsigned)a.nq, wpb * 32, smem, st>>>(a.aligned, a.D, a.d, a.ids, a.heads, a.xr2, a.qp, a.qr2,
                                                           a.f1_off, a.f1_cnt, a.f1_pos, a.f1_head, a.f1_diso, a.f1_id,
                                                           a.qorder, fuse, a.mode, a.eps_r, a.tau0, a.f2_cnt, a.f2_pos,
-                                                          a.f2_head, a.s1_cnt, a.tau1, !fuse || a.store_f1);
+                                                          a.f2_head, a.s1_cnt, a.tau1, !fuse || a.store_f1, sk ? 1 : 0,
+                                                          a.surv_cnt);
     }
     if (after_gather) MRQ_CUDA_TRY(cudaEventRecord(after_gather, st));
     if (fuse) return MRQ_OK;   // F2 written by the gather kernel

@@ -48,7 +48,7 @@ class Stats(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in ("scanned", "stage1_pass", "stage2_pass", "exact", "seeds")] + \
                [(n, C.c_double) for n in ("ms_total", "ms_qprep", "ms_probe", "ms_quant", "ms_seed", "ms_scan",
                                           "ms_stage2", "ms_rerank", "ms_topk", "ms_comm", "ms_head",
-                                          "ms_probe_gemm")]
+                                          "ms_probe_gemm", "ms_sketch")] + [("sketch_pass", C.c_uint64)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

@@ -1,8 +1,11 @@
-"""Parity at BASELINE.json's full size (configs[1], SIFT-shaped: N = 1M,
-Q = 10k, D = 128, d = 64, k = 4096) in the launch configuration bench.py
+"""Parity at BASELINE.json's full sizes in the launch configuration bench.py
 times: the whole batch goes through the device API on an explicit stream
 (graph replay on), then sampled queries are checked against the oracle one
 by one (the oracle searches only the sample; its index encode covers all N).
+
+  sift: configs[1] (N = 1M, Q = 10k, D = 128, d = 64, k = 4096)
+  deep: configs[2] (N = 10M, Q = 10k, D = 96, d = 64, k = 16384) -- the
+        largest single-GPU workload and bench.py's default
 """
 import os
 
@@ -12,30 +15,36 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 pytestmark = pytest.mark.gpu
 
+FULL = {"sift": ("sift", 64, 16), "deep": ("deep", 64, 16)}
 
-@pytest.fixture(scope="module")
-def full_sift():
+
+@pytest.fixture(scope="module", params=list(FULL))
+def full(request):
     import torch
     import oracle
     import synth
     from oracle import build as B
     import paper_2411_06158_b200 as m
-    cfg = synth.config_by_name("sift")
+    name, d, npb = FULL[request.param]
+    bfile = os.path.join(ROOT, "data", name, "build_d%d.mrqb" % d)
+    if not os.path.exists(bfile):
+        pytest.skip("no committed oracle build file for %s" % name)
+    cfg = synth.config_by_name(name)
     X, Q = synth.generate(cfg, device="cuda")
-    bfile = os.path.join(ROOT, "data", "sift", "build_d64.mrqb")
     bf = B.read(bfile)
     assert synth.base_sha256(X) == bf.sha
-    h = m.mrq_index_load(bfile, X, 64, device=0)
+    h = m.mrq_index_load(bfile, X, d, device=0)
     ox = oracle.Index(bf, X)
-    yield dict(m=m, h=h, X=X, Q=Q, ox=ox, torch=torch)
+    yield dict(name=name, m=m, h=h, X=X, Q=Q, ox=ox, torch=torch, npb=npb)
     m.mrq_free(h)
+    del ox
 
 
 @pytest.mark.parametrize("tau", ["LOOSE", "TIGHT"])
-def test_full_batch_sampled_parity(full_sift, tau):
-    m, h, Q, ox, torch = (full_sift[k] for k in ("m", "h", "Q", "ox", "torch"))
+def test_full_batch_sampled_parity(full, tau):
+    m, h, Q, ox, torch, npb = (full[k] for k in ("m", "h", "Q", "ox", "torch", "npb"))
     dev = torch.device("cuda", 0)
-    nq, K, npb = Q.shape[0], 10, 16
+    nq, K = Q.shape[0], 10
     dq = torch.from_numpy(Q).to(dev)
     ids = torch.empty((nq, K), dtype=torch.int64, device=dev)
     dist = torch.empty((nq, K), dtype=torch.float32, device=dev)
@@ -55,11 +64,11 @@ def test_full_batch_sampled_parity(full_sift, tau):
     assert all(len(set(r.tolist())) == K for r in gi[:500])
 
 
-def test_full_batch_recall(full_sift):
+def test_full_batch_recall(full):
     """recall@10 of the bench operating point against the committed fp64 ground truth."""
-    m, h, Q = full_sift["m"], full_sift["h"], full_sift["Q"]
-    gt = np.load(os.path.join(ROOT, "data", "sift", "gt_k10.npy"))
-    ids, _, _ = m.mrq_search_batch(h, Q, m.SearchParams.make(K=10, nprobe=16, tau_schedule="LOOSE", seed_lists=2),
-                                   with_stats=False)
+    m, h, Q = full["m"], full["h"], full["Q"]
+    gt = np.load(os.path.join(ROOT, "data", full["name"], "gt_k10.npy"))
+    ids, _, _ = m.mrq_search_batch(h, Q, m.SearchParams.make(K=10, nprobe=full["npb"], tau_schedule="LOOSE",
+                                                             seed_lists=2), with_stats=False)
     hits = sum(len(set(a.tolist()) & set(b.tolist())) for a, b in zip(ids, gt))
     assert hits / gt.size >= 0.95

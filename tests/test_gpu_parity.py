@@ -418,3 +418,37 @@ def test_probe_overflow_and_sync_fallbacks(case):
     finally:
         m.mrq_debug_set(gx.h, "probe_capp", 256)
         m.mrq_debug_set(gx.h, "cand_budget_mb", 8192)
+
+
+def test_head_sketch_prefilter_exact(case):
+    """The int8 head-sketch pre-pass of the stage-2 gather (LOOSE)
+    prunes with a proven lower bound of the canonical HEAD, so F2 (as a set,
+    with bit-exact exact distances), tau1, the top-K and every counter equal
+    the oracle's; the pre-pass must actually prune (survivors < |F1|)."""
+    m, gx, ox, Q = case["m"], case["gx"], case["ox"], case["Q"]
+    nq = Q.shape[0]
+    pruned = 0
+    for npb in case["nprobe"]:
+        m.mrq_debug_set(gx.h, "dump_dis", 0)
+        m.mrq_debug_set(gx.h, "sketch", 1)
+        gi, gd, gst = gx.search(Q, K=10, nprobe=npb, tau_schedule="LOOSE")
+        surv = gx.fetch("surv_cnt", "u32").astype(np.int64)
+        f1c = gx.fetch("f1_cnt", "u32").astype(np.int64)
+        f2 = _segments(gx, nq, "f2_cnt", "f2_pos", "f2_exact")
+        oi, od, ost, dp = ox.search(Q, K=10, nprobe=npb, tau_schedule="LOOSE", dump=True)
+        assert np.array_equal(gi, oi) and np.array_equal(gd.view(np.uint32), od.view(np.uint32))
+        assert (gst.stage1_pass, gst.stage2_pass, gst.exact) == (ost["f1"], ost["f2"], ost["exact"])
+        assert np.array_equal(gx.fetch("tau1", "f64"), dp["tau1"])
+        for q in range(nq):
+            oid = dp["f2_ids"][q, :dp["f2_cnt"][q]]
+            oex = dict(zip(oid.tolist(), dp["f2_exact"][q, :dp["f2_cnt"][q]].tolist()))
+            gid, gex = f2[q]
+            assert sorted(gid.tolist()) == sorted(oid.tolist())
+            assert all(oex[i] == v for i, v in zip(gid.tolist(), gex.tolist()))
+        assert np.all(surv <= f1c) and np.all(surv >= dp["f2_cnt"])
+        pruned += int((f1c - surv).sum())
+        m.mrq_debug_set(gx.h, "sketch", 0)
+        hi, hd, hst = gx.search(Q, K=10, nprobe=npb, tau_schedule="LOOSE")
+        m.mrq_debug_set(gx.h, "sketch", 1)
+        assert np.array_equal(hi, gi) and np.array_equal(hd, gd) and hst.exact == gst.exact
+    assert pruned > 0
