@@ -384,17 +384,17 @@ def main():
         "k_scan": {"unit": "scanned code", "bytes_per_unit": bcode, "units_per_launch": scanned, "ms": ms_scan},
         "k_head_b": {"unit": "F1 survivor", "bytes_per_unit": bhead, "units_per_launch": int(f1), "ms": ms_head},
     }
-    if ms_sketch > 0.002:
-        # the head gather split in two launches (DESIGN.md §5 head sketch): the
-        # sketch pre-pass reads (dq + 18) B per F1 entry, the fp32 gather 4d + 8
-        # B per sketch survivor; k_head_b's entry above is the pair together
+    sketch_on = sk_pass < f1 - 0.5
+    if sketch_on:
+        # the fused head-sketch test runs inside the scan: per F1
+        # entry it reads the int8 sketch row (dq B) and the 16-B (s, E, xr2)
+        # record; k_head_b then gathers only the sketch survivors
         dqb = (d + 15) // 16 * 16
-        kern["k_head_b"]["note"] = ("sketch pre-pass + fp32 gather of the %.0f%% survivors; algorithmic bytes "
-                                    "%.0f B per F1 entry" % (100.0 * sk_pass / max(f1, 1),
-                                                             dqb + 18 + bhead * sk_pass / max(f1, 1)))
-        kern["k_head_b"]["bytes_per_unit_design"] = round(dqb + 18 + bhead * sk_pass / max(f1, 1), 1)
-        kern["k_head_sketch"] = {"unit": "F1 entry (sketch row + slot/probe/scale/E/xr2)", "bytes_per_unit": dqb + 18,
-                                 "units_per_launch": int(f1), "ms": ms_sketch}
+        kern["k_scan"]["bytes_per_unit"] = round(bcode + (dqb + 16) * f1 / max(scanned, 1), 3)
+        kern["k_scan"]["unit"] = ("scanned code (%d B) + its share of the fused sketch test (%d B per F1 entry, "
+                                  "%.1f%% of the scanned)" % (bcode, dqb + 16, 100.0 * f1 / max(scanned, 1)))
+        kern["k_head_b"]["units_per_launch"] = int(sk_pass)
+        kern["k_head_b"]["unit"] = "sketch survivor (F1 entry the head sketch could not prune)"
     f2 = float(np.mean([s.stage2_pass for s in sts]))
     D_ = int(X.shape[1])
     kern["k_topk_w"] = {"unit": "F2 survivor (exact re-rank gather; the launch also selects the top-K)",
@@ -408,7 +408,7 @@ def main():
         if kk["traffic"]:   # the DRAM side: ncu bytes per launch over the same launch time
             kk["dram_gbs"] = round(kk["traffic"] / (kk["ms"] * 1e-3) / 1e9, 1)
             kk["dram_frac"] = round(kk["dram_gbs"] / hbm, 4)
-    dom = max((n for n in kern if n != "k_head_sketch"), key=lambda n: kern[n]["ms"])
+    dom = max(kern, key=lambda n: kern[n]["ms"])
     # the probe screen GEMM on the tensor cores (kind::tf32): its flops against
     # the tf32 peak = measured bf16 burst x the nominal tf32/bf16 ratio (1.1/2.25)
     ms_gemm = float(np.mean([s.ms_probe_gemm for s in sts]))
@@ -488,7 +488,7 @@ def main():
                      "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": kern[dom]["traffic"],
                      "bytes_per_unit": kern[dom]["bytes_per_unit"], "unit_kind": kern[dom]["unit"],
                      "kernels": kern, "codes_per_s_per_gpu": round(scanned / (ms_scan * 1e-3), 1),
-                     "scan_frac_of_hbm": kern["k_scan"]["frac"], "probe_gemm": probe_tc,
+                     "scan_frac_of_hbm": round(scanned / (ms_scan * 1e-3) * bcode / 1e9 / hbm, 4), "probe_gemm": probe_tc,
                      "note": "achieved = algorithmic bytes / launch time; above 1.0 when L2 serves re-reads "
                              "(list-locality query order): dram_gbs / dram_frac give the DRAM side"},
         "e2e": {"value": round(nq / e2e_s, 1), "unit": "queries/s", "h2d_bytes_per_step": int(nq * X.shape[1] * 4),

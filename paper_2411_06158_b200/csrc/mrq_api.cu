@@ -584,13 +584,13 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
         double *qp_r = qp + q0 * D, *qn_r = qnorm + q0, *pq_r = probe_qn2 + q0 * np;
         uint32_t *pr_r = probe + q0 * np;
         if (mrq_probe_tc_fusable(ix, np)) {   // tcgen05 screen with the running top-np in its epilogue
-            const int P = mrq_probe_tc_parts(ix, nr), capp = ix->probe_capp;
+            const int P = mrq_probe_tc_parts(ix, nr), capp = mrq_probe_tc_capp(ix, np);
             uint2 *cbuf;
             uint32_t *ccnt;
             float *kvbuf;
             SCR("probe_cbuf", uint2, (size_t)nr * P * capp, cbuf);
             SCR("probe_ccnt", uint32_t, (size_t)nr * P, ccnt);
-            SCR("probe_kv", float, (size_t)nr * P * 16, kvbuf);
+            SCR("probe_kv", float, (size_t)nr * P * np, kvbuf);
             const double kappa = mrq_probe_tc_kappa(ix);
             TRY(mrq_probe_tc_run_fused(ix, qa3 + q0 * 3 * d, nr, np, qn_r, kappa, cbuf, capp, ccnt, kvbuf, st));
             if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[11], st));

@@ -104,18 +104,19 @@ __host__ __device__ constexpr uint32_t tf32_idesc(int M, int N)
     return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-// Fused selection (FUSED = true, np <= TC_NPMAX).  A row's columns are split
-// into parts (CTA column range x epilogue half, at most P = 2 maxparts); the thread
-// owning (row, part) keeps the 16 smallest screen values of its part sorted
-// in registers and appends every (a_c, c) with
-// a_c <= RU(its current np-th smallest + 2 delta_q) to the part's candidate
-// buffer.  A part's running np-th smallest never drops below the row's final
-// a_(np), so every member of the margin set {c : a_c <= a_(np) + 2 delta_q}
-// is appended by its part; the parts' 16 smallest go to kvbuf so that
-// k_probe_finish_w can form a_(np) and rescore the margin set.
-#define TC_NPMAX 16
+// Fused selection (FUSED = true, np <= NPM, NPM = 16 or TC_NPMAX = 64).  A
+// row's columns are split into parts (CTA column range x epilogue half, at
+// most P = 2 maxparts); the thread owning (row, part) keeps the np smallest
+// screen values of its part sorted in NPM registers (NPM - np placeholders
+// first) and appends every (a_c, c) with a_c <= RU(its current np-th
+// smallest + 2 delta_q) to the part's candidate buffer.  A part's running
+// np-th smallest never drops below the row's final a_(np), so every member of
+// the margin set {c : a_c <= a_(np) + 2 delta_q} is appended by its part; the
+// parts' np smallest go to kvbuf ([row][part][np]) so that k_probe_finish_w
+// can form a_(np) and rescore the margin set.
+#define TC_NPMAX 64
 
-template <bool FUSED>
+template <bool FUSED, int NPM>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_probe_tc(const __grid_constant__ CUtensorMap mapA,
                                                             const __grid_constant__ CUtensorMap mapB, int nq, int k,
                                                             int d, int G, int maxparts, const float *__restrict__ cn32,
@@ -226,7 +227,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_probe_tc(const __grid_constan
         const int half = (warp - 2) >> 2;     // column chunks half, half + 2, ... of each tile
         const int P = 2 * maxparts;
         const float FINF = __int_as_float(0x7f800000);
-        float kv[TC_NPMAX];                   // FUSED: the np smallest screen values, ascending
+        float kv[NPM];                        // FUSED: the np smallest screen values, ascending
         float tf = FINF;                      // FUSED: append threshold RU(kv[np-1] + margin)
         uint32_t cnt = 0;
         float margin = 0.f;                   // RU(2 delta_q): th + margin rounded up >= th + 2 delta_q
@@ -236,16 +237,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_probe_tc(const __grid_constan
         auto flush = [&]() {
             if (FUSED && cur_mb >= 0 && row < nq) {
                 ccnt[(int64_t)row * P + part] = cnt;
-                float4 *kvo = (float4 *)(kvbuf + ((int64_t)row * P + part) * TC_NPMAX);
+                float *kvo = kvbuf + ((int64_t)row * P + part) * np;
 #pragma unroll
-                for (int i = 0; i < TC_NPMAX; i += 4) {   // placeholders are not row values: +inf
-                    float4 o = make_float4(kv[i], kv[i + 1], kv[i + 2], kv[i + 3]);
-                    if (o.x == -FINF) o.x = FINF;
-                    if (o.y == -FINF) o.y = FINF;
-                    if (o.z == -FINF) o.z = FINF;
-                    if (o.w == -FINF) o.w = FINF;
-                    kvo[i / 4] = o;
-                }
+                for (int i = 0; i < NPM; i++)   // the np values after the NPM - np placeholders
+                    if (i >= NPM - np) kvo[i - (NPM - np)] = kv[i];
             }
         };
         int it = 0;
@@ -259,10 +254,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_probe_tc(const __grid_constan
                 cnt = 0;
                 tf = FINF;
                 if (FUSED) {
-                    // kv holds 16 - np placeholders (-inf) followed by the np smallest
-                    // values, so the running np-th smallest is always kv[TC_NPMAX - 1]
+                    // kv holds NPM - np placeholders (-inf) followed by the np smallest
+                    // values, so the running np-th smallest is always kv[NPM - 1]
 #pragma unroll
-                    for (int j = 0; j < TC_NPMAX; j++) kv[j] = j < TC_NPMAX - np ? -FINF : FINF;
+                    for (int j = 0; j < NPM; j++) kv[j] = j < NPM - np ? -FINF : FINF;
                     if (row < nq) {
                         const double g = qnorm[row] + cmax;
                         margin = __double2float_ru(2.0 * (kappa * (g * g)));
@@ -319,15 +314,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_probe_tc(const __grid_constan
                             if (!(a <= tf)) continue;
                             if (cnt < (uint32_t)capp) rb[cnt] = make_uint2(__float_as_uint(a), (uint32_t)(n0 + c + j));
                             cnt++;
-                            if (a < kv[TC_NPMAX - 1]) {   // insertion (compare-exchange chain)
+                            if (a < kv[NPM - 1]) {   // insertion (compare-exchange chain)
                                 float x = a;
 #pragma unroll
-                                for (int i = 0; i < TC_NPMAX; i++) {
+                                for (int i = 0; i < NPM; i++) {
                                     const float lo = fminf(kv[i], x);
                                     x = fmaxf(kv[i], x);
                                     kv[i] = lo;
                                 }
-                                const float th = kv[TC_NPMAX - 1];
+                                const float th = kv[NPM - 1];
                                 tf = __fadd_ru(th, margin);   // +inf stays +inf
                             }
                         }
@@ -424,9 +419,11 @@ int mrq_probe_tc_init(mrq_index *ix)
         delete tc;
         return rc;
     }
-    cudaError_t e = cudaFuncSetAttribute(k_probe_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
+    cudaError_t e = cudaFuncSetAttribute(k_probe_tc<false, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_probe_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
+        e = cudaFuncSetAttribute(k_probe_tc<true, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_probe_tc<true, TC_NPMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
     if (e != cudaSuccess) {
         delete tc;
         mrq_set_error("k_probe_tc smem attribute: %s", cudaGetErrorString(e));
@@ -471,11 +468,16 @@ int mrq_probe_tc_run(mrq_index *ix, const float *qd32, int64_t nq, float *approx
     int rc = make_map(tc, &mapA, qd32, (int)nq, 3 * ix->d, TC_BM);
     if (rc != MRQ_OK) return rc;
     const int G = tc_grid(ix, nq);
-    k_probe_tc<false><<<G, TC_THREADS, TC_SMEM, st>>>(mapA, tc->mapB, (int)nq, ix->k, 3 * ix->d, G, 1, ix->cn32, approx,
+    k_probe_tc<false, 16><<<G, TC_THREADS, TC_SMEM, st>>>(mapA, tc->mapB, (int)nq, ix->k, 3 * ix->d, G, 1, ix->cn32, approx,
                                                        0, nullptr, 0.0, 0.0, nullptr, 0, nullptr, nullptr);
     MRQ_CUDA_TRY(cudaGetLastError());
     return MRQ_OK;
 }
+
+// per-part candidate buffer: a part of n columns appends about np (1 + ln(n /
+// np)) values (running top-np records) plus the margin set; 256 covers np <=
+// 16, 8 np beyond (an overflow only costs a full rescore of the row)
+int mrq_probe_tc_capp(const mrq_index *ix, int np) { return std::max(ix->probe_capp, ix->probe_capp == 256 ? 8 * np : 0); }
 
 bool mrq_probe_tc_fusable(const mrq_index *ix, int np)
 {
@@ -502,8 +504,9 @@ int mrq_probe_tc_run_fused(mrq_index *ix, const float *qd32, int64_t nq, int np,
     if (rc != MRQ_OK) return rc;
     const int G = tc_grid(ix, nq);
     const int maxparts = mrq_probe_tc_parts(ix, nq) / 2;
-    k_probe_tc<true><<<G, TC_THREADS, TC_SMEM, st>>>(mapA, tc->mapB, (int)nq, ix->k, 3 * ix->d, G, maxparts, ix->cn32,
-                                                      nullptr, np, qnorm, ix->cmax, kappa, cbuf, capp, ccnt, kvbuf);
+    auto fn = np <= 16 ? k_probe_tc<true, 16> : k_probe_tc<true, TC_NPMAX>;
+    fn<<<G, TC_THREADS, TC_SMEM, st>>>(mapA, tc->mapB, (int)nq, ix->k, 3 * ix->d, G, maxparts, ix->cn32, nullptr, np,
+                                        qnorm, ix->cmax, kappa, cbuf, capp, ccnt, kvbuf);
     MRQ_CUDA_TRY(cudaGetLastError());
     return MRQ_OK;
 }

@@ -991,10 +991,10 @@ __device__ __forceinline__ double sqdist_rows8(const double *__restrict__ cr, co
     return acc;
 }
 
-// Finish of the fused tensor-core probe (k_probe_tc<true>), warp per query.
-// a_(np) = np-th smallest of the parts' 16 smallest screen values (their
-// union holds the row's 16 smallest, np <= 16; radix select on
-// order-preserving keys).  The margin set {(a, c) in the parts' candidate
+// Finish of the fused tensor-core probe (k_probe_tc<true, NPM>), warp per
+// query.  a_(np) = np-th smallest of the parts' np smallest screen values
+// (their union holds the row's np smallest, np <= 64; radix select on
+// order-preserving keys, MK per lane).  The margin set {(a, c) in the parts' candidate
 // buffers : a <= a_(np) + 2 delta_q} (every member was appended, see
 // mrq_probe_tc.cu) is rescored in fp64 left to right over i and the np
 // smallest (qn2, c) are kept.  If a buffer overflowed, all k centroids are
@@ -1002,7 +1002,8 @@ __device__ __forceinline__ double sqdist_rows8(const double *__restrict__ cr, co
 #ifndef MRQ_PF_MINB
 #define MRQ_PF_MINB 10   // <= 48 registers: more resident warps (measured)
 #endif
-__global__ void __launch_bounds__(128, MRQ_PF_MINB) k_probe_finish_w(int64_t nq, int k, int d, int np, const double *__restrict__ qp,
+template <int MK>
+__global__ void __launch_bounds__(128, MK <= 8 ? MRQ_PF_MINB : 6) k_probe_finish_w(int64_t nq, int k, int d, int np, const double *__restrict__ qp,
                                                         int D, const double *__restrict__ C,
                                                         const double *__restrict__ qnorm, double cmax, double kappa,
                                                         const uint2 *__restrict__ cbuf, int P, int capp, int G,
@@ -1020,13 +1021,13 @@ __global__ void __launch_bounds__(128, MRQ_PF_MINB) k_probe_finish_w(int64_t nq,
     // a_(np): the used parts' 16 smallest, up to 8 per lane (<= 16 parts);
     // buffers are laid out with P parts per row, of which Pq are used
     const int Pq = tc_parts_of(q / TC_BM, nq, k, G);
-    const int nv = Pq * 16;
-    uint32_t key[8];
+    const int nv = Pq * np;   // <= 32 MK
+    uint32_t key[MK];
     bool all = false;
 #pragma unroll
-    for (int j = 0; j < 8; j++) {
+    for (int j = 0; j < MK; j++) {
         const int i = j * 32 + lane;
-        key[j] = i < nv ? f2key(kvbuf[q * P * 16 + i]) : 0xFFFFFFFFu;
+        key[j] = i < nv ? f2key(kvbuf[q * P * np + i]) : 0xFFFFFFFFu;
     }
     for (int pp = lane; pp < Pq; pp += 32) all |= ccnt[q * P + pp] > (uint32_t)capp;
     all = __any_sync(0xffffffffu, all);
@@ -1035,7 +1036,7 @@ __global__ void __launch_bounds__(128, MRQ_PF_MINB) k_probe_finish_w(int64_t nq,
         const uint32_t t = res | (1u << bit);
         int cnt = 0;
 #pragma unroll
-        for (int j = 0; j < 8; j++)
+        for (int j = 0; j < MK; j++)
             if (j * 32 < nv) cnt += __popc(__ballot_sync(0xffffffffu, key[j] < t));
         if (cnt < np) res = t;
     }
@@ -1119,10 +1120,11 @@ int launch_probe_finish_w(int64_t nq, int k, int d, int np, const double *qp, in
     }
     const int wpb = 4;
     const size_t smem = (size_t)wpb * MRQ_SELREG(np) * sizeof(SelItem);
-    int rc = set_attr((const void *)k_probe_finish_w, smem);
+    auto fn = P * np <= 256 ? k_probe_finish_w<8> : k_probe_finish_w<32>;
+    int rc = set_attr((const void *)fn, smem);
     if (rc) return rc;
-    k_probe_finish_w<<<(unsigned)((nq + wpb - 1) / wpb), wpb * 32, smem, st>>>(
-        nq, k, d, np, qp, D, C, qnorm, cmax, kappa, cbuf, P, capp, G, ccnt, kvbuf, cand, probe, probe_qn2, ncand);
+    fn<<<(unsigned)((nq + wpb - 1) / wpb), wpb * 32, smem, st>>>(nq, k, d, np, qp, D, C, qnorm, cmax, kappa, cbuf, P,
+                                                                 capp, G, ccnt, kvbuf, cand, probe, probe_qn2, ncand);
     return MRQ_OK;
 }
 

@@ -254,8 +254,8 @@ def test_probe_tensor_core_screen_bound(case):
     m.mrq_debug_set(gx.h, "cuda_core_probe", 0)
     assert np.array_equal(probe_tc, gx.fetch("probe", "u32"))
     assert np.array_equal(g1[0], g2[0]) and np.array_equal(g1[1], g2[1])
-    m.mrq_debug_set(gx.h, "probe_unfused", 0)     # fused screen + running top-np (np <= 16)
-    for npb in sorted({1, min(np_, 16), min(16, k)}):
+    m.mrq_debug_set(gx.h, "probe_unfused", 0)     # fused screen + running top-np (np <= 16, np <= 64)
+    for npb in sorted({1, min(np_, 16), min(16, k), min(24, k), min(64, k)}):
         m.mrq_debug_set(gx.h, "probe_unfused", 1)
         gu = gx.search(Q, K=10, nprobe=npb)
         pu = gx.fetch("probe", "u32").copy()
