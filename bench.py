@@ -3,9 +3,10 @@
 
 A "step" is one mrq_search_batch over the whole query batch of the workload
 (all hot-path rows: projection, probe, quantization, seeds, scan, stage 2,
-re-rank, top-K; plus the merge at N > 1).  Workload: BASELINE.json configs[1]
-(SIFT-shaped: N = 1M, Q = 10k, D = 128, d = 64, k = 4096, K = 10), synthetic
-and seeded (synth/), index built by the oracle's committed build file.
+re-rank, top-K; plus the merge at N > 1).  Default workload: BASELINE.json
+configs[2], the largest configuration that fits one GPU (Deep-shaped: N = 10M,
+Q = 10k, D = 96, d = 64, k = 16384, K = 10), synthetic and seeded (synth/),
+index from the oracle's committed seeded build file (data/deep/build_d64.mrqb).
 
   value  = queries/s of the whole job with queries and outputs resident in HBM
   e2e    = the same through the host-buffer C ABI call (H2D queries + D2H ids/dists inside the timed region)
@@ -189,8 +190,9 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="mrq", choices=["mrq", "reference"])
-    ap.add_argument("--config", default="sift",
-                    help="tiny | sift (BASELINE.json configs[1], default) | gist | deep (GPU-built index)")
+    ap.add_argument("--config", default="deep",
+                    help="deep (BASELINE.json configs[2], the largest single-GPU workload; default) | sift | gist | "
+                         "tiny | emb (GPU-built index when no committed build file)")
     ap.add_argument("--d", type=int, default=0, help="code length (build file build_d<d>.mrqb); 0 = config default")
     ap.add_argument("--nprobe", type=int, default=0, help="0 = smallest grid nprobe with recall@10 >= 0.95")
     ap.add_argument("--K", type=int, default=10)
