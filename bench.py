@@ -168,15 +168,18 @@ def cpu_oracle_leg(bfile, X, Q, K, nprobe, budget_s=15.0, **kw):
     import oracle
     from oracle import build as B
     bf = B.read(bfile)
+    smax = min(Q.shape[0], 4000 if X.shape[1] <= 256 else 400)
     t0 = time.time()
-    ox = oracle.Index(bf, X)
+    # the oracle encodes only the lists the sampled queries can probe (their
+    # searches read nothing else; oracle.probe_lists) -- untimed setup
+    ox = oracle.Index(bf, X, lists=oracle.probe_lists(bf, Q[:smax], nprobe))
     enc = time.time() - t0
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
     n = 16
     t = time.time()
     ox.search(Q[:n], K=K, nprobe=nprobe, **kw)
     dt = max(time.time() - t, 1e-3)
-    n2 = int(min(Q.shape[0], max(32, n * budget_s / dt)))
+    n2 = int(min(smax, max(32, n * budget_s / dt)))
     t = time.time()
     ox.search(Q[:n2], K=K, nprobe=nprobe, **kw)
     dt = time.time() - t
@@ -522,14 +525,16 @@ def reference_arm(args, rank, world, cfg_name, bfile, gtfile):
     nprobe = args.nprobe or cfg.nprobe[0]
     tau = "LOOSE" if args.tau == "auto" else args.tau
     bf = B.read(bfile)
-    ox = oracle.Index(bf, X)
     K = args.K
     sample = 200
+    used = min(Q.shape[0], args.steps * sample + 16)
+    # encode only the lists the sampled queries can probe (oracle.probe_lists)
+    ox = oracle.Index(bf, X, lists=oracle.probe_lists(bf, Q[:used], nprobe))
     for _ in range(max(args.warmup, 1)):
         ox.search(Q[:16], K=K, nprobe=nprobe, tau_schedule=tau, seed_lists=args.seed_lists, seed_mult=args.seed_mult)
     ts = []
     for i in range(args.steps):
-        s = (i * sample) % Q.shape[0]
+        s = (i * sample) % max(used - sample, 1)
         t = time.time()
         ox.search(Q[s:s + sample], K=K, nprobe=nprobe, tau_schedule=tau, seed_lists=args.seed_lists,
                   seed_mult=args.seed_mult)

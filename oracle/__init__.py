@@ -78,7 +78,11 @@ class OrcDump(C.Structure):
 class Index:
     """Oracle index: build-file arrays + Alg.1 L3-L8 encoding of the base."""
 
-    def __init__(self, bf, X: np.ndarray):
+    def __init__(self, bf, X: np.ndarray, lists=None):
+        """lists: optional iterable of IVF list ids -- only their vectors are
+        encoded (searches must then probe only those lists; see
+        probe_lists()).  The arrays stay full-size (untouched pages cost no
+        memory)."""
         X = np.ascontiguousarray(X, dtype=np.float32)
         N, D = X.shape
         if D != bf.D or N != bf.N:
@@ -106,7 +110,13 @@ class Index:
         self.s = OrcIndex(N, D, d, self.k, self.W, *[_p(getattr(self, n)) for n in (
             "mu", "P", "lam", "R", "C", "assign", "head", "tail", "xr2f", "code", "f1", "f2", "f3",
             "list_off", "list_ids", "Rc")])
-        lib().orc_encode(C.byref(self.s), _p(X))
+        if lists is None:
+            lib().orc_encode(C.byref(self.s), _p(X))
+        else:
+            only = np.zeros(self.k, np.uint8)
+            only[np.asarray(list(lists), np.int64)] = 1
+            self.only = only
+            lib().orc_encode_subset(C.byref(self.s), _p(X), _p(only))
 
     def list_sizes(self):
         return np.diff(self.list_off)
@@ -152,6 +162,22 @@ class Index:
         if dump:
             return ids, dist, stats, out
         return ids, dist, stats
+
+
+def probe_lists(bf, X_queries, nprobe, margin=8):
+    """The lists a search of these queries can probe: for each query the
+    nprobe + margin nearest projected centroids (fp64 numpy; the margin covers
+    any ordering difference against the oracle's own canonical probe, which
+    orc_search re-derives).  Used to encode only what a sampled search reads."""
+    Qv = np.asarray(X_queries, np.float64)
+    qd = (Qv - bf.mu) @ bf.P[:bf.d].T
+    cn = (bf.C * bf.C).sum(1)
+    out = set()
+    for s in range(0, qd.shape[0], 256):
+        dd = cn[None, :] - 2.0 * qd[s:s + 256] @ bf.C.T
+        m = min(bf.k, nprobe + margin)
+        out.update(np.argpartition(dd, m - 1, axis=1)[:, :m].ravel().tolist())
+    return sorted(out)
 
 
 def bruteforce(X, Qv, K):

@@ -129,13 +129,17 @@ double orc_encode_head(int d, const double *R, const double *t, uint32_t *code, 
  *   f2 = fp32(||t|| / u)                 scale of the quantized cross term C2
  *   f3 = fp32(||t|| sqrt(1-u^2) / (u sqrt(d-1)))   Eq.5 radical times ||t||
  * Also builds the inverted lists (ids ascending, A-28) and R c_j.
+ * orc_encode_subset: only the vectors of the lists with only[c] != 0 (a
+ * search that probes only those lists reads nothing else; the full-size GPU
+ * parity tests encode just the lists their sampled queries probe).
  */
-void orc_encode(orc_index *ix, const float *X)
+void orc_encode_subset(orc_index *ix, const float *X, const uint8_t *only)
 {
     const int N = ix->N, D = ix->D, d = ix->d, k = ix->k, W = ix->W;
     const double sqd1 = sqrt((double)(d - 1));
     #pragma omp parallel for schedule(static)
     for (int64_t n = 0; n < N; n++) {
+        if (only && !only[ix->assign[n]]) continue;   /* a list no search will probe: left unencoded */
         double *u = (double *)malloc(sizeof(double) * D);
         double *xp = (double *)malloc(sizeof(double) * D);
         double *t = (double *)malloc(sizeof(double) * d);
@@ -171,6 +175,8 @@ void orc_encode(orc_index *ix, const float *X)
         for (int j = 0; j < d; j++)
             ix->Rc[(size_t)c * d + j] = dot(ix->R + (size_t)j * d, ix->C + (size_t)c * d, d);
 }
+
+void orc_encode(orc_index *ix, const float *X) { orc_encode_subset(ix, X, NULL); }
 
 /* ------------------------------------------------ L1: query quantizer (A-12) */
 

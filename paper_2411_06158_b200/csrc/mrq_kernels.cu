@@ -902,7 +902,8 @@ void launch_fill_f64(double *p, int64_t n, double v, cudaStream_t st)
 template <int W, bool SK>
 static int launch_scan_ws(const LaunchScan &a, cudaStream_t st)
 {
-    if (a.smem > 48 * 1024)
+    // the opt-in covers static + dynamic shared memory (SK adds a static per-warp queue)
+    if (a.smem + (SK ? (MRQ_SCAN_THREADS / 32) * MRQ_SKQ * 6 + 64 : 64) > 48 * 1024)
         MRQ_CUDA_TRY(cudaFuncSetAttribute(k_scan<W, SK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a.smem));
     ScanSketch sk;
     sk.hq = a.hq; sk.hs = a.hs; sk.qsk_b = a.qsk_b; sk.qsk_c = a.qsk_c; sk.qr2 = a.qr2;

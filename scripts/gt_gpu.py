@@ -2,8 +2,8 @@
 §8d.4): a torch fp64 screen (||x||^2 - 2 <q, x> via float64 matmuls on the
 GPU, in blocks) keeps the K + 64 best per query, every survivor is rescored
 with the oracle's plain fp64 loop (oracle.groundtruth's rescoring) and the K
-smallest (dist, id) are kept.  Cross-checked against oracle.groundtruth on a
-query subsample (--check N) before anything is written.
+smallest (dist, id) are kept.  Cross-checked against the plain-loop
+oracle.bruteforce on a query subsample (--check N) before anything is written.
   python scripts/gt_gpu.py deep --out=gpurun_out/data --check 64
 """
 import ctypes as C
@@ -64,9 +64,11 @@ def main(name, outroot, check):
     print(name, "gpu gt K=%d %.1fs" % (Kmax, time.time() - t), flush=True)
     if check:
         t = time.time()
-        oi, _ = oracle.groundtruth(X, Q[:check], Kmax)
-        assert np.array_equal(oi, ids[:check]), "GPU ground truth differs from oracle.groundtruth"
-        print(name, "cross-check vs oracle.groundtruth on %d queries ok %.1fs" % (check, time.time() - t), flush=True)
+        # plain-loop fp64 brute force (oracle.bruteforce; pinned equal to
+        # oracle.groundtruth by tests/test_oracle_pins.py) on the first queries
+        oi, _ = oracle.bruteforce(X, Q[:check], Kmax)
+        assert np.array_equal(oi, ids[:check]), "GPU ground truth differs from oracle.bruteforce"
+        print(name, "cross-check vs oracle.bruteforce on %d queries ok %.1fs" % (check, time.time() - t), flush=True)
     out = os.path.join(outroot, name)
     os.makedirs(out, exist_ok=True)
     for K in cfg.K:

@@ -6,6 +6,8 @@ by one (the oracle searches only the sample; its index encode covers all N).
   sift: configs[1] (N = 1M, Q = 10k, D = 128, d = 64, k = 4096)
   deep: configs[2] (N = 10M, Q = 10k, D = 96, d = 64, k = 16384) -- the
         largest single-GPU workload and bench.py's default
+  emb:  configs[4] (N = 5M, Q = 10k, D = 1536, d = 512, k = 16384), index
+        from the GPU builder (MRQ_FULLSIZE_EMB=1; ~31 GB of base vectors)
 """
 import os
 
@@ -15,7 +17,8 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 pytestmark = pytest.mark.gpu
 
-FULL = {"sift": ("sift", 64, 16), "deep": ("deep", 64, 16)}
+FULL = {"sift": ("sift", 64, 16), "deep": ("deep", 64, 16), "emb": ("emb", 512, 32)}
+SAMPLE = 48
 
 
 @pytest.fixture(scope="module", params=list(FULL))
@@ -27,15 +30,26 @@ def full(request):
     import paper_2411_06158_b200 as m
     name, d, npb = FULL[request.param]
     bfile = os.path.join(ROOT, "data", name, "build_d%d.mrqb" % d)
-    if not os.path.exists(bfile):
-        pytest.skip("no committed oracle build file for %s" % name)
     cfg = synth.config_by_name(name)
+    if not os.path.exists(bfile):
+        if name != "emb" or os.environ.get("MRQ_FULLSIZE_EMB") != "1":
+            pytest.skip("no committed oracle build file for %s (emb: set MRQ_FULLSIZE_EMB=1 to build on the GPU)"
+                        % name)
     X, Q = synth.generate(cfg, device="cuda")
+    if not os.path.exists(bfile):
+        # Embedding-shaped (5M x 1536): the index comes from the GPU builder
+        # (SURVEY NEXT-1); both sides read the same build file, so the
+        # parity below is unaffected by who built it
+        bfile = "/tmp/mrq_fullsize_emb_d%d.mrqb" % d
+        m.mrq_build_gpu(X, d, cfg.k, bfile, device=0)
     bf = B.read(bfile)
     assert synth.base_sha256(X) == bf.sha
     h = m.mrq_index_load(bfile, X, d, device=0)
-    ox = oracle.Index(bf, X)
-    yield dict(name=name, m=m, h=h, X=X, Q=Q, ox=ox, torch=torch, npb=npb)
+    rng = np.random.default_rng(11)
+    sample = np.sort(rng.choice(Q.shape[0], SAMPLE, replace=False))
+    # the oracle encodes only the lists the sampled queries can probe
+    ox = oracle.Index(bf, X, lists=oracle.probe_lists(bf, Q[sample], npb))
+    yield dict(name=name, m=m, h=h, X=X, Q=Q, ox=ox, torch=torch, npb=npb, sample=sample)
     m.mrq_free(h)
     del ox
 
@@ -54,8 +68,7 @@ def test_full_batch_sampled_parity(full, tau):
         m.mrq_search_batch_device(h, dq, p, ids, dist, None, s.cuda_stream)
     torch.cuda.synchronize()
     gi, gd = ids.cpu().numpy(), dist.cpu().numpy()
-    rng = np.random.default_rng(11)
-    sample = np.sort(rng.choice(nq, 48, replace=False))
+    sample = full["sample"]
     oi, od, ost = ox.search(Q[sample], K=K, nprobe=npb, tau_schedule=tau, seed_lists=2)
     assert np.array_equal(gi[sample], oi)
     assert np.array_equal(gd[sample].view(np.uint32), od.view(np.uint32))
@@ -67,7 +80,10 @@ def test_full_batch_sampled_parity(full, tau):
 def test_full_batch_recall(full):
     """recall@10 of the bench operating point against the committed fp64 ground truth."""
     m, h, Q = full["m"], full["h"], full["Q"]
-    gt = np.load(os.path.join(ROOT, "data", full["name"], "gt_k10.npy"))
+    gtp = os.path.join(ROOT, "data", full["name"], "gt_k10.npy")
+    if not os.path.exists(gtp):
+        pytest.skip("no committed ground truth")
+    gt = np.load(gtp)
     ids, _, _ = m.mrq_search_batch(h, Q, m.SearchParams.make(K=10, nprobe=full["npb"], tau_schedule="LOOSE",
                                                              seed_lists=2), with_stats=False)
     hits = sum(len(set(a.tolist()) & set(b.tolist())) for a, b in zip(ids, gt))

@@ -576,3 +576,21 @@ def test_kmeans_blobs_and_determinism():
     assert np.abs(Cc[0] - b.mean(0)).max() < 0.1 and np.abs(Cc[1] - a.mean(0)).max() < 0.1
     assert np.allclose(B.kmeans(X, 1)[0], X.mean(0))
     assert np.array_equal(B.kmeans(X, 7), B.kmeans(X, 7))
+
+
+def test_subset_encode_identical():
+    """Test infrastructure: encoding only the lists a sampled search can probe
+    (oracle.probe_lists, orc_encode_subset) gives the full encode's results
+    for those queries (the full-size GPU parity tests rely on it)."""
+    import synth
+    cfg = synth.config_by_name("sift")
+    X, Q = synth.generate(cfg, N=30_000, Q=12)
+    bf = B.build(X, 64, 128)
+    full = oracle.Index(bf, X)
+    L = oracle.probe_lists(bf, Q, 8)
+    assert len(L) < bf.k
+    sub = oracle.Index(bf, X, lists=L)
+    for tau in ("TIGHT", "LOOSE"):
+        a = full.search(Q, K=10, nprobe=8, tau_schedule=tau)
+        b = sub.search(Q, K=10, nprobe=8, tau_schedule=tau)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and a[2] == b[2]
