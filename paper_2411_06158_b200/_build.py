@@ -61,7 +61,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     def comp(src):
         o = _obj(src, flags)
-        if force or not os.path.exists(o) or os.path.getmtime(o) < max(os.path.getmtime(src), hdr_t):
+        if (force and force != "relink") or not os.path.exists(o) or \
+                os.path.getmtime(o) < max(os.path.getmtime(src), hdr_t):
             subprocess.check_call(["nvcc"] + flags + ["-c", src, "-o", o + ".tmp"])
             os.replace(o + ".tmp", o)
         return o

@@ -221,11 +221,7 @@ static int load_impl(mrq_index *ix, const char *build_file, const float *base, i
     ix->D = D;
     ix->d = d;
     ix->k = (int)b.k;
-    ix->W = (d + 31) / 32;
-    if (!supported_W(ix->W)) {
-        mrq_set_error("InvalidConfig: d=%d (ceil(d/32)=%d code words) not supported", d, ix->W);
-        return MRQ_EINVAL;
-    }
+    ix->W = (d + 31) / 32;   // any d loads; the MRQ modes need supported_W (d <= 512), EXACT does not
     const int k = ix->k, W = ix->W;
 
     // multi-GPU placement: owned lists (greedy by size), device
@@ -579,11 +575,16 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
     // ---- a2: probe (Alg.2 L7): screen + exact selection, rows [q0, q0 + nr)
     if (nr > 0) {
         uint32_t *cand, *ncand;
-        SCR("probe_cand", uint32_t, nr * k, cand);
+        // the margin set per query: <= k entries (unfused), <= the parts'
+        // buffers when fused (an overflowing row rescores all k without it)
+        const bool fused = mrq_probe_tc_fusable(ix, np);
+        const int64_t cper = fused ? std::min<int64_t>(k, (int64_t)mrq_probe_tc_parts(ix, nr) * mrq_probe_tc_capp(ix, np))
+                                   : k;
+        SCR("probe_cand", uint32_t, nr * cper, cand);
         SCR("probe_ncand", uint32_t, nr, ncand);
         double *qp_r = qp + q0 * D, *qn_r = qnorm + q0, *pq_r = probe_qn2 + q0 * np;
         uint32_t *pr_r = probe + q0 * np;
-        if (mrq_probe_tc_fusable(ix, np)) {   // tcgen05 screen with the running top-np in its epilogue
+        if (fused) {   // tcgen05 screen with the running top-np in its epilogue
             const int P = mrq_probe_tc_parts(ix, nr), capp = mrq_probe_tc_capp(ix, np);
             uint2 *cbuf;
             uint32_t *ccnt;
@@ -627,8 +628,8 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
         return MRQ_OK;
     };
     if (!fshard) TRY(fork_offsets());   // beside the quantizer
-    if (nr > 0) {
-        MRQ_CUDA_TRY(cudaStreamWaitEvent(st, ix->ev_fork[3], 0));   // r0
+    MRQ_CUDA_TRY(cudaStreamWaitEvent(st, ix->ev_fork[3], 0));   // r0 (joins the side stream in every mode)
+    if (nr > 0 && mode != 2) {   // EXACT reads no code: no query quantization
         launch_quant(probe + q0 * np, probe_qn2 + q0 * np, nr, np, d, W, r0 + q0 * d, ix->Rc, qr2 + q0, p->eps0,
                      planes + q0 * np * MRQ_BQ * W, qconst + q0 * np * 8, qsk_b ? qsk_b + q0 * np * ix->dq : nullptr,
                      qsk_c ? qsk_c + q0 * np * 4 : nullptr, ix->dq, qnorm + q0, ix->cmax, st);
@@ -754,8 +755,11 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
             a.hq = ix->hq; a.hs = ix->hs; a.qsk_b = qsk_b; a.qsk_c = qsk_c; a.qr2 = qr2;
             a.dq = ix->dq; a.surv_cnt = surv_cnt;   // NULL: plain F1 (no fused sketch test)
             if (surv_cnt) a.smem = mrq_scan_smem_sk(np, W, ix->dq);
-            TRY(launch_scan(W, a, st));
-            if (ix->dbg_dump_dis) {
+            if (mode == 2)
+                launch_f1_all(probe, nq, np, ix->list_off, ix->list_size, f1_off, f1_cnt, f1_pos, st);
+            else
+                TRY(launch_scan(W, a, st));
+            if (ix->dbg_dump_dis && mode != 2) {
                 double *dd, *dl;
                 SCR("dbg_dis", double, total, dd);
                 SCR("dbg_lb1", double, total, dl);
@@ -865,9 +869,14 @@ static int check_params(const mrq_index *ix, int64_t nq, const mrq_search_params
                       p->resid_scale, MRQ_MAX_SEEDS);
         return MRQ_EINVAL;
     }
+    if (p->mode != 2 && !supported_W(ix->W)) {
+        mrq_set_error("InvalidConfig: mode %d needs d <= 512 and ceil(d/32) in {1,2,3,4,8,16} (d=%d); "
+                      "mode EXACT works for any d", p->mode, ix->d);
+        return MRQ_EINVAL;
+    }
     // the scan stages every probed list's constants and bit-planes in shared memory
     const size_t scan_smem = mrq_scan_smem(std::min(p->nprobe, ix->k), ix->W);
-    if (scan_smem > (size_t)ix->smem_optin) {
+    if (p->mode != 2 && scan_smem > (size_t)ix->smem_optin) {
         mrq_set_error("InvalidConfig: nprobe=%d with d=%d needs %zu B of scan shared memory (device max %d)",
                       p->nprobe, ix->d, scan_smem, ix->smem_optin);
         return MRQ_EINVAL;

@@ -677,7 +677,9 @@ __device__ __forceinline__ bool mrq_sketch_decide(int ab, int aa, float4 se, con
 // shared memory with a shuffle scan.  SK: F1 candidates go through a per-warp
 // shared-memory queue and are sketch-tested 32 at a time (lane per
 // candidate); only the survivors are appended (see ScanSketch).
+#ifndef MRQ_SCAN_TILE
 #define MRQ_SCAN_TILE 128
+#endif
 #ifndef MRQ_SCAN_THREADS
 #define MRQ_SCAN_THREADS 128   // 4 warps per query: a smaller end-of-query tail than 8 (measured)
 #endif
@@ -885,6 +887,33 @@ __global__ void __launch_bounds__(MRQ_SCAN_THREADS, (W <= 3 ? 1024 / MRQ_SCAN_TH
         f1_cnt[q] = sh_cnt;
         if (SK) sk.surv_cnt[q] = sh_surv;
     }
+}
+
+// mode EXACT (IVF*-restricted exact search, every probed candidate is
+// re-ranked): F1 = all of them, written in probe order then slot order
+// without evaluating any code (so any code length d works in this mode).
+// Block per query.
+__global__ void k_f1_all(const uint32_t *__restrict__ probe, int np, const uint32_t *__restrict__ list_off,
+                         const uint32_t *__restrict__ list_size, const uint64_t *__restrict__ f1_off,
+                         uint32_t *__restrict__ f1_cnt, uint32_t *__restrict__ f1_pos)
+{
+    const int64_t q = blockIdx.x;
+    uint32_t *out = f1_pos + f1_off[q];
+    uint32_t at = 0;
+    for (int p = 0; p < np; p++) {
+        const uint32_t c = probe[q * np + p];
+        if (c == 0xFFFFFFFFu) continue;
+        const uint32_t st = list_off[c], sz = list_size[c];
+        for (uint32_t e = threadIdx.x; e < sz; e += blockDim.x) out[at + e] = st + e;
+        at += sz;
+    }
+    if (threadIdx.x == 0) f1_cnt[q] = at;
+}
+
+void launch_f1_all(const uint32_t *probe, int64_t nq, int np, const uint32_t *list_off, const uint32_t *list_size,
+                   const uint64_t *f1_off, uint32_t *f1_cnt, uint32_t *f1_pos, cudaStream_t st)
+{
+    k_f1_all<<<(unsigned)nq, 256, 0, st>>>(probe, np, list_off, list_size, f1_off, f1_cnt, f1_pos);
 }
 
 __global__ void k_fill_f64(double *p, int64_t n, double v)

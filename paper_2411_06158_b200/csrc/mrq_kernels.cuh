@@ -91,6 +91,8 @@ inline size_t mrq_scan_smem(int np, int W)
 inline size_t mrq_scan_smem_sk(int np, int W, int dq) { return mrq_scan_smem(np, W) + (size_t)np * 24 + 16 + (size_t)np * dq; }
 int launch_scan(int W, const LaunchScan &a, cudaStream_t st);
 bool supported_W(int W);
+void launch_f1_all(const uint32_t *probe, int64_t nq, int np, const uint32_t *list_off, const uint32_t *list_size,
+                   const uint64_t *f1_off, uint32_t *f1_cnt, uint32_t *f1_pos, cudaStream_t st);
 void launch_scan_dbg(int W, const LaunchScan &a, double *dis, double *lb1, cudaStream_t st);
 int launch_probe_finish_w(int64_t nq, int k, int d, int np, const double *qp, int D, const double *C,
                           const double *qnorm, double cmax, double kappa, const uint2 *cbuf, int P, int capp,

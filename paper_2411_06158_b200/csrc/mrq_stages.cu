@@ -1009,6 +1009,7 @@ __global__ void __launch_bounds__(128, MK <= 8 ? MRQ_PF_MINB : 6) k_probe_finish
                                                         const uint2 *__restrict__ cbuf, int P, int capp, int G,
                                                         const uint32_t *__restrict__ ccnt,
                                                         const float *__restrict__ kvbuf, uint32_t *__restrict__ cand,
+                                                        int64_t cstride,
                                                         uint32_t *__restrict__ probe, double *__restrict__ probe_qn2,
                                                         uint32_t *__restrict__ ncand_out)
 {
@@ -1042,7 +1043,7 @@ __global__ void __launch_bounds__(128, MK <= 8 ? MRQ_PF_MINB : 6) k_probe_finish
     }
     const double g = qnorm[q] + cmax;
     const double thr = (double)key2f(res) + 2.0 * (kappa * (g * g));
-    uint32_t *cq = cand + q * k;
+    uint32_t *cq = cand + q * cstride;   // margin set (<= min(k, P capp) entries)
     uint32_t nc = 0;
     if (all) {
         nc = (uint32_t)k;
@@ -1123,8 +1124,10 @@ int launch_probe_finish_w(int64_t nq, int k, int d, int np, const double *qp, in
     auto fn = P * np <= 256 ? k_probe_finish_w<8> : k_probe_finish_w<32>;
     int rc = set_attr((const void *)fn, smem);
     if (rc) return rc;
+    const int64_t cstride = std::min<int64_t>(k, (int64_t)P * capp);
     fn<<<(unsigned)((nq + wpb - 1) / wpb), wpb * 32, smem, st>>>(nq, k, d, np, qp, D, C, qnorm, cmax, kappa, cbuf, P,
-                                                                 capp, G, ccnt, kvbuf, cand, probe, probe_qn2, ncand);
+                                                                 capp, G, ccnt, kvbuf, cand, cstride, probe, probe_qn2,
+                                                                 ncand);
     return MRQ_OK;
 }
 

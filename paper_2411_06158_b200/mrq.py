@@ -11,7 +11,10 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmrq.so")
+# MRQ_LIB_VARIANT=name loads libmrq_<name>.so built next to it (A/B timing of
+# compile-time variants, scripts/variant.sh); default: libmrq.so
+LIB_PATH = os.path.join(HERE, "libmrq%s.so" % (("_" + os.environ["MRQ_LIB_VARIANT"]) if os.environ.get("MRQ_LIB_VARIANT")
+                                                 else ""))
 
 MRQ_MODES = {"FULL": 0, "STAGE1_ONLY": 1, "EXACT": 2, "NOCORR": 3}
 ERRORS = {-1: "EINVAL", -2: "EDIM", -3: "EFORMAT", -4: "EVERSION", -5: "EDEGENERATE", -6: "ECUDA",

@@ -1,13 +1,23 @@
 #!/bin/bash
-# A/B build: copy the committed-or-working tree (sources only) to ./<name>/
-# (git-ignored, travels with gpurun) and build it with extra nvcc flags.
-# usage: scripts/variant.sh NAME "-DFOO=1 ..."   (data/ is shared via symlink)
+# A/B build of a compile-time variant: builds libmrq_<name>.so next to
+# libmrq.so with extra nvcc flags (objects are cached per flag set under
+# paper_2411_06158_b200/build/).  Load it with MRQ_LIB_VARIANT=<name>.
+# usage: scripts/variant.sh NAME "-DFOO=1 ..."
 set -e
 cd "$(dirname "$0")/.."
 name=$1; shift
-rm -rf "$name"; mkdir "$name"
-tar --exclude=./data --exclude=./gpurun_out --exclude=./.git --exclude='./ab*' --exclude='./var_*' -cf - . | tar -xf - -C "$name"
-ln -s ../data "$name/data"
-rm -f "$name"/paper_2411_06158_b200/libmrq.so
-(cd "$name" && MRQ_NVCC_EXTRA="$*" python -c "from paper_2411_06158_b200 import _build; _build.build(force=True)")
-echo "built $name with: $*"
+MRQ_NVCC_EXTRA="$*" python - <<PY
+import os, shutil
+from paper_2411_06158_b200 import _build
+lib = _build.LIB
+tmp = lib + ".main"
+if os.path.exists(lib):
+    shutil.copy2(lib, tmp)
+try:
+    _build.LIB = lib.replace("libmrq.so", "libmrq_$name.so")
+    _build.build(force="relink")
+finally:
+    if os.path.exists(tmp):
+        os.replace(tmp, lib)
+print("built", _build.LIB)
+PY

@@ -452,3 +452,30 @@ def test_head_sketch_prefilter_exact(case):
         m.mrq_debug_set(gx.h, "sketch", 1)
         assert np.array_equal(hi, gi) and np.array_equal(hd, gd) and hst.exact == gst.exact
     assert pruned > 0
+
+
+def test_exact_mode_any_code_length():
+    """mode EXACT reads no code, so any d loads and searches (the d = D index
+    of the Exp-2 ablation, with D = 960 > 512): ids and
+    distances equal the oracle's; the MRQ modes reject such d with EINVAL."""
+    m = _gpu()
+    import tempfile
+    cfg = synth.config_by_name("gist")
+    X, Qv = synth.generate(cfg, N=3_000, Q=20, D=960)
+    bf = B.build(X, 960, 12)
+    path = os.path.join(tempfile.mkdtemp(), "gist_dD.mrqb")
+    B.write(path, bf)
+    ox = oracle.Index(bf, X)
+    gx = m.Index(path, X, 960)
+    try:
+        for npb in (1, 4, 12):
+            gi, gd, gst = gx.search(Qv, K=10, nprobe=npb, mode="EXACT")
+            oi, od, ost = ox.search(Qv, K=10, nprobe=npb, mode="EXACT")
+            assert np.array_equal(gi, oi) and np.array_equal(gd.view(np.uint32), od.view(np.uint32)), npb
+            assert gst.scanned == ost["scanned"] and gst.exact == ost["exact"]
+        for mode in ("FULL", "STAGE1_ONLY", "NOCORR"):
+            with pytest.raises(m.MRQError) as e:
+                gx.search(Qv, K=10, nprobe=4, mode=mode)
+            assert e.value.code == -1
+    finally:
+        gx.close()
