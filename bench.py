@@ -460,8 +460,9 @@ def main():
             cpu = {"value": None, "unit": "queries/s", "cores": os.cpu_count(), "kind": "oracle",
                    "sample": "failed: %s" % e}
 
-    # 13 kernels per search, + k_stage2_w for TIGHT; sharded: + k_xmerge (S0, final),
-    # + k_xmerge (S1) + k_f2_w for TIGHT
+    # 13 kernels per search (k_rowmat x2, k_qtail, k_qorder, k_probe_tc, k_probe_finish_w,
+    # k_quant_g, k_cand_count, k_exclusive_scan, k_seed_w, k_scan, k_head_b, k_topk_w), + k_stage2_w for
+    # TIGHT; sharded: + k_xmerge (S0, final), + k_xmerge (S1) + k_f2_w for TIGHT
     tight_sel = tau_sel == "TIGHT"
     launches_per_step = 13 + (1 if tight_sel else 0) + ((4 if tight_sel else 2) if world > 1 else 0)
     out = {

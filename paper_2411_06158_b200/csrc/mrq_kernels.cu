@@ -668,7 +668,7 @@ __device__ __forceinline__ bool mrq_sketch_decide(int ab, int aa, float4 se, con
 }
 
 // The code scan (hot loop of Alg.2 L7-L12): block per query, every
-// warp streams (list, MRQ_SCAN_TILE-slot) tiles of the query's probed lists.
+// warp streams (list, 128 H-slot) tiles of the query's probed lists.
 // Each lane owns slots base + 128 h .. base + 128 h + 3 of its tile and reads
 // them with 128-bit loads (W code words of the word-major planes
 // codes[w][slot], then f1/f2/f3) before evaluating any, evaluates LB1 in
@@ -677,15 +677,16 @@ __device__ __forceinline__ bool mrq_sketch_decide(int ab, int aa, float4 se, con
 // shared memory with a shuffle scan.  SK: F1 candidates go through a per-warp
 // shared-memory queue and are sketch-tested 32 at a time (lane per
 // candidate); only the survivors are appended (see ScanSketch).
-#ifndef MRQ_SCAN_TILE
-#define MRQ_SCAN_TILE 128
-#endif
+// tiles of 128 H slots (H = 1 or 2, a template parameter): H = 2 keeps twice
+// the loads in flight per lane, which pays when the code stream comes from
+// DRAM (Deep-shaped: scan 0.79 -> 0.74 ms) and costs a little when it sits
+// in L2 (SIFT-shaped: 0.315 -> 0.322 ms); launch_scan picks H = 2 when the
+// index's code + factor stream exceeds 64 MB
 #ifndef MRQ_SCAN_THREADS
 #define MRQ_SCAN_THREADS 128   // 4 warps per query: a smaller end-of-query tail than 8 (measured)
 #endif
-#define MRQ_SCAN_H (MRQ_SCAN_TILE / 128)
 #define MRQ_SKQ 640            // per-warp sketch queue, drained after the tile loop
-template <int W, bool SK>
+template <int W, bool SK, int H>
 __global__ void __launch_bounds__(MRQ_SCAN_THREADS, (W <= 3 ? 1024 / MRQ_SCAN_THREADS : 1)) k_scan(
     const uint32_t *__restrict__ probe, int np, int64_t npad, const uint32_t *__restrict__ list_off,
     const uint32_t *__restrict__ list_size, const uint32_t *__restrict__ codes, const float *__restrict__ f1,
@@ -726,7 +727,7 @@ __global__ void __launch_bounds__(MRQ_SCAN_THREADS, (W <= 3 ? 1024 / MRQ_SCAN_TH
                 if (c != 0xFFFFFFFFu) {
                     st = list_off[c];
                     sz = list_size[c];
-                    nt = (sz + MRQ_SCAN_TILE - 1) / MRQ_SCAN_TILE;
+                    nt = (sz + 128 * H - 1) / (128 * H);
                 }
             }
             uint32_t x = nt;
@@ -815,11 +816,11 @@ __global__ void __launch_bounds__(MRQ_SCAN_THREADS, (W <= 3 ? 1024 / MRQ_SCAN_TH
             for (int i = 0; i < 5; i++) qc[i] = gc[i];
         }
         const uint32_t lend = lst_end[p];
-        const uint32_t base = lst_start[p] + (t - tile_pre[p]) * MRQ_SCAN_TILE + lane * 4;
-        uint4 cw[MRQ_SCAN_H][W];
-        float4 a1[MRQ_SCAN_H], a2[MRQ_SCAN_H], a3[MRQ_SCAN_H];
+        const uint32_t base = lst_start[p] + (t - tile_pre[p]) * (128 * H) + lane * 4;
+        uint4 cw[H][W];
+        float4 a1[H], a2[H], a3[H];
 #pragma unroll
-        for (int h = 0; h < MRQ_SCAN_H; h++) {
+        for (int h = 0; h < H; h++) {
             const uint32_t b = base + h * 128;
 #pragma unroll
             for (int w = 0; w < W; w++) cw[h][w] = __ldg((const uint4 *)(codes + (int64_t)w * npad + b));
@@ -828,7 +829,7 @@ __global__ void __launch_bounds__(MRQ_SCAN_THREADS, (W <= 3 ? 1024 / MRQ_SCAN_TH
             a3[h] = __ldg((const float4 *)(f3 + b));
         }
 #pragma unroll
-        for (int h = 0; h < MRQ_SCAN_H; h++) {
+        for (int h = 0; h < H; h++) {
             const uint32_t b = base + h * 128;
             bool fl[4];
 #pragma unroll
@@ -928,16 +929,16 @@ void launch_fill_f64(double *p, int64_t n, double v, cudaStream_t st)
 }
 
 // ================================================================ launchers
-template <int W, bool SK>
+template <int W, bool SK, int H>
 static int launch_scan_ws(const LaunchScan &a, cudaStream_t st)
 {
     // the opt-in covers static + dynamic shared memory (SK adds a static per-warp queue)
     if (a.smem + (SK ? (MRQ_SCAN_THREADS / 32) * MRQ_SKQ * 6 + 64 : 64) > 48 * 1024)
-        MRQ_CUDA_TRY(cudaFuncSetAttribute(k_scan<W, SK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a.smem));
+        MRQ_CUDA_TRY(cudaFuncSetAttribute(k_scan<W, SK, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a.smem));
     ScanSketch sk;
     sk.hq = a.hq; sk.hs = a.hs; sk.qsk_b = a.qsk_b; sk.qsk_c = a.qsk_c; sk.qr2 = a.qr2;
     sk.dq = a.dq; sk.surv_cnt = a.surv_cnt;
-    k_scan<W, SK><<<a.nq, MRQ_SCAN_THREADS, a.smem, st>>>(a.probe, a.np, a.npad, a.list_off, a.list_size, a.codes,
+    k_scan<W, SK, H><<<a.nq, MRQ_SCAN_THREADS, a.smem, st>>>(a.probe, a.np, a.npad, a.list_off, a.list_size, a.codes,
                                                            a.f1, a.f2, a.f3, a.planes, a.qconst, a.eps_r, a.tau0,
                                                            a.isd, a.f1_off, a.f1_cnt, a.f1_pos, a.qorder, sk);
     MRQ_CUDA_TRY(cudaGetLastError());
@@ -947,7 +948,9 @@ static int launch_scan_ws(const LaunchScan &a, cudaStream_t st)
 template <int W>
 static int launch_scan_w(const LaunchScan &a, cudaStream_t st)
 {
-    return a.surv_cnt ? launch_scan_ws<W, true>(a, st) : launch_scan_ws<W, false>(a, st);
+    const bool dram = (uint64_t)a.npad * (4 * W + 12) > ((uint64_t)64 << 20);   // the stream cannot live in L2
+    if (a.surv_cnt) return dram ? launch_scan_ws<W, true, 2>(a, st) : launch_scan_ws<W, true, 1>(a, st);
+    return dram ? launch_scan_ws<W, false, 2>(a, st) : launch_scan_ws<W, false, 1>(a, st);
 }
 
 int launch_scan(int W, const LaunchScan &a, cudaStream_t st)
