@@ -1,14 +1,18 @@
 #!/usr/bin/env python
-"""Exp-2 of the paper on the SIFT-shaped
-workload: IVF with full-D centroids vs IVF* with centroids on the d leading
-PCA dimensions, at equal nprobe, exact distances (mode EXACT).
+"""Exp-2 of the paper: IVF with full-D centroids
+vs IVF* with centroids on the d leading PCA dimensions, at equal nprobe,
+exact distances (mode EXACT).
 
 Full-D IVF is the d = D build (k-means on x_p[0:D], the probe on all D
-dimensions); IVF* is the bench's d = 64 build.  Both run through libmrq on
-the GPU; recall@10 is against the fp64 ground truth.  The paper reports that
-IVF* loses "almost no recall" at equal nprobe.
-  python scripts/exp2_ivf_ablation.py > profiles/r01_exp2_ivf_ablation.json
+dimensions; mode EXACT reads no code, so any d works); IVF* is the workload's
+MRQ build.  Both are the oracle's committed build files and run through
+libmrq on the GPU; recall@10 is against the fp64 ground truth.  The d = D
+index is also checked against the oracle on sampled queries (ids and fp32
+distances bit for bit).  The paper reports that IVF* loses "almost no
+recall" at equal nprobe (its Exp-2 uses GIST and OpenAI-1536).
+  python scripts/exp2_ivf_ablation.py --config gist --d 128 > profiles/r02_exp2_ivf_ablation_gist.json
 """
+import argparse
 import json
 import os
 import sys
@@ -20,26 +24,46 @@ sys.path.insert(0, ROOT)
 
 
 def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="gist")
+    ap.add_argument("--d", type=int, default=128)
+    ap.add_argument("--check", type=int, default=32)
+    args = ap.parse_args()
     import bench
+    import oracle
     import paper_2411_06158_b200 as mrq
     import synth
     from oracle import build as B
-    cfg = synth.config_by_name("sift")
+    cfg = synth.config_by_name(args.config)
     X, Q = synth.generate(cfg, device="cuda")
-    gt = np.load(os.path.join(ROOT, "data", "sift", "gt_k10.npy"))
-    full = os.path.join(ROOT, "data", "sift", "build_d128.mrqb")
-    if not os.path.exists(full):
-        B.write(full, B.build(X, 128, cfg.k))          # the oracle's build, d = D
-    out = {"workload": bench.WORKLOADS["sift"], "mode": "EXACT", "K": 10, "curves": {}}
-    for name, d in (("IVF* (d=64 centroids)", 64), ("IVF (full-D centroids)", 128)):
-        h = mrq.mrq_index_load(os.path.join(ROOT, "data", "sift", "build_d%d.mrqb" % d), X, d, device=0)
+    D = X.shape[1]
+    gt = np.load(os.path.join(ROOT, "data", args.config, "gt_k10.npy"))
+    out = {"workload": bench.WORKLOADS[args.config], "mode": "EXACT", "K": 10, "curves": {}, "parity": {}}
+    grid = (1, 2, 4, 8, 16, 24, 32, 48, 64)
+    for name, d in (("IVF* (d=%d centroids)" % args.d, args.d), ("IVF (full-D centroids, d=%d)" % D, D)):
+        path = os.path.join(ROOT, "data", args.config, "build_d%d.mrqb" % d)
+        h = mrq.mrq_index_load(path, X, d, device=0)
         pts = []
-        for npb in (1, 2, 4, 8, 16, 24, 32, 48, 64):
-            ids, _, st = mrq.mrq_search_batch(h, Q, mrq.SearchParams.make(K=10, nprobe=npb, mode="EXACT"))
+        for npb in grid:
+            ids, dist, st = mrq.mrq_search_batch(h, Q, mrq.SearchParams.make(K=10, nprobe=npb, mode="EXACT"))
             pts.append({"nprobe": npb, "recall10": round(bench.recall_at_k(ids, gt, 10), 4),
-                        "scanned_per_q": round(st.scanned / Q.shape[0], 1)})
+                        "scanned_per_q": round(st.scanned / Q.shape[0], 1), "ms": round(st.ms_total, 3)})
             print(name, pts[-1], file=sys.stderr, flush=True)
         out["curves"][name] = pts
+        if d == D and args.check:
+            # oracle parity on the d = D index (sampled queries, subset encode)
+            bf = B.read(path)
+            rng = np.random.default_rng(5)
+            sample = np.sort(rng.choice(Q.shape[0], args.check, replace=False))
+            ox = oracle.Index(bf, X, lists=oracle.probe_lists(bf, Q[sample], 16))
+            res = {}
+            for npb in (1, 4, 16):
+                gi, gd, _ = mrq.mrq_search_batch(h, Q[sample], mrq.SearchParams.make(K=10, nprobe=npb, mode="EXACT"))
+                oi, od, _ = ox.search(Q[sample], K=10, nprobe=npb, mode="EXACT")
+                ok = bool(np.array_equal(gi, oi) and np.array_equal(gd.view(np.uint32), od.view(np.uint32)))
+                res["nprobe=%d" % npb] = ok
+                assert ok, "d = D index differs from the oracle at nprobe=%d" % npb
+            out["parity"] = {"index": "d = D = %d" % D, "queries": int(args.check), "ids_and_fp32_dist_equal": res}
         mrq.mrq_free(h)
     print(json.dumps(out, indent=1))
 
