@@ -10,6 +10,8 @@
 #include <cmath>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "mrq_internal.cuh"
 #include "mrq_kernels.cuh"
 #include "mrq_probe_tc.cuh"
@@ -474,6 +476,24 @@ extern "C" int mrq_index_info(const mrq_index *ix, int64_t *n, int32_t *D, int32
 }
 
 // ------------------------------------------------------------------ search
+// NVTX ranges: one range per search with a nested range per
+// stage (host-side; nvtx3 is header-only and free without a tool attached)
+struct NvtxStages {
+    bool open = false;
+    NvtxStages() { nvtxRangePushA("mrq_search"); }
+    void stage(const char *name)
+    {
+        if (open) nvtxRangePop();
+        nvtxRangePushA(name);
+        open = true;
+    }
+    ~NvtxStages()
+    {
+        if (open) nvtxRangePop();
+        nvtxRangePop();
+    }
+};
+
 static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_search_params *p, int64_t *d_ids,
                        float *d_dist, mrq_stats *stats, cudaStream_t st)
 {
@@ -483,6 +503,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
     const int mode = p->mode, tight = p->tau_schedule == 0;
     const double isd = 1.0 / std::sqrt((double)d);
     const bool timed = stats != nullptr;
+    NvtxStages nvtx;
     if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[0], st));
     uint32_t *qorder = nullptr;
 
@@ -553,6 +574,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
         SCR("qkey", uint16_t, nrow, qkey);
     }
     // ---- a1: query projection (Alg.2 L1-L4), rows [q0, q0 + nr)
+    nvtx.stage("a1 projection");
     if (nr > 0) {
         launch_rowmat_f32(d_q + q0 * D, nr, D, D, ix->mu, ix->PT, D, qp + q0 * D, D, st);   // q_p = P (q - mu)
         const size_t qsmem = (size_t)D * 8 * 9;                                              // lambda + 8 query rows
@@ -573,6 +595,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
     if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[1], st));
 
     // ---- a2: probe (Alg.2 L7): screen + exact selection, rows [q0, q0 + nr)
+    nvtx.stage("a2 probe");
     if (nr > 0) {
         uint32_t *cand, *ncand;
         // the margin set per query: <= k entries (unfused), <= the parts'
@@ -618,6 +641,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
     if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[2], st));
 
     // ---- a3: per-(query, list) quantization into bit-planes, rows [q0, q0 + nr)
+    nvtx.stage("a3 quantization");
     auto fork_offsets = [&]() -> int {   // F1 segment offsets of all nq queries on the side stream
         MRQ_CUDA_TRY(cudaEventRecord(ix->ev_fork[1], st));
         MRQ_CUDA_TRY(cudaStreamWaitEvent(ix->side, ix->ev_fork[1], 0));
@@ -675,6 +699,18 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
         MRQ_CUDA_TRY(cudaMemcpyAsync(&total, f1_off + nq, 8, cudaMemcpyDeviceToHost, st));
         MRQ_CUDA_TRY(cudaStreamSynchronize(st));
     }
+#if defined(MRQ_CHECK) && MRQ_CHECK
+    {   // the host bound must cover the exact candidate total (MRQ_CHECK build only: one sync)
+        uint64_t exact_total = 0;
+        MRQ_CUDA_TRY(cudaMemcpyAsync(&exact_total, f1_off + nq, 8, cudaMemcpyDeviceToHost, st));
+        MRQ_CUDA_TRY(cudaStreamSynchronize(st));
+        if (exact_total > total) {
+            mrq_set_error("MRQ_CHECK: candidate total %llu exceeds the scratch bound %llu",
+                          (unsigned long long)exact_total, (unsigned long long)total);
+            return MRQ_EINVAL;
+        }
+    }
+#endif
     ix->last_total = total;
     uint32_t *f1_pos, *f2_pos;
     double *f1_head, *f1_diso, *f2_head, *f2_exact;
@@ -727,6 +763,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
         if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[8], st));
     } else {
         // ---- a4: seeds S0 and tau0 (decision T); EXACT mode scans everything
+        nvtx.stage("a4 seeds");
         if (mode == 2) {
             launch_fill_f64(tau0, nq, INFINITY, st);
             MRQ_CUDA_TRY(cudaMemsetAsync(s0_cnt, 0, nq * 4, st));
@@ -744,6 +781,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
         if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[4], st));
 
         // ---- a5: the code scan -> F1
+        nvtx.stage("a5 scan");
         {
             LaunchScan a;
             a.nq = nq;
@@ -769,6 +807,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
         if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[5], st));
 
         // ---- a6: stage 2 -> F2 (and S1, tau1)
+        nvtx.stage("a6 stage 2");
         if (sharded && mode == 0 && tight) {   // local S1 -> all-gather -> global S1, tau1 -> F2
             StageArgs sx = sa;
             sx.xout = xsend;
@@ -786,6 +825,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
         if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[7], st));
 
         // ---- a8: per-query top-K
+        nvtx.stage("a7+a8 re-rank, top-K");
         if (sharded) {
             StageArgs sx = sa;
             sx.xout = xsend;
@@ -796,6 +836,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
         if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[8], st));
     }
     // ---- a9: multi-GPU merge (all-gather of the per-rank top-K)
+    nvtx.stage("a9 merge");
     if (sharded) {
         TRY(mrq_allgather(ix, xsend, xrecv, (size_t)nq * K * sizeof(XItem), st));
         TRY(launch_xmerge(2, sa, ix->world, ix->rank, xrecv, st));

@@ -8,6 +8,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <cstdio>
 #include <stdint.h>
 
 #include <exception>
@@ -56,6 +57,25 @@ int mrq_guard(F &&f)
         return MRQ_EINVAL;
     }
 }
+
+// Device-side bounds checks of the MRQ_CHECK build (scripts/variant.sh check
+// -DMRQ_CHECK=1; compute-sanitizer is not available on the GPU pool): a
+// violated invariant prints its location and traps (the launch fails with an
+// error instead of corrupting memory).  Compiled out otherwise.
+#if defined(MRQ_CHECK) && MRQ_CHECK
+#define MRQ_ASSERT(cond)                                                                                   \
+    do {                                                                                                   \
+        if (!(cond)) {                                                                                     \
+            printf("MRQ_CHECK failed: %s at %s:%d (block %d thread %d)\n", #cond, __FILE__, __LINE__,       \
+                   (int)blockIdx.x, (int)threadIdx.x);                                                     \
+            __trap();                                                                                      \
+        }                                                                                                  \
+    } while (0)
+#else
+#define MRQ_ASSERT(cond) \
+    do {                 \
+    } while (0)
+#endif
 
 // ------------------------------------------------------------ index object
 struct DevArr {

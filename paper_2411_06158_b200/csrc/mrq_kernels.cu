@@ -800,7 +800,10 @@ __global__ void __launch_bounds__(MRQ_SCAN_THREADS, (W <= 3 ? 1024 / MRQ_SCAN_TH
                 uint32_t o = 0;
                 if (lane == 0) o = atomicAdd(&sh_surv, (uint32_t)__popc(bal));
                 o = __shfl_sync(0xffffffffu, o, 0) + __popc(bal & ((1u << lane) - 1u));
-                if (keep) out[o] = slot[u];
+                if (keep) {
+                MRQ_ASSERT(o < (uint32_t)(f1_off[q + 1] - f1_off[q]) && slot[u] < npad);
+                out[o] = slot[u];
+            }
             }
         }
     };
@@ -856,6 +859,7 @@ __global__ void __launch_bounds__(MRQ_SCAN_THREADS, (W <= 3 ? 1024 / MRQ_SCAN_TH
                     if (lane == 0) atomicAdd(&sh_cnt, (uint32_t)tot);
                     const uint32_t o0 = qn + __popc(b0 & lt), o1 = qn + n0 + __popc(b1 & lt);
                     const uint32_t o2 = qn + n0 + n1 + __popc(b2 & lt), o3 = qn + n0 + n1 + n2 + __popc(b3 & lt);
+                    MRQ_ASSERT(qn + tot <= MRQ_SKQ);
                     if (fl[0]) { wq[o0] = b; wp[o0] = (uint16_t)p; }
                     if (fl[1]) { wq[o1] = b + 1; wp[o1] = (uint16_t)p; }
                     if (fl[2]) { wq[o2] = b + 2; wp[o2] = (uint16_t)p; }
@@ -871,6 +875,7 @@ __global__ void __launch_bounds__(MRQ_SCAN_THREADS, (W <= 3 ? 1024 / MRQ_SCAN_TH
                     wb = __shfl_sync(0xffffffffu, wb, 0);
                     const uint32_t o0 = wb + __popc(b0 & lt), o1 = wb + n0 + __popc(b1 & lt);
                     const uint32_t o2 = wb + n0 + n1 + __popc(b2 & lt), o3 = wb + n0 + n1 + n2 + __popc(b3 & lt);
+                    MRQ_ASSERT(wb + tot <= (uint32_t)(f1_off[q + 1] - f1_off[q]));
                     if (fl[0]) out[o0] = b;
                     if (fl[1]) out[o1] = b + 1;
                     if (fl[2]) out[o2] = b + 2;
@@ -905,6 +910,7 @@ __global__ void k_f1_all(const uint32_t *__restrict__ probe, int np, const uint3
         const uint32_t c = probe[q * np + p];
         if (c == 0xFFFFFFFFu) continue;
         const uint32_t st = list_off[c], sz = list_size[c];
+        MRQ_ASSERT(at + sz <= (uint32_t)(f1_off[q + 1] - f1_off[q]));
         for (uint32_t e = threadIdx.x; e < sz; e += blockDim.x) out[at + e] = st + e;
         at += sz;
     }

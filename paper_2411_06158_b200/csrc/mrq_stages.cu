@@ -299,6 +299,7 @@ __global__ void __launch_bounds__(128) k_head_b(
                           if (lane == 0) o = atomicAdd(&f2n, (uint32_t)__popc(bal));
                           o = __shfl_sync(0xffffffffu, o, 0) + __popc(bal & ((1u << lane) - 1u));
                           if (pass) {
+                              MRQ_ASSERT(o < (uint32_t)n1);
                               f2_pos[base + o] = slotv;
                               f2_head[base + o] = head;
                           }
@@ -1081,7 +1082,10 @@ __global__ void __launch_bounds__(128, MK <= 8 ? MRQ_PF_MINB : 6) k_probe_finish
             for (int u = 0; u < 4; u++) {
                 const bool ok = in[u] && (double)__uint_as_float(x[u].x) <= thr;
                 const unsigned bal = __ballot_sync(0xffffffffu, ok);
-                if (ok) cq[nc + __popc(bal & ((1u << lane) - 1u))] = x[u].y;
+                if (ok) {
+                    MRQ_ASSERT(nc + __popc(bal & ((1u << lane) - 1u)) < (uint32_t)cstride && x[u].y < (uint32_t)k);
+                    cq[nc + __popc(bal & ((1u << lane) - 1u))] = x[u].y;
+                }
                 nc += __popc(bal);
             }
         }
