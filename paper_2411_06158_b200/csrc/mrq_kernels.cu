@@ -436,6 +436,9 @@ __global__ void __launch_bounds__(256) k_quant_g(const uint32_t *__restrict__ pr
         // (rounded up; margins cover the fp64 rounding of f and of r0 - Rc)
         const double mx = fmax(fabs(lo), fabs(hi));
         const double tq = (ok && mx > 0.0) ? mx / 127.0 : 0.0;
+        // any int8 b is valid (F bounds the residual of the b actually chosen),
+        // so the level uses a reciprocal multiply, not a division
+        const double itq = tq > 0.0 ? 1.0 / tq : 0.0;
         double f2 = 0.0;
         int B = 0;
         uint32_t pk[E / 4];
@@ -446,7 +449,7 @@ __global__ void __launch_bounds__(256) k_quant_g(const uint32_t *__restrict__ pr
             const int j = s * E + t;
             int b = 0;
             if (ok && j < d) {
-                if (tq > 0.0) b = (int)fmin(127.0, fmax(-127.0, rint(rv[t] / tq)));
+                if (tq > 0.0) b = (int)fmin(127.0, fmax(-127.0, rint(rv[t] * itq)));
                 const double f = rv[t] - tq * (double)b;
                 f2 = f2 + f * f;
             }
