@@ -10,8 +10,9 @@
 //   L3-L5  heads x_d = P[0:d] (x - mu) for all N (k_rowmat, fp64);
 //   L6     IVF* k-means on the heads: a strided sample of <= km_sample_per_k k
 //          rows, initial centroids = k strided sample rows, <= km_iters Lloyd
-//          iterations (fp32 register-tiled distance kernel, fp64 centroid
-//          sums), stop when the relative WCSS gain < 1e-4, an empty cluster is
+//          iterations (the assignment step on the tensor cores: the search
+//          path's tcgen05 probe with np = 1 and its exact fp64 rescore,
+//          TcAssign; fp64 centroid sums), stop when the relative WCSS gain < 1e-4, an empty cluster is
 //          re-seeded at the farthest member of the largest cluster; final
 //          assignment of all N to the nearest centroid;
 //   P_r    Haar d x d rotation: modified Gram-Schmidt (twice) of a Gaussian
@@ -32,6 +33,7 @@
 
 #include "mrq_internal.cuh"
 #include "mrq_kernels.cuh"
+#include "mrq_probe_tc.cuh"
 
 namespace {
 
@@ -198,6 +200,138 @@ __global__ void __launch_bounds__(256) k_assign(const float *__restrict__ X, int
         }
     }
 }
+
+// ------------------------------------------------ tensor-core assignment
+// The k-means assignment step (nearest centroid, Alg.1 L6) on the tensor
+// cores: the search path's probe (k_probe_tc<true, 16> screen with np = 1 +
+// k_probe_finish_w's exact fp64 rescore of the margin set, DESIGN.md §4 "probe
+// exactness") run on a build-time pseudo index that holds the current
+// centroids.  a[i] = argmin_c ||x_i - c||^2 (ties -> smaller c), evaluated
+// exactly in fp64 for the fp32 points; dmin[i] = that squared distance.
+__global__ void k_f32_rows_to_probe(const float *__restrict__ X, int64_t n, int d, double *__restrict__ x64,
+                                    float *__restrict__ qa3, double *__restrict__ qnorm)
+{
+    const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (i >= n) return;
+    double n2 = 0.0;
+    for (int j = lane; j < d; j += 32) {
+        const float x = X[i * d + j];
+        x64[i * d + j] = (double)x;
+        float hi, lo;
+        tf32_split(x, hi, lo);
+        qa3[i * 3 * d + j] = hi;
+        qa3[i * 3 * d + d + j] = hi;
+        qa3[i * 3 * d + 2 * d + j] = lo;
+        n2 += (double)x * (double)x;
+    }
+    for (int o = 16; o > 0; o >>= 1) n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+    if (lane == 0) qnorm[i] = sqrt(n2) * (1.0 + 0x1p-40);   // >= ||x|| (the bound's input)
+}
+
+__global__ void k_centroid_norms(const double *__restrict__ C, int k, int d, float *__restrict__ cn32,
+                                 double *__restrict__ cnorm)
+{
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= k) return;
+    double s = 0.0;
+    for (int j = 0; j < d; j++) {
+        const double v = (double)(float)C[(int64_t)c * d + j];   // of the fp32 centroid the screen uses
+        s += v * v;
+    }
+    cn32[c] = (float)s;
+    double t = 0.0;
+    for (int j = 0; j < d; j++) t += C[(int64_t)c * d + j] * C[(int64_t)c * d + j];
+    cnorm[c] = sqrt(t);
+}
+
+#define TRY_S(x)                         \
+    do {                                 \
+        int _r = (x);                    \
+        if (_r != MRQ_OK) return _r;     \
+    } while (0)
+
+struct TcAssign {
+    mrq_index ix;                  // pseudo index: the current centroids only
+    float *cn32 = nullptr;
+    double *cnorm = nullptr;
+    int capp = 32;                 // np = 1: about 1 + ln(k / P) appends per part
+    bool ok = false;
+    ~TcAssign()
+    {
+        mrq_probe_tc_free(&ix);
+        if (cn32) cudaFree(cn32);
+        if (cnorm) cudaFree(cnorm);
+        for (auto &kv : ix.scratch)
+            if (kv.second.p) cudaFree(kv.second.p);
+    }
+    int init(int k, int d, int sm_count)
+    {
+        ix.k = k;
+        ix.d = d;
+        ix.D = d;
+        ix.sm_count = sm_count;
+        ix.stream = 0;
+        ix.device = -1;
+        const int kp = (k + 255) / 256 * 256;
+        if (cudaMalloc(&cn32, (size_t)kp * 4) != cudaSuccess || cudaMalloc(&cnorm, (size_t)k * 8) != cudaSuccess) {
+            mrq_set_error("cudaMalloc (tensor-core assignment)");
+            return MRQ_ENOMEM;
+        }
+        std::vector<float> inf(kp, INFINITY);
+        MRQ_CUDA_TRY(cudaMemcpy(cn32, inf.data(), (size_t)kp * 4, cudaMemcpyHostToDevice));
+        ix.cn32 = cn32;
+        return MRQ_OK;
+    }
+    // new centroids: C fp64 [k][d], Cf = fp32(C)
+    int set_centroids(double *C, float *Cf)
+    {
+        ix.C = C;
+        ix.C32 = Cf;
+        k_centroid_norms<<<(ix.k + 255) / 256, 256>>>(C, ix.k, ix.d, cn32, cnorm);
+        std::vector<double> nr(ix.k);
+        MRQ_CUDA_TRY(cudaMemcpy(nr.data(), cnorm, (size_t)ix.k * 8, cudaMemcpyDeviceToHost));
+        double mx = 0.0;
+        for (double v : nr) mx = std::max(mx, v);
+        ix.cmax = mx * (1.0 + 1e-9) + 1e-300;
+        mrq_probe_tc_free(&ix);
+        const int rc = mrq_probe_tc_init(&ix);
+        if (rc != MRQ_OK) return rc;
+        ok = mrq_probe_tc_fusable(&ix, 1);
+        return MRQ_OK;
+    }
+    // a[i], dmin[i] (fp64) for n fp32 rows X [n][d], in chunks
+    int assign(const float *X, int64_t n, uint32_t *a, double *dmin)
+    {
+        const int d = ix.d, k = ix.k;
+        const int64_t CH = 1 << 19;
+        for (int64_t r0 = 0; r0 < n; r0 += CH) {
+            const int64_t m = std::min<int64_t>(CH, n - r0);
+            double *x64, *qn;
+            float *qa3;
+            TRY_S(mrq_scratch(&ix, "a_x64", (size_t)m * d * 8, (void **)&x64));
+            TRY_S(mrq_scratch(&ix, "a_qa3", (size_t)m * 3 * d * 4, (void **)&qa3));
+            TRY_S(mrq_scratch(&ix, "a_qn", (size_t)m * 8, (void **)&qn));
+            k_f32_rows_to_probe<<<(unsigned)((m + 7) / 8), 256>>>(X + r0 * d, m, d, x64, qa3, qn);
+            const int P = mrq_probe_tc_parts(&ix, m);
+            uint2 *cbuf;
+            uint32_t *ccnt, *cand, *ncand;
+            float *kv;
+            TRY_S(mrq_scratch(&ix, "a_cbuf", (size_t)m * P * capp * 8, (void **)&cbuf));
+            TRY_S(mrq_scratch(&ix, "a_ccnt", (size_t)m * P * 4, (void **)&ccnt));
+            TRY_S(mrq_scratch(&ix, "a_kv", (size_t)m * P * 4, (void **)&kv));
+            const int64_t cs = std::min<int64_t>(k, (int64_t)P * capp);
+            TRY_S(mrq_scratch(&ix, "a_cand", (size_t)m * cs * 4, (void **)&cand));
+            TRY_S(mrq_scratch(&ix, "a_ncand", (size_t)m * 4, (void **)&ncand));
+            const double kappa = mrq_probe_tc_kappa(&ix);
+            TRY_S(mrq_probe_tc_run_fused(&ix, qa3, m, 1, qn, kappa, cbuf, capp, ccnt, kv, 0));
+            TRY_S(launch_probe_finish_w(m, k, d, 1, x64, d, ix.C, qn, ix.cmax, kappa, cbuf, P, capp,
+                                        mrq_probe_tc_grid(&ix, m), ccnt, kv, cand, a + r0, dmin + r0, ncand, 0));
+        }
+        MRQ_CUDA_TRY(cudaGetLastError());
+        return MRQ_OK;
+    }
+};
 
 __global__ void k_accumulate(const float *__restrict__ X, int64_t n, int d, const uint32_t *__restrict__ a,
                              double *__restrict__ sums, uint32_t *__restrict__ cnt)
@@ -561,9 +695,28 @@ static int build_gpu_impl(const float *base, int64_t n, int32_t D, int32_t d, co
         MRQ_CUDA_TRY(cudaMemcpy(dC, c64.data(), c64.size() * 8, cudaMemcpyHostToDevice));
     }
     k_rownorm<<<(unsigned)((k + 255) / 256), 256>>>(dCf, k, d, dcn);
+    // the assignment step on the tensor cores (TcAssign: the search's probe with
+    // np = 1, exact fp64 nearest centroid) when d % 4 == 0; else CUDA cores
+    TcAssign tc;
+    int sm_count = 148;
+    MRQ_CUDA_TRY(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, device >= 0 ? device : 0));
+    BTRY(tc.init(k, d, sm_count));
+    double *ddmin64;
+    BTRY(dv.alloc(&ddmin64, std::max<int64_t>(m, n)));
+    auto assign_step = [&](const float *Xr, const float *xn, int64_t nr) -> int {
+        BTRY(tc.set_centroids(dC, dCf));
+        if (tc.ok) {
+            BTRY(tc.assign(Xr, nr, dA, ddmin64));
+            k_to_f32<<<(unsigned)((nr + 255) / 256), 256>>>(ddmin64, nr, ddmin);
+        } else {
+            k_assign<<<(unsigned)((nr + 63) / 64), 256>>>(Xr, nr, d, dCf, dcn, k, xn, dA, ddmin);
+        }
+        MRQ_CUDA_TRY(cudaGetLastError());
+        return MRQ_OK;
+    };
     double prev = INFINITY;
     for (int it = 0; it < bp->km_iters; it++) {
-        k_assign<<<(unsigned)((m + 63) / 64), 256>>>(dS, m, d, dCf, dcn, k, dSn, dA, ddmin);
+        BTRY(assign_step(dS, dSn, m));
         MRQ_CUDA_TRY(cudaMemset(dw, 0, 8));
         k_sum_f32<<<256, 256>>>(ddmin, m, dw);
         MRQ_CUDA_TRY(cudaMemset(dsums, 0, (size_t)k * d * 8));
@@ -607,7 +760,7 @@ static int build_gpu_impl(const float *base, int64_t n, int32_t D, int32_t d, co
     float *dHn;
     BTRY(dv.alloc(&dHn, n));
     k_rownorm<<<(unsigned)((n + 255) / 256), 256>>>(dH, n, d, dHn);
-    k_assign<<<(unsigned)((n + 63) / 64), 256>>>(dH, n, d, dCf, dcn, k, dHn, dA, ddmin);
+    BTRY(assign_step(dH, dHn, n));
     std::vector<uint32_t> assign(n);
     std::vector<double> C((size_t)k * d);
     MRQ_CUDA_TRY(cudaMemcpy(assign.data(), dA, (size_t)n * 4, cudaMemcpyDeviceToHost));
