@@ -380,6 +380,7 @@ def main():
     sk_pass = float(np.mean([s.sketch_pass for s in sts]))
     hbm, peak_kind = peaks()
     traffic = ncu_traffic(cfg_name, nprobe)
+    fused_topk = tau_sel != "TIGHT" and K <= 32   # k_head_topk replaces k_head_b + k_topk_w
     # algorithmic bytes per unit: scan = one
     # scanned code (W code words + f1/f2/f3); head gather = one F1 survivor
     # (fp32 head row, ||x_r||^2, id)
@@ -402,9 +403,21 @@ def main():
         kern["k_head_b"]["unit"] = "sketch survivor (F1 entry the head sketch could not prune)"
     f2 = float(np.mean([s.stage2_pass for s in sts]))
     D_ = int(X.shape[1])
-    kern["k_topk_w"] = {"unit": "F2 survivor (exact re-rank gather; the launch also selects the top-K)",
-                        "bytes_per_unit": 4 * (D_ - d) + 20, "units_per_launch": int(f2),
-                        "ms": float(np.mean([s.ms_topk for s in sts]))}
+    btail = 4 * (D_ - d) + 20   # fp32 tail row + slot + id + head (F2 re-rank)
+    ms_topk = float(np.mean([s.ms_topk for s in sts]))
+    if fused_topk:
+        # k_head_topk: the head gather of the survivors, the F2
+        # test, the F2 tail gather (exact re-rank) and the top-K in one launch
+        hb = kern.pop("k_head_b")
+        units = hb["units_per_launch"]
+        kern["k_head_topk"] = {
+            "unit": "%s: head row (%d B) + its share of the F2 tail gather (%d B per F2 entry, %.1f%% of them)"
+                    % (hb["unit"], bhead, btail, 100.0 * f2 / max(units, 1)),
+            "bytes_per_unit": round(bhead + btail * f2 / max(units, 1), 3), "units_per_launch": units,
+            "ms": ms_head}
+    else:
+        kern["k_topk_w"] = {"unit": "F2 survivor (exact re-rank gather; the launch also selects the top-K)",
+                            "bytes_per_unit": btail, "units_per_launch": int(f2), "ms": ms_topk}
     for nm, kk in kern.items():
         kk["achieved_gbs"] = round(kk["bytes_per_unit"] * kk["units_per_launch"] / (kk["ms"] * 1e-3) / 1e9, 1)
         kk["frac"] = round(kk["achieved_gbs"] / hbm, 4)
@@ -462,9 +475,11 @@ def main():
 
     # 13 kernels per search (k_rowmat x2, k_qtail, k_qorder, k_probe_tc, k_probe_finish_w,
     # k_quant_g, k_cand_count, k_exclusive_scan, k_seed_w, k_scan, k_head_b, k_topk_w), + k_stage2_w for
-    # TIGHT; sharded: + k_xmerge (S0, final), + k_xmerge (S1) + k_f2_w for TIGHT
+    # TIGHT, k_head_topk in place of k_head_b + k_topk_w without S1 (K <= 32); sharded: + k_xmerge
+    # (S0, final), + k_xmerge (S1) + k_f2_w for TIGHT
     tight_sel = tau_sel == "TIGHT"
-    launches_per_step = 13 + (1 if tight_sel else 0) + ((4 if tight_sel else 2) if world > 1 else 0)
+    launches_per_step = (13 + (1 if tight_sel else 0) - (1 if fused_topk else 0) +
+                         ((4 if tight_sel else 2) if world > 1 else 0))
     out = {
         "metric": METRIC,
         "value": round(nq / (ms * 1e-3), 1),

@@ -747,6 +747,8 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
     sa.list_size_g = ix->list_size_g; sa.s0_id = s0_id; sa.s1_id = s1_id; sa.xout = nullptr;
     sa.store_f1 = ix->dbg_dump_dis;
     sa.sketch = want_sketch; sa.surv_cnt = surv_cnt;
+    sa.fuse_topk = ix->fuse_topk_on;
+    const bool fuse_topk = mode != 3 && mrq_head_topk_used(sa);
 
     if (mode == 3) {
         // ---- NOCORR: top-K by dis' over every probed candidate, no bounds, no re-rank
@@ -815,6 +817,11 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
             TRY(mrq_allgather(ix, xsend, xrecv, (size_t)nq * Kp * sizeof(XItem), st));
             TRY(launch_xmerge(1, sa, ix->world, ix->rank, xrecv, st));
             TRY(launch_f2_w(sa, st));
+        } else if (fuse_topk) {   // stage 2 + a7 + a8 in one kernel (k_head_topk)
+            StageArgs sx = sa;
+            if (sharded) sx.xout = xsend;
+            TRY(launch_head_topk(sx, st));
+            if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[10], st));
         } else {
             TRY(launch_stage2_w(sa, st, timed ? ix->ev[10] : nullptr));
         }
@@ -826,7 +833,9 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
 
         // ---- a8: per-query top-K
         nvtx.stage("a7+a8 re-rank, top-K");
-        if (sharded) {
+        if (fuse_topk) {
+            // (done by k_head_topk)
+        } else if (sharded) {
             StageArgs sx = sa;
             sx.xout = xsend;
             TRY(launch_topk_w(sx, st));
@@ -1153,6 +1162,10 @@ extern "C" int mrq_debug_set(mrq_index *ix, const char *name, int64_t value)
     }
     if (std::string(name) == "sketch") {           // head-sketch pre-pass of the stage-2 gather (default 1)
         ix->sketch_on = (int)value;
+        return MRQ_OK;
+    }
+    if (std::string(name) == "fuse_topk") {   // stage 2 + re-rank + top-K in one kernel (default 1)
+        ix->fuse_topk_on = value ? 1 : 0;
         return MRQ_OK;
     }
     if (std::string(name) == "probe_capp") {       // per-part candidate buffer of the fused probe (default 256)

@@ -44,6 +44,7 @@ struct StageArgs {
     int64_t *out_ids;
     float *out_dist;
     const uint32_t *qorder;   // processing order of the queries (NULL: 0..nq-1)
+    int fuse_topk;            // allow k_head_topk (stage 2 + re-rank + top-K in one kernel)
 };
 
 // the fused head-sketch test of the scan (FULL with tau1 = tau0, i.e. LOOSE;
@@ -55,6 +56,8 @@ inline bool mrq_sketch_used(const StageArgs &a)
 int launch_seed_w(int W, const StageArgs &a, cudaStream_t st);
 int launch_stage2_w(const StageArgs &a, cudaStream_t st, cudaEvent_t after_gather = nullptr);
 int launch_topk_w(const StageArgs &a, cudaStream_t st);
+bool mrq_head_topk_used(const StageArgs &a);
+int launch_head_topk(const StageArgs &a, cudaStream_t st);
 int launch_nocorr_w(int W, const StageArgs &a, cudaStream_t st);
 int launch_exact_count(const StageArgs &a, cudaStream_t st);
 int launch_f2_w(const StageArgs &a, cudaStream_t st);

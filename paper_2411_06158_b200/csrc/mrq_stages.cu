@@ -317,6 +317,152 @@ __global__ void __launch_bounds__(128) k_head_b(
     }
 }
 
+// Stage 2 + exact re-rank + top-K in one block per query (every schedule
+// without S1 -- LOOSE, STAGE1_ONLY, EXACT -- and K <= 32): the F2 test of
+// k_head_b on the gathered head rows (phase 1), then the block's warps split
+// the F2 tail rows (Alg.2 L14 P:316: exact = HEAD continued over the tail,
+// left to right, R-8) and each offers its exact distances to a warp top-K
+// (phase 2); warp 0 merges the warps' lists with S0 (de-duplicated) into the
+// K smallest (exact, id) (Alg.2 L15-L16 P:317-321).  Same sets and values as
+// k_head_b + k_topk_w (the F2 exact distances are stored too, f2_exact).  Sharded (xout != NULL): the local top-K goes to the
+// exchange.
+__global__ void __launch_bounds__(128) k_head_topk(
+    int aligned, int aligned_t, int D, int d, int K, int Kp, const uint32_t *__restrict__ ids,
+    const float *__restrict__ heads, const float *__restrict__ tails, const float *__restrict__ xr2,
+    const double *__restrict__ qp, const double *__restrict__ qr2_arr, const uint64_t *__restrict__ f1_off,
+    const uint32_t *__restrict__ f1_cnt, const uint32_t *__restrict__ f1_pos, const uint32_t *__restrict__ qorder,
+    int mode, const double *__restrict__ eps_r_arr, const double *__restrict__ tau0_arr,
+    uint32_t *__restrict__ f2_cnt, uint32_t *__restrict__ f2_pos, double *__restrict__ f2_head,
+    double *__restrict__ f2_exact, uint32_t *__restrict__ s1_cnt, double *__restrict__ tau1_arr, int sketch,
+    const uint32_t *__restrict__ surv_cnt,
+    const uint32_t *__restrict__ s0_cnt, const uint32_t *__restrict__ s0_pos, const uint32_t *__restrict__ s0_id,
+    const double *__restrict__ s0_exact, int64_t *__restrict__ out_ids, float *__restrict__ out_dist,
+    XItem *__restrict__ xout)
+{
+    extern __shared__ unsigned char wsm[];
+    __shared__ uint32_t f2n;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+    const int64_t q = qorder ? (int64_t)qorder[blockIdx.x] : (int64_t)blockIdx.x;
+    // shared memory: [query row][gather tiles][per-warp selection lists + queues][merge list + queue]
+    double *qs = (double *)wsm;
+    float *tile = (float *)(qs + MRQ_QS(D)) + warp * MRQ_RG_FLOATS;
+    SelItem *sel = (SelItem *)((float *)(qs + MRQ_QS(D)) + wpb * MRQ_RG_FLOATS);
+    SelItem *lst = sel + (size_t)warp * MRQ_SELREG(K);
+    for (int i = threadIdx.x; i < D; i += blockDim.x) qs[i] = qp[q * D + i];
+    if (threadIdx.x == 0) f2n = 0;
+    __syncthreads();
+    const uint64_t base = f1_off[q];
+    const int n1 = (int)f1_cnt[q];
+    const double qr2 = qr2_arr[q], eps_r = eps_r_arr[q], tau1 = tau0_arr[q];
+    // ---- phase 1: HEAD and dis_o' of the (sketch-surviving) F1 rows; the F2 test (Alg.2 L13)
+    const uint32_t *rows = f1_pos + base;
+    const int n = sketch ? (int)surv_cnt[q] : n1;
+    float xr2v = 0.f;
+    uint32_t slotv = 0;
+    warp_rows(aligned, heads, d, 0, d, qs, n, tile, [&](int e) { return rows[e]; },
+              [&](int, uint32_t slot) {
+                  xr2v = xr2[slot];
+                  slotv = slot;
+                  return 0.0;
+              },
+              [&](int, bool v, double head) {
+                  const double diso = (head + (double)xr2v) + qr2;
+                  const bool pass = v && ((mode != 0) || (diso - eps_r < tau1));
+                  const unsigned bal = __ballot_sync(0xffffffffu, pass);
+                  if (bal) {
+                      uint32_t o = 0;
+                      if (lane == 0) o = atomicAdd(&f2n, (uint32_t)__popc(bal));
+                      o = __shfl_sync(0xffffffffu, o, 0) + __popc(bal & ((1u << lane) - 1u));
+                      if (pass) {
+                          MRQ_ASSERT(o < (uint32_t)n1);
+                          f2_pos[base + o] = slotv;
+                          f2_head[base + o] = head;
+                      }
+                  }
+              },
+              warp, wpb);
+    __syncthreads();
+    const int n2 = (int)f2n;
+    if (threadIdx.x == 0) {
+        f2_cnt[q] = n2;
+        s1_cnt[q] = 0;
+        tau1_arr[q] = tau1;
+    }
+    // ---- phase 2: exact distances of F2 (the warps split the tail rows), per-warp top-K
+    WarpSel top;
+    top.init(lst, K, true, lst + K);   // F2 entries are distinct
+    uint32_t idv = 0;
+    if (D > d) {
+        warp_rows(aligned_t, tails, D - d, 0, D - d, qs + d, n2, tile, [&](int e) { return f2_pos[base + e]; },
+                  [&](int e, uint32_t slot) {
+                      slotv = slot;
+                      idv = ids[slot];
+                      return f2_head[base + e];
+                  },
+                  [&](int e, bool v, double ex) {
+                      if (v) f2_exact[base + e] = ex;
+                      SelItem it;
+                      it.key = ex;
+                      it.id = idv;
+                      it.pay = slotv;
+                      top.offer(it, v);
+                  },
+                  warp, wpb);
+    } else {
+        for (int g = warp * 32; g < n2; g += wpb * 32) {
+            const int e = g + lane;
+            SelItem it = sel_inf();
+            if (e < n2) {
+                it.pay = f2_pos[base + e];
+                it.id = ids[it.pay];
+                it.key = f2_head[base + e];
+                f2_exact[base + e] = it.key;
+            }
+            top.offer(it, e < n2);
+        }
+    }
+    top.finish();
+    __syncthreads();
+    if (warp != 0) return;
+    // ---- merge: S0 u (the warps' lists), de-duplicated, the K smallest (exact, id)
+    SelItem *fl = sel + (size_t)wpb * MRQ_SELREG(K);
+    WarpSel fin;
+    fin.init(fl, K, false, fl + K);
+    const int ns0 = (int)s0_cnt[q];
+    for (int g = 0; g < ns0; g += 32) {
+        const int e = g + lane;
+        SelItem it = sel_inf();
+        if (e < ns0) {
+            it.key = s0_exact[q * Kp + e];
+            it.id = s0_id[q * Kp + e];
+            it.pay = s0_pos[q * Kp + e];
+        }
+        fin.offer(it, e < ns0 && it.pay != MRQ_PAD_ID);
+    }
+    for (int w = 0; w < wpb; w++) {
+        const SelItem *wl = sel + (size_t)w * MRQ_SELREG(K);
+        SelItem it = sel_inf();
+        if (lane < K) it = wl[lane];
+        fin.offer(it, lane < K && it.id != MRQ_PAD_ID);
+    }
+    fin.finish();
+    for (int i = lane; i < K; i += 32) {
+        const SelItem x = fl[i];
+        if (xout) {
+            XItem o;
+            o.key = x.key;
+            o.exact = x.key;
+            o.id = x.id;
+            o.slot = x.pay;
+            xout[q * K + i] = o;
+        } else {
+            const bool ok = x.id != 0xFFFFFFFFu;
+            out_ids[q * K + i] = ok ? (int64_t)x.id : (int64_t)-1;
+            out_dist[q * K + i] = ok ? (float)x.key : __int_as_float(0x7f800000);
+        }
+    }
+}
+
 // Stage 2, decision half, warp per query.  TIGHT: S1 = the K' smallest
 // (dis_o', id) of F1, their exact distances (HEAD continued over the tail),
 // tau1 = K-th smallest distinct exact over S0 u S1; LOOSE: tau1 = tau0.
@@ -794,6 +940,27 @@ int launch_stage2_w(const StageArgs &a, cudaStream_t st, cudaEvent_t after_gathe
         a.nq, a.aligned_tails, a.mode, a.tight, a.K, a.Kp, a.D, a.d, a.tails, a.qp, a.eps_r, a.tau0, a.f1_off, a.f1_cnt,
         a.f1_pos, a.f1_head, a.f1_diso, a.f1_id, a.s0_cnt, a.s0_id, a.s0_exact, a.s1_cnt, a.s1_pos, a.s1_id,
         a.s1_exact, a.tau1, a.f2_cnt, a.f2_pos, a.f2_head, a.xout, a.qorder);
+    return MRQ_OK;
+}
+
+bool mrq_head_topk_used(const StageArgs &a)
+{
+    return !(a.mode == 0 && a.tight) && a.K <= 32 && !a.store_f1 && a.fuse_topk;
+}
+
+int launch_head_topk(const StageArgs &a, cudaStream_t st)
+{
+    const int wpb = MRQ_HEAD_WPB;
+    const size_t smem = (size_t)MRQ_QS(a.D) * 8 + (size_t)wpb * MRQ_RG_FLOATS * 4 +
+                        (size_t)(wpb + 1) * MRQ_SELREG(a.K) * sizeof(SelItem);
+    int rc = set_attr((const void *)k_head_topk, smem);
+    if (rc) return rc;
+    const bool sk = mrq_sketch_used(a);
+    k_head_topk<<<(unsigned)a.nq, wpb * 32, smem, st>>>(
+        a.aligned, a.aligned_tails, a.D, a.d, a.K, a.Kp, a.ids, a.heads, a.tails, a.xr2, a.qp, a.qr2, a.f1_off,
+        a.f1_cnt, a.f1_pos, a.qorder, a.mode, a.eps_r, a.tau0, a.f2_cnt, a.f2_pos, a.f2_head, a.f2_exact, a.s1_cnt,
+        a.tau1,
+        sk ? 1 : 0, a.surv_cnt, a.s0_cnt, a.s0_pos, a.s0_id, a.s0_exact, a.out_ids, a.out_dist, a.xout);
     return MRQ_OK;
 }
 

@@ -454,6 +454,30 @@ def test_head_sketch_prefilter_exact(case):
     assert pruned > 0
 
 
+@pytest.mark.parametrize("K", [1, 10, 32])
+def test_head_topk_fused_equals_oracle(case, K):
+    """Stage 2 + exact re-rank + top-K fused in one kernel (k_head_topk: every
+    schedule without S1, K <= 32) returns the oracle's ids and distances and
+    F2 counts, and the same as the unfused kernels (k_head_b + k_topk_w)."""
+    m, gx, ox, Q = case["m"], case["gx"], case["ox"], case["Q"]
+    m.mrq_debug_set(gx.h, "dump_dis", 0)
+    for mode, tau in (("FULL", "LOOSE"), ("STAGE1_ONLY", "TIGHT"), ("EXACT", "TIGHT")):
+        for npb in case["nprobe"]:
+            m.mrq_debug_set(gx.h, "fuse_topk", 1)
+            gi, gd, gst = gx.search(Q, K=K, nprobe=npb, mode=mode, tau_schedule=tau)
+            oi, od, ost = ox.search(Q, K=K, nprobe=npb, mode=mode, tau_schedule=tau)
+            assert np.array_equal(gi, oi), (mode, npb)
+            assert np.array_equal(gd.view(np.uint32), od.view(np.uint32)), (mode, npb)
+            assert gst.exact == ost["exact"]
+            if mode == "FULL":
+                assert gst.stage2_pass == ost["f2"]
+            m.mrq_debug_set(gx.h, "fuse_topk", 0)
+            hi, hd, hst = gx.search(Q, K=K, nprobe=npb, mode=mode, tau_schedule=tau)
+            assert np.array_equal(hi, gi) and np.array_equal(hd.view(np.uint32), gd.view(np.uint32))
+            assert (hst.stage2_pass, hst.exact) == (gst.stage2_pass, gst.exact)
+    m.mrq_debug_set(gx.h, "fuse_topk", 1)
+
+
 def test_exact_mode_any_code_length():
     """mode EXACT reads no code, so any d loads and searches (the d = D index
     of the Exp-2 ablation, with D = 960 > 512): ids and
