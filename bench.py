@@ -281,6 +281,9 @@ def main():
                            host_allgather=hx, tails_host=args.tails_host)
     load_s = time.time() - t0
     info = mrq.mrq_index_info(h)
+    for kv in filter(None, os.environ.get("MRQ_DEBUG_SET", "").split(",")):   # A/B switches (mrq_debug_set)
+        k_, v_ = kv.split("=")
+        mrq.mrq_debug_set(h, k_, int(v_))
     log("index loaded in %.2fs: %s (sha match %s)" % (load_s, info, sha_ok))
 
     dq = torch.from_numpy(Q).to(dev)

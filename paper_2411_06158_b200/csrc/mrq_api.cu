@@ -615,8 +615,10 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
             SCR("probe_cbuf", uint2, (size_t)nr * P * capp, cbuf);
             SCR("probe_ccnt", uint32_t, (size_t)nr * P, ccnt);
             SCR("probe_kv", float, (size_t)nr * P * np, kvbuf);
+            uint32_t *gkey = nullptr;
+            if (ix->probe_share) SCR("probe_gkey", uint32_t, (size_t)nr, gkey);
             const double kappa = mrq_probe_tc_kappa(ix);
-            TRY(mrq_probe_tc_run_fused(ix, qa3 + q0 * 3 * d, nr, np, qn_r, kappa, cbuf, capp, ccnt, kvbuf, st));
+            TRY(mrq_probe_tc_run_fused(ix, qa3 + q0 * 3 * d, nr, np, qn_r, kappa, cbuf, capp, ccnt, kvbuf, gkey, st));
             if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[11], st));
             TRY(launch_probe_finish_w(nr, k, d, np, qp_r, D, ix->C, qn_r, ix->cmax, kappa, cbuf, P, capp,
                                       mrq_probe_tc_grid(ix, nr), ccnt, kvbuf, cand, pr_r, pq_r, ncand, st));
@@ -1100,6 +1102,7 @@ static int debug_fetch(mrq_index *ix, const char *name, void *dst, size_t dst_by
             {"fallback", 4}, {"approx", (size_t)nq * k * 4}, {"probe_ncand", (size_t)nq * 4},
             {"dbg_dis", (size_t)ix->last_total * 8}, {"dbg_lb1", (size_t)ix->last_total * 8},
             {"surv_cnt", (size_t)nq * 4},
+            {"probe_ccnt", ix->scratch.count("probe_ccnt") ? ix->scratch["probe_ccnt"].bytes : 0},
         };
         for (auto &e : per)
             if (nm == e.n) {
@@ -1166,6 +1169,10 @@ extern "C" int mrq_debug_set(mrq_index *ix, const char *name, int64_t value)
     }
     if (std::string(name) == "fuse_topk") {   // stage 2 + re-rank + top-K in one kernel (default 1)
         ix->fuse_topk_on = value ? 1 : 0;
+        return MRQ_OK;
+    }
+    if (std::string(name) == "probe_share") {   // the fused probe's parts share their bounds (default 1)
+        ix->probe_share = value ? 1 : 0;
         return MRQ_OK;
     }
     if (std::string(name) == "probe_capp") {       // per-part candidate buffer of the fused probe (default 256)

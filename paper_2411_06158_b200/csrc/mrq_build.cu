@@ -324,7 +324,9 @@ struct TcAssign {
             TRY_S(mrq_scratch(&ix, "a_cand", (size_t)m * cs * 4, (void **)&cand));
             TRY_S(mrq_scratch(&ix, "a_ncand", (size_t)m * 4, (void **)&ncand));
             const double kappa = mrq_probe_tc_kappa(&ix);
-            TRY_S(mrq_probe_tc_run_fused(&ix, qa3, m, 1, qn, kappa, cbuf, capp, ccnt, kv, 0));
+            uint32_t *gkey;
+            TRY_S(mrq_scratch(&ix, "a_gkey", (size_t)m * 4, (void **)&gkey));
+            TRY_S(mrq_probe_tc_run_fused(&ix, qa3, m, 1, qn, kappa, cbuf, capp, ccnt, kv, gkey, 0));
             TRY_S(launch_probe_finish_w(m, k, d, 1, x64, d, ix.C, qn, ix.cmax, kappa, cbuf, P, capp,
                                         mrq_probe_tc_grid(&ix, m), ccnt, kv, cand, a + r0, dmin + r0, ncand, 0));
         }

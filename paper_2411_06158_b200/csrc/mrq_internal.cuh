@@ -115,6 +115,7 @@ struct mrq_index {
     int sm_count = 148;
     int sketch_on = 1;                         // mrq_debug_set("sketch"): head-sketch pre-pass of the stage-2 gather
     int probe_capp = 256;                      // mrq_debug_set("probe_capp"): fused-probe candidate buffer per part
+    int probe_share = 1;                       // mrq_debug_set("probe_share"): parts of a row share their bound
     int fuse_topk_on = 1;                      // mrq_debug_set("fuse_topk"): k_head_topk where it applies
     uint64_t cand_budget = (uint64_t)8 << 30;  // mrq_debug_set("cand_budget_mb"): host-bound scratch budget
     int smem_optin = 227 * 1024;               // max dynamic shared memory per block (opt-in)

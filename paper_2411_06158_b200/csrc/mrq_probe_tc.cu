@@ -113,7 +113,14 @@ __host__ __device__ constexpr uint32_t tf32_idesc(int M, int N)
 // np-th smallest never drops below the row's final a_(np), so every member of
 // the margin set {c : a_c <= a_(np) + 2 delta_q} is appended by its part; the
 // parts' np smallest go to kvbuf ([row][part][np]) so that k_probe_finish_w
-// can form a_(np) and rescore the margin set.
+// can form a_(np) and rescore the margin set.  The parts of a row share
+// their bounds: each publishes its running np-th smallest to gkey[row]
+// (atomicMin on order-preserving keys) and each tile starts from the
+// smallest published one -- every published value is some part's running
+// np-th smallest, so >= a_(np), and the append threshold stays valid.  (The
+// parts are small -- a CTA range of a 256-column tile run split in two
+// halves -- so a fresh part appends about np (1 + ln(n / np)) values; with
+// the shared bound the parts a row reaches later start nearly converged.)
 #define TC_NPMAX 64
 
 template <bool FUSED, int NPM>
@@ -123,7 +130,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_probe_tc(const __grid_constan
                                                             float *__restrict__ approx, int np,
                                                             const double *__restrict__ qnorm, double cmax,
                                                             double kappa, uint2 *__restrict__ cbuf, int capp,
-                                                            uint32_t *__restrict__ ccnt, float *__restrict__ kvbuf)
+                                                            uint32_t *__restrict__ ccnt, float *__restrict__ kvbuf,
+                                                            uint32_t *__restrict__ gkey)
 {
     extern __shared__ __align__(1024) unsigned char tsm[];
     unsigned char *ring = (unsigned char *)(((uintptr_t)tsm + 1023) & ~(uintptr_t)1023);
@@ -265,6 +273,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_probe_tc(const __grid_constan
                     }
                 }
             }
+            if (FUSED && gkey && row < nq) {   // the row's shared bound, published by any part
+                const uint32_t gk = __ldcg(gkey + row);
+                if (gk < 0xFF800000u) tf = fminf(tf, __fadd_ru(key2f(gk), margin));
+            }
             const int b = it & 1;
             mbar_wait(tfull + b, ((uint32_t)it >> 1) & 1u);
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
@@ -323,7 +335,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_probe_tc(const __grid_constan
                                     kv[i] = lo;
                                 }
                                 const float th = kv[NPM - 1];
-                                tf = __fadd_ru(th, margin);   // +inf stays +inf
+                                tf = fminf(tf, __fadd_ru(th, margin));   // +inf stays +inf
+                                if (gkey && th < FINF) atomicMin(gkey + row, f2key(th));
                             }
                         }
                     }
@@ -469,7 +482,7 @@ int mrq_probe_tc_run(mrq_index *ix, const float *qd32, int64_t nq, float *approx
     if (rc != MRQ_OK) return rc;
     const int G = tc_grid(ix, nq);
     k_probe_tc<false, 16><<<G, TC_THREADS, TC_SMEM, st>>>(mapA, tc->mapB, (int)nq, ix->k, 3 * ix->d, G, 1, ix->cn32, approx,
-                                                       0, nullptr, 0.0, 0.0, nullptr, 0, nullptr, nullptr);
+                                                       0, nullptr, 0.0, 0.0, nullptr, 0, nullptr, nullptr, nullptr);
     MRQ_CUDA_TRY(cudaGetLastError());
     return MRQ_OK;
 }
@@ -496,7 +509,7 @@ int mrq_probe_tc_parts(const mrq_index *ix, int64_t nq)
 }
 
 int mrq_probe_tc_run_fused(mrq_index *ix, const float *qd32, int64_t nq, int np, const double *qnorm, double kappa,
-                           uint2 *cbuf, int capp, uint32_t *ccnt, float *kvbuf, cudaStream_t st)
+                           uint2 *cbuf, int capp, uint32_t *ccnt, float *kvbuf, uint32_t *gkey, cudaStream_t st)
 {
     ProbeTC *tc = (ProbeTC *)ix->probe_tc;
     CUtensorMap mapA;
@@ -504,9 +517,10 @@ int mrq_probe_tc_run_fused(mrq_index *ix, const float *qd32, int64_t nq, int np,
     if (rc != MRQ_OK) return rc;
     const int G = tc_grid(ix, nq);
     const int maxparts = mrq_probe_tc_parts(ix, nq) / 2;
+    if (gkey) MRQ_CUDA_TRY(cudaMemsetAsync(gkey, 0xFF, (size_t)nq * 4, st));   // no bound published yet
     auto fn = np <= 16 ? k_probe_tc<true, 16> : k_probe_tc<true, TC_NPMAX>;
     fn<<<G, TC_THREADS, TC_SMEM, st>>>(mapA, tc->mapB, (int)nq, ix->k, 3 * ix->d, G, maxparts, ix->cn32, nullptr, np,
-                                        qnorm, ix->cmax, kappa, cbuf, capp, ccnt, kvbuf);
+                                        qnorm, ix->cmax, kappa, cbuf, capp, ccnt, kvbuf, gkey);
     MRQ_CUDA_TRY(cudaGetLastError());
     return MRQ_OK;
 }

@@ -10,7 +10,8 @@ int mrq_probe_tc_run(mrq_index *ix, const float *qd32, int64_t nq, float *approx
 // Fused screen + running top-np (np <= 64), the row's columns split into P
 // parts (mrq_probe_tc_parts): per-(row, part) candidate buffers
 // cbuf[nq][P][capp] of (screen value bits, centroid), counts ccnt[nq][P] and
-// the part's np smallest screen values kvbuf[nq][P][np]; finished by
+// the part's np smallest screen values kvbuf[nq][P][np]; gkey[nq] (scratch,
+// or NULL) carries the bound the parts of a row share; finished by
 // launch_probe_finish_w.
 bool mrq_probe_tc_fusable(const mrq_index *ix, int np);
 int mrq_probe_tc_capp(const mrq_index *ix, int np);
@@ -40,4 +41,4 @@ __host__ __device__ __forceinline__ int tc_parts_of(int64_t mb, int64_t nq, int 
     return (int)(2 * (tc_owner((mb + 1) * ntiles - 1, U, G) - tc_owner(mb * ntiles, U, G) + 1));
 }
 int mrq_probe_tc_run_fused(mrq_index *ix, const float *qd32, int64_t nq, int np, const double *qnorm, double kappa,
-                           uint2 *cbuf, int capp, uint32_t *ccnt, float *kvbuf, cudaStream_t st);
+                           uint2 *cbuf, int capp, uint32_t *ccnt, float *kvbuf, uint32_t *gkey, cudaStream_t st);

@@ -46,6 +46,9 @@ def main():
     gx = m.Index(os.path.join(ROOT, "data", cfgname, "build_d%d.mrqb" % d), X, d)
     nq = Q.shape[0]
     P = parts(nq, gx.info["k"])
+    for kv in filter(None, os.environ.get("SET", "").split(",")):   # SET=name=value,... (mrq_debug_set)
+        k_, v_ = kv.split("=")
+        m.mrq_debug_set(gx.h, k_, int(v_))
     import torch
     torch.cuda.profiler.start()   # ncu --profile-from-start off: only the searches below are profiled
     for T in [int(x) for x in os.environ.get("BOUND_T", "64").split(",")]:
