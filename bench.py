@@ -454,13 +454,16 @@ def main():
     for _ in range(2):
         mrq.mrq_search_batch(h, hq, p, with_stats=False, out_ids=h_ids, out_dist=h_dist)
     e2e_t = []
-    for i in range(args.steps):
+    e2e_steps = max(args.steps, 20)   # wall-clock steps: more of them, a host hiccup weighs less in the mean
+    for i in range(e2e_steps):
         flush.fill_(float(i))
         torch.cuda.synchronize()
         t = time.perf_counter()
         mrq.mrq_search_batch(h, hq, p, with_stats=False, out_ids=h_ids, out_dist=h_dist)
         e2e_t.append(time.perf_counter() - t)
     e2e_s = float(np.mean(e2e_t))
+    log("e2e ms per step: mean %.3f median %.3f min %.3f max %.3f" % tuple(
+        1e3 * f(e2e_t) for f in (np.mean, np.median, np.min, np.max)))
     if world > 1:
         t = torch.tensor([e2e_s], device="cpu" if host_x else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -516,7 +519,8 @@ def main():
                      "note": "achieved = algorithmic bytes / launch time; above 1.0 when L2 serves re-reads "
                              "(list-locality query order): dram_gbs / dram_frac give the DRAM side"},
         "e2e": {"value": round(nq / e2e_s, 1), "unit": "queries/s", "h2d_bytes_per_step": int(nq * X.shape[1] * 4),
-                "d2h_bytes_per_step": int(nq * K * 12)},
+                "d2h_bytes_per_step": int(nq * K * 12), "steps": e2e_steps,
+                "ms_per_step": {"mean": round(1e3 * e2e_s, 4), "median": round(1e3 * float(np.median(e2e_t)), 4)}},
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),
         "cpu_baseline": cpu,

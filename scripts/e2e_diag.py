@@ -50,4 +50,22 @@ print("D2H %d B (pinned):                  %.3f ms" % (hi.numel() * 12, med(
     lambda: (hi.copy_(di, non_blocking=True), hd.copy_(dd, non_blocking=True)))))
 print("python wrapper + ctypes, nq = 0:       %.3f ms" % med(
     lambda: mrq.mrq_search_batch(h, hq.numpy()[:0], p, with_stats=False)))
+flush = torch.empty(512 << 18, dtype=torch.float32, device="cuda")   # 512 MB (> L2), as bench.py
+
+
+def flushed(f):
+    def g():
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        f()
+        torch.cuda.synchronize()
+        return time.perf_counter() - t
+    return 1e3 * float(np.median([g() for _ in range(20)]))
+
+
+print("host call after an L2 flush:           %.3f ms" % flushed(
+    lambda: mrq.mrq_search_batch(h, hq.numpy(), p, with_stats=False, out_ids=hi.numpy(), out_dist=hd.numpy())))
+print("device call + sync after an L2 flush:  %.3f ms" % flushed(
+    lambda: mrq.mrq_search_batch_device(h, dq, p, di, dd, None, s.cuda_stream)))
 mrq.mrq_free(h)
