@@ -43,7 +43,7 @@
 #define TC_B_BYTES (TC_BN * TC_BK * 4) // 32 KB
 #define TC_STAGE_BYTES (TC_A_BYTES + TC_B_BYTES)
 #define TC_THREADS 320                 // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
-#define TC_SMEM (TC_STAGES * TC_STAGE_BYTES + 1024 + 256 + 256 * 33 * 4)
+#define TC_SMEM (TC_STAGES * TC_STAGE_BYTES + 1024 + 256 + 256 * 32 * 4)
 
 struct ProbeTC {
     bool enabled = false;
@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_probe_tc(const __grid_constan
     uint64_t *tfull = empty + TC_STAGES;    // [2]
     uint64_t *tempty = tfull + 2;           // [2]
     uint32_t *tmem_slot = (uint32_t *)(tempty + 2);
-    float *scratch = (float *)(tmem_slot + 4);   // FUSED: 256 x 33 floats (per-thread chunk staging)
+    float *scratch = (float *)(tmem_slot + 4);   // FUSED: 256 x 32 floats (per-thread chunk staging)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ntiles = (k + TC_BN - 1) / TC_BN;
@@ -316,13 +316,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_probe_tc(const __grid_constan
                         for (int j = 0; j < 32; j++) mask |= av[j] <= tf ? (1u << j) : 0u;
                     }
                     if (mask) {   // rare after warm-up: stage the chunk, walk the passing values
-                        float *sc = scratch + ((warp - 2) * 32 + lane) * 33;
+                        // the thread's 32 values as 8 16-byte stores; chunk u of the row
+                        // goes to position u ^ (lane & 7), so the 8 lanes of a quarter-warp
+                        // hit distinct bank groups
+                        float *sc = scratch + ((warp - 2) * 32 + lane) * 32;
+                        const int sw = lane & 7;
 #pragma unroll
-                        for (int j = 0; j < 32; j++) sc[j] = av[j];
+                        for (int u = 0; u < 8; u++)
+                            *(float4 *)(sc + 4 * (u ^ sw)) = make_float4(av[4 * u], av[4 * u + 1], av[4 * u + 2], av[4 * u + 3]);
                         while (mask) {
                             const int j = __ffs(mask) - 1;
                             mask &= mask - 1;
-                            const float a = sc[j];
+                            const float a = sc[4 * ((j >> 2) ^ sw) + (j & 3)];
                             if (!(a <= tf)) continue;
                             if (cnt < (uint32_t)capp) rb[cnt] = make_uint2(__float_as_uint(a), (uint32_t)(n0 + c + j));
                             cnt++;
