@@ -18,14 +18,16 @@
 // hold >= K' candidates and number >= seed_lists form the pool; S0 = the K' smallest (dis', id) of the
 // pool; exact distances ||x_p - q_p||^2 (Alg.2 L14 P:316) of S0; tau0 = K-th
 // smallest exact over S0 (+inf if |S0| < K).
-// The S0 rows (<= K' <= a few dozen) go through the register-staged gather
-// (warp_rows_sqdist, a 32 x 33 tile) rather than the double-buffered cp.async
-// stages: a third of the shared memory per warp, so more one-warp blocks fit
-// on an SM (the kernel is latency-bound; shared memory limited it to 18).
-#ifndef MRQ_SEED_REGGATHER
-#define MRQ_SEED_REGGATHER 1
+// Short rows (D <= MRQ_SEED_REG_D): the S0 rows (<= K' <= a few dozen) go
+// through the register-staged gather (warp_rows_sqdist, a 32 x 33 tile)
+// rather than the double-buffered cp.async stages: a third of the shared
+// memory per warp, so more one-warp blocks fit on an SM (the kernel is
+// latency-bound; shared memory limited it to 18; Deep-shaped 0.251 -> 0.206
+// ms).  Long rows keep the cp.async pipeline (GIST-shaped, D = 960: 0.069 vs
+// 0.126 ms).
+#ifndef MRQ_SEED_REG_D
+#define MRQ_SEED_REG_D 256
 #endif
-#define MRQ_SEED_TILE (MRQ_SEED_REGGATHER ? 32 * 33 : MRQ_RG_FLOATS)
 #ifndef MRQ_SEED_MINB
 #define MRQ_SEED_MINB 32  // one-warp blocks, 32 resident per SM: <= 64 registers (seed 0.134 -> 0.126 ms); 0: plain bounds
 #endif
@@ -53,11 +55,12 @@ __global__ void MRQ_SEED_LB k_seed_w(
     const int64_t q = qorder ? (int64_t)qorder[qi] : qi;
     // shared memory: [query rows (MRQ_QS(D) doubles per warp)][gather tiles][selection lists]
     double *qs = (double *)wsm + (size_t)warp * MRQ_QS(D);
-    float *tile = (float *)((double *)wsm + (size_t)wpb * MRQ_QS(D)) + warp * MRQ_SEED_TILE;
-    SelItem *lst = (SelItem *)((float *)((double *)wsm + (size_t)wpb * MRQ_QS(D)) + wpb * MRQ_SEED_TILE) +
+    const int tilef = D <= MRQ_SEED_REG_D ? 32 * 33 : MRQ_RG_FLOATS;   // per-warp gather tile (floats)
+    float *tile = (float *)((double *)wsm + (size_t)wpb * MRQ_QS(D)) + warp * tilef;
+    SelItem *lst = (SelItem *)((float *)((double *)wsm + (size_t)wpb * MRQ_QS(D)) + wpb * tilef) +
                    (size_t)warp * MRQ_SELREG(Kp);
     SelItem *queue = lst + Kp;
-    if (MRQ_SEED_REGGATHER) aligned = aligned_t = 0;   // the register-staged gather (warp_rows_sqdist)
+    if (D <= MRQ_SEED_REG_D) aligned = aligned_t = 0;   // the register-staged gather (warp_rows_sqdist)
     for (int i = lane; i < D; i += 32) qs[i] = qp[q * D + i];   // the query row, read by every gathered row
     __syncwarp();
     const double eps_r = eps_r_arr[q];
@@ -861,7 +864,8 @@ static int set_attr(const void *fn, size_t smem)
 
 int launch_seed_w(int W, const StageArgs &a, cudaStream_t st)
 {
-    const size_t per = (size_t)MRQ_QS(a.D) * 8 + MRQ_SEED_TILE * 4 + (size_t)MRQ_SELREG(a.Kp) * sizeof(SelItem);
+    const size_t per = (size_t)MRQ_QS(a.D) * 8 + (size_t)(a.D <= MRQ_SEED_REG_D ? 32 * 33 : MRQ_RG_FLOATS) * 4 +
+                       (size_t)MRQ_SELREG(a.Kp) * sizeof(SelItem);
     const int wpb = warps_for(per);
     const size_t smem = per * wpb;
     const unsigned grid = (unsigned)((a.nq + wpb - 1) / wpb);

@@ -420,6 +420,30 @@ def test_probe_overflow_and_sync_fallbacks(case):
         m.mrq_debug_set(gx.h, "cand_budget_mb", 8192)
 
 
+def test_probe_shared_bound_exact(case):
+    """The fused probe's parts share their running np-th smallest (a per-row
+    bound): with and without sharing the probe lists and their
+    qn2 equal the oracle's exact top-np for every query, at every nprobe of
+    the case (the multi-part rows of sift_k2048 included)."""
+    m, gx, ox, Q = case["m"], case["gx"], case["ox"], case["Q"]
+    try:
+        for share in (1, 0):
+            m.mrq_debug_set(gx.h, "probe_share", share)
+            for npb in case["nprobe"]:
+                m.mrq_debug_set(gx.h, "dump_dis", 1)
+                gx.search(Q, K=10, nprobe=npb)
+                oi, od, ost, dp = ox.search(Q, K=10, nprobe=npb, dump=True)
+                npr = min(npb, ox.k)
+                nq = Q.shape[0]
+                got = gx.fetch("probe", "u32").reshape(nq, npr).astype(np.int64)
+                assert np.array_equal(got, dp["probe"]), (share, npb)
+                assert np.array_equal(gx.fetch("probe_qn2", "f64").reshape(nq, npr), dp["probe_qn2"]), (share, npb)
+                assert np.array_equal(gx.search(Q, K=10, nprobe=npb)[0], oi)
+    finally:
+        m.mrq_debug_set(gx.h, "probe_share", 1)
+        m.mrq_debug_set(gx.h, "dump_dis", 0)
+
+
 def test_head_sketch_prefilter_exact(case):
     """The int8 head-sketch pre-pass of the stage-2 gather (LOOSE)
     prunes with a proven lower bound of the canonical HEAD, so F2 (as a set,
