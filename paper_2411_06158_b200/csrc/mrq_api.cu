@@ -644,10 +644,27 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
 
     // ---- a3: per-(query, list) quantization into bit-planes, rows [q0, q0 + nr)
     nvtx.stage("a3 quantization");
+    // list-major scan: the (query, list) pairs grouped by list,
+    // built on the side stream beside the quantizer
+    const bool use_lm = ix->scan_lm && mode != 2 && W <= 4 && !ix->dbg_dump_dis;
+    const int lm_qg = ix->scan_lm == 2 ? 8 : ix->lm_qg;   // the tensor-core form takes 8 pairs (one MMA n-block)
+    LmScratch lms;
+    memset(&lms, 0, sizeof lms);
+    if (use_lm) {
+        SCR("lm_lcnt", uint32_t, k, lms.lcnt);
+        SCR("lm_lfill", uint32_t, k, lms.lfill);
+        SCR("lm_loff", uint32_t, k + 1, lms.loff);
+        SCR("lm_upre", uint32_t, k + 1, lms.upre);
+        SCR("lm_pairs", uint32_t, std::max<int64_t>(nq * np, 1), lms.pairs);
+        SCR("lm_unit", uint32_t, 1, lms.unit_ctr);
+        // units of list c = tiles_c ceil(n_c / qg) <= tiles_c n_c: at most ceil(max_list / 128) per pair
+        SCR("lm_units", uint32_t, std::max<int64_t>(nq * np * (int64_t)((ix->max_list + 127) / 128), 1), lms.unit_list);
+    }
     auto fork_offsets = [&]() -> int {   // F1 segment offsets of all nq queries on the side stream
         MRQ_CUDA_TRY(cudaEventRecord(ix->ev_fork[1], st));
         MRQ_CUDA_TRY(cudaStreamWaitEvent(ix->side, ix->ev_fork[1], 0));
         if (qkey && fshard) launch_qorder(qkey, nq, qorder, ix->side);
+        if (use_lm) TRY(mrq_lm_build(probe, nq, np, k, ix->list_size, lm_qg, lms, ix->side));
         k_cand_count<<<(unsigned)((nq + 255) / 256), 256, 0, ix->side>>>(probe, nq, np, ix->list_size, cand_cnt);
         k_exclusive_scan<<<1, 1024, 0, ix->side>>>(cand_cnt, nq, f1_off);
         MRQ_CUDA_TRY(cudaEventRecord(ix->ev_fork[2], ix->side));
@@ -797,6 +814,13 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
             a.hq = ix->hq; a.hs = ix->hs; a.qsk_b = qsk_b; a.qsk_c = qsk_c; a.qr2 = qr2;
             a.dq = ix->dq; a.surv_cnt = surv_cnt;   // NULL: plain F1 (no fused sketch test)
             if (surv_cnt) a.smem = mrq_scan_smem_sk(np, W, ix->dq);
+            a.lm = use_lm ? ix->scan_lm : 0; a.k = k; a.qg = lm_qg;
+            a.pairs = lms.pairs; a.loff = lms.loff; a.upre = lms.upre; a.unit_ctr = lms.unit_ctr;
+            a.unit_list = lms.unit_list;
+            if (use_lm) {   // the list-major scan accumulates the per-query counters atomically
+                MRQ_CUDA_TRY(cudaMemsetAsync(f1_cnt, 0, (size_t)nq * 4, st));
+                if (surv_cnt) MRQ_CUDA_TRY(cudaMemsetAsync(surv_cnt, 0, (size_t)nq * 4, st));
+            }
             if (mode == 2)
                 launch_f1_all(probe, nq, np, ix->list_off, ix->list_size, f1_off, f1_cnt, f1_pos, st);
             else
@@ -1169,6 +1193,18 @@ extern "C" int mrq_debug_set(mrq_index *ix, const char *name, int64_t value)
     }
     if (std::string(name) == "fuse_topk") {   // stage 2 + re-rank + top-K in one kernel (default 1)
         ix->fuse_topk_on = value ? 1 : 0;
+        return MRQ_OK;
+    }
+    if (std::string(name) == "scan_lm") {   // list-major code scan: 0 off, 1 CUDA-core, 2 tensor-core S (d <= 128)
+        ix->scan_lm = value < 0 ? 0 : (value > 2 ? 2 : (int)value);
+        return MRQ_OK;
+    }
+    if (std::string(name) == "scan_lm_qg") {   // pairs of a list per list-major work unit (default 16)
+        if (value < 1 || value > 4096) {
+            mrq_set_error("scan_lm_qg must be in [1, 4096]");
+            return MRQ_EINVAL;
+        }
+        ix->lm_qg = (int)value;
         return MRQ_OK;
     }
     if (std::string(name) == "probe_share") {   // the fused probe's parts share their bounds (default 1)

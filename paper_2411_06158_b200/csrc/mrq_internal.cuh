@@ -117,6 +117,8 @@ struct mrq_index {
     int probe_capp = 256;                      // mrq_debug_set("probe_capp"): fused-probe candidate buffer per part
     int probe_share = 1;                       // mrq_debug_set("probe_share"): parts of a row share their bound
     int fuse_topk_on = 1;                      // mrq_debug_set("fuse_topk"): k_head_topk where it applies
+    int scan_lm = 0;                           // mrq_debug_set("scan_lm"): list-major scan (1 CUDA-core, 2 tensor-core S; d <= 128)
+    int lm_qg = 16;                            // mrq_debug_set("scan_lm_qg"): pairs per list-major work unit
     uint64_t cand_budget = (uint64_t)8 << 30;  // mrq_debug_set("cand_budget_mb"): host-bound scratch budget
     int smem_optin = 227 * 1024;               // max dynamic shared memory per block (opt-in)
     uint64_t scratch_gen = 0;                  // bumped whenever a scratch buffer is reallocated (graph key)

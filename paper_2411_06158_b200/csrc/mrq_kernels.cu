@@ -145,6 +145,7 @@ __device__ void mrq_head_sketch(const double *y, double ynorm_bound, float xr2, 
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     const float s = mx > 0.0 ? __double2float_ru(mx / 127.0) : 0.f;
     double e2 = 0.0;
+    int aa = 0;   // <a, a> (<= 512 * 127^2 < 2^24: exact in the fp32 record)
     for (int i = lane; i < dq; i += 32) {
         int a = 0;
         if (i < d && s > 0.f) {
@@ -156,15 +157,17 @@ __device__ void mrq_head_sketch(const double *y, double ynorm_bound, float xr2, 
             e2 = e2 + y[i] * y[i];
         }
         out[i] = (uint8_t)(int8_t)a;
+        aa += a * a;
     }
     for (int o = 16; o > 0; o >>= 1) e2 = e2 + __shfl_xor_sync(0xffffffffu, e2, o);
+    for (int o = 16; o > 0; o >>= 1) aa += __shfl_xor_sync(0xffffffffu, aa, o);
     if (lane == 0) {
         // margins: the fp64 residual e per element <= 2^-50 mx; the matvec
         // y_j = sum_i R_ji (h_i - c_i) (d terms, |R_j| = 1) per element <=
         // (d + 2) 2^-53 ||h - c|| <= (d + 2) 2^-52 ynorm_bound
         const double E = __dsqrt_ru(e2) * (1.0 + 0x1p-40) + 0x1p-49 * mx * sqrt((double)d) +
                          0x1p-50 * (double)(d + 2) * sqrt((double)d) * ynorm_bound;
-        *se = make_float4(s, __double2float_ru(E), xr2, 0.f);   // (s, E, ||x_r||^2, -)
+        *se = make_float4(s, __double2float_ru(E), xr2, (float)aa);   // (s, E, ||x_r||^2, <a,a>)
     }
     __syncwarp();
 }
@@ -622,7 +625,7 @@ __global__ void k_exclusive_scan(const uint64_t *__restrict__ in, int64_t n, uin
 // (count surv_cnt) for the canonical fp32 head gather of k_head_b.
 struct ScanSketch {
     const uint8_t *hq;      // [npad][dq] int8 sketch rows
-    const float4 *hs;       // [npad] (s, E, ||x_r||^2, -): one 16-byte gather
+    const float4 *hs;       // [npad] (s, E, ||x_r||^2, <a,a>): one 16-byte gather
     const uint8_t *qsk_b;   // [nq][np][dq] query-side int8 rows
     const double *qsk_c;    // [nq][np][4] (t, F, <b,b>, 0)
     const double *qr2;      // [nq]
@@ -643,17 +646,13 @@ struct ScanSketch {
 // in HEAD under round-to-nearest, so a candidate whose bound already fails
 // the F2 test (dlo - eps_r >= tau1) is not in F2: the canonical test decides
 // it the same way.  keep = true: the candidate must be gathered.
-// <a,b> and <a,a> over one 16-byte chunk of packed int8:
-__device__ __forceinline__ void mrq_dp4a_chunk(const uint4 &u, const uint4 &b, int &ab, int &aa)
+// <a,b> over one 16-byte chunk of packed int8 (<a,a> is the record's fourth field)
+__device__ __forceinline__ void mrq_dp4a_ab(const uint4 &u, const uint4 &b, int &ab)
 {
     ab = __dp4a((int)u.x, (int)b.x, ab);
     ab = __dp4a((int)u.y, (int)b.y, ab);
     ab = __dp4a((int)u.z, (int)b.z, ab);
     ab = __dp4a((int)u.w, (int)b.w, ab);
-    aa = __dp4a((int)u.x, (int)u.x, aa);
-    aa = __dp4a((int)u.y, (int)u.y, aa);
-    aa = __dp4a((int)u.z, (int)u.z, aa);
-    aa = __dp4a((int)u.w, (int)u.w, aa);
 }
 __device__ __forceinline__ bool mrq_sketch_decide(int ab, int aa, float4 se, const double *bc, double qr2, double eps_r,
                                                   double tau1)
@@ -793,8 +792,10 @@ __global__ void __launch_bounds__(MRQ_SCAN_THREADS, (W <= 3 ? 1024 / MRQ_SCAN_TH
             for (int u = 0; u < 2; u++)
 #pragma unroll
                 for (int c = 0; c < 2; c++)
-                    if (w0 + c < nw) mrq_dp4a_chunk(r[u][c], ((const uint4 *)(skb_s + pp[u] * sk.dq))[w0 + c], ab[u], aa[u]);
+                    if (w0 + c < nw) mrq_dp4a_ab(r[u][c], ((const uint4 *)(skb_s + pp[u] * sk.dq))[w0 + c], ab[u]);
         }
+#pragma unroll
+        for (int u = 0; u < 2; u++) aa[u] = (int)se[u].w;
 #pragma unroll
         for (int u = 0; u < 2; u++) {
             const bool keep = in[u] && mrq_sketch_decide(ab[u], aa[u], se[u], skc_s + pp[u] * 3, qr2, eps_r, tau0);
@@ -898,6 +899,610 @@ __global__ void __launch_bounds__(MRQ_SCAN_THREADS, (W <= 3 ? 1024 / MRQ_SCAN_TH
     }
 }
 
+// ------------------------------------------------------------ list-major scan
+// The same F1 test (and the same fused sketch test) as k_scan, with the work
+// grouped by LIST instead of by query (DESIGN.md §5 "list-major scan"): in a
+// batch many queries probe the same list (Deep-shaped: 160k (query, list)
+// pairs over 16384 lists), so a warp loads a 128-slot tile of a list's code
+// words and factors once, keeps them in registers (factors widened to fp64
+// once), and evaluates them against every query of its chunk of the list's
+// pairs.  The code stream is read about once per list instead of once per
+// pair, and the per-pair work is the AND+POPC + fp64 epilogue only.  Every
+// decision is the canonical one (mrq_pop_S + the fp64 LB1 in the oracle's
+// order), so F1 and the sketch survivors are the same sets as k_scan's; only
+// their order in a query's segment differs (appends are atomic per query).
+
+// pairs per list
+__global__ void k_lm_count(const uint32_t *__restrict__ probe, int64_t npairs, const uint32_t *__restrict__ list_size,
+                           uint32_t *__restrict__ lcnt)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= npairs) return;
+    const uint32_t c = probe[i];
+    if (c != 0xFFFFFFFFu && list_size[c] > 0) atomicAdd(&lcnt[c], 1u);
+}
+
+// one block: exclusive prefixes of the pair counts (loff) and of the units
+// (upre) over the k lists; clears the scatter fill counters and the unit counter
+__global__ void __launch_bounds__(1024) k_lm_offsets(const uint32_t *__restrict__ lcnt,
+                                                     const uint32_t *__restrict__ list_size, int k, int qg,
+                                                     uint32_t *__restrict__ lfill, uint32_t *__restrict__ loff,
+                                                     uint32_t *__restrict__ upre, uint32_t *__restrict__ unit_ctr)
+{
+    __shared__ uint32_t wsum[2][32];
+    const int per = (k + blockDim.x - 1) / blockDim.x;
+    const int c0 = threadIdx.x * per, c1 = min(k, c0 + per);
+    uint32_t sp = 0, su = 0;
+#pragma unroll 16
+    for (int c = c0; c < c1; c++) {   // (unrolled: the loads of a thread's range are in flight together)
+        const uint32_t n = lcnt[c];
+        sp += n;
+        su += ((list_size[c] + 127) / 128) * ((n + qg - 1) / qg);
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t xp = sp, xu = su;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t yp = __shfl_up_sync(0xffffffffu, xp, o), yu = __shfl_up_sync(0xffffffffu, xu, o);
+        if (lane >= o) {
+            xp += yp;
+            xu += yu;
+        }
+    }
+    if (lane == 31) {
+        wsum[0][warp] = xp;
+        wsum[1][warp] = xu;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        const int nw = blockDim.x >> 5;
+        uint32_t a = lane < nw ? wsum[0][lane] : 0u, b = lane < nw ? wsum[1][lane] : 0u;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t ya = __shfl_up_sync(0xffffffffu, a, o), yb = __shfl_up_sync(0xffffffffu, b, o);
+            if (lane >= o) {
+                a += ya;
+                b += yb;
+            }
+        }
+        wsum[0][lane] = a;   // inclusive warp prefixes
+        wsum[1][lane] = b;
+    }
+    __syncthreads();
+    uint32_t op = xp - sp + (warp ? wsum[0][warp - 1] : 0u), ou = xu - su + (warp ? wsum[1][warp - 1] : 0u);
+#pragma unroll 16
+    for (int c = c0; c < c1; c++) {
+        const uint32_t n = lcnt[c];
+        loff[c] = op;
+        upre[c] = ou;
+        lfill[c] = 0u;
+        op += n;
+        ou += ((list_size[c] + 127) / 128) * ((n + qg - 1) / qg);
+    }
+    if (threadIdx.x == blockDim.x - 1) {
+        loff[k] = op;
+        upre[k] = ou;
+        *unit_ctr = 0u;
+    }
+}
+
+__global__ void k_lm_scatter(const uint32_t *__restrict__ probe, int64_t npairs, const uint32_t *__restrict__ list_size,
+                             const uint32_t *__restrict__ loff, uint32_t *__restrict__ lfill, uint32_t *__restrict__ pairs)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= npairs) return;
+    const uint32_t c = probe[i];
+    if (c != 0xFFFFFFFFu && list_size[c] > 0) pairs[loff[c] + atomicAdd(&lfill[c], 1u)] = (uint32_t)i;
+}
+
+// unit -> list table (warp per list)
+__global__ void k_lm_units(const uint32_t *__restrict__ upre, int k, uint32_t *__restrict__ unit_list)
+{
+    const int c = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    if (c >= k) return;
+    const uint32_t e = upre[c + 1];
+    for (uint32_t u = upre[c] + (threadIdx.x & 31); u < e; u += 32) unit_list[u] = (uint32_t)c;
+}
+
+int mrq_lm_build(const uint32_t *probe, int64_t nq, int np, int k, const uint32_t *list_size, int qg,
+                 const LmScratch &s, cudaStream_t st)
+{
+    const int64_t npairs = nq * np;
+    MRQ_CUDA_TRY(cudaMemsetAsync(s.lcnt, 0, (size_t)k * 4, st));
+    if (npairs > 0)
+        k_lm_count<<<(unsigned)((npairs + 255) / 256), 256, 0, st>>>(probe, npairs, list_size, s.lcnt);
+    k_lm_offsets<<<1, 1024, 0, st>>>(s.lcnt, list_size, k, qg, s.lfill, s.loff, s.upre, s.unit_ctr);
+    if (npairs > 0)
+        k_lm_scatter<<<(unsigned)((npairs + 255) / 256), 256, 0, st>>>(probe, npairs, list_size, s.loff, s.lfill,
+                                                                     s.pairs);
+    k_lm_units<<<(unsigned)((k + 7) / 8), 256, 0, st>>>(s.upre, k, s.unit_list);
+    MRQ_CUDA_TRY(cudaGetLastError());
+    return MRQ_OK;
+}
+
+// the canonical fp64 LB1 from (pop, S) with the factors already widened
+// (the same operations as mrq_lb1_ps: (double)f is exact)
+__device__ __forceinline__ double mrq_lb1_psd(int pop, int S, const double *qc, double isd, double eps_r, double f1,
+                                              double f2, double f3)
+{
+    const double t1 = qc[0] * i2d_exact(pop);
+    const double t2 = qc[1] * i2d_exact(S);
+    const double t4 = (t1 + t2) - qc[2];
+    const double ip = t4 * isd;
+    const double t5 = f1 + qc[3];
+    const double t6 = f2 * ip;
+    const double dis = t5 - 2.0 * t6;
+    return (dis - qc[4] * f3) - eps_r;
+}
+
+#define MRQ_LM_RING 256   // per-warp ring of F1 entries awaiting the sketch test (power of 2, >= 64 + 128)
+#ifndef MRQ_LM_MINB
+#define MRQ_LM_MINB 6
+#endif
+template <int W, bool SK>
+__global__ void __launch_bounds__(128, MRQ_LM_MINB) k_scan_lm(LaunchScan a)
+{
+    __shared__ uint2 ring[SK ? 4 * MRQ_LM_RING : 1];   // (slot, pair)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned FULL = 0xffffffffu;
+    const uint32_t lt = (1u << lane) - 1u;
+    const uint32_t np = (uint32_t)a.np;
+    const double inv_np = 1.0 / (double)a.np;
+    auto qof = [&](uint32_t pair) -> uint32_t {   // pair / np: fp64 estimate (off by at most one), one correction
+        uint32_t q = (uint32_t)((double)pair * inv_np);
+        const int32_t r = (int32_t)(pair - q * np);
+        return r < 0 ? q - 1 : (r >= (int32_t)np ? q + 1 : q);
+    };
+    uint2 *wr = ring + warp * MRQ_LM_RING;
+    uint32_t rh = 0, rt = 0;   // ring head / tail (warp-uniform, monotone)
+    const uint32_t nunits = a.upre[a.k];
+    // sketch test of ring entries [h0, h0 + n), n <= 64: two per lane, all
+    // rows in flight before any arithmetic; survivors appended to their
+    // query's segment (one atomic per query present in the batch)
+    auto drain = [&](uint32_t h0, uint32_t n) {
+        const int nw = a.dq / 16;
+        uint32_t slot[2], pair[2], q[2];
+        bool in[2];
+        float4 se[2];
+        int ab[2] = {0, 0};
+#pragma unroll
+        for (int u = 0; u < 2; u++) {
+            const uint32_t i = u * 32 + lane;
+            in[u] = i < n;
+            const uint2 e = in[u] ? wr[(h0 + i) & (MRQ_LM_RING - 1)] : make_uint2(0u, 0u);
+            slot[u] = e.x;
+            pair[u] = e.y;
+            q[u] = qof(e.y);
+            se[u] = in[u] ? a.hs[slot[u]] : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        for (int w0 = 0; w0 < nw; w0 += 2) {
+            uint4 r[2][2], b[2][2];
+#pragma unroll
+            for (int u = 0; u < 2; u++)
+#pragma unroll
+                for (int c = 0; c < 2; c++) {
+                    const bool ok = in[u] && w0 + c < nw;
+                    r[u][c] = ok ? __ldg((const uint4 *)(a.hq + (int64_t)slot[u] * a.dq) + w0 + c) : make_uint4(0u, 0u, 0u, 0u);
+                    b[u][c] = ok ? __ldg((const uint4 *)(a.qsk_b + (int64_t)pair[u] * a.dq) + w0 + c)
+                                 : make_uint4(0u, 0u, 0u, 0u);
+                }
+#pragma unroll
+            for (int u = 0; u < 2; u++)
+#pragma unroll
+                for (int c = 0; c < 2; c++)
+                    if (w0 + c < nw) mrq_dp4a_ab(r[u][c], b[u][c], ab[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < 2; u++) {
+            bool keep = false;
+            if (in[u]) {
+                const double *g = a.qsk_c + (int64_t)pair[u] * 4;
+                const double bc[3] = {__ldg(g), __ldg(g + 1), __ldg(g + 2)};
+                keep = mrq_sketch_decide(ab[u], (int)se[u].w, se[u], bc, __ldg(a.qr2 + q[u]), __ldg(a.eps_r + q[u]),
+                                         __ldg(a.tau0 + q[u]));
+            }
+            if (__ballot_sync(FULL, keep)) {
+                const unsigned grp = __match_any_sync(FULL, keep ? q[u] : 0xFFFFFFFFu);
+                if (keep) {
+                    const int leader = __ffs(grp) - 1;
+                    uint32_t o = 0;
+                    if (lane == leader) o = atomicAdd(&a.surv_cnt[q[u]], (uint32_t)__popc(grp));
+                    o = __shfl_sync(grp, o, leader) + __popc(grp & lt);
+                    MRQ_ASSERT(o < (uint32_t)(a.f1_off[q[u] + 1] - a.f1_off[q[u]]) && slot[u] < a.npad);
+                    a.f1_pos[a.f1_off[q[u]] + o] = slot[u];
+                }
+            }
+        }
+    };
+    for (;;) {
+        uint32_t u = 0;
+        if (lane == 0) u = atomicAdd(a.unit_ctr, 1u);
+        u = __shfl_sync(FULL, u, 0);
+        if (u >= nunits) break;
+        const int c = (int)__ldg(a.unit_list + u);
+        const uint32_t pb = __ldg(a.loff + c), pe = __ldg(a.loff + c + 1);
+        const uint32_t nch = (pe - pb + a.qg - 1) / a.qg;
+        const uint32_t local = u - __ldg(a.upre + c);
+        const uint32_t tile = local / nch, ch = local - tile * nch;
+        const uint32_t lst = __ldg(a.list_off + c), lend = lst + __ldg(a.list_size + c);
+        const uint32_t b = lst + tile * 128 + lane * 4;
+        uint4 cw[W];
+#pragma unroll
+        for (int w = 0; w < W; w++) cw[w] = __ldg((const uint4 *)(a.codes + (int64_t)w * a.npad + b));
+        const float4 x1 = __ldg((const float4 *)(a.f1 + b)), x2 = __ldg((const float4 *)(a.f2 + b)),
+                     x3 = __ldg((const float4 *)(a.f3 + b));
+        const float d1[4] = {x1.x, x1.y, x1.z, x1.w}, d2[4] = {x2.x, x2.y, x2.z, x2.w},
+                    d3[4] = {x3.x, x3.y, x3.z, x3.w};
+        bool valid[4];
+#pragma unroll
+        for (int r = 0; r < 4; r++) valid[r] = b + r < lend;
+        const uint32_t j1 = min(pe, pb + (ch + 1) * a.qg);
+        for (uint32_t j = pb + ch * a.qg; j < j1; j++) {
+            const uint32_t pair = __ldg(a.pairs + j);
+            const uint32_t q = qof(pair);
+            uint32_t pl[MRQ_BQ * W];
+            {
+                const uint4 *g = (const uint4 *)(a.planes + (int64_t)pair * (MRQ_BQ * W));
+#pragma unroll
+                for (int i = 0; i < W; i++) {
+                    const uint4 v = __ldg(g + i);
+                    pl[4 * i] = v.x;
+                    pl[4 * i + 1] = v.y;
+                    pl[4 * i + 2] = v.z;
+                    pl[4 * i + 3] = v.w;
+                }
+            }
+            double qc[5];
+            {
+                const double2 *g = (const double2 *)(a.qconst + (int64_t)pair * 8);
+                const double2 v0 = __ldg(g), v1 = __ldg(g + 1), v2 = __ldg(g + 2);
+                qc[0] = v0.x; qc[1] = v0.y; qc[2] = v1.x; qc[3] = v1.y; qc[4] = v2.x;
+            }
+            const double eps_r = __ldg(a.eps_r + q), tau0 = __ldg(a.tau0 + q);
+            bool fl[4];
+#pragma unroll
+            for (int r = 0; r < 4; r++) {
+                uint32_t code[W];
+#pragma unroll
+                for (int w = 0; w < W; w++) code[w] = r == 0 ? cw[w].x : r == 1 ? cw[w].y : r == 2 ? cw[w].z : cw[w].w;
+                int pop, S;
+                mrq_pop_S<W>(code, pl, pop, S);
+                fl[r] = valid[r] && (mrq_lb1_psd(pop, S, qc, a.isd, eps_r, d1[r], d2[r], d3[r]) < tau0);
+            }
+            const unsigned b0 = __ballot_sync(FULL, fl[0]), b1 = __ballot_sync(FULL, fl[1]);
+            const unsigned b2 = __ballot_sync(FULL, fl[2]), b3 = __ballot_sync(FULL, fl[3]);
+            const int n0 = __popc(b0), n1 = __popc(b1), n2 = __popc(b2), n3 = __popc(b3);
+            const int tot = n0 + n1 + n2 + n3;
+            if (!tot) continue;
+            uint32_t wb;
+            if (SK) {
+                if (lane == 0) atomicAdd(&a.f1_cnt[q], (uint32_t)tot);   // F1 is counted; members queue for the sketch
+                wb = rt;
+            } else {
+                wb = 0;
+                if (lane == 0) wb = atomicAdd(&a.f1_cnt[q], (uint32_t)tot);
+                wb = __shfl_sync(FULL, wb, 0);
+            }
+            const uint32_t o0 = wb + __popc(b0 & lt), o1 = wb + n0 + __popc(b1 & lt);
+            const uint32_t o2 = wb + n0 + n1 + __popc(b2 & lt), o3 = wb + n0 + n1 + n2 + __popc(b3 & lt);
+            if (SK) {
+                if (fl[0]) wr[o0 & (MRQ_LM_RING - 1)] = make_uint2(b, pair);
+                if (fl[1]) wr[o1 & (MRQ_LM_RING - 1)] = make_uint2(b + 1, pair);
+                if (fl[2]) wr[o2 & (MRQ_LM_RING - 1)] = make_uint2(b + 2, pair);
+                if (fl[3]) wr[o3 & (MRQ_LM_RING - 1)] = make_uint2(b + 3, pair);
+                rt += tot;
+                __syncwarp();
+                while (rt - rh >= 64) {
+                    drain(rh, 64);
+                    rh += 64;
+                }
+                __syncwarp();
+            } else {
+                uint32_t *out = a.f1_pos + a.f1_off[q];
+                MRQ_ASSERT(wb + tot <= (uint32_t)(a.f1_off[q + 1] - a.f1_off[q]));
+                if (fl[0]) out[o0] = b;
+                if (fl[1]) out[o1] = b + 1;
+                if (fl[2]) out[o2] = b + 2;
+                if (fl[3]) out[o3] = b + 3;
+            }
+        }
+    }
+    if (SK) {
+        __syncwarp();
+        while (rt != rh) {
+            const uint32_t n = min(64u, rt - rh);
+            drain(rh, n);
+            rh += n;
+        }
+    }
+}
+
+// ------------------------------------------------- list-major scan, tensor-core S
+// Work unit = (list, 128-slot tile, chunk of <= 8 of the list's pairs).  The
+// integer inner products are dense int8 contractions in this layout, so they
+// run on the tensor cores (mma.sync m16n8k32 s8 -> s32, exact):
+//   S[slot][pair]  = sum_i code_i(slot) * level_i(pair)   (codes as 0/1 bytes,
+//                    levels 0..15 from the query's 4 bit-planes; = the popc form)
+//   AB[slot][pair] = <a(slot), b(pair)>                     (SK: head-sketch rows)
+// written to the warp's shared memory; then lanes take 4 slots each and run
+// the canonical fp64 LB1 (mrq_lb1_ps) per pair, and the F1 entries are
+// sketch-tested from AB (mrq_sketch_decide) in compacted batches of 32.
+#define MRQ_TC_ROW 132                  // shared row stride (ints) of S / AB: conflict-free fragment stores
+#ifndef MRQ_TC_MINB
+#define MRQ_TC_MINB 5
+#endif
+__device__ __forceinline__ uint32_t nib2bytes(uint32_t x)   // 4 low bits -> 4 bytes of 0/1
+{
+    return ((x & 0xFu) * 0x00204081u) & 0x01010101u;
+}
+__device__ __forceinline__ void mma_s8(int (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                       uint32_t b1)
+{
+    asm volatile("mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                 "{%0,%1,%2,%3};\n"
+                 : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+                 : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+template <int W, bool SK>
+__global__ void __launch_bounds__(128, MRQ_TC_MINB) k_scan_tc(LaunchScan a)
+{
+    constexpr int KQ = 2 * W;   // sketch k-steps of 32 bytes: dq <= 32 W bytes (dq = d rounded up to 16)
+    __shared__ __align__(16) int s_S[4][8 * MRQ_TC_ROW];
+    __shared__ __align__(16) int s_AB[SK ? 4 : 1][SK ? 8 * MRQ_TC_ROW : 1];
+    __shared__ __align__(16) uint32_t s_code[4][W * 128];     // the tile's code words (word-major)
+    __shared__ __align__(16) double s_pc[4][8][12];            // per pair: qc[0..4], eps_r, tau0, t, F, B, qr2, -
+    __shared__ uint32_t s_pq[4][8][2];                         // per pair: (pair, q)
+    __shared__ uint16_t s_ring[SK ? 4 : 1][SK ? 256 : 1];      // F1 entries: slot in the tile | pair index << 8
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const unsigned FULL = 0xffffffffu;
+    const uint32_t lt = (1u << lane) - 1u;
+    const uint32_t np = (uint32_t)a.np;
+    const double inv_np = 1.0 / (double)a.np;
+    int *sS = s_S[warp];
+    int *sAB = s_AB[SK ? warp : 0];
+    uint32_t *sC = s_code[warp];
+    uint16_t *ring = s_ring[SK ? warp : 0];
+    const uint32_t nunits = a.upre[a.k];
+    const int dq = a.dq;
+    uint32_t u_next = 0;
+    if (lane == 0) u_next = atomicAdd(a.unit_ctr, 1u);
+    u_next = __shfl_sync(FULL, u_next, 0);
+    for (;;) {
+        const uint32_t u = u_next;
+        if (u >= nunits) break;
+        if (lane == 0) u_next = atomicAdd(a.unit_ctr, 1u);   // the next unit, fetched during this one
+        const int c = (int)__ldg(a.unit_list + u);
+        const uint32_t pb = __ldg(a.loff + c), pe = __ldg(a.loff + c + 1);
+        const uint32_t nch = (pe - pb + 7) / 8;
+        const uint32_t local = u - __ldg(a.upre + c);
+        const uint32_t tile = local / nch, ch = local - tile * nch;
+        const uint32_t lst = __ldg(a.list_off + c), lend = lst + __ldg(a.list_size + c);
+        const uint32_t tb = lst + tile * 128;
+        const uint32_t j0 = pb + ch * 8;
+        const int npc = (int)min(8u, pe - j0);   // pairs in this chunk
+        const uint32_t b = tb + lane * 4;
+        // stage: the tile's code words (coalesced) and the chunk's per-pair constants
+        int pop[4];
+        {
+            uint4 cw[W];
+#pragma unroll
+            for (int w = 0; w < W; w++) {
+                cw[w] = __ldg((const uint4 *)(a.codes + (int64_t)w * a.npad + b));
+                *(uint4 *)(sC + w * 128 + lane * 4) = cw[w];
+            }
+#pragma unroll
+            for (int r = 0; r < 4; r++) {
+                int pc = 0;
+#pragma unroll
+                for (int w = 0; w < W; w++) pc += __popc(r == 0 ? cw[w].x : r == 1 ? cw[w].y : r == 2 ? cw[w].z : cw[w].w);
+                pop[r] = pc;
+            }
+        }
+        if (lane < npc) {
+            const uint32_t pair = __ldg(a.pairs + j0 + lane);
+            uint32_t q = (uint32_t)((double)pair * inv_np);   // pair / np (fp64 estimate, one correction)
+            const int32_t rr = (int32_t)(pair - q * np);
+            q = rr < 0 ? q - 1 : (rr >= (int32_t)np ? q + 1 : q);
+            s_pq[warp][lane][0] = pair;
+            s_pq[warp][lane][1] = q;
+            double *pc = s_pc[warp][lane];
+            const double2 *gq = (const double2 *)(a.qconst + (int64_t)pair * 8);
+            const double2 w0 = __ldg(gq), w1 = __ldg(gq + 1);
+            pc[0] = w0.x; pc[1] = w0.y; pc[2] = w1.x; pc[3] = w1.y; pc[4] = __ldg(a.qconst + (int64_t)pair * 8 + 4);
+            pc[5] = __ldg(a.eps_r + q);
+            pc[6] = __ldg(a.tau0 + q);
+            if (SK) {
+                const double *gs = a.qsk_c + (int64_t)pair * 4;
+                pc[7] = __ldg(gs); pc[8] = __ldg(gs + 1); pc[9] = __ldg(gs + 2);
+                pc[10] = __ldg(a.qr2 + q);
+            }
+        }
+        __syncwarp();
+        // ---- phase A: S (and AB) of the tile's 128 slots x the chunk's pairs on the tensor cores
+        {
+            const bool bval = g < npc;
+            const uint32_t pn = bval ? s_pq[warp][g][0] : 0u;   // B column g
+            uint32_t b1f[W][2];
+#pragma unroll
+            for (int kk = 0; kk < W; kk++) {
+                uint32_t x0 = 0, x1 = 0;
+                if (bval) {
+#pragma unroll
+                    for (int jb = 0; jb < MRQ_BQ; jb++) {
+                        const uint32_t w = __ldg(a.planes + (int64_t)pn * (MRQ_BQ * W) + jb * W + kk);
+                        x0 |= nib2bytes(w >> (4 * t)) << jb;
+                        x1 |= nib2bytes(w >> (16 + 4 * t)) << jb;
+                    }
+                }
+                b1f[kk][0] = x0;
+                b1f[kk][1] = x1;
+            }
+            uint32_t b2f[SK ? KQ : 1][2];
+            if (SK) {
+#pragma unroll
+                for (int kk = 0; kk < KQ; kk++) {
+                    const int k0 = kk * 32 + 4 * t;
+                    const uint8_t *row = a.qsk_b + (int64_t)pn * dq;
+                    b2f[kk][0] = (bval && k0 < dq) ? __ldg((const uint32_t *)(row + k0)) : 0u;
+                    b2f[kk][1] = (bval && k0 + 16 < dq) ? __ldg((const uint32_t *)(row + k0 + 16)) : 0u;
+                }
+            }
+#pragma unroll 4
+            for (int mt = 0; mt < 8; mt++) {
+                const int col = mt * 16 + g;
+                uint32_t ha[SK ? KQ : 1][4];
+                if (SK) {   // the sketch rows' fragments first: their loads overlap the code MMAs
+                    const uint8_t *h0 = a.hq + (int64_t)(tb + col) * dq, *h1 = h0 + 8 * dq;
+#pragma unroll
+                    for (int kk = 0; kk < KQ; kk++) {
+                        const int k0 = kk * 32 + 4 * t;
+                        const bool lo_ok = k0 < dq, hi_ok = k0 + 16 < dq;
+                        ha[kk][0] = lo_ok ? __ldg((const uint32_t *)(h0 + k0)) : 0u;
+                        ha[kk][1] = lo_ok ? __ldg((const uint32_t *)(h1 + k0)) : 0u;
+                        ha[kk][2] = hi_ok ? __ldg((const uint32_t *)(h0 + k0 + 16)) : 0u;
+                        ha[kk][3] = hi_ok ? __ldg((const uint32_t *)(h1 + k0 + 16)) : 0u;
+                    }
+                }
+                int acc[4] = {0, 0, 0, 0};
+#pragma unroll
+                for (int kk = 0; kk < W; kk++) {
+                    const uint32_t c0 = sC[kk * 128 + col], c1 = sC[kk * 128 + col + 8];
+                    mma_s8(acc, nib2bytes(c0 >> (4 * t)), nib2bytes(c1 >> (4 * t)), nib2bytes(c0 >> (16 + 4 * t)),
+                           nib2bytes(c1 >> (16 + 4 * t)), b1f[kk][0], b1f[kk][1]);
+                }
+                sS[(2 * t) * MRQ_TC_ROW + col] = acc[0];
+                sS[(2 * t + 1) * MRQ_TC_ROW + col] = acc[1];
+                sS[(2 * t) * MRQ_TC_ROW + col + 8] = acc[2];
+                sS[(2 * t + 1) * MRQ_TC_ROW + col + 8] = acc[3];
+                if (SK) {
+                    int ac2[4] = {0, 0, 0, 0};
+#pragma unroll
+                    for (int kk = 0; kk < KQ; kk++)
+                        if (kk * 32 < dq) mma_s8(ac2, ha[kk][0], ha[kk][1], ha[kk][2], ha[kk][3], b2f[kk][0], b2f[kk][1]);
+                    sAB[(2 * t) * MRQ_TC_ROW + col] = ac2[0];
+                    sAB[(2 * t + 1) * MRQ_TC_ROW + col] = ac2[1];
+                    sAB[(2 * t) * MRQ_TC_ROW + col + 8] = ac2[2];
+                    sAB[(2 * t + 1) * MRQ_TC_ROW + col + 8] = ac2[3];
+                }
+            }
+        }
+        __syncwarp();
+        // ---- phase B: lane-per-slot canonical LB1 for every pair of the chunk
+        const float4 x1 = __ldg((const float4 *)(a.f1 + b)), x2 = __ldg((const float4 *)(a.f2 + b)),
+                     x3 = __ldg((const float4 *)(a.f3 + b));
+        const float v1[4] = {x1.x, x1.y, x1.z, x1.w}, v2[4] = {x2.x, x2.y, x2.z, x2.w}, v3[4] = {x3.x, x3.y, x3.z, x3.w};
+        uint32_t rh = 0, rt = 0;   // SK: ring head / tail (warp-uniform; circular, < 256 pending)
+        // SK: sketch test of ring entries [rh, rh + n) (n <= 32, lane per entry) from AB; survivors appended
+        auto drain = [&](uint32_t n) {
+            const bool in = (uint32_t)lane < n;
+            const uint32_t e = in ? ring[(rh + lane) & 255u] : 0u;
+            const uint32_t sl = e & 0xFFu, j = e >> 8;
+            bool keep = false;
+            uint32_t q = 0;
+            if (in) {
+                q = s_pq[warp][j][1];
+                const double *pc = s_pc[warp][j];
+                const float4 se = a.hs[tb + sl];
+                keep = mrq_sketch_decide(sAB[j * MRQ_TC_ROW + sl], (int)se.w, se, pc + 7, pc[10], pc[5], pc[6]);
+            }
+            if (__ballot_sync(FULL, keep)) {
+                const unsigned grp = __match_any_sync(FULL, keep ? q : 0xFFFFFFFFu);
+                if (keep) {
+                    const int leader = __ffs(grp) - 1;
+                    uint32_t o = 0;
+                    if (lane == leader) o = atomicAdd(&a.surv_cnt[q], (uint32_t)__popc(grp));
+                    o = __shfl_sync(grp, o, leader) + __popc(grp & lt);
+                    MRQ_ASSERT(o < (uint32_t)(a.f1_off[q + 1] - a.f1_off[q]));
+                    a.f1_pos[a.f1_off[q] + o] = tb + sl;
+                }
+            }
+            rh += n;
+        };
+        for (int j = 0; j < npc; j++) {
+            const uint32_t q = s_pq[warp][j][1];
+            const double *pc = s_pc[warp][j];
+            const double qc[5] = {pc[0], pc[1], pc[2], pc[3], pc[4]};
+            const double eps_r = pc[5], tau0 = pc[6];
+            const int4 Sv = *(const int4 *)(sS + j * MRQ_TC_ROW + lane * 4);
+            const int Sr[4] = {Sv.x, Sv.y, Sv.z, Sv.w};
+            bool fl[4];
+#pragma unroll
+            for (int r = 0; r < 4; r++) {
+                double dis;
+                fl[r] = (b + r < lend) && (mrq_lb1_ps(pop[r], Sr[r], qc, a.isd, eps_r, v1[r], v2[r], v3[r], &dis) < tau0);
+            }
+            const unsigned b0 = __ballot_sync(FULL, fl[0]), b1 = __ballot_sync(FULL, fl[1]);
+            const unsigned b2 = __ballot_sync(FULL, fl[2]), b3 = __ballot_sync(FULL, fl[3]);
+            const int n0 = __popc(b0), n1 = __popc(b1), n2 = __popc(b2), n3 = __popc(b3);
+            const int tot = n0 + n1 + n2 + n3;
+            if (!tot) continue;
+            uint32_t wb;
+            if (SK) {
+                if (lane == 0) atomicAdd(&a.f1_cnt[q], (uint32_t)tot);   // F1 is counted; members queue for the sketch
+                wb = rt;
+            } else {
+                wb = 0;
+                if (lane == 0) wb = atomicAdd(&a.f1_cnt[q], (uint32_t)tot);
+                wb = __shfl_sync(FULL, wb, 0);
+            }
+            const uint32_t o0 = wb + __popc(b0 & lt), o1 = wb + n0 + __popc(b1 & lt);
+            const uint32_t o2 = wb + n0 + n1 + __popc(b2 & lt), o3 = wb + n0 + n1 + n2 + __popc(b3 & lt);
+            if (SK) {
+                const uint16_t jj = (uint16_t)(j << 8), sl = (uint16_t)(lane * 4);
+                if (fl[0]) ring[o0 & 255u] = jj | sl;
+                if (fl[1]) ring[o1 & 255u] = jj | (sl + 1);
+                if (fl[2]) ring[o2 & 255u] = jj | (sl + 2);
+                if (fl[3]) ring[o3 & 255u] = jj | (sl + 3);
+                rt += tot;
+                __syncwarp();
+                while (rt - rh >= 32) drain(32);
+            } else {
+                uint32_t *out = a.f1_pos + a.f1_off[q];
+                MRQ_ASSERT(wb + tot <= (uint32_t)(a.f1_off[q + 1] - a.f1_off[q]));
+                if (fl[0]) out[o0] = b;
+                if (fl[1]) out[o1] = b + 1;
+                if (fl[2]) out[o2] = b + 2;
+                if (fl[3]) out[o3] = b + 3;
+            }
+        }
+        if (SK && rt != rh) drain(rt - rh);
+        u_next = __shfl_sync(FULL, u_next, 0);
+        __syncwarp();   // the next unit's staging overwrites this unit's shared tiles
+    }
+}
+
+template <int W, bool SK>
+static int launch_scan_tc_ws(const LaunchScan &a, cudaStream_t st)
+{
+    static int grid = 0;
+    if (!grid) {
+        int dev = 0, nsm = 0, per = 0;
+        MRQ_CUDA_TRY(cudaGetDevice(&dev));
+        MRQ_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        MRQ_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_scan_tc<W, SK>, 128, 0));
+        grid = nsm * std::max(per, 1);
+    }
+    k_scan_tc<W, SK><<<grid, 128, 0, st>>>(a);
+    MRQ_CUDA_TRY(cudaGetLastError());
+    return MRQ_OK;
+}
+
+template <int W, bool SK>
+static int launch_scan_lm_ws(const LaunchScan &a, cudaStream_t st)
+{
+    static int grid = 0;   // resident blocks of this instance on the device (one per process: one device type)
+    if (!grid) {
+        int dev = 0, nsm = 0, per = 0;
+        MRQ_CUDA_TRY(cudaGetDevice(&dev));
+        MRQ_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        MRQ_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_scan_lm<W, SK>, 128, 0));
+        grid = nsm * std::max(per, 1);
+    }
+    k_scan_lm<W, SK><<<grid, 128, 0, st>>>(a);
+    MRQ_CUDA_TRY(cudaGetLastError());
+    return MRQ_OK;
+}
+
 // mode EXACT (IVF*-restricted exact search, every probed candidate is
 // re-ranked): F1 = all of them, written in probe order then slot order
 // without evaluating any code (so any code length d works in this mode).
@@ -957,6 +1562,15 @@ static int launch_scan_ws(const LaunchScan &a, cudaStream_t st)
 template <int W>
 static int launch_scan_w(const LaunchScan &a, cudaStream_t st)
 {
+    if (a.lm) {
+        if (W > 4) {
+            mrq_set_error("list-major scan: W=%d > 4", W);
+            return MRQ_EINVAL;
+        }
+        constexpr int WL = W > 4 ? 1 : W;
+        if (a.lm == 2) return a.surv_cnt ? launch_scan_tc_ws<WL, true>(a, st) : launch_scan_tc_ws<WL, false>(a, st);
+        return a.surv_cnt ? launch_scan_lm_ws<WL, true>(a, st) : launch_scan_lm_ws<WL, false>(a, st);
+    }
     const bool dram = (uint64_t)a.npad * (4 * W + 12) > ((uint64_t)64 << 20);   // the stream cannot live in L2
     if (a.surv_cnt) return dram ? launch_scan_ws<W, true, 2>(a, st) : launch_scan_ws<W, true, 1>(a, st);
     return dram ? launch_scan_ws<W, false, 2>(a, st) : launch_scan_ws<W, false, 1>(a, st);

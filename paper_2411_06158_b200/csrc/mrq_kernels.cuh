@@ -83,7 +83,23 @@ struct LaunchScan {
     const double *qsk_c, *qr2;
     int dq;
     uint32_t *surv_cnt;
+    // list-major scan (lm != 0): the (query, probed list) pairs
+    // grouped by list (mrq_lm_build); the work units are (list, 128-slot tile,
+    // chunk of <= qg of the list's pairs), handed out by an atomic counter
+    int lm, k, qg;
+    const uint32_t *pairs, *loff, *upre, *unit_list;
+    uint32_t *unit_ctr;
 };
+
+// scratch of the list-major scan's pair grouping (all device, k + 1 / nq np entries)
+struct LmScratch {
+    uint32_t *lcnt, *lfill, *loff, *upre, *pairs, *unit_ctr;
+    uint32_t *unit_list;   // [units]: the list of each work unit
+};
+// pairs of list c: pairs[loff[c] .. loff[c + 1]) (pair = q np + p); units of
+// list c: upre[c] .. upre[c + 1) = ceil(size_c / 128) ceil(count_c / qg)
+int mrq_lm_build(const uint32_t *probe, int64_t nq, int np, int k, const uint32_t *list_size, int qg,
+                 const LmScratch &s, cudaStream_t st);
 
 // dynamic shared memory of k_scan: per probed list 5 constants, 4 W plane words, tile prefix / start / end
 inline size_t mrq_scan_smem(int np, int W)

@@ -527,3 +527,50 @@ def test_exact_mode_any_code_length():
             assert e.value.code == -1
     finally:
         gx.close()
+
+
+@pytest.mark.parametrize("lm,qg", [(2, 16), (1, 1), (1, 3), (1, 16)])
+def test_list_major_scan_equals_oracle(case, lm, qg):
+    """The list-major scan (the (query, list) pairs grouped by
+    list, a 128-slot tile evaluated against a chunk of its list's queries,
+    per-query appends by atomics; lm = 2: the integer inner products S and
+    <a, b> of a tile x 8 pairs on the tensor cores, lm = 1: AND+POPC on the
+    CUDA cores with qg pairs per unit) produces the oracle's F1 sets (TIGHT:
+    f1_pos holds all of F1), the oracle's F2 sets and top-K, and for LOOSE
+    sketch survivors between F2 and F1 -- the same as the query-major scan.
+    qg = 1 / 3 splits the lists' pairs over many work units."""
+    m, gx, ox, Q = case["m"], case["gx"], case["ox"], case["Q"]
+    nq, d = Q.shape[0], case["d"]
+    if d > 128:
+        pytest.skip("list-major scan is for d <= 128")
+    m.mrq_debug_set(gx.h, "dump_dis", 0)
+    m.mrq_debug_set(gx.h, "scan_lm_qg", qg)
+    try:
+        for npb in case["nprobe"]:
+            oi, od, ost, dp = ox.search(Q, K=10, nprobe=npb, tau_schedule="TIGHT", dump=True)
+            m.mrq_debug_set(gx.h, "scan_lm", lm)
+            gi, gd, gst = gx.search(Q, K=10, nprobe=npb, tau_schedule="TIGHT")
+            assert np.array_equal(gi, oi) and np.array_equal(gd.view(np.uint32), od.view(np.uint32)), npb
+            assert (gst.scanned, gst.stage1_pass, gst.stage2_pass) == (ost["scanned"], ost["f1"], ost["f2"])
+            f1 = _segments(gx, nq, "f1_cnt", "f1_pos")
+            for q in range(nq):
+                assert sorted(f1[q][0].tolist()) == sorted(dp["f1_ids"][q, :dp["f1_cnt"][q]].tolist()), (npb, q)
+            oi, od, ost, dp = ox.search(Q, K=10, nprobe=npb, tau_schedule="LOOSE", dump=True)
+            gi, gd, gst = gx.search(Q, K=10, nprobe=npb, tau_schedule="LOOSE")
+            assert np.array_equal(gi, oi) and np.array_equal(gd.view(np.uint32), od.view(np.uint32)), npb
+            assert (gst.stage1_pass, gst.stage2_pass, gst.exact) == (ost["f1"], ost["f2"], ost["exact"])
+            f2 = _segments(gx, nq, "f2_cnt", "f2_pos")
+            for q in range(nq):
+                assert sorted(f2[q][0].tolist()) == sorted(dp["f2_ids"][q, :dp["f2_cnt"][q]].tolist()), (npb, q)
+            if gst.sketch_pass != gst.stage1_pass:   # the sketch ran: survivors between F2 and F1
+                surv = gx.fetch("surv_cnt", "u32").astype(np.int64)
+                f1c = gx.fetch("f1_cnt", "u32").astype(np.int64)
+                assert np.all(surv <= f1c) and np.all(surv >= dp["f2_cnt"])
+                assert np.array_equal(f1c, dp["f1_cnt"].astype(np.int64))
+            m.mrq_debug_set(gx.h, "scan_lm", 0)
+            hi, hd, hst = gx.search(Q, K=10, nprobe=npb, tau_schedule="LOOSE")
+            assert np.array_equal(hi, gi) and np.array_equal(hd.view(np.uint32), gd.view(np.uint32))
+            assert (hst.stage1_pass, hst.stage2_pass, hst.exact) == (gst.stage1_pass, gst.stage2_pass, gst.exact)
+    finally:
+        m.mrq_debug_set(gx.h, "scan_lm", 0)
+        m.mrq_debug_set(gx.h, "scan_lm_qg", 16)
