@@ -479,12 +479,14 @@ def main():
             cpu = {"value": None, "unit": "queries/s", "cores": os.cpu_count(), "kind": "oracle",
                    "sample": "failed: %s" % e}
 
-    # 13 kernels per search (k_rowmat x2, k_qtail, k_qorder, k_probe_tc, k_probe_finish_w,
-    # k_quant_g, k_cand_count, k_exclusive_scan, k_seed_w, k_scan, k_head_b, k_topk_w), + k_stage2_w for
-    # TIGHT, k_head_topk in place of k_head_b + k_topk_w without S1 (K <= 32); sharded: + k_xmerge
-    # (S0, final), + k_xmerge (S1) + k_f2_w for TIGHT
+    # 12 kernels per search (k_rowmat x2, k_qtail, k_probe_tc, k_probe_finish_w, k_quant_g,
+    # k_cand_count, k_offsets_order, k_seed_w, k_scan, k_head_b, k_topk_w), + k_stage2_w for TIGHT,
+    # k_head_topk in place of k_head_b + k_topk_w without S1 (K <= 32); the order key from the projection
+    # (MRQ_DEBUG_SET qorder=1) has k_qorder and k_exclusive_scan in place of k_offsets_order (+1); sharded:
+    # + k_xmerge (S0, final), + k_xmerge (S1) + k_f2_w for TIGHT
     tight_sel = tau_sel == "TIGHT"
-    launches_per_step = (13 + (1 if tight_sel else 0) - (1 if fused_topk else 0) +
+    qorder_pc = "qorder=1" in os.environ.get("MRQ_DEBUG_SET", "")
+    launches_per_step = (12 + (1 if qorder_pc else 0) + (1 if tight_sel else 0) - (1 if fused_topk else 0) +
                          ((4 if tight_sel else 2) if world > 1 else 0))
     out = {
         "metric": METRIC,

@@ -9,6 +9,7 @@
 #include <functional>
 #include <cmath>
 #include <vector>
+#include <thread>
 
 #include <nvtx3/nvToolsExt.h>
 
@@ -206,6 +207,105 @@ static int read_build_file(const char *path, BuildFile &b, int32_t D_call, int32
 }
 
 // -------------------------------------------------------------------- load
+// Locality key of every list (the query processing order, DESIGN.md §5
+// "query order"): the centroids are grouped around G = k / 16 (<= 1024)
+// centres by a short host k-means (2 Lloyd steps from a strided start, on
+// their leading <= 64 principal coordinates; the assignment split over host
+// threads), the groups chained greedily (each followed by its nearest
+// unvisited group), and a list's key is its rank in (chain position, id)
+// order scaled to [0, MRQ_QO_KEYS).  What matters is that the groups are
+// fine and that neighbours in the chain are neighbours in space: measured on
+// the Deep-shaped probe lists, the lists a window of 1184 consecutive
+// queries touches (relative to their probes) fall 0.55 (given order) -> 0.32
+// (3 principal coordinates) -> 0.24 (128 groups) -> 0.15 (1024 groups).
+// Only the ORDER in which queries are processed depends on it -- never a
+// result.
+static inline float sqdist_f32(const float *x, const float *y, int n)
+{
+    float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    int i = 0;
+    for (; i + 8 <= n; i += 8)
+        for (int u = 0; u < 8; u++) {
+            const float t = x[i + u] - y[i + u];
+            a[u] += t * t;
+        }
+    float s = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+    for (; i < n; i++) {
+        const float t = x[i] - y[i];
+        s += t * t;
+    }
+    return s;
+}
+
+static std::vector<uint16_t> list_locality_keys(const std::vector<float> &C32, int k, int d)
+{
+    std::vector<uint16_t> key((size_t)k, 0);
+    int G = std::min(1024, std::max(2, k / 16));
+    if (const char *e = getenv("MRQ_QO_GROUPS")) G = std::max(2, std::min(k, atoi(e)));   // A/B experiments
+    if (k < 4) return key;
+    const int dd = std::min(d, 64);
+    std::vector<float> g((size_t)G * dd);
+    for (int j = 0; j < G; j++)
+        for (int i = 0; i < dd; i++) g[(size_t)j * dd + i] = C32[(size_t)((int64_t)j * k / G) * d + i];
+    std::vector<int> asg((size_t)k, 0), cnt((size_t)G);
+    std::vector<double> sum((size_t)G * dd);
+    const int nth = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    for (int it = 0; it < 2; it++) {
+        auto assign = [&](int c0, int c1) {
+            for (int c = c0; c < c1; c++) {
+                const float *x = &C32[(size_t)c * d];
+                float best = INFINITY;
+                int bj = 0;
+                for (int j = 0; j < G; j++) {
+                    const float s = sqdist_f32(x, &g[(size_t)j * dd], dd);
+                    if (s < best) {
+                        best = s;
+                        bj = j;
+                    }
+                }
+                asg[c] = bj;
+            }
+        };
+        std::vector<std::thread> th;
+        for (int t = 1; t < nth; t++)
+            th.emplace_back(assign, (int)((int64_t)k * t / nth), (int)((int64_t)k * (t + 1) / nth));
+        assign(0, (int)((int64_t)k / nth));
+        for (auto &t : th) t.join();
+        std::fill(cnt.begin(), cnt.end(), 0);
+        std::fill(sum.begin(), sum.end(), 0.0);
+        for (int c = 0; c < k; c++) {
+            cnt[asg[c]]++;
+            for (int i = 0; i < dd; i++) sum[(size_t)asg[c] * dd + i] += C32[(size_t)c * d + i];
+        }
+        for (int j = 0; j < G; j++)
+            if (cnt[j] > 0)
+                for (int i = 0; i < dd; i++) g[(size_t)j * dd + i] = (float)(sum[(size_t)j * dd + i] / cnt[j]);
+    }
+    // greedy chain over the groups
+    std::vector<int> pos((size_t)G, -1);
+    int cur = 0;
+    for (int n = 0; n < G; n++) {
+        pos[cur] = n;
+        float best = INFINITY;
+        int bj = -1;
+        for (int j = 0; j < G; j++) {
+            if (pos[j] >= 0) continue;
+            const float s = sqdist_f32(&g[(size_t)cur * dd], &g[(size_t)j * dd], dd);
+            if (s < best || bj < 0) {
+                best = s;
+                bj = j;
+            }
+        }
+        if (bj < 0) break;
+        cur = bj;
+    }
+    std::vector<int> order((size_t)k);
+    for (int c = 0; c < k; c++) order[c] = c;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return pos[asg[a]] < pos[asg[b]]; });
+    for (int r = 0; r < k; r++) key[order[r]] = (uint16_t)((int64_t)r * MRQ_QO_KEYS / k);
+    return key;
+}
+
 static int load_impl(mrq_index *ix, const char *build_file, const float *base, int64_t n, int32_t D, int32_t d,
                      const mrq_dist_cfg *dist)
 {
@@ -324,6 +424,10 @@ static int load_impl(mrq_index *ix, const char *build_file, const float *base, i
     TRY(upload(ix, &ix->list_size, ix->h_list_size.data(), k));
     TRY(upload(ix, &ix->list_size_g, cnt.data(), k));
     TRY(upload(ix, &ix->ids, ids.data(), npad));
+    {
+        const std::vector<uint16_t> lkey = list_locality_keys(C32, k, d);
+        TRY(upload(ix, &ix->list_key, lkey.data(), (size_t)k));
+    }
     TRY(dalloc(ix, (void **)&ix->Rc, (size_t)k * d * 8));
     k_rc<<<(k + 7) / 8, 256, 0, ix->stream>>>(ix->C, ix->RT, k, d, W, ix->Rc);
 
@@ -573,6 +677,23 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
         SCR("qorder", uint32_t, nq, qorder);
         SCR("qkey", uint16_t, nrow, qkey);
     }
+    const bool pc_key = qkey && ix->qorder_on == 1;   // key from the projection (k_qtail); else from the probe
+    // side stream: r0 = R q_d (only the quantizer needs it) and, with the
+    // order key from the projection (qorder = 1), the order's single-block
+    // sort (all queries are local unless the front end is sharded).  Forked
+    // right after k_qtail with qorder = 1; with the key from the probe
+    // (qorder = 2) after the probe screen has been launched, so that the
+    // persistent probe CTAs take their SMs first and r0 runs beside the probe
+    // finish (forked before the screen, r0's blocks delayed some probe CTAs:
+    // screen + 5 us).
+    auto fork_r0 = [&]() -> int {
+        MRQ_CUDA_TRY(cudaEventRecord(ix->ev_fork[0], st));
+        MRQ_CUDA_TRY(cudaStreamWaitEvent(ix->side, ix->ev_fork[0], 0));
+        if (pc_key && !fshard) launch_qorder(qkey, nq, qorder, ix->side);
+        launch_rowmat_f64(qp + q0 * D, nr, D, d, nullptr, ix->RT, d, r0 + q0 * d, d, ix->side);
+        MRQ_CUDA_TRY(cudaEventRecord(ix->ev_fork[3], ix->side));
+        return MRQ_OK;
+    };
     // ---- a1: query projection (Alg.2 L1-L4), rows [q0, q0 + nr)
     nvtx.stage("a1 projection");
     if (nr > 0) {
@@ -582,15 +703,8 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
             MRQ_CUDA_TRY(cudaFuncSetAttribute(k_qtail, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsmem));
         k_qtail<<<(unsigned)((nr + 7) / 8), 256, qsmem, st>>>(
             qp + q0 * D, nr, D, d, W, ix->lam, ix->RT, p->resid_scale, p->m, qr2 + q0, eps_r + q0, r0 + q0 * d,
-            qd32 + q0 * d, qnorm + q0, qkey ? qkey + q0 : nullptr, qa3 ? qa3 + q0 * 3 * d : nullptr);
-        // side stream, beside the probe: the order's single-block sort (all
-        // queries are local unless the front end is sharded) and r0 = R q_d
-        // (only the quantizer needs it)
-        MRQ_CUDA_TRY(cudaEventRecord(ix->ev_fork[0], st));
-        MRQ_CUDA_TRY(cudaStreamWaitEvent(ix->side, ix->ev_fork[0], 0));
-        if (qkey && !fshard) launch_qorder(qkey, nq, qorder, ix->side);
-        launch_rowmat_f64(qp + q0 * D, nr, D, d, nullptr, ix->RT, d, r0 + q0 * d, d, ix->side);
-        MRQ_CUDA_TRY(cudaEventRecord(ix->ev_fork[3], ix->side));
+            qd32 + q0 * d, qnorm + q0, pc_key ? qkey + q0 : nullptr, qa3 ? qa3 + q0 * 3 * d : nullptr);
+        if (pc_key) TRY(fork_r0());
     }
     if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[1], st));
 
@@ -619,6 +733,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
             if (ix->probe_share) SCR("probe_gkey", uint32_t, (size_t)nr, gkey);
             const double kappa = mrq_probe_tc_kappa(ix);
             TRY(mrq_probe_tc_run_fused(ix, qa3 + q0 * 3 * d, nr, np, qn_r, kappa, cbuf, capp, ccnt, kvbuf, gkey, st));
+            if (!pc_key) TRY(fork_r0());
             if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[11], st));
             TRY(launch_probe_finish_w(nr, k, d, np, qp_r, D, ix->C, qn_r, ix->cmax, kappa, cbuf, P, capp,
                                       mrq_probe_tc_grid(ix, nr), ccnt, kvbuf, cand, pr_r, pq_r, ncand, st));
@@ -633,6 +748,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
                 k_probe_approx<<<grid, 256, 8 * d * sizeof(float), st>>>(qd32 + q0 * d, nr, d, k, ix->C32T, approx);
                 kappa = std::ldexp(1.0, -24) * (2.0 * d + 8.0);
             }
+            if (!pc_key) TRY(fork_r0());
             if (timed) MRQ_CUDA_TRY(cudaEventRecord(ix->ev[11], st));
             TRY(launch_probe_select_w(approx, nr, k, d, np, qp_r, D, ix->C, qn_r, ix->cmax, kappa, cand, pr_r, pq_r,
                                       ncand, st));
@@ -663,10 +779,16 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
     auto fork_offsets = [&]() -> int {   // F1 segment offsets of all nq queries on the side stream
         MRQ_CUDA_TRY(cudaEventRecord(ix->ev_fork[1], st));
         MRQ_CUDA_TRY(cudaStreamWaitEvent(ix->side, ix->ev_fork[1], 0));
-        if (qkey && fshard) launch_qorder(qkey, nq, qorder, ix->side);
+        if (pc_key && fshard) launch_qorder(qkey, nq, qorder, ix->side);
         if (use_lm) TRY(mrq_lm_build(probe, nq, np, k, ix->list_size, lm_qg, lms, ix->side));
-        k_cand_count<<<(unsigned)((nq + 255) / 256), 256, 0, ix->side>>>(probe, nq, np, ix->list_size, cand_cnt);
-        k_exclusive_scan<<<1, 1024, 0, ix->side>>>(cand_cnt, nq, f1_off);
+        // (qorder = 2: the order key of the nearest probed list -- every query's probe row is here by now)
+        const bool probe_key = qkey && !pc_key;
+        k_cand_count<<<(unsigned)((nq + 255) / 256), 256, 0, ix->side>>>(probe, nq, np, ix->list_size, cand_cnt,
+                                                                         ix->list_key, probe_key ? qkey : nullptr);
+        if (probe_key)
+            k_offsets_order<<<2, 1024, 0, ix->side>>>(cand_cnt, nq, f1_off, qkey, qorder);
+        else
+            k_exclusive_scan<<<1, 1024, 0, ix->side>>>(cand_cnt, nq, f1_off);
         MRQ_CUDA_TRY(cudaEventRecord(ix->ev_fork[2], ix->side));
         return MRQ_OK;
     };
@@ -692,7 +814,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
         sec(probe_qn2, (size_t)np * 8);
         sec(planes, (size_t)np * MRQ_BQ * W * 4);
         sec(qconst, (size_t)np * 8 * 8);
-        if (qkey) sec(qkey, 2);
+        if (pc_key) sec(qkey, 2);
         if (qsk_b) {
             sec(qsk_b, (size_t)np * ix->dq);
             sec(qsk_c, (size_t)np * 4 * 8);

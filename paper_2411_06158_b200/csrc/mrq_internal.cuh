@@ -103,9 +103,10 @@ struct mrq_index {
     void *probe_tc = nullptr;                  // tcgen05 probe state (mrq_probe_tc.cu)
     int force_cuda_core_probe = 0;             // mrq_debug_set("cuda_core_probe"): CUDA-core screen instead
 #ifndef MRQ_QORDER_DEFAULT
-#define MRQ_QORDER_DEFAULT 1
+#define MRQ_QORDER_DEFAULT 2
 #endif
-    int qorder_on = MRQ_QORDER_DEFAULT;        // mrq_debug_set("qorder"): list-locality query order
+    int qorder_on = MRQ_QORDER_DEFAULT;        // mrq_debug_set("qorder"): query processing order (0 as given,
+                                               // 1 key from 3 principal coordinates, 2 key of the nearest probed list)
     int force_probe_unfused = 0;               // mrq_debug_set("probe_unfused"): screen to HBM + k_probe_select_w
     int graphs = 1;                            // CUDA-graph replay of repeated searches (mrq_debug_set "graphs")
     int tails_host = 0;                        // MRQ_LOAD_TAILS_HOST: tails in mapped pinned host memory
@@ -138,6 +139,7 @@ struct mrq_index {
     uint32_t *list_off = nullptr, *list_size = nullptr;                   // [k+1], [k] (owned lists; 0 if not owned)
     uint32_t *list_size_g = nullptr;                                      // [k] global list sizes (seed pool, decision T)
     uint32_t *ids = nullptr;                                              // [npad] global id of each slot
+    uint16_t *list_key = nullptr;                                         // [k] locality key of each list (< MRQ_QO_KEYS)
     uint32_t *codes = nullptr;                                            // [W][npad]
     float *f1 = nullptr, *f2 = nullptr, *f3 = nullptr, *xr2 = nullptr;    // [npad]
     float *heads = nullptr, *tails = nullptr;                             // [npad][d], [npad][D-d]

@@ -524,8 +524,8 @@ void launch_quant(const uint32_t *probe, const double *probe_qn2, int64_t nq, in
 // lists, so the list-major kernels that follow (scan, head gather, re-rank)
 // run neighbouring queries at the same time and share the lists' codes and
 // rows in L2.  One block; order within a key is arbitrary.
-__global__ void __launch_bounds__(1024) k_qorder(const uint16_t *__restrict__ qkey, int64_t nq,
-                                                 uint32_t *__restrict__ order)
+__device__ __forceinline__ void dev_qorder(const uint16_t *__restrict__ qkey, int64_t nq,
+                                           uint32_t *__restrict__ order)
 {
     __shared__ uint32_t hist[MRQ_QO_KEYS];
     __shared__ uint32_t wsum[32];
@@ -563,17 +563,34 @@ __global__ void __launch_bounds__(1024) k_qorder(const uint16_t *__restrict__ qk
     for (int64_t q = threadIdx.x; q < nq; q += blockDim.x) order[atomicAdd(&hist[qkey[q]], 1u)] = (uint32_t)q;
 }
 
+__global__ void __launch_bounds__(1024) k_qorder(const uint16_t *__restrict__ qkey, int64_t nq,
+                                                 uint32_t *__restrict__ order)
+{
+    dev_qorder(qkey, nq, order);
+}
+
 void launch_qorder(const uint16_t *qkey, int64_t nq, uint32_t *order, cudaStream_t st)
 {
     k_qorder<<<1, 1024, 0, st>>>(qkey, nq, order);
 }
 
 // Candidate count per query (sum of its probed list sizes) ...
+// qkey (qorder = 2): also the query's order key, the locality key of its
+// nearest probed list (list_key, built at load time from the centroids:
+// mrq_api.cu list_locality_keys).  Queries whose nearest lists are close
+// share most of their np probed lists, whatever the dimension; the key from
+// three principal coordinates (mrq_qorder_key) separates them poorly when
+// the spectrum is flat.
 __global__ void k_cand_count(const uint32_t *__restrict__ probe, int64_t nq, int np,
-                             const uint32_t *__restrict__ list_size, uint64_t *__restrict__ cnt)
+                             const uint32_t *__restrict__ list_size, uint64_t *__restrict__ cnt,
+                             const uint16_t *__restrict__ list_key, uint16_t *__restrict__ qkey)
 {
     const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= nq) return;
+    if (qkey) {
+        const uint32_t c0 = probe[q * np];
+        qkey[q] = c0 == 0xFFFFFFFFu ? (uint16_t)0 : list_key[c0];
+    }
     uint64_t s = 0;
     for (int p = 0; p < np; p++) {
         uint32_t c = probe[q * np + p];
@@ -583,7 +600,8 @@ __global__ void k_cand_count(const uint32_t *__restrict__ probe, int64_t nq, int
 }
 
 // ... and its exclusive prefix sum (one block; out[nq] = total).
-__global__ void k_exclusive_scan(const uint64_t *__restrict__ in, int64_t n, uint64_t *__restrict__ out)
+__device__ __forceinline__ void dev_exclusive_scan(const uint64_t *__restrict__ in, int64_t n,
+                                                   uint64_t *__restrict__ out)
 {
     // thread t owns the contiguous run [t per, (t + 1) per): its total, a
     // block scan of the totals, then the run's prefixes -- two passes over in[]
@@ -616,6 +634,27 @@ __global__ void k_exclusive_scan(const uint64_t *__restrict__ in, int64_t n, uin
         run += in[i];
     }
     if (t == (int)blockDim.x - 1) out[n] = run;
+}
+
+__global__ void __launch_bounds__(1024) k_exclusive_scan(const uint64_t *__restrict__ in, int64_t n,
+                                                         uint64_t *__restrict__ out)
+{
+    dev_exclusive_scan(in, n, out);
+}
+
+// The two single-block passes of the side stream in one launch of two blocks
+// (block 0: the F1 segment offsets; block 1: the query order from qkey): two
+// 1024-thread blocks find room beside the quantizer's blocks sooner one after
+// the other than two dependent launches do.
+__global__ void __launch_bounds__(1024) k_offsets_order(const uint64_t *__restrict__ cnt, int64_t nq,
+                                                        uint64_t *__restrict__ off,
+                                                        const uint16_t *__restrict__ qkey,
+                                                        uint32_t *__restrict__ order)
+{
+    if (blockIdx.x == 0)
+        dev_exclusive_scan(cnt, nq, off);
+    else
+        dev_qorder(qkey, nq, order);
 }
 
 // Sketch arguments of the fused scan (SK = true; LOOSE FULL, tau1 = tau0):

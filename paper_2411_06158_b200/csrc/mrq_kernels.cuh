@@ -21,7 +21,10 @@ void launch_quant(const uint32_t *probe, const double *probe_qn2, int64_t nq, in
                   const double *r0, const double *Rc, const double *qr2, double eps0, uint32_t *planes,
                   double *qconst, uint8_t *qsk_b, double *qsk_c, int dq, const double *qnorm, double cmax,
                   cudaStream_t st);
-__global__ void k_cand_count(const uint32_t *probe, int64_t nq, int np, const uint32_t *list_size, uint64_t *cnt);
+__global__ void k_cand_count(const uint32_t *probe, int64_t nq, int np, const uint32_t *list_size, uint64_t *cnt,
+                             const uint16_t *list_key, uint16_t *qkey);
+__global__ void k_offsets_order(const uint64_t *cnt, int64_t nq, uint64_t *off, const uint16_t *qkey,
+                                uint32_t *order);
 __global__ void k_exclusive_scan(const uint64_t *in, int64_t n, uint64_t *out);
 struct StageArgs {
     int64_t nq;
