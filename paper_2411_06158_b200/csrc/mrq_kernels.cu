@@ -727,6 +727,9 @@ __device__ __forceinline__ bool mrq_sketch_decide(int ab, int aa, float4 se, con
 #define MRQ_SCAN_THREADS 128   // 4 warps per query: a smaller end-of-query tail than 8 (measured)
 #endif
 #define MRQ_SKQ 640            // per-warp sketch queue, drained after the tile loop
+#ifndef MRQ_SK_CB
+#define MRQ_SK_CB 2            // 16-byte chunks of a sketch row loaded before any is used
+#endif
 template <int W, bool SK, int H>
 __global__ void __launch_bounds__(MRQ_SCAN_THREADS, (W <= 3 ? 1024 / MRQ_SCAN_THREADS : 1)) k_scan(
     const uint32_t *__restrict__ probe, int np, int64_t npad, const uint32_t *__restrict__ list_off,
@@ -743,7 +746,11 @@ __global__ void __launch_bounds__(MRQ_SCAN_THREADS, (W <= 3 ? 1024 / MRQ_SCAN_TH
     uint32_t *tile_pre = pl_s + np * (MRQ_BQ * W);       // np + 1
     uint32_t *lst_start = tile_pre + np + 1;             // np
     uint32_t *lst_end = lst_start + np;                  // np
-    uint8_t *skb_s = (uint8_t *)(((uintptr_t)(lst_end + np) + 15) & ~(uintptr_t)15);   // SK: np x dq sketch rows
+    // SK: np sketch rows of dq bytes, each padded by 16 bytes (rows of odd and even index fall
+    // in different banks: a quarter-warp's 16-byte reads of 8 distinct rows do not conflict);
+    // addressed as uint4 off the shared base so that the reads are LDS.128
+    uint4 *skb4 = (uint4 *)csm + (((int)((unsigned char *)(lst_end + np) - csm) + 15) >> 4);
+    const int skrow = SK ? sk.dq / 16 + 1 : 1;
     __shared__ uint32_t sh_cnt, sh_surv;
     __shared__ uint32_t skq[SK ? (MRQ_SCAN_THREADS / 32) * MRQ_SKQ : 1];   // SK: per-warp queue, slots
     __shared__ uint16_t skp[SK ? (MRQ_SCAN_THREADS / 32) * MRQ_SKQ : 1];
@@ -756,7 +763,8 @@ __global__ void __launch_bounds__(MRQ_SCAN_THREADS, (W <= 3 ? 1024 / MRQ_SCAN_TH
     if (SK) {
         for (int i = threadIdx.x; i < np * 3; i += blockDim.x) skc_s[i] = sk.qsk_c[(q * np + i / 3) * 4 + i % 3];
         const uint4 *src = (const uint4 *)(sk.qsk_b + q * np * sk.dq);
-        for (int i = threadIdx.x; i < np * sk.dq / 16; i += blockDim.x) ((uint4 *)skb_s)[i] = src[i];
+        const int nw = sk.dq / 16;
+        for (int i = threadIdx.x; i < np * nw; i += blockDim.x) skb4[(i / nw) * skrow + i % nw] = src[i];
     }
     if (warp == 0) {
         uint32_t carry = 0;
@@ -819,19 +827,19 @@ __global__ void __launch_bounds__(MRQ_SCAN_THREADS, (W <= 3 ? 1024 / MRQ_SCAN_TH
             pp[u] = in[u] ? wp[i] : 0;
             se[u] = in[u] ? sk.hs[slot[u]] : make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        for (int w0 = 0; w0 < nw; w0 += 2) {   // 2 chunks x 2 entries of loads in flight
-            uint4 r[2][2];
+        for (int w0 = 0; w0 < nw; w0 += MRQ_SK_CB) {   // MRQ_SK_CB chunks x 2 entries of loads in flight
+            uint4 r[2][MRQ_SK_CB];
 #pragma unroll
             for (int u = 0; u < 2; u++)
 #pragma unroll
-                for (int c = 0; c < 2; c++)
+                for (int c = 0; c < MRQ_SK_CB; c++)
                     r[u][c] = (in[u] && w0 + c < nw) ? __ldg((const uint4 *)(sk.hq + (int64_t)slot[u] * sk.dq) + w0 + c)
                                                      : make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
             for (int u = 0; u < 2; u++)
 #pragma unroll
-                for (int c = 0; c < 2; c++)
-                    if (w0 + c < nw) mrq_dp4a_ab(r[u][c], ((const uint4 *)(skb_s + pp[u] * sk.dq))[w0 + c], ab[u]);
+                for (int c = 0; c < MRQ_SK_CB; c++)
+                    if (w0 + c < nw) mrq_dp4a_ab(r[u][c], skb4[pp[u] * skrow + w0 + c], ab[u]);
         }
 #pragma unroll
         for (int u = 0; u < 2; u++) aa[u] = (int)se[u].w;

@@ -110,7 +110,7 @@ inline size_t mrq_scan_smem(int np, int W)
     return (size_t)np * 5 * 8 + (size_t)np * MRQ_BQ * W * 4 + (size_t)(3 * np + 1) * 4;
 }
 // ... plus, with the fused head-sketch test, the per-list sketch constants and rows
-inline size_t mrq_scan_smem_sk(int np, int W, int dq) { return mrq_scan_smem(np, W) + (size_t)np * 24 + 16 + (size_t)np * dq; }
+inline size_t mrq_scan_smem_sk(int np, int W, int dq) { return mrq_scan_smem(np, W) + (size_t)np * 24 + 16 + (size_t)np * (dq + 16); }
 int launch_scan(int W, const LaunchScan &a, cudaStream_t st);
 bool supported_W(int W);
 void launch_f1_all(const uint32_t *probe, int64_t nq, int np, const uint32_t *list_off, const uint32_t *list_size,
