@@ -665,6 +665,7 @@ static int search_impl(mrq_index *ix, const float *d_q, int64_t nq, const mrq_se
     // head sketch: the scan drops F1 entries whose lower bound
     // of the canonical dis_o' already fails the F2 test (LOOSE: tau1 = tau0)
     const bool want_sketch = ix->sketch_on && mode == 0 && !tight && !ix->dbg_dump_dis &&
+                             mrq_scan_sketch_fits(np, ix->npad) &&
                              mrq_scan_smem_sk(np, W, ix->dq) <= (size_t)std::min(ix->smem_optin, 64 * 1024);
     uint8_t *qsk_b = nullptr;
     double *qsk_c = nullptr;

@@ -670,6 +670,7 @@ struct ScanSketch {
     const double *qr2;      // [nq]
     int dq;
     uint32_t *surv_cnt;     // [nq]
+    int pshift;             // a queue entry is (probe index << pshift) | slot (launch_scan_ws)
 };
 
 // Head-sketch test of one F1 candidate (DESIGN.md §5 "head sketch"): in the
@@ -726,7 +727,9 @@ __device__ __forceinline__ bool mrq_sketch_decide(int ab, int aa, float4 se, con
 #ifndef MRQ_SCAN_THREADS
 #define MRQ_SCAN_THREADS 128   // 4 warps per query: a smaller end-of-query tail than 8 (measured)
 #endif
-#define MRQ_SKQ 640            // per-warp sketch queue, drained after the tile loop
+#ifndef MRQ_SKQ
+#define MRQ_SKQ 960            // per-warp sketch queue (4-byte entries), drained after the tile loop
+#endif
 #ifndef MRQ_SK_CB
 #define MRQ_SK_CB 2            // 16-byte chunks of a sketch row loaded before any is used
 #endif
@@ -752,8 +755,8 @@ __global__ void __launch_bounds__(MRQ_SCAN_THREADS, (W <= 3 ? 1024 / MRQ_SCAN_TH
     uint4 *skb4 = (uint4 *)csm + (((int)((unsigned char *)(lst_end + np) - csm) + 15) >> 4);
     const int skrow = SK ? sk.dq / 16 + 1 : 1;
     __shared__ uint32_t sh_cnt, sh_surv;
-    __shared__ uint32_t skq[SK ? (MRQ_SCAN_THREADS / 32) * MRQ_SKQ : 1];   // SK: per-warp queue, slots
-    __shared__ uint16_t skp[SK ? (MRQ_SCAN_THREADS / 32) * MRQ_SKQ : 1];
+    // SK: per-warp queue of F1 entries, (probe index << pshift) | slot in one word
+    __shared__ uint32_t skq[SK ? (MRQ_SCAN_THREADS / 32) * MRQ_SKQ : 1];
     const int64_t q = qorder ? (int64_t)qorder[blockIdx.x] : (int64_t)blockIdx.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nwarps = blockDim.x >> 5;
@@ -807,7 +810,8 @@ __global__ void __launch_bounds__(MRQ_SCAN_THREADS, (W <= 3 ? 1024 / MRQ_SCAN_TH
     int cur_p = -1;
     // SK: the warp's queue of F1 candidates awaiting the sketch test
     uint32_t *wq = skq + warp * MRQ_SKQ;
-    uint16_t *wp = skp + warp * MRQ_SKQ;
+    const int pshift = SK ? sk.pshift : 0;
+    const uint32_t smask = SK ? (pshift < 32 ? (1u << pshift) - 1u : 0xFFFFFFFFu) : 0u;
     int qn = 0;
     const double qr2 = SK ? sk.qr2[q] : 0.0;
     // SK: sketch-test queue entries [i0, i0 + 64): two per lane, both rows in
@@ -823,8 +827,9 @@ __global__ void __launch_bounds__(MRQ_SCAN_THREADS, (W <= 3 ? 1024 / MRQ_SCAN_TH
         for (int u = 0; u < 2; u++) {
             const int i = i0 + u * 32 + lane;
             in[u] = i < qn;
-            slot[u] = in[u] ? wq[i] : 0u;
-            pp[u] = in[u] ? wp[i] : 0;
+            const uint32_t e = in[u] ? wq[i] : 0u;
+            slot[u] = e & smask;
+            pp[u] = pshift < 32 ? (int)(e >> pshift) : 0;
             se[u] = in[u] ? sk.hs[slot[u]] : make_float4(0.f, 0.f, 0.f, 0.f);
         }
         for (int w0 = 0; w0 < nw; w0 += MRQ_SK_CB) {   // MRQ_SK_CB chunks x 2 entries of loads in flight
@@ -911,10 +916,11 @@ __global__ void __launch_bounds__(MRQ_SCAN_THREADS, (W <= 3 ? 1024 / MRQ_SCAN_TH
                     const uint32_t o0 = qn + __popc(b0 & lt), o1 = qn + n0 + __popc(b1 & lt);
                     const uint32_t o2 = qn + n0 + n1 + __popc(b2 & lt), o3 = qn + n0 + n1 + n2 + __popc(b3 & lt);
                     MRQ_ASSERT(qn + tot <= MRQ_SKQ);
-                    if (fl[0]) { wq[o0] = b; wp[o0] = (uint16_t)p; }
-                    if (fl[1]) { wq[o1] = b + 1; wp[o1] = (uint16_t)p; }
-                    if (fl[2]) { wq[o2] = b + 2; wp[o2] = (uint16_t)p; }
-                    if (fl[3]) { wq[o3] = b + 3; wp[o3] = (uint16_t)p; }
+                    const uint32_t e = b | (pshift < 32 ? (uint32_t)p << pshift : 0u);
+                    if (fl[0]) wq[o0] = e;
+                    if (fl[1]) wq[o1] = e + 1;
+                    if (fl[2]) wq[o2] = e + 2;
+                    if (fl[3]) wq[o3] = e + 3;
                     qn += tot;
                 } else {
                     // (SK with a full queue: these F1 members skip the sketch test and are
@@ -1594,11 +1600,16 @@ template <int W, bool SK, int H>
 static int launch_scan_ws(const LaunchScan &a, cudaStream_t st)
 {
     // the opt-in covers static + dynamic shared memory (SK adds a static per-warp queue)
-    if (a.smem + (SK ? (MRQ_SCAN_THREADS / 32) * MRQ_SKQ * 6 + 64 : 64) > 48 * 1024)
+    if (a.smem + (SK ? (MRQ_SCAN_THREADS / 32) * MRQ_SKQ * 4 + 64 : 64) > 48 * 1024)
         MRQ_CUDA_TRY(cudaFuncSetAttribute(k_scan<W, SK, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a.smem));
     ScanSketch sk;
     sk.hq = a.hq; sk.hs = a.hs; sk.qsk_b = a.qsk_b; sk.qsk_c = a.qsk_c; sk.qr2 = a.qr2;
     sk.dq = a.dq; sk.surv_cnt = a.surv_cnt;
+    sk.pshift = mrq_scan_pshift(a.np);
+    if (SK && !mrq_scan_sketch_fits(a.np, a.npad)) {
+        mrq_set_error("scan sketch queue: np=%d npad=%lld do not pack into one word", a.np, (long long)a.npad);
+        return MRQ_EINVAL;
+    }
     k_scan<W, SK, H><<<a.nq, MRQ_SCAN_THREADS, a.smem, st>>>(a.probe, a.np, a.npad, a.list_off, a.list_size, a.codes,
                                                            a.f1, a.f2, a.f3, a.planes, a.qconst, a.eps_r, a.tau0,
                                                            a.isd, a.f1_off, a.f1_cnt, a.f1_pos, a.qorder, sk);
@@ -1618,7 +1629,13 @@ static int launch_scan_w(const LaunchScan &a, cudaStream_t st)
         if (a.lm == 2) return a.surv_cnt ? launch_scan_tc_ws<WL, true>(a, st) : launch_scan_tc_ws<WL, false>(a, st);
         return a.surv_cnt ? launch_scan_lm_ws<WL, true>(a, st) : launch_scan_lm_ws<WL, false>(a, st);
     }
-    const bool dram = (uint64_t)a.npad * (4 * W + 12) > ((uint64_t)64 << 20);   // the stream cannot live in L2
+#ifndef MRQ_SCAN_H2_MB
+#define MRQ_SCAN_H2_MB 64
+#endif
+    // H = 2 when the stream cannot live in L2 AND the queries run in the given order; in the
+    // list-locality order (a.qorder) most of it is served by L2 all the same (Deep-shaped: L2 hit
+    // rate 60%, DRAM 1.5 GB of 3.9 GB) and H = 1 is faster (scan 0.686 -> 0.666 ms)
+    const bool dram = (uint64_t)a.npad * (4 * W + 12) > ((uint64_t)MRQ_SCAN_H2_MB << 20) && !a.qorder;
     if (a.surv_cnt) return dram ? launch_scan_ws<W, true, 2>(a, st) : launch_scan_ws<W, true, 1>(a, st);
     return dram ? launch_scan_ws<W, false, 2>(a, st) : launch_scan_ws<W, false, 1>(a, st);
 }

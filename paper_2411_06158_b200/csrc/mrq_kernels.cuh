@@ -111,6 +111,16 @@ inline size_t mrq_scan_smem(int np, int W)
 }
 // ... plus, with the fused head-sketch test, the per-list sketch constants and rows
 inline size_t mrq_scan_smem_sk(int np, int W, int dq) { return mrq_scan_smem(np, W) + (size_t)np * 24 + 16 + (size_t)np * (dq + 16); }
+// The fused sketch's queue entry packs (probe index, slot) into 32 bits: the probe index takes
+// ceil(log2 np) high bits, the slot the rest (np = 16: up to 2^28 slots per GPU; np = 64: 2^26).
+// A search that does not fit runs without the sketch (same results).
+inline int mrq_scan_pshift(int np)
+{
+    int b = 0;
+    while ((1 << b) < np) b++;
+    return 32 - b;
+}
+inline bool mrq_scan_sketch_fits(int np, int64_t npad) { return npad <= ((int64_t)1 << mrq_scan_pshift(np)); }
 int launch_scan(int W, const LaunchScan &a, cudaStream_t st);
 bool supported_W(int W);
 void launch_f1_all(const uint32_t *probe, int64_t nq, int np, const uint32_t *list_off, const uint32_t *list_size,

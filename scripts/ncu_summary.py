@@ -24,6 +24,12 @@ WANT = {
     "smsp__inst_executed.sum": "instructions",
     "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active": "tensor_pipe_pct",
     "sm__inst_executed_pipe_tensor.avg.pct_of_peak_sustained_active": "tensor_inst_pct",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_active_pct",
+    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active": "pipe_xu_pct",
+    "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active": "pipe_alu_pct",
+    "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active": "pipe_fp64_pct",
+    "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed": "l1_lsu_wavefronts_pct",
+    "lts__t_bytes.sum": "l2_bytes",
     "launch__grid_size": "grid",
     "launch__block_size": "block",
 }
@@ -52,7 +58,7 @@ def main():
             except ValueError:
                 continue
             u = units[i]
-            if key in ("dram_read", "dram_write"):
+            if key in ("dram_read", "dram_write", "l2_bytes"):
                 v *= SCALE.get(u, 1)
             if key == "duration":
                 v *= SCALE.get(u, 1)
