@@ -205,8 +205,13 @@ def main():
     ap.add_argument("--tau", default="auto", choices=["auto", "TIGHT", "LOOSE"],
                     help="decision-T schedule; auto = the faster one at the operating point")
     ap.add_argument("--seed-lists", type=int, default=2, help="decision T: seed pool spans >= this many lists")
-    ap.add_argument("--seed-mult", type=int, default=2, help="decision T: K' = seed_mult * K")
+    ap.add_argument("--seed-mult", type=int, default=None,
+                    help="decision T: K' = seed_mult * K (default: 3 while K' fits one warp's 32 lanes, else 2)")
     args = ap.parse_args()
+    if args.seed_mult is None:
+        # K' = 3 K seeds give a tighter tau0 than 2 K (Deep-shaped: F1 2074 -> 1826 per query, step
+        # 1.734 -> 1.673 ms) as long as the K' items still sit one per lane of the selecting warp
+        args.seed_mult = 3 if 3 * args.K <= 32 else 2
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # launched without torchrun: start one process per GPU ourselves
         # (the same launch the driver uses; rendezvous on 127.0.0.1)

@@ -1249,6 +1249,7 @@ static int debug_fetch(mrq_index *ix, const char *name, void *dst, size_t dst_by
             {"fallback", 4}, {"approx", (size_t)nq * k * 4}, {"probe_ncand", (size_t)nq * 4},
             {"dbg_dis", (size_t)ix->last_total * 8}, {"dbg_lb1", (size_t)ix->last_total * 8},
             {"surv_cnt", (size_t)nq * 4},
+            {"qorder", (size_t)nq * 4},        {"qkey", (size_t)nq * 2},
             {"probe_ccnt", ix->scratch.count("probe_ccnt") ? ix->scratch["probe_ccnt"].bytes : 0},
         };
         for (auto &e : per)
@@ -1286,7 +1287,8 @@ extern "C" int mrq_debug_set(mrq_index *ix, const char *name, int64_t value)
     ix->gexec = nullptr;
     memset(ix->g_key, 0, sizeof(GraphKey));
     memset(ix->g_pending, 0, sizeof(GraphKey));
-    if (std::string(name) == "qorder") {           // list-locality query processing order (default 1)
+    if (std::string(name) == "qorder") {           // query processing order: 0 as given, 1 key from the projection,
+                                                   // 2 (default) key of the nearest probed list
         ix->qorder_on = (int)value;
         return MRQ_OK;
     }

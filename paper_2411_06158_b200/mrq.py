@@ -250,7 +250,7 @@ def mrq_index_info(h):
     return {"n": n.value, "D": D.value, "d": d.value, "k": k.value, "npad": npad.value}
 
 
-_DT = {"u32": np.uint32, "u64": np.uint64, "f32": np.float32, "f64": np.float64}
+_DT = {"u16": np.uint16, "u32": np.uint32, "u64": np.uint64, "f32": np.float32, "f64": np.float64}
 
 
 def mrq_debug_set(h, name: str, value: int):

@@ -58,7 +58,7 @@ def main():
             pass
         print("== probe_bound_T", T)
         for _ in range(4):
-            _, _, st = gx.search(Q, K=10, nprobe=nprobe, tau_schedule="LOOSE", seed_lists=2, seed_mult=2)
+            _, _, st = gx.search(Q, K=10, nprobe=nprobe, tau_schedule="LOOSE", seed_lists=2, seed_mult=int(os.environ.get("SEED_MULT", "3")))
             print("probe %.4f gemm %.4f finish %.4f total %.4f" % (st.ms_probe, st.ms_probe_gemm,
                                                                   st.ms_probe - st.ms_probe_gemm, st.ms_total),
                   flush=True)

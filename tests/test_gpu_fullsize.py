@@ -63,13 +63,13 @@ def test_full_batch_sampled_parity(full, tau):
     ids = torch.empty((nq, K), dtype=torch.int64, device=dev)
     dist = torch.empty((nq, K), dtype=torch.float32, device=dev)
     s = torch.cuda.Stream(dev)
-    p = m.SearchParams.make(K=K, nprobe=npb, tau_schedule=tau, seed_lists=2)
+    p = m.SearchParams.make(K=K, nprobe=npb, tau_schedule=tau, seed_lists=2, seed_mult=3)
     for _ in range(3):   # plain, capture, replay: the bench's timed path
         m.mrq_search_batch_device(h, dq, p, ids, dist, None, s.cuda_stream)
     torch.cuda.synchronize()
     gi, gd = ids.cpu().numpy(), dist.cpu().numpy()
     sample = full["sample"]
-    oi, od, ost = ox.search(Q[sample], K=K, nprobe=npb, tau_schedule=tau, seed_lists=2)
+    oi, od, ost = ox.search(Q[sample], K=K, nprobe=npb, tau_schedule=tau, seed_lists=2, seed_mult=3)
     assert np.array_equal(gi[sample], oi)
     assert np.array_equal(gd[sample].view(np.uint32), od.view(np.uint32))
     # whole batch: ascending (dist, id) rows, no padding, distinct ids
@@ -85,6 +85,6 @@ def test_full_batch_recall(full):
         pytest.skip("no committed ground truth")
     gt = np.load(gtp)
     ids, _, _ = m.mrq_search_batch(h, Q, m.SearchParams.make(K=10, nprobe=full["npb"], tau_schedule="LOOSE",
-                                                             seed_lists=2), with_stats=False)
+                                                             seed_lists=2, seed_mult=3), with_stats=False)
     hits = sum(len(set(a.tolist()) & set(b.tolist())) for a, b in zip(ids, gt))
     assert hits / gt.size >= 0.95

@@ -119,7 +119,7 @@ def _segments(gx, nq, cnt_name, pos_name, extra=None):
 
 
 @pytest.mark.parametrize("tau", ["TIGHT", "LOOSE"])
-@pytest.mark.parametrize("seed_lists,seed_mult", [(1, 2), (4, 4)])
+@pytest.mark.parametrize("seed_lists,seed_mult", [(1, 2), (2, 3), (4, 4)])   # (2, 3): bench.py's operating point
 def test_stagewise_parity(case, tau, seed_lists, seed_mult):
     gx, ox, Q = case["gx"], case["ox"], case["Q"]
     nq, D, d = Q.shape[0], ox.D, case["d"]
@@ -302,26 +302,41 @@ def test_host_resident_tails_identical(case):
 
 
 def test_query_order_invariance(case):
-    """The list-locality processing order (k_qorder, a permutation of the
-    queries) changes no result: ids, distances, tau0/tau1 and every survivor
-    count equal the identity order's, for both schedules and K = 1 / 10 / 100."""
+    """The list-locality processing order (a permutation of the queries: 1 =
+    key from three principal coordinates, k_qorder; 2 = key of the nearest
+    probed list, k_cand_count + k_offsets_order, the default) changes no
+    result: ids, distances, tau0/tau1 and every survivor count equal the
+    identity order's, for both schedules and K = 1 / 10 / 100; the order is a
+    permutation, sorted by its key, and the mode-2 key is the locality key of
+    probe[q][0] (one key per list, every key < 4096)."""
     m, gx, Q = case["m"], case["gx"], case["Q"]
     npb = case["nprobe"][-1]
+    nq = Q.shape[0]
     try:
         for tau in ("TIGHT", "LOOSE"):
             for K in (1, 10, 100):
                 res = []
-                for on in (0, 1):
+                for on in (0, 1, 2):
                     m.mrq_debug_set(gx.h, "qorder", on)
                     ids, dist, st = gx.search(Q, K=K, nprobe=npb, tau_schedule=tau)
                     res.append((ids, dist, st, gx.fetch("tau0", "f64").copy(), gx.fetch("tau1", "f64").copy()))
-                a, b = res
-                assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
-                assert np.array_equal(a[3], b[3]) and np.array_equal(a[4], b[4])
-                for f in ("scanned", "stage1_pass", "stage2_pass", "exact", "seeds"):
-                    assert getattr(a[2], f) == getattr(b[2], f), f
+                    if on:
+                        order = gx.fetch("qorder", "u32")[:nq].astype(np.int64)
+                        key = gx.fetch("qkey", "u16")[:nq].astype(np.int64)
+                        assert np.array_equal(np.sort(order), np.arange(nq))
+                        assert np.all(np.diff(key[order]) >= 0) and key.max() < 4096
+                    if on == 2:
+                        top1 = gx.fetch("probe", "u32").reshape(nq, -1)[:, 0].astype(np.int64)
+                        for c in np.unique(top1):          # one key per list
+                            assert len(np.unique(key[top1 == c])) == 1
+                a = res[0]
+                for b in res[1:]:
+                    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+                    assert np.array_equal(a[3], b[3]) and np.array_equal(a[4], b[4])
+                    for f in ("scanned", "stage1_pass", "stage2_pass", "exact", "seeds"):
+                        assert getattr(a[2], f) == getattr(b[2], f), f
     finally:
-        m.mrq_debug_set(gx.h, "qorder", 1)
+        m.mrq_debug_set(gx.h, "qorder", 2)
 
 
 def test_nocorr_parity(case):
