@@ -155,6 +155,18 @@ def ncu_traffic(cfg_name, nprobe):
         return {}
 
 
+def ncu_counters(cfg_name, nprobe):
+    """The other per-launch ncu figures of the same committed summary (L2 hit
+    rate, issue-active, XU / fp64 pipe, L1 LSU wavefronts, occupancy; percent)."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic_%s_np%d.json" % (cfg_name, nprobe))
+    try:
+        with open(path) as f:
+            return {k: {a: round(b, 1) for a, b in v.items() if a != "dram_bytes_per_launch"}
+                    for k, v in json.load(f)["kernels"].items()}
+    except Exception:
+        return {}
+
+
 def recall_at_k(found, gt, K):
     f = np.asarray(found)[:, :K]
     g = np.asarray(gt)[:, :K]
@@ -388,6 +400,7 @@ def main():
     sk_pass = float(np.mean([s.sketch_pass for s in sts]))
     hbm, peak_kind = peaks()
     traffic = ncu_traffic(cfg_name, nprobe)
+    counters = ncu_counters(cfg_name, nprobe)
     fused_topk = tau_sel != "TIGHT" and K <= 32   # k_head_topk replaces k_head_b + k_topk_w
     # algorithmic bytes per unit: scan = one
     # scanned code (W code words + f1/f2/f3); head gather = one F1 survivor
@@ -434,6 +447,9 @@ def main():
         if kk["traffic"]:   # the DRAM side: ncu bytes per launch over the same launch time
             kk["dram_gbs"] = round(kk["traffic"] / (kk["ms"] * 1e-3) / 1e9, 1)
             kk["dram_frac"] = round(kk["dram_gbs"] / hbm, 4)
+        cn = counters.get(nm, next((v for k, v in counters.items() if k.startswith(nm + "<")), None))
+        if cn:   # what binds the kernel when DRAM does not (committed ncu --set full capture)
+            kk["ncu"] = cn
     dom = max(kern, key=lambda n: kern[n]["ms"])
     # the probe screen GEMM on the tensor cores (kind::tf32): its flops against
     # the tf32 peak = measured bf16 burst x the nominal tf32/bf16 ratio (1.1/2.25)
@@ -523,8 +539,9 @@ def main():
                      "bytes_per_unit": kern[dom]["bytes_per_unit"], "unit_kind": kern[dom]["unit"],
                      "kernels": kern, "codes_per_s_per_gpu": round(scanned / (ms_scan * 1e-3), 1),
                      "scan_frac_of_hbm": round(scanned / (ms_scan * 1e-3) * bcode / 1e9 / hbm, 4), "probe_gemm": probe_tc,
-                     "note": "achieved = algorithmic bytes / launch time; above 1.0 when L2 serves re-reads "
-                             "(list-locality query order): dram_gbs / dram_frac give the DRAM side"},
+                     "note": "achieved = algorithmic bytes / launch time; L2 serves most re-reads in the "
+                             "list-locality query order: dram_gbs / dram_frac give the DRAM side, ncu.* (percent, "
+                             "committed --set full capture) what binds the kernel then (issue slots, XU pipe)"},
         "e2e": {"value": round(nq / e2e_s, 1), "unit": "queries/s", "h2d_bytes_per_step": int(nq * X.shape[1] * 4),
                 "d2h_bytes_per_step": int(nq * K * 12), "steps": e2e_steps,
                 "ms_per_step": {"mean": round(1e3 * e2e_s, 4), "median": round(1e3 * float(np.median(e2e_t)), 4)}},

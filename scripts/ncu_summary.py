@@ -72,7 +72,9 @@ def main():
                    "(ncu flushes caches between replays)", "kernels": res}, f, indent=1)
     if traffic_out:
         with open(traffic_out, "w") as f:
-            json.dump({"source": out, "kernels": {n: {"dram_bytes_per_launch": v.get("dram_bytes_per_launch")}
+            keep = ("dram_bytes_per_launch", "l2_hit_pct", "issue_active_pct", "pipe_xu_pct", "pipe_fp64_pct",
+                    "l1_lsu_wavefronts_pct", "achieved_occupancy_pct")
+            json.dump({"source": out, "kernels": {n: {k: v.get(k) for k in keep if v.get(k) is not None}
                                                   for n, v in res.items()}}, f, indent=1)
     for n, v in res.items():
         print("%-22s %8.1f us  dram %8.1f MB  dram%% %5.1f  L2hit %5.1f  tensor %s" % (
