@@ -401,6 +401,8 @@ def main():
     hbm, peak_kind = peaks()
     traffic = ncu_traffic(cfg_name, nprobe)
     counters = ncu_counters(cfg_name, nprobe)
+    sm_count = torch.cuda.get_device_properties(local).multi_processor_count
+    sm_max_mhz = clk.mx or 1965
     fused_topk = tau_sel != "TIGHT" and K <= 32   # k_head_topk replaces k_head_b + k_topk_w
     # algorithmic bytes per unit: scan = one
     # scanned code (W code words + f1/f2/f3); head gather = one F1 survivor
@@ -450,6 +452,14 @@ def main():
         cn = counters.get(nm, next((v for k, v in counters.items() if k.startswith(nm + "<")), None))
         if cn:   # what binds the kernel when DRAM does not (committed ncu --set full capture)
             kk["ncu"] = cn
+            if cn.get("instructions"):
+                # the ALU-side roofline: executed warp instructions per launch (ncu) over the live launch
+                # time against the issue peak, SMs x 4 schedulers x the max SM clock (one warp
+                # instruction per scheduler per cycle)
+                issue_peak = sm_count * 4 * sm_max_mhz * 1e6
+                kk["issue"] = {"bound": "alu", "achieved": round(cn["instructions"] / (kk["ms"] * 1e-3) / 1e9, 1),
+                               "peak": round(issue_peak / 1e9, 1), "unit": "G warp-instructions/s",
+                               "frac": round(cn["instructions"] / (kk["ms"] * 1e-3) / issue_peak, 4)}
     dom = max(kern, key=lambda n: kern[n]["ms"])
     # the probe screen GEMM on the tensor cores (kind::tf32): its flops against
     # the tf32 peak = measured bf16 burst x the nominal tf32/bf16 ratio (1.1/2.25)

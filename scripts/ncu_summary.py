@@ -73,7 +73,7 @@ def main():
     if traffic_out:
         with open(traffic_out, "w") as f:
             keep = ("dram_bytes_per_launch", "l2_hit_pct", "issue_active_pct", "pipe_xu_pct", "pipe_fp64_pct",
-                    "l1_lsu_wavefronts_pct", "achieved_occupancy_pct")
+                    "l1_lsu_wavefronts_pct", "achieved_occupancy_pct", "instructions")
             json.dump({"source": out, "kernels": {n: {k: v.get(k) for k in keep if v.get(k) is not None}
                                                   for n, v in res.items()}}, f, indent=1)
     for n, v in res.items():
