@@ -69,6 +69,16 @@ def main():
         print(json.dumps(out), flush=True)
         return out
 
+    if args.grid == "quick":   # np = 16 with both query-order keys (mrq_debug_set qorder = 1 | 2)
+        for qo in (1, 2):
+            m.mrq_debug_set(h, "qorder", qo)
+            print(json.dumps({"event": "qorder", "value": qo}), flush=True)
+            point(16, mode="EXACT")
+            for mm in (8.0, 16.0):
+                point(16, "FULL", "LOOSE", mm)
+            point(16, "FULL", "TIGHT", 16.0)
+        m.mrq_free(h)
+        return
     for npb in (16, 32, 64, 128):
         point(npb, mode="EXACT")
     for npb in (16, 32, 64):
